@@ -1,0 +1,107 @@
+"""ctypes binding of libdippm_b200.so (the C ABI declared in include/dippm_b200.h).
+
+This is the only way the package reaches compute: there is no CPU or
+PyTorch-eager fallback.  If the library is missing, or no CUDA device is
+visible when a compute entry point is used, a DeviceUnavailable error is
+raised.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import DippmError, NonFinite, ShapeMismatch
+
+LIB_PATH = Path(__file__).resolve().parent / "libdippm_b200.so"
+
+OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+DT_F32, DT_BF16, DT_TF32X3 = 0, 1, 2
+GEMM_FWD, GEMM_STORE, GEMM_WGRAD = 0, 1, 2
+
+
+class DeviceUnavailable(DippmError):
+    """The CUDA library or a CUDA device is not available (no fallback exists)."""
+
+
+class KernelError(DippmError):
+    """A CUDA launch or runtime error reported by the native library."""
+
+
+class Act(C.Structure):
+    """dippm_act_t: activation matrix view."""
+    _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
+
+
+class GemmArgs(C.Structure):
+    """dippm_gemm_args_t."""
+    _fields_ = [
+        ("kind", C.c_int64), ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+        ("a", Act), ("a_mn_major", C.c_int64), ("b", Act), ("b_mn_major", C.c_int64),
+        ("bias", C.c_void_p), ("relu", C.c_int64), ("out", Act),
+        ("c", C.c_void_p), ("ldc", C.c_int64), ("splits", C.c_int64),
+    ]
+
+
+P, I32, I64, U64, F32, F64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_size_t
+
+# name -> (restype, argtypes); must match include/dippm_b200.h
+SIGNATURES = {
+    "dippm_last_error": (C.c_char_p, []),
+    "dippm_abi_version": (I32, []),
+    "dippm_device_sm_count": (I32, []),
+    "dippm_mig_code": (I32, [F64, C.POINTER(I32)]),
+    "dippm_mig_codes": (I32, [P, I64, I64, P, P, P]),
+    "dippm_csr_workspace_bytes": (SZ, [I64, I64]),
+    "dippm_build_csr": (I32, [P, P, I64, I64, P, P, P, P, P, P, P, P, SZ, P]),
+    "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
+    "dippm_colsum_blocks": (I32, [I64]),
+    "dippm_sage_backward_gather": (I32, [P, I64, I32, Act, Act, I64, P, P, P, P, P]),
+    "dippm_readout_backward": (I32, [P, I64, P, I64, I32, Act, Act, I64, P, P]),
+    "dippm_reduce_rows": (I32, [P, I64, I64, I32, F64, P, P]),
+    "dippm_wgrad_splits": (I32, [I64, I64, I64]),
+    "dippm_gemm": (I32, [C.POINTER(GemmArgs), I32, P]),
+    "dippm_splitk_reduce_t": (I32, [P, I32, I64, I64, F64, P, I64, P]),
+    "dippm_pool_concat": (I32, [Act, P, I64, I32, P, P, P, P]),
+    "dippm_head_forward": (I32, [P, I64, I32, P, P, P, I32, F32, U64, P, P, P, P, P, P]),
+    "dippm_huber": (I32, [P, P, I64, P, F64, P, P, P]),
+    "dippm_head_backward": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
+    "dippm_head_scratch_floats": (SZ, [I64, I32]),
+    "dippm_adam": (I32, [P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
+    "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
+    "dippm_gather_rows": (I32, [P, P, I64, I32, P, P]),
+}
+
+_lib = None
+
+
+def load():
+    """Load the native library (once) and bind every exported symbol."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise DeviceUnavailable(
+            f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == OK:
+        return
+    msg = load().dippm_last_error().decode(errors="replace")
+    if status == ERR_NONFINITE:
+        raise NonFinite(msg)
+    if status in (ERR_ARG, ERR_UNSUPPORTED):
+        raise ShapeMismatch(f"{what}: {msg}" if what else msg)
+    raise KernelError(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

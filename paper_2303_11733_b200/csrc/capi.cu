@@ -1,0 +1,164 @@
+// C-ABI plumbing: error state, device queries, MIG rule, Adam, weight packing.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace dippm {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return DIPPM_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+__global__ void k_mig_codes(const double* mem, int64_t stride, int64_t n, int8_t* codes, int32_t* nonfinite) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a = mem[i * stride];
+  if (!isfinite(a)) {
+    atomicExch(nonfinite, 1);
+    codes[i] = -1;
+    return;
+  }
+  codes[i] = (int8_t)mig_rule(a);
+}
+
+// numerics.py:93-114 in the same operation order (t already incremented).
+__global__ void k_adam(double* __restrict__ p, double* __restrict__ m, double* __restrict__ v,
+                       const float* __restrict__ g, int64_t n, double lr, double b1, double b2, double eps,
+                       double bc1, double bc2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    double gi = (double)g[i];
+    double mi = m[i] * b1;
+    mi += (1.0 - b1) * gi;
+    double tmp = gi * gi;
+    tmp *= 1.0 - b2;
+    double vi = v[i] * b2;
+    vi += tmp;
+    double denom = vi / bc2;
+    denom = sqrt(denom);
+    denom += eps;
+    double step = mi / bc1;
+    step /= denom;
+    step *= -lr;
+    step += p[i];
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = step;
+  }
+}
+
+__global__ void k_pack(const double* __restrict__ w, int64_t rows, int64_t cols, int transpose, ActView dst) {
+  // 32x32 tile transpose through shared memory when transpose != 0.
+  __shared__ float tile[32][33];
+  int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? (float)w[r * cols + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    if (transpose) {
+      int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst[c, r] = w[r, c]
+      if (r < rows && c < cols) act_store(dst, c, r, tile[threadIdx.x][i]);
+    } else {
+      int64_t r = r0 + i, c = c0 + threadIdx.x;
+      if (r < rows && c < cols) act_store(dst, r, c, tile[i][threadIdx.x]);
+    }
+  }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ src, const int64_t* __restrict__ src_row, int64_t rows,
+                              int cols, float* __restrict__ dst) {
+  int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const float* s = src + src_row[r] * cols;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) dst[r * cols + c] = s[c];
+}
+
+}  // namespace dippm
+
+using namespace dippm;
+
+extern "C" {
+
+const char* dippm_last_error(void) { return g_err; }
+int32_t dippm_abi_version(void) { return DIPPM_ABI_VERSION; }
+int32_t dippm_device_sm_count(void) { return num_sms(); }
+
+int32_t dippm_mig_code(double alpha_mb, int32_t* code) {
+  if (!code) {
+    set_error("dippm_mig_code: null output");
+    return DIPPM_ERR_ARG;
+  }
+  if (!std::isfinite(alpha_mb)) {
+    set_error("memory prediction is not finite: %g", alpha_mb);
+    return DIPPM_ERR_NONFINITE;
+  }
+  *code = mig_rule(alpha_mb);
+  return DIPPM_OK;
+}
+
+int32_t dippm_mig_codes(const double* mem_mb, int64_t stride, int64_t count, int8_t* codes, int32_t* nonfinite,
+                        void* stream) {
+  DIPPM_ARG_CHECK(count >= 0 && stride >= 1, "dippm_mig_codes: bad count/stride");
+  if (count == 0) return DIPPM_OK;
+  k_mig_codes<<<ceil_div_i(count, 256), 256, 0, (cudaStream_t)stream>>>(mem_mb, stride, count, codes, nonfinite);
+  DIPPM_LAUNCH_CHECK("k_mig_codes");
+  return DIPPM_OK;
+}
+
+int32_t dippm_adam(double* params, double* m, double* v, const float* grads, int64_t n, int64_t t, double lr,
+                   double beta1, double beta2, double eps, void* stream) {
+  DIPPM_ARG_CHECK(n >= 0 && t >= 1, "dippm_adam: bad n/t");
+  if (n == 0) return DIPPM_OK;
+  double bc1 = 1.0 - pow(beta1, (double)t);
+  double bc2 = 1.0 - pow(beta2, (double)t);
+  int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 4 * num_sms());
+  k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, n, lr, beta1, beta2, eps, bc1, bc2);
+  DIPPM_LAUNCH_CHECK("k_adam");
+  return DIPPM_OK;
+}
+
+int32_t dippm_pack(const double* w, int64_t rows, int64_t cols, int32_t transpose, dippm_act_t dst, void* stream) {
+  DIPPM_ARG_CHECK(rows > 0 && cols > 0, "dippm_pack: empty matrix");
+  dim3 grid(ceil_div_i(cols, 32), ceil_div_i(rows, 32));
+  k_pack<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(w, rows, cols, transpose, make_view(dst));
+  DIPPM_LAUNCH_CHECK("k_pack");
+  return DIPPM_OK;
+}
+
+int32_t dippm_gather_rows(const float* src, const int64_t* src_row, int64_t rows, int32_t cols, float* dst,
+                          void* stream) {
+  if (rows == 0) return DIPPM_OK;
+  k_gather_rows<<<(unsigned)rows, 128, 0, (cudaStream_t)stream>>>(src, src_row, rows, cols, dst);
+  DIPPM_LAUNCH_CHECK("k_gather_rows");
+  return DIPPM_OK;
+}
+
+}  // extern "C"

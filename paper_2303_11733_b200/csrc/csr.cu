@@ -1,0 +1,281 @@
+// K1 — deterministic CSR construction from a batched edge list.
+//
+// Replaces the reference's dense aggregation matrix (gnn.py:130-137):
+//     deg[dst] += 1 per edge (duplicates counted);  agg[dst, src] = 1/deg[dst]
+// The dense matrix is assignment-based, so a duplicated (src, dst) pair is
+// *counted twice* in deg but *summed once*; self loops are honoured.  The CSR
+// therefore keeps the distinct src of each row (ascending) and the
+// duplicate-counting in-degree.  Integer atomics only decide slot positions
+// inside a row; a rank-by-value placement afterwards makes the output
+// independent of atomic order, i.e. bit-exact and deterministic.
+#include "common.cuh"
+
+namespace dippm {
+
+constexpr int kScanItems = 8;
+constexpr int kScanThreads = 1024;
+constexpr int kScanTile = kScanItems * kScanThreads;  // 8192 elements per block
+
+// Block-wide exclusive scan of kScanTile int32 (in registers, 8 per thread).
+__device__ __forceinline__ int block_scan_excl(int (&v)[kScanItems], int* smem_warp) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int t = v[i];
+    v[i] = local;
+    local += t;
+  }
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) smem_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < (kScanThreads / 32)) ? smem_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int n = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += n;
+    }
+    smem_warp[lane] = wi - w;       // exclusive prefix of warp totals
+    if (lane == 31) smem_warp[32] = wi;  // block total
+  }
+  __syncthreads();
+  int base = smem_warp[warp] + incl - local;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v[i] += base;
+  int total = smem_warp[32];
+  __syncthreads();
+  return total;
+}
+
+// Pass 1: per-tile sums.
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restrict__ in, int64_t n, int* tile_sums) {
+  __shared__ int sw[33];
+  int v[kScanItems];
+  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < n) ? in[base + i] : 0;
+  int total = block_scan_excl(v, sw);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// Pass 2: scan of tile sums (single block; supports up to kScanTile tiles).
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* tile_sums, int ntiles) {
+  __shared__ int sw[33];
+  int v[kScanItems];
+  int base = threadIdx.x * kScanItems;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < ntiles) ? tile_sums[base + i] : 0;
+  block_scan_excl(v, sw);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < ntiles) tile_sums[base + i] = v[i];
+}
+
+// Pass 3: out[i] = exclusive prefix; out[n] = total.
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int* __restrict__ in, int64_t n,
+                                                             const int* __restrict__ tile_sums, int* out) {
+  __shared__ int sw[33];
+  int v[kScanItems], orig[kScanItems];
+  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) orig[i] = v[i] = (base + i < n) ? in[base + i] : 0;
+  block_scan_excl(v, sw);
+  int off = tile_sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    if (idx < n) out[idx] = v[i] + off;
+    if (idx == n - 1) out[n] = v[i] + off + orig[i];
+  }
+}
+
+// exclusive scan of in[0..n) into out[0..n] (out[n] = total).  tile_sums >= ceil(n/8192) ints.
+static int exclusive_scan(const int* in, int64_t n, int* out, int* tile_sums, cudaStream_t s) {
+  if (n == 0) {
+    DIPPM_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(int), s));
+    return DIPPM_OK;
+  }
+  int ntiles = ceil_div_i(n, kScanTile);
+  if (ntiles > kScanTile) {
+    set_error("scan: %lld elements exceed the 2-level scan capacity", (long long)n);
+    return DIPPM_ERR_UNSUPPORTED;
+  }
+  k_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(in, n, tile_sums);
+  k_scan_sums<<<1, kScanThreads, 0, s>>>(tile_sums, ntiles);
+  k_scan_apply<<<ntiles, kScanThreads, 0, s>>>(in, n, tile_sums, out);
+  DIPPM_LAUNCH_CHECK("exclusive_scan");
+  return DIPPM_OK;
+}
+
+// gnn.py:133-134 — in-degree with duplicates (integer atomics, order-free).
+__global__ void k_count(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t E, int64_t N,
+                        int* deg_cnt, int* bad) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int64_t s = src[e], d = dst[e];
+  if (s < 0 || s >= N || d < 0 || d >= N) {
+    atomicExch(bad, 1);
+    return;
+  }
+  atomicAdd(&deg_cnt[d], 1);
+}
+
+__global__ void k_fill(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t E, int64_t N,
+                       const int* __restrict__ raw_ptr, int* cursor, int* raw_src) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int64_t s = src[e], d = dst[e];
+  if (s < 0 || s >= N || d < 0 || d >= N) return;
+  int slot = raw_ptr[d] + atomicAdd(&cursor[d], 1);
+  raw_src[slot] = (int)s;
+}
+
+// Warp per row: count distinct src (first occurrence in slot order); also
+// finalise deg / inv_deg (gnn.py:136: 1/deg, zero row when isolated).
+__global__ void k_row_unique(const int* __restrict__ raw_ptr, const int* __restrict__ raw_src, int64_t N,
+                             int* ucount, int* deg, float* inv_deg, int* raw_first) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  int b = raw_ptr[row], e = raw_ptr[row + 1];
+  int cnt = 0;
+  for (int i = b + lane; i < e; i += 32) {
+    int si = raw_src[i];
+    bool first = true;
+    for (int j = b; j < i; ++j)
+      if (raw_src[j] == si) { first = false; break; }
+    raw_first[i] = first ? 1 : 0;
+    cnt += first ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) {
+    int d = e - b;
+    ucount[row] = cnt;
+    deg[row] = d;
+    inv_deg[row] = d > 0 ? 1.0f / (float)d : 0.0f;
+  }
+}
+
+// Warp per row: place each distinct src at its rank among the row's distinct
+// values (ascending) — independent of the atomic slot order.
+__global__ void k_row_place(const int* __restrict__ raw_ptr, const int* __restrict__ raw_src,
+                            const int* __restrict__ raw_first, int64_t N, const int* __restrict__ rowptr, int* col,
+                            int* tcount) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  int b = raw_ptr[row], e = raw_ptr[row + 1];
+  int out = rowptr[row];
+  for (int i = b + lane; i < e; i += 32) {
+    if (!raw_first[i]) continue;
+    int si = raw_src[i];
+    int rank = 0;
+    for (int j = b; j < e; ++j) rank += (raw_first[j] && raw_src[j] < si) ? 1 : 0;
+    col[out + rank] = si;
+    atomicAdd(&tcount[si], 1);
+  }
+}
+
+__global__ void k_tfill(const int* __restrict__ rowptr, const int* __restrict__ col, int64_t N,
+                        const int* __restrict__ t_rowptr, int* tcursor, int* t_raw) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  for (int i = rowptr[row] + lane; i < rowptr[row + 1]; i += 32) {
+    int u = col[i];
+    int slot = t_rowptr[u] + atomicAdd(&tcursor[u], 1);
+    t_raw[slot] = (int)row;
+  }
+}
+
+// Warp per transposed row: values are distinct, rank = #smaller.
+__global__ void k_trow_place(const int* __restrict__ t_rowptr, const int* __restrict__ t_raw, int64_t N,
+                             int* t_col) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  int b = t_rowptr[row], e = t_rowptr[row + 1];
+  for (int i = b + lane; i < e; i += 32) {
+    int vi = t_raw[i];
+    int rank = 0;
+    for (int j = b; j < e; ++j) rank += (t_raw[j] < vi) ? 1 : 0;
+    t_col[b + rank] = vi;
+  }
+}
+
+struct CsrWs {
+  int *deg_cnt, *raw_ptr, *cursor, *raw_src, *raw_first, *ucount, *tcount, *tcursor, *t_raw, *tiles;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t carve(void* base, int64_t N, int64_t E, CsrWs* w) {
+  size_t off = 0;
+  auto take = [&](int** p, size_t count) {
+    if (w) *p = reinterpret_cast<int*>(static_cast<char*>(base) + off);
+    off += align_up(count * sizeof(int));
+  };
+  CsrWs dummy;
+  CsrWs* t = w ? w : &dummy;
+  take(&t->deg_cnt, N);
+  take(&t->raw_ptr, N + 1);
+  take(&t->cursor, N);
+  take(&t->raw_src, E > 0 ? E : 1);
+  take(&t->raw_first, E > 0 ? E : 1);
+  take(&t->ucount, N);
+  take(&t->tcount, N);
+  take(&t->tcursor, N);
+  take(&t->t_raw, E > 0 ? E : 1);
+  take(&t->tiles, ceil_div_i(N + 1, kScanTile) + 1);
+  return off;
+}
+
+}  // namespace dippm
+
+using namespace dippm;
+
+extern "C" size_t dippm_csr_workspace_bytes(int64_t num_nodes, int64_t num_edges) {
+  return carve(nullptr, num_nodes, num_edges, nullptr);
+}
+
+extern "C" int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64_t E, int64_t N, int32_t* rowptr,
+                                   int32_t* col, int32_t* deg, float* inv_deg, int32_t* t_rowptr, int32_t* t_col,
+                                   int32_t* bad_edge, void* workspace, size_t workspace_bytes, void* stream) {
+  DIPPM_ARG_CHECK(N >= 1, "build_csr: need at least one node");
+  DIPPM_ARG_CHECK(E >= 0 && E < (int64_t)1 << 31 && N < (int64_t)1 << 31, "build_csr: size out of int32 range");
+  size_t need = carve(nullptr, N, E, nullptr);
+  DIPPM_ARG_CHECK(workspace && workspace_bytes >= need, "build_csr: workspace too small (%zu < %zu)",
+                  workspace_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  CsrWs w;
+  carve(workspace, N, E, &w);
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(w.deg_cnt, 0, N * sizeof(int), s));
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(w.cursor, 0, N * sizeof(int), s));
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(w.tcount, 0, N * sizeof(int), s));
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(w.tcursor, 0, N * sizeof(int), s));
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(bad_edge, 0, sizeof(int), s));
+  int eb = ceil_div_i(E > 0 ? E : 1, 256);
+  int rb = ceil_div_i(N * 32, 256);
+  if (E > 0) k_count<<<eb, 256, 0, s>>>(src, dst, E, N, w.deg_cnt, bad_edge);
+  int st = exclusive_scan(w.deg_cnt, N, w.raw_ptr, w.tiles, s);
+  if (st) return st;
+  if (E > 0) k_fill<<<eb, 256, 0, s>>>(src, dst, E, N, w.raw_ptr, w.cursor, w.raw_src);
+  k_row_unique<<<rb, 256, 0, s>>>(w.raw_ptr, w.raw_src, N, w.ucount, deg, inv_deg, w.raw_first);
+  st = exclusive_scan(w.ucount, N, rowptr, w.tiles, s);
+  if (st) return st;
+  k_row_place<<<rb, 256, 0, s>>>(w.raw_ptr, w.raw_src, w.raw_first, N, rowptr, col, w.tcount);
+  st = exclusive_scan(w.tcount, N, t_rowptr, w.tiles, s);
+  if (st) return st;
+  k_tfill<<<rb, 256, 0, s>>>(rowptr, col, N, t_rowptr, w.tcursor, w.t_raw);
+  k_trow_place<<<rb, 256, 0, s>>>(t_rowptr, w.t_raw, N, t_col);
+  DIPPM_LAUNCH_CHECK("build_csr");
+  return DIPPM_OK;
+}

@@ -1,0 +1,475 @@
+// K3 — SAGE projections and their gradients on the 5th-generation tensor cores.
+//
+//   FWD   z = [h | m] @ [W_self; W_neigh] + b, h' = relu(z)     gnn.py:207-209
+//   STORE dA = dz @ [W_self; W_neigh]^T                           gnn.py:232
+//   WGRAD dW = [h | m]^T @ dz (split over node-row chunks)        gnn.py:228-229
+//
+// One persistent kernel template, warp-specialised (192 threads, 1 CTA/SM):
+//   warp 0      TMA producer: 3-D tensor maps (cols, rows, plane) with 128B
+//               swizzle feed a kStages-deep shared-memory ring (mbarriers);
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; the fp32
+//               accumulator (128 x BN) lives in TMEM, double-buffered so the
+//               epilogue of tile i overlaps the MMAs of tile i+1;
+//   warps 2-5   epilogue: tcgen05.ld (32x32b.x32) -> bias/ReLU -> store.
+// Operand precision:
+//   bf16  kind::f16, one pass;
+//   tf32x3 kind::tf32 on hi/lo planes, 3 passes (hi*hi + hi*lo + lo*hi) so
+//          products carry ~22 mantissa bits: fp32-grade results on tensor cores.
+// Operand majorness: K-major for FWD/STORE; both MN-major for WGRAD (dz and
+// [h|m] are row-major [nodes, features] and the reduction runs over nodes),
+// which the UMMA descriptors express directly (no transposed copies).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace dippm {
+namespace tc {
+
+constexpr int kThreads = 192;
+constexpr int kBM = 128;
+enum { EPI_FWD = 0, EPI_STORE = 1, EPI_PARTIAL = 2 };
+
+struct Params {
+  int64_t M, N, K;
+  int splits;
+  int m_tiles, n_tiles;
+  const float* bias;
+  int relu;
+  ActView out;
+  float* c;
+  int64_t ldc;
+};
+
+// ------------------------------------------------------------------ PTX shims
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: a protocol bug traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    ++spins;
+    if (spins == 64) t0 = globaltimer();
+    if (spins > 64 && (spins & 255) == 0 && globaltimer() - t0 > 2000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int kFmt>
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (kFmt == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4
+// [16,30), SBO>>4 [32,46), version 1 at bit 46, swizzle mode 2 (128B) [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor, kind::f16 / kind::tf32: D fp32 [4,6), A/B format
+// [7,10)/[10,13) (1 = bf16, 2 = tf32), A/B MN-major bits 15/16, N>>3 [17,23),
+// M>>4 [24,29).
+__host__ __device__ constexpr uint32_t make_idesc(int fmt, bool a_mn, bool b_mn, int M, int N) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int kFmt, int kBN>
+struct Cfg {
+  static constexpr int kElem = kFmt == 1 ? 2 : 4;
+  static constexpr int kBK = 128 / kElem;       // one 128-byte swizzle row of K (or of MN) per k-block
+  static constexpr int kUK = 32 / kElem;        // K per tcgen05.mma (16 bf16 / 8 tf32)
+  static constexpr int kPlanes = kFmt == 1 ? 1 : 2;
+  static constexpr int kATile = kBM * 128;      // bytes per plane
+  static constexpr int kBTile = kBN * 128;
+  static constexpr int kStageBytes = kPlanes * (kATile + kBTile);
+  static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
+  static constexpr int kTmemCols = 2 * kBN;     // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+};
+
+template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  using C = Cfg<kFmt, kBN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int tiles_mn = p.m_tiles * p.n_tiles;
+  const int total = tiles_mn * p.splits;
+  const int kb_total = (int)((p.K + C::kBK - 1) / C::kBK);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int split = t / tiles_mn, r = t % tiles_mn;
+        const int m0 = (r / p.n_tiles) * kBM, n0 = (r % p.n_tiles) * kBN;
+        const int kb0 = (int)((int64_t)split * kb_total / p.splits);
+        const int kb1 = (int)((int64_t)(split + 1) * kb_total / p.splits);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+          uint8_t* sa = smem + s * C::kStageBytes;
+          uint8_t* sb = sa + C::kPlanes * C::kATile;
+          mbar_expect_tx(&full[s], C::kStageBytes);
+          const int k0 = kb * C::kBK;
+#pragma unroll
+          for (int pl = 0; pl < C::kPlanes; ++pl) {
+            if constexpr (!kAMN) {
+              tma_load_3d(sa + pl * C::kATile, &tmA, &full[s], k0, m0, pl);
+            } else {
+#pragma unroll
+              for (int c = 0; c < kBM / C::kBK; ++c)
+                tma_load_3d(sa + pl * C::kATile + c * C::kBK * 128, &tmA, &full[s], m0 + c * C::kBK, k0, pl);
+            }
+            if constexpr (!kBMN) {
+              tma_load_3d(sb + pl * C::kBTile, &tmB, &full[s], k0, n0, pl);
+            } else {
+#pragma unroll
+              for (int c = 0; c < kBN / C::kBK; ++c)
+                tma_load_3d(sb + pl * C::kBTile + c * C::kBK * 128, &tmB, &full[s], n0 + c * C::kBK, k0, pl);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (one thread) =====
+      constexpr uint32_t idesc = make_idesc(kFmt, kAMN, kBMN, kBM, kBN);
+      constexpr uint32_t a_lbo = kAMN ? C::kBK * 128 : 16, b_lbo = kBMN ? C::kBK * 128 : 16;
+      constexpr uint32_t a_step = kAMN ? C::kUK * 128 : 32, b_step = kBMN ? C::kUK * 128 : 32;
+      uint32_t it = 0, local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int split = t / tiles_mn;
+        const int kb0 = (int)((int64_t)split * kb_total / p.splits);
+        const int kb1 = (int)((int64_t)(split + 1) * kb_total / p.splits);
+        const uint32_t acc = local & 1, use = local >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + acc * kBN;
+        uint32_t first = 1;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&full[s], (it / C::kStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
+          const uint32_t sb = sa + C::kPlanes * C::kATile;
+#pragma unroll
+          for (int j = 0; j < C::kBK / C::kUK; ++j) {
+            const uint64_t a_hi = sdesc(sa + j * a_step, a_lbo, 1024);
+            const uint64_t b_hi = sdesc(sb + j * b_step, b_lbo, 1024);
+            umma<kFmt>(d, a_hi, b_hi, idesc, first ? 0u : 1u);
+            first = 0;
+            if constexpr (C::kPlanes == 2) {
+              const uint64_t a_lo = sdesc(sa + C::kATile + j * a_step, a_lbo, 1024);
+              const uint64_t b_lo = sdesc(sb + C::kBTile + j * b_step, b_lbo, 1024);
+              umma<kFmt>(d, a_hi, b_lo, idesc, 1u);
+              umma<kFmt>(d, a_lo, b_hi, idesc, 1u);
+            }
+          }
+          umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4 =====
+    const int q = warp & 3;
+    uint32_t local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int split = t / tiles_mn, r = t % tiles_mn;
+      const int m0 = (r / p.n_tiles) * kBM, n0 = (r % p.n_tiles) * kBN;
+      const uint32_t acc = local & 1, use = local >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int64_t row = (int64_t)m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int ch = 0; ch < kBN / 32; ++ch) {
+        uint32_t raw[32];
+        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
+        if (row < p.M) {
+          const int n = n0 + ch * 32;
+          if constexpr (kEpi == EPI_FWD) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                float x = __uint_as_float(raw[g * 8 + i]) + __ldg(p.bias + n + g * 8 + i);
+                v[i] = p.relu ? fmaxf(x, 0.f) : x;
+              }
+              act_store8(p.out, row, n + g * 8, v);
+            }
+          } else {
+            float* dst = p.c + (kEpi == EPI_PARTIAL ? (int64_t)split * p.M * p.ldc : 0) + row * p.ldc + n;
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              reinterpret_cast<float4*>(dst)[g] =
+                  make_float4(__uint_as_float(raw[4 * g]), __uint_as_float(raw[4 * g + 1]),
+                              __uint_as_float(raw[4 * g + 2]), __uint_as_float(raw[4 * g + 3]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over (cols, rows, plane) of a row-major operand; box = one 128-byte
+// swizzle row of columns by box_rows rows.
+static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return DIPPM_ERR_CUDA;
+  }
+  const int elem = v.dtype == DIPPM_DT_BF16 ? 2 : 4;
+  const int planes = v.dtype == DIPPM_DT_TF32X3 ? 2 : 1;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+  int64_t pstride = planes == 2 ? v.plane_stride : rows * v.ld;
+  cuuint64_t strides[2] = {(cuuint64_t)(v.ld * elem), (cuuint64_t)(pstride * elem)};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, v.dtype == DIPPM_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  3, v.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r, (long long)rows,
+              (long long)cols, (long long)v.ld, box_cols, box_rows);
+    return DIPPM_ERR_ARG;
+  }
+  return DIPPM_OK;
+}
+
+template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi>
+static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
+  using Cf = Cfg<kFmt, kBN>;
+  auto kern = k_tc_gemm<kFmt, kAMN, kBMN, kBN, kEpi>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    DIPPM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes));
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  int st;
+  // A logical (M x K); B logical (N x K).
+  if (!kAMN) st = make_map(&ma, a->a, a->M, a->K, Cf::kBK, kBM);
+  else st = make_map(&ma, a->a, a->K, a->M, Cf::kBK, Cf::kBK);
+  if (st) return st;
+  if (!kBMN) st = make_map(&mb, a->b, a->N, a->K, Cf::kBK, kBN);
+  else st = make_map(&mb, a->b, a->K, a->N, Cf::kBK, Cf::kBK);
+  if (st) return st;
+  Params p{};
+  p.M = a->M;
+  p.N = a->N;
+  p.K = a->K;
+  const int kb_total = ceil_div_i(a->K, Cf::kBK);
+  p.splits = kEpi == EPI_PARTIAL ? (int)std::max<int64_t>(1, a->splits) : 1;
+  if (p.splits > kb_total) {
+    set_error("gemm: %d splits exceed %d k-blocks (use dippm_wgrad_splits)", p.splits, kb_total);
+    return DIPPM_ERR_ARG;
+  }
+  p.m_tiles = ceil_div_i(a->M, kBM);
+  p.n_tiles = (int)(a->N / kBN);
+  p.bias = a->bias;
+  p.relu = (int)a->relu;
+  p.out = make_view(a->out);
+  p.c = a->c;
+  p.ldc = a->ldc;
+  const int total = p.m_tiles * p.n_tiles * p.splits;
+  const int grid = std::min(total, num_sms());
+  kern<<<grid, kThreads, Cf::kSmemBytes, s>>>(ma, mb, p);
+  DIPPM_LAUNCH_CHECK("k_tc_gemm");
+  return DIPPM_OK;
+}
+
+template <int kFmt, bool kMN, int kEpi>
+static int run_bn(const dippm_gemm_args_t* a, cudaStream_t s) {
+  if (a->N % 256 == 0) return run<kFmt, kMN, kMN, 256, kEpi>(a, s);
+  if (a->N % 128 == 0) return run<kFmt, kMN, kMN, 128, kEpi>(a, s);
+  return run<kFmt, kMN, kMN, 64, kEpi>(a, s);
+}
+
+template <int kFmt>
+static int dispatch(const dippm_gemm_args_t* a, cudaStream_t s) {
+  switch (a->kind) {
+    case DIPPM_GEMM_FWD: return run_bn<kFmt, false, EPI_FWD>(a, s);
+    case DIPPM_GEMM_STORE: return run_bn<kFmt, false, EPI_STORE>(a, s);
+    default: return run_bn<kFmt, true, EPI_PARTIAL>(a, s);
+  }
+}
+
+}  // namespace tc
+}  // namespace dippm
+
+using namespace dippm;
+
+extern "C" int32_t dippm_gemm_simt_impl(const dippm_gemm_args_t* a, cudaStream_t s);
+
+extern "C" int32_t dippm_wgrad_splits(int64_t M, int64_t N, int64_t K) {
+  const int bn = N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64);
+  const int64_t tiles = (int64_t)ceil_div_i(M, tc::kBM) * (N / bn);
+  const int kb_total = ceil_div_i(K, 64);  // bf16 k-block; tf32 uses 32-row blocks (twice as many)
+  int want = (int)std::max<int64_t>(1, num_sms() / std::max<int64_t>(1, tiles));
+  return std::min(want, kb_total);  // every split owns >= 1 k-block for both k-block sizes
+}
+
+extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void* stream) {
+  DIPPM_ARG_CHECK(a != nullptr, "gemm: null args");
+  DIPPM_ARG_CHECK(a->M >= 1 && a->N >= 1 && a->K >= 1, "gemm: empty problem %lldx%lldx%lld", (long long)a->M,
+                  (long long)a->N, (long long)a->K);
+  DIPPM_ARG_CHECK(a->a.dtype == a->b.dtype, "gemm: operand dtypes differ");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (backend == 1) return dippm_gemm_simt_impl(a, s);
+  DIPPM_ARG_CHECK(a->a.dtype == DIPPM_DT_BF16 || a->a.dtype == DIPPM_DT_TF32X3,
+                  "gemm: tensor-core path needs bf16 or tf32x3 operands");
+  DIPPM_ARG_CHECK(a->N % 64 == 0, "gemm: N=%lld must be a multiple of 64", (long long)a->N);
+  const bool mn = a->kind == DIPPM_GEMM_WGRAD;
+  DIPPM_ARG_CHECK(mn == (a->a_mn_major != 0) && mn == (a->b_mn_major != 0),
+                  "gemm: FWD/STORE take K-major operands, WGRAD MN-major");
+  const int bk = a->a.dtype == DIPPM_DT_BF16 ? 64 : 32;
+  DIPPM_ARG_CHECK(mn || a->K % bk == 0, "gemm: K=%lld must be a multiple of %d", (long long)a->K, bk);
+  if (a->a.dtype == DIPPM_DT_BF16) return tc::dispatch<1>(a, s);
+  return tc::dispatch<2>(a, s);
+}
+
+// Fixed-order split-K reduction with transpose: out[j*ldo + i] = scale * sum_s in[s][i][j].
+__global__ void k_splitk_reduce_t(const float* __restrict__ in, int splits, int64_t M, int64_t N, double scale,
+                                  float* __restrict__ out, int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    double acc = 0.0;
+    if (i < M && j < N)
+      for (int sp = 0; sp < splits; ++sp) acc += (double)in[(int64_t)sp * M * N + i * N + j];
+    tile[r][threadIdx.x] = (float)(acc * scale);
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < M && j < N) out[j * ldo + i] = tile[threadIdx.x][r];
+  }
+}
+
+extern "C" int32_t dippm_splitk_reduce_t(const float* in, int32_t splits, int64_t M, int64_t N, double scale,
+                                         float* out, int64_t ldo, void* stream) {
+  DIPPM_ARG_CHECK(splits >= 1 && M >= 1 && N >= 1, "splitk_reduce_t: bad shape");
+  dim3 grid(ceil_div_i(N, 32), ceil_div_i(M, 32));
+  k_splitk_reduce_t<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(in, splits, M, N, scale, out, ldo);
+  DIPPM_LAUNCH_CHECK("k_splitk_reduce_t");
+  return DIPPM_OK;
+}

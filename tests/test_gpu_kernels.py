@@ -1,0 +1,187 @@
+"""Kernel-level parity on the B200: K1 CSR bit-exact vs the reference's dense
+aggregation pattern, K2 aggregation, K3 tensor-core GEMMs vs the SIMT fp32
+anchor and fp64 numpy, K4 pooling, MIG codes."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import unpack_records
+from oracle import dippm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2303_11733_b200 import _lib, device as dev  # noqa: E402
+from paper_2303_11733_b200.device import ActBuf, upload_batch  # noqa: E402
+
+
+def _batch_from(recs):
+    n = np.array([r[0] for r in recs])
+    gp = np.zeros(len(recs) + 1, np.int32)
+    np.cumsum(n, out=gp[1:])
+    src, dst = [], []
+    for g, r in enumerate(recs):
+        e = np.asarray(r[1], np.int64).reshape(-1, 2)
+        src.append(e[:, 0] + gp[g])
+        dst.append(e[:, 1] + gp[g])
+    x = np.concatenate([r[2] for r in recs]).astype(np.float32)
+    fs = np.stack([r[3] for r in recs]).astype(np.float32)
+    return upload_batch(x, np.concatenate(src), np.concatenate(dst), gp, fs)
+
+
+def test_csr_bit_exact_vs_reference_pattern(golden):
+    recs = unpack_records(golden)
+    b = _batch_from(recs)
+    rowptr, col, deg = b.rowptr.cpu().numpy(), b.col.cpu().numpy(), b.deg.cpu().numpy()
+    inv = b.inv_deg.cpu().numpy()
+    assert int(b.bad.item()) == 0
+    gp = b.graph_ptr.cpu().numpy()
+    rp_off = col_off = 0
+    for i, r in enumerate(recs):
+        n = r[0]
+        g_rp = golden["csr_rowptr"][rp_off:rp_off + n + 1]
+        g_col = golden["csr_col"][col_off:col_off + golden["csr_ncol"][i]]
+        lo = gp[i]
+        mine_rp = rowptr[lo:lo + n + 1] - rowptr[lo]
+        mine_col = col[rowptr[lo]:rowptr[lo + n]] - lo
+        assert np.array_equal(mine_rp, g_rp), i
+        assert np.array_equal(mine_col, g_col), i
+        assert np.array_equal(deg[lo:lo + n], golden["csr_deg"][lo:lo + n]), i
+        rp_off += n + 1
+        col_off += len(g_col)
+    nz = deg > 0
+    assert np.array_equal(inv[nz], (1.0 / deg[nz]).astype(np.float32))
+    assert np.all(inv[~nz] == 0)
+    # transposed CSR is the exact transpose of the pattern, dst ascending per src row
+    t_rowptr, t_col = b.t_rowptr.cpu().numpy(), b.t_col.cpu().numpy()
+    pairs = sorted((int(c), int(v)) for v in range(b.N) for c in col[rowptr[v]:rowptr[v + 1]])
+    mine = [(u, int(t_col[j])) for u in range(b.N) for j in range(t_rowptr[u], t_rowptr[u + 1])]
+    assert mine == pairs
+
+
+def test_csr_deterministic_and_bad_edges():
+    rng = np.random.default_rng(1)
+    N, E = 5000, 40000
+    src = rng.integers(0, N, E)
+    dst = rng.integers(0, N, E)
+    x = np.zeros((N, 32), np.float32)
+    fs = np.zeros((1, 5), np.float32)
+    gp = np.array([0, N], np.int32)
+    a = upload_batch(x, src, dst, gp, fs)
+    b = upload_batch(x, src, dst, gp, fs)
+    for k in ("rowptr", "col", "deg", "t_rowptr", "t_col"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    rowptr, col, deg = O.csr_of_aggregation(N, list(zip(src.tolist(), dst.tolist())))
+    assert np.array_equal(a.rowptr.cpu().numpy(), rowptr)
+    assert np.array_equal(a.col.cpu().numpy()[:len(col)], col)
+    assert np.array_equal(a.deg.cpu().numpy(), deg)
+    bad = upload_batch(x, np.array([0, N + 3]), np.array([1, 2]), gp, fs)
+    assert int(bad.bad.item()) == 1
+
+
+@pytest.mark.parametrize("width", [32, 64, 512])
+def test_aggregate_matches_dense(width):
+    rng = np.random.default_rng(width)
+    N = 777
+    src = rng.integers(0, N, 2000)
+    dst = rng.integers(0, N, 2000)
+    b = upload_batch(np.zeros((N, 32), np.float32), src, dst, np.array([0, N], np.int32), np.zeros((1, 5), np.float32))
+    h = rng.normal(size=(N, width)).astype(np.float32)
+    ht = torch.from_numpy(h).cuda()
+    m = torch.empty(N, width, device="cuda")
+    s = torch.empty(N, width, device="cuda")
+    _lib.call("dippm_sage_aggregate", dev.f32_act(ht), dev.f32_act(m), dev.f32_act(s), N, width,
+              b.rowptr.data_ptr(), b.col.data_ptr(), b.inv_deg.data_ptr(), dev._stream())
+    ref = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist()))) @ h.astype(np.float64)
+    assert np.allclose(m.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
+    assert torch.equal(s, ht)
+
+
+def _rand_act(rows, cols, dt, rng, scale=1.0):
+    a = ActBuf(rows, cols, dt, "cuda")
+    v = (rng.normal(size=(rows, cols)) * scale).astype(np.float32)
+    t = torch.from_numpy(v).cuda()
+    _lib.call("dippm_pack", torch.from_numpy(v.astype(np.float64)).cuda().data_ptr(), rows, cols, 0, a.view(),
+              dev._stream())
+    return a, a.to_float().double().cpu().numpy(), t
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,N,K", [(300, 512, 64), (1000, 512, 1024), (129, 64, 64), (5000, 256, 512)])
+def test_tc_gemm_fwd(prec, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    dt = dev.PRECISIONS[prec]
+    A, a64, _ = _rand_act(M, K, dt, rng)
+    B, b64, _ = _rand_act(N, K, dt, rng, 0.05)
+    bias = torch.from_numpy(rng.normal(size=N).astype(np.float32)).cuda()
+    ref = np.maximum(a64 @ b64.T + bias.double().cpu().numpy(), 0)
+    for backend in (0, 1):
+        out = ActBuf(M, N, dev.DT_F32, "cuda")
+        out.t.fill_(float("nan"))
+        args = _lib.GemmArgs(_lib.GEMM_FWD, M, N, K, A.view(), 0, B.view(), 0, bias.data_ptr(), 1, out.view(),
+                             None, 0, 1)
+        _lib.check(_lib.load().dippm_gemm(args, backend, dev._stream()))
+        got = out.t.double().cpu().numpy()
+        tol = 1e-5 * np.abs(ref).max()
+        assert np.max(np.abs(got - ref)) <= tol, (backend, np.max(np.abs(got - ref)), tol)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 512), (77, 128, 64)])
+def test_tc_gemm_store(prec, M, N, K):
+    rng = np.random.default_rng(7 + M)
+    dt = dev.PRECISIONS[prec]
+    A, a64, _ = _rand_act(M, K, dt, rng)
+    B, b64, _ = _rand_act(N, K, dt, rng)
+    ref = a64 @ b64.T
+    c = torch.full((M, N), float("nan"), device="cuda")
+    args = _lib.GemmArgs(_lib.GEMM_STORE, M, N, K, A.view(), 0, B.view(), 0, None, 0, dev.NULL_ACT, c.data_ptr(), N, 1)
+    _lib.check(_lib.load().dippm_gemm(args, 0, dev._stream()))
+    assert np.max(np.abs(c.double().cpu().numpy() - ref)) <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("R,M,N", [(3000, 512, 1024), (777, 64, 64), (20000, 512, 64)])
+def test_tc_gemm_wgrad(prec, R, M, N):
+    """C = dz^T @ A over R node rows, both operands MN-major, split-K + fixed-order reduce."""
+    rng = np.random.default_rng(R)
+    dt = dev.PRECISIONS[prec]
+    dz, dz64, _ = _rand_act(R, M, dt, rng)
+    A, a64, _ = _rand_act(R, N, dt, rng)
+    ref = (a64.T @ dz64)  # [N, M] = dW layout
+    lib = _lib.load()
+    S = lib.dippm_wgrad_splits(M, N, R)
+    ws = torch.full((S, M, N), float("nan"), device="cuda")
+    out = torch.full((N, M), float("nan"), device="cuda")
+    for backend in (0, 1):
+        args = _lib.GemmArgs(_lib.GEMM_WGRAD, M, N, R, dz.view(), 1, A.view(), 1, None, 0, dev.NULL_ACT,
+                             ws.data_ptr(), N, S)
+        _lib.check(lib.dippm_gemm(args, backend, dev._stream()))
+        _lib.call("dippm_splitk_reduce_t", ws.data_ptr(), S, M, N, 1.0, out.data_ptr(), M, dev._stream())
+        err = np.max(np.abs(out.double().cpu().numpy() - ref))
+        assert err <= 1e-5 * np.abs(ref).max(), (backend, err)
+
+
+def test_pool_concat_and_mig_codes(golden):
+    rng = np.random.default_rng(3)
+    G = 37
+    n = rng.integers(1, 50, G)
+    gp = np.zeros(G + 1, np.int32)
+    np.cumsum(n, out=gp[1:])
+    h = rng.normal(size=(gp[-1], 64)).astype(np.float32)
+    fs = rng.normal(size=(G, 5)).astype(np.float32)
+    norm = np.concatenate([np.zeros(6), rng.normal(size=5), rng.uniform(0.5, 2, 5)])
+    u = torch.empty(G, 69, device="cuda")
+    _lib.call("dippm_pool_concat", dev.f32_act(torch.from_numpy(h).cuda()), torch.from_numpy(gp).cuda().data_ptr(),
+              G, 64, torch.from_numpy(fs).cuda().data_ptr(), torch.from_numpy(norm).cuda().data_ptr(), u.data_ptr(),
+              dev._stream())
+    got = u.cpu().numpy()
+    for g in range(G):
+        assert np.allclose(got[g, :64], h[gp[g]:gp[g + 1]].astype(np.float64).mean(0), atol=1e-6)
+        assert np.allclose(got[g, 64:], (fs[g] - norm[6:11]) / norm[11:16], atol=1e-6)
+    alphas = torch.from_numpy(golden["mig_alpha"]).cuda()
+    codes = torch.empty(len(alphas), dtype=torch.int8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("dippm_mig_codes", alphas.data_ptr(), 1, len(alphas), codes.data_ptr(), flag.data_ptr(), dev._stream())
+    assert codes.cpu().numpy().tolist() == golden["mig_code"].tolist()
+    assert int(flag.item()) == 0
