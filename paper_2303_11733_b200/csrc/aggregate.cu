@@ -111,10 +111,9 @@ __global__ void __launch_bounds__(kAggThreads) k_dz(const float* __restrict__ dA
       } else {
         while (graph_ptr[g + 1] <= row) ++g;
         const float inv_n = 1.0f / (float)(graph_ptr[g + 1] - graph_ptr[g]);
-        const float4* p = reinterpret_cast<const float4*>(dA + (int64_t)g * ld_da + c);
-        float4 a0 = p[0], a1 = p[1];
-        v[0] = a0.x * inv_n; v[1] = a0.y * inv_n; v[2] = a0.z * inv_n; v[3] = a0.w * inv_n;
-        v[4] = a1.x * inv_n; v[5] = a1.y * inv_n; v[6] = a1.z * inv_n; v[7] = a1.w * inv_n;
+        const float* p = dA + (int64_t)g * ld_da + c;  // du rows (ld = width + 5) are not 16B aligned
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(p + k) * inv_n;
       }
       float hg[8];
       act_load8(gate, row, c, hg);

@@ -123,9 +123,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4
 // [16,30), SBO>>4 [32,46), version 1 at bit 46, swizzle mode 2 (128B) [61,64).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint64_t layout = 2) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
 }
 // Instruction descriptor, kind::f16 / kind::tf32: D fp32 [4,6), A/B format
 // [7,10)/[10,13) (1 = bf16, 2 = tf32), A/B MN-major bits 15/16, N>>3 [17,23),
@@ -231,6 +231,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = make_idesc(kFmt, kAMN, kBMN, kBM, kBN);
       constexpr uint32_t a_lbo = kAMN ? C::kBK * 128 : 16, b_lbo = kBMN ? C::kBK * 128 : 16;
       constexpr uint32_t a_step = kAMN ? C::kUK * 128 : 32, b_step = kBMN ? C::kUK * 128 : 32;
+      // 32-bit MN-major operands use the 128B swizzle with 32-byte atoms
+      // (UMMA layout 1 = SWIZZLE_128B_BASE32B, 4-row atoms of 512 B); all
+      // others the plain 128B swizzle (layout 2, 8-row atoms of 1024 B).
+      constexpr bool a32 = kAMN && kFmt == 2, b32 = kBMN && kFmt == 2;
+      constexpr uint64_t a_lay = a32 ? 1 : 2, b_lay = b32 ? 1 : 2;
+      constexpr uint32_t a_sbo = a32 ? 512 : 1024, b_sbo = b32 ? 512 : 1024;
       uint32_t it = 0, local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int split = t / tiles_mn;
@@ -249,13 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sb = sa + C::kPlanes * C::kATile;
 #pragma unroll
           for (int j = 0; j < C::kBK / C::kUK; ++j) {
-            const uint64_t a_hi = sdesc(sa + j * a_step, a_lbo, 1024);
-            const uint64_t b_hi = sdesc(sb + j * b_step, b_lbo, 1024);
+            const uint64_t a_hi = sdesc(sa + j * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t b_hi = sdesc(sb + j * b_step, b_lbo, b_sbo, b_lay);
             umma<kFmt>(d, a_hi, b_hi, idesc, first ? 0u : 1u);
             first = 0;
             if constexpr (C::kPlanes == 2) {
-              const uint64_t a_lo = sdesc(sa + C::kATile + j * a_step, a_lbo, 1024);
-              const uint64_t b_lo = sdesc(sb + C::kBTile + j * b_step, b_lbo, 1024);
+              const uint64_t a_lo = sdesc(sa + C::kATile + j * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t b_lo = sdesc(sb + C::kBTile + j * b_step, b_lbo, b_sbo, b_lay);
               umma<kFmt>(d, a_hi, b_lo, idesc, 1u);
               umma<kFmt>(d, a_lo, b_hi, idesc, 1u);
             }
@@ -330,7 +336,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 3-D map over (cols, rows, plane) of a row-major operand; box = one 128-byte
 // swizzle row of columns by box_rows rows.
-static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows,
+                    bool atom32 = false) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -344,7 +351,8 @@ static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_
   cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, v.dtype == DIPPM_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                  3, v.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  3, v.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r, (long long)rows,
@@ -367,10 +375,10 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   int st;
   // A logical (M x K); B logical (N x K).
   if (!kAMN) st = make_map(&ma, a->a, a->M, a->K, Cf::kBK, kBM);
-  else st = make_map(&ma, a->a, a->K, a->M, Cf::kBK, Cf::kBK);
+  else st = make_map(&ma, a->a, a->K, a->M, Cf::kBK, Cf::kBK, kFmt == 2);
   if (st) return st;
   if (!kBMN) st = make_map(&mb, a->b, a->N, a->K, Cf::kBK, kBN);
-  else st = make_map(&mb, a->b, a->K, a->N, Cf::kBK, Cf::kBK);
+  else st = make_map(&mb, a->b, a->K, a->N, Cf::kBK, Cf::kBK, kFmt == 2);
   if (st) return st;
   Params p{};
   p.M = a->M;

@@ -313,7 +313,7 @@ class Engine:
 
     def set_normalizer(self, norm) -> None:
         vec = np.concatenate([np.asarray(norm.y_mean, np.float64), np.asarray(norm.y_std, np.float64),
-                              np.asarray(norm.fs_mean, np.float64), np.asarray(norm.fs_std, np.float64), [0.0]])
+                              np.asarray(norm.fs_mean, np.float64), np.asarray(norm.fs_std, np.float64)])
         self.norm.copy_(torch.from_numpy(vec))
 
     def reset_adam(self) -> None:

@@ -101,8 +101,8 @@ def _rand_act(rows, cols, dt, rng, scale=1.0):
     a = ActBuf(rows, cols, dt, "cuda")
     v = (rng.normal(size=(rows, cols)) * scale).astype(np.float32)
     t = torch.from_numpy(v).cuda()
-    _lib.call("dippm_pack", torch.from_numpy(v.astype(np.float64)).cuda().data_ptr(), rows, cols, 0, a.view(),
-              dev._stream())
+    v64 = torch.from_numpy(v.astype(np.float64)).cuda()
+    _lib.call("dippm_pack", v64.data_ptr(), rows, cols, 0, a.view(), dev._stream())
     return a, a.to_float().double().cpu().numpy(), t
 
 
@@ -172,9 +172,9 @@ def test_pool_concat_and_mig_codes(golden):
     fs = rng.normal(size=(G, 5)).astype(np.float32)
     norm = np.concatenate([np.zeros(6), rng.normal(size=5), rng.uniform(0.5, 2, 5)])
     u = torch.empty(G, 69, device="cuda")
-    _lib.call("dippm_pool_concat", dev.f32_act(torch.from_numpy(h).cuda()), torch.from_numpy(gp).cuda().data_ptr(),
-              G, 64, torch.from_numpy(fs).cuda().data_ptr(), torch.from_numpy(norm).cuda().data_ptr(), u.data_ptr(),
-              dev._stream())
+    keep = [torch.from_numpy(a).cuda() for a in (h, gp, fs, norm)]  # hold the buffers across the launch
+    _lib.call("dippm_pool_concat", dev.f32_act(keep[0]), keep[1].data_ptr(), G, 64, keep[2].data_ptr(),
+              keep[3].data_ptr(), u.data_ptr(), dev._stream())
     got = u.cpu().numpy()
     for g in range(G):
         assert np.allclose(got[g, :64], h[gp[g]:gp[g + 1]].astype(np.float64).mean(0), atol=1e-6)

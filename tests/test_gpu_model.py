@@ -23,6 +23,14 @@ FP32_ABS = 1e-5
 BF16_ABS = 2e-2
 
 
+def grad_close(got, ref, rel=1e-4, abs_per_elem=1e-6):
+    """Stated fp32 gradient tolerance: ||d|| <= 1e-4 ||g|| + 1e-6 sqrt(n).  The
+    absolute floor covers reductions whose terms cancel (e.g. fc3.b = mean
+    residual), where the ~1e-6 fp32 forward error dominates the tiny sum."""
+    d = np.linalg.norm(np.asarray(got) - ref)
+    return d <= rel * np.linalg.norm(ref) + abs_per_elem * np.sqrt(np.size(ref))
+
+
 class _FS:
     def __init__(self, v):
         self.as_vector = np.asarray(v)
@@ -77,8 +85,7 @@ def test_backward_matches_reference(golden):
     assert gnn.batch_loss(model, batch) == pytest.approx(float(golden["h32_batch_loss"]), rel=1e-5, abs=1e-7)
     for name, _ in model.param_items():
         ref = golden[f"h32_grad_{name}"]
-        err = np.linalg.norm(grads[name] - ref) / max(np.linalg.norm(ref), 1e-30)
-        assert err <= 1e-4, (name, err)
+        assert grad_close(grads[name], ref), name
 
 
 def test_backward_hidden512_vs_oracle(golden):
@@ -94,8 +101,7 @@ def test_backward_hidden512_vs_oracle(golden):
     ref_loss, ref_grads = O.backward(params, norm, orecs)
     assert loss == pytest.approx(ref_loss, rel=1e-5)
     for name in O.SAGE_PARAM_NAMES:
-        err = np.linalg.norm(grads[name] - ref_grads[name]) / max(np.linalg.norm(ref_grads[name]), 1e-30)
-        assert err <= 1e-4, (name, err)
+        assert grad_close(grads[name], ref_grads[name]), name
 
 
 def test_sage_forward_reference_cases(golden):
