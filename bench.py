@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""DIPPM GraphSAGE training throughput on B200 (BASELINE.json metric, configs[1]).
+
+Workload (configs[1]): one training epoch over a synthetic 10,508-graph
+dataset shaped like the paper's corpus (N ~ U[270, 330] nodes, E/N ~ 1.33,
+32-wide node rows, 5 static features), batch 256, hidden 512, Adam, dropout
+0.05.  A "step" = one training step on one batch of 256 graphs: K1 CSR build
+from the batch's edge list, 3 SAGE layers (K2 aggregation + K3 tcgen05 GEMM),
+K4 pooling, K5 head, Huber loss, full backward, fused Adam, weight repack.
+
+  value  graphs/s with the epoch's batches already resident in HBM
+  e2e    graphs/s through the public batch-training call with HOST pinned
+         batches: H2D of the batch + step + D2H of the loss inside the timing
+  roofline  the dominant kernel family (tcgen05 GEMMs) vs measured peak
+  cpu_baseline  the CPU oracle (numpy fp64 restatement of the reference,
+         `oracle/`) on a bounded sample on this box's host cores
+
+Multi-GPU (torchrun, one process per GPU): data parallel, weak scaling — each
+rank trains on its own batch of 256 per step, gradients are summed with one
+NCCL all-reduce (the path's only exchange) and averaged inside Adam.
+Inputs per step exceed L2 (≈76.8k node rows, >150 MB of activations; the
+epoch cycles through 41 distinct batches), so no explicit L2 flush is used.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DIPPM graphs/sec (inference & training) at 1/2/4/8 B200; % of roofline"
+DATA = "synthetic (generator B, seeded): paper-shaped 10,508-graph corpus, random-init weights"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
+    p.add_argument("--graphs", type=int, default=10508)
+    p.add_argument("--batch", type=int, default=256)
+    p.add_argument("--hidden", type=int, default=512)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-steps", type=int, default=6, help="CPU baseline sample: steps of one batch each")
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.file, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.file.flush()
+        rows = [r.split(", ") for r in Path(self.file.name).read_text().strip().splitlines() if r.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons = [], None, set()
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (fp64 numpy restatement of gnn.backward + Adam)
+
+_SHM = {}
+
+
+def _cpu_worker_init(shm_name, shapes, hidden):
+    from multiprocessing import shared_memory
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    shm = shared_memory.SharedMemory(name=shm_name)
+    _SHM["shm"] = shm
+    flat = np.ndarray((sum(int(np.prod(s)) for _, s in shapes),), dtype=np.float64, buffer=shm.buf)
+    params, off = {}, 0
+    for name, s in shapes:
+        n = int(np.prod(s))
+        params[name] = flat[off:off + n].reshape(s)
+        off += n
+    _SHM["params"] = params
+    _SHM["hidden"] = hidden
+
+
+def _cpu_worker_grads(args):
+    from oracle import dippm_oracle as O
+    recs, norm = args
+    loss, grads = O.backward(_SHM["params"], norm, recs, hidden=_SHM["hidden"])
+    n = len(recs)
+    return loss * n, {k: g * n for k, g in grads.items()}, n
+
+
+def cpu_baseline(ds, hidden, batch, steps, procs, seed=0):
+    """Batch-protocol CPU training step (gnn.backward over `batch` records + 15
+    Adam updates) on `procs` worker processes, 1 BLAS thread each."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    from oracle import dippm_oracle as O
+
+    rng = np.random.default_rng(seed)
+    params = O.init_params(hidden, rng)
+    shapes = [(k, params[k].shape) for k in O.SAGE_PARAM_NAMES]
+    total = sum(int(np.prod(s)) for _, s in shapes)
+    shm = shared_memory.SharedMemory(create=True, size=total * 8)
+    flat = np.ndarray((total,), dtype=np.float64, buffer=shm.buf)
+    off = 0
+    views = {}
+    for k, s in shapes:
+        n = int(np.prod(s))
+        flat[off:off + n] = params[k].ravel()
+        views[k] = flat[off:off + n].reshape(s)
+        off += n
+    norm = O.normalizer_fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    state = {k: (np.zeros(s), np.zeros(s)) for k, s in shapes}
+    ids = rng.permutation(ds.num_graphs)[:steps * batch]
+    recs = [(r.encoding.num_nodes, r.encoding.edges, r.encoding.features, r.fs.as_vector, r.target.as_array)
+            for r in ds.records(ids)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_cpu_worker_init, initargs=(shm.name, shapes, hidden)) as pool:
+        pool.map(_cpu_worker_grads, [(recs[:1], norm)] * procs)  # warm the workers
+        t0 = time.perf_counter()
+        for s in range(steps):
+            chunk = recs[s * batch:(s + 1) * batch]
+            parts = [(chunk[i::procs], norm) for i in range(procs) if chunk[i::procs]]
+            out = pool.map(_cpu_worker_grads, parts)
+            n = sum(o[2] for o in out)
+            grads = {k: sum(o[1][k] for o in out) / n for k, _ in shapes}
+            for k, _ in shapes:
+                m, v = state[k]
+                views[k][...] = O.adam_step(views[k], grads[k], m, v, s + 1)
+        dt = time.perf_counter() - t0
+    shm.close()
+    shm.unlink()
+    return steps * batch / dt, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_dict(args, world):
+    return {"workload": "configs[1]: GraphSAGE training epoch, synthetic 10,508-graph paper-shaped corpus, "
+                        "batch 256/rank, Adam",
+            "graphs": args.graphs, "batch_per_rank": args.batch, "global_batch": args.batch * world,
+            "hidden": args.hidden, "nodes_per_graph": "U[270,330]", "edges_per_node": 1.33,
+            "parallelism": f"dp{world}", "l2": "inputs larger than L2 (no flush)"}
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2303_11733_b200.synth import make_dataset
+    ds = make_dataset(args.graphs, seed=2)
+    procs = host_cores()
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        v, dt = cpu_baseline(ds, args.hidden, args.batch, 1, procs, seed=100 + i)
+        if i >= args.warmup:
+            per_step.append(dt)
+    total = sum(per_step)
+    value = args.steps * args.batch / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": DATA, "config": config_dict(args, 1),
+            "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": procs, "kind": "port",
+                             "sample": f"{args.steps} timed steps x {args.batch} graphs, oracle gnn.backward + "
+                                       f"Adam (fp64 numpy), {procs} procs x 1 BLAS thread, {cpu_model()}"},
+            "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+class GemmTimer:
+    """CUDA-event pairs around each tensor-core GEMM launch (on the launching stream)."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.recs = []
+
+    def __call__(self, phase, flops):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if phase == "pre":
+            self.recs.append([ev, None, flops])
+        else:
+            self.recs[-1][1] = ev
+
+    def summary(self):
+        self.torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b, _ in self.recs]
+        flops = [f for _, _, f in self.recs]
+        return sum(flops), sum(ms), len(ms)
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2303_11733_b200 import _lib, gnn
+    from paper_2303_11733_b200.device import Engine, Workspace, build_batch_csr, upload_batch
+    from paper_2303_11733_b200.synth import make_dataset
+    from paper_2303_11733_b200.trainer import BatchTrainer
+
+    lib = _lib.load()
+    ds = make_dataset(args.graphs, seed=2)
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(ds.num_graphs)[rank::world]
+    nb = len(perm) // args.batch
+    batches_host = [ds.collate(perm[i * args.batch:(i + 1) * args.batch]) for i in range(nb)]
+
+    norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    model = gnn.create_model(hidden=args.hidden, seed=0, normalizer=norm)
+    trainer = BatchTrainer(model, precision=args.dtype, lr=gnn.DEFAULT_LEARNING_RATE, seed=11,
+                           allreduce=(lambda t: dist.all_reduce(t)) if world > 1 else None, world_size=world)
+    eng = trainer.engine
+    # resident epoch: every batch collated in HBM before timing (CSR is rebuilt each step)
+    resident = [upload_batch(*b, device=eng.device, build_csr=False) for b in batches_host]
+    n_max = max(b.N for b in resident)
+    trainer.reserve(n_max, args.batch)
+    torch.cuda.synchronize()
+
+    def step(i):
+        trainer.step_resident(resident[i % nb])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = lib.dippm_launch_count()
+    t_wall = time.perf_counter()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    end.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    launches = lib.dippm_launch_count() - l0
+    clocks = sampler.stop()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    graphs = args.steps * args.batch * world
+    value = graphs / (ms / 1000.0)
+
+    # roofline pass: same steps with CUDA events around every tcgen05 GEMM
+    timer = GemmTimer()
+    eng.gemm_hook = timer
+    for i in range(args.steps):
+        step(args.warmup + args.steps + i)
+    eng.gemm_hook = None
+    g_flops, g_ms, g_n = timer.summary()
+    pk, pk_src = peaks()
+    peak_tf = pk["bf16_tflops_sustained"] if args.dtype == "bf16" else pk["bf16_tflops_sustained"] / 6.0
+    achieved = g_flops / (g_ms / 1000.0) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(f"gemm_dram_bytes_per_launch_{args.dtype}")
+
+    # e2e: public batch-training call with host pinned batches
+    e2e = None
+    if not args.no_e2e:
+        pinned = [[torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in b] for b in batches_host]
+        h2d = sum(sum(t.numel() * t.element_size() for t in b) for b in pinned) / len(pinned)
+        for i in range(2):
+            trainer.step_host(*pinned[i % nb])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            trainer.step_host(*pinned[(args.warmup + i) % nb])
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": graphs / (ems / 1000.0), "unit": "graphs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = host_cores()
+        v, dt = cpu_baseline(ds, args.hidden, args.batch, args.cpu_steps, procs)
+        cpu = {"value": v, "unit": "graphs/s", "cores": procs, "kind": "port",
+               "sample": f"{args.cpu_steps} steps x {args.batch} graphs of the same corpus: oracle gnn.backward + "
+                         f"Adam (fp64 numpy), {procs} procs x 1 BLAS thread, {cpu_model()}, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": args.dtype, "data": DATA, "config": config_dict(args, world),
+                "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": {"bound": "tensor", "kernel": "k_tc_gemm (tcgen05 fwd/dgrad/wgrad, all launches)",
+                             "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
+                             "traffic": traffic, "peak_source": pk_src + (
+                                 "" if args.dtype == "bf16" else "; fp32 mode = 3-pass tf32: bf16 sustained / 2 / 3"),
+                             "gemm_share_of_step": (g_ms / args.steps) / (ms / args.steps),
+                             "gemm_launches_per_step": g_n / args.steps,
+                             "algorithmic_tflop_per_step": g_flops / args.steps / 1e12},
+                "cpu_baseline": cpu, "clocks": clocks, "wall_s_timed_region": wall}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

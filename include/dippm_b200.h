@@ -59,6 +59,8 @@ typedef struct dippm_act {
 
 const char* dippm_last_error(void);
 int32_t dippm_abi_version(void);
+/* Total kernel launches issued by this library since load (bench evidence). */
+uint64_t dippm_launch_count(void);
 /* Number of SMs of the current device (grid sizing; 148 on B200). */
 int32_t dippm_device_sm_count(void);
 
@@ -193,9 +195,10 @@ size_t dippm_head_scratch_floats(int64_t num_graphs, int32_t width);
 
 /* ---------------------------------------------------------------------------
  * K8 — bias-corrected Adam, numerics.py:93-114, same op order, on fp64
- * master parameters (fp32 gradients), one launch for all 15 tensors. */
-int32_t dippm_adam(double* params, double* m, double* v, const float* grads, int64_t n, int64_t t, double lr,
-                   double beta1, double beta2, double eps, void* stream);
+ * master parameters (fp32 gradients, multiplied by grad_scale first — 1/world
+ * size after a data-parallel sum), one launch for all 15 tensors. */
+int32_t dippm_adam(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
+                   int64_t t, double lr, double beta1, double beta2, double eps, void* stream);
 
 /* Pack fp64 master weights into compute copies.
  *  w [rows, cols] fp64 row-major  ->  dst view (bf16 or tf32 hi/lo or f32);

@@ -49,6 +49,7 @@ P, I32, I64, U64, F32, F64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C
 SIGNATURES = {
     "dippm_last_error": (C.c_char_p, []),
     "dippm_abi_version": (I32, []),
+    "dippm_launch_count": (C.c_uint64, []),
     "dippm_device_sm_count": (I32, []),
     "dippm_mig_code": (I32, [F64, C.POINTER(I32)]),
     "dippm_mig_codes": (I32, [P, I64, I64, P, P, P]),
@@ -67,7 +68,7 @@ SIGNATURES = {
     "dippm_huber": (I32, [P, P, I64, P, F64, P, P, P]),
     "dippm_head_backward": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
     "dippm_head_scratch_floats": (SZ, [I64, I32]),
-    "dippm_adam": (I32, [P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
+    "dippm_adam": (I32, [P, P, P, P, F64, I64, I64, F64, F64, F64, F64, P]),
     "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
     "dippm_gather_rows": (I32, [P, P, I64, I32, P, P]),
 }

@@ -1,4 +1,5 @@
 // C-ABI plumbing: error state, device queries, MIG rule, Adam, weight packing.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -8,6 +9,9 @@
 namespace dippm {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -48,12 +52,12 @@ __global__ void k_mig_codes(const double* mem, int64_t stride, int64_t n, int8_t
 
 // numerics.py:93-114 in the same operation order (t already incremented).
 __global__ void k_adam(double* __restrict__ p, double* __restrict__ m, double* __restrict__ v,
-                       const float* __restrict__ g, int64_t n, double lr, double b1, double b2, double eps,
+                       const float* __restrict__ g, double gscale, int64_t n, double lr, double b1, double b2, double eps,
                        double bc1, double bc2) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    double gi = (double)g[i];
+    double gi = (double)g[i] * gscale;
     double mi = m[i] * b1;
     mi += (1.0 - b1) * gi;
     double tmp = gi * gi;
@@ -109,6 +113,7 @@ extern "C" {
 
 const char* dippm_last_error(void) { return g_err; }
 int32_t dippm_abi_version(void) { return DIPPM_ABI_VERSION; }
+uint64_t dippm_launch_count(void) { return g_launches.load(); }
 int32_t dippm_device_sm_count(void) { return num_sms(); }
 
 int32_t dippm_mig_code(double alpha_mb, int32_t* code) {
@@ -133,14 +138,16 @@ int32_t dippm_mig_codes(const double* mem_mb, int64_t stride, int64_t count, int
   return DIPPM_OK;
 }
 
-int32_t dippm_adam(double* params, double* m, double* v, const float* grads, int64_t n, int64_t t, double lr,
+int32_t dippm_adam(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n, int64_t t,
+                   double lr,
                    double beta1, double beta2, double eps, void* stream) {
   DIPPM_ARG_CHECK(n >= 0 && t >= 1, "dippm_adam: bad n/t");
   if (n == 0) return DIPPM_OK;
   double bc1 = 1.0 - pow(beta1, (double)t);
   double bc2 = 1.0 - pow(beta2, (double)t);
   int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 4 * num_sms());
-  k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, n, lr, beta1, beta2, eps, bc1, bc2);
+  k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1, beta2, eps,
+                                                    bc1, bc2);
   DIPPM_LAUNCH_CHECK("k_adam");
   return DIPPM_OK;
 }

@@ -25,11 +25,16 @@ int cuda_status(cudaError_t e, const char* what);
     cudaError_t _e = (expr);                                       \
     if (_e != cudaSuccess) return ::dippm::cuda_status(_e, #expr); \
   } while (0)
-#define DIPPM_LAUNCH_CHECK(what)                                   \
+// Every kernel launch is counted (dippm_launch_count) so the bench can report
+// exactly how many of this library's kernels ran in its timed region.
+void count_launches(int n);
+#define DIPPM_LAUNCH_CHECK_N(n, what)                              \
   do {                                                             \
+    ::dippm::count_launches(n);                                    \
     cudaError_t _e = cudaGetLastError();                           \
     if (_e != cudaSuccess) return ::dippm::cuda_status(_e, what);  \
   } while (0)
+#define DIPPM_LAUNCH_CHECK(what) DIPPM_LAUNCH_CHECK_N(1, what)
 #define DIPPM_ARG_CHECK(cond, ...)                                 \
   do {                                                             \
     if (!(cond)) {                                                 \

@@ -110,7 +110,7 @@ static int exclusive_scan(const int* in, int64_t n, int* out, int* tile_sums, cu
   k_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(in, n, tile_sums);
   k_scan_sums<<<1, kScanThreads, 0, s>>>(tile_sums, ntiles);
   k_scan_apply<<<ntiles, kScanThreads, 0, s>>>(in, n, tile_sums, out);
-  DIPPM_LAUNCH_CHECK("exclusive_scan");
+  DIPPM_LAUNCH_CHECK_N(3, "exclusive_scan");
   return DIPPM_OK;
 }
 
@@ -276,6 +276,6 @@ extern "C" int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64
   if (st) return st;
   k_tfill<<<rb, 256, 0, s>>>(rowptr, col, N, t_rowptr, w.tcursor, w.t_raw);
   k_trow_place<<<rb, 256, 0, s>>>(t_rowptr, w.t_raw, N, t_col);
-  DIPPM_LAUNCH_CHECK("build_csr");
+  DIPPM_LAUNCH_CHECK_N(E > 0 ? 6 : 4, "build_csr");
   return DIPPM_OK;
 }

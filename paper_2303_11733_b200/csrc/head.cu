@@ -313,7 +313,7 @@ int32_t dippm_head_backward(const float* u, int64_t G, int32_t width, const floa
   k_colsum<<<ceil_div_i(width, 128), 128, 0, s>>>(d1, G, width, grads_head + o.b1);
   st = launch_simt(dense(d1, width, 1), dense(head_w + o.w1, 1, width), G, in1, width, epi_plain(du, in1), s);
   if (st) return st;
-  DIPPM_LAUNCH_CHECK("head_backward");
+  DIPPM_LAUNCH_CHECK_N(3, "head_backward");
   return DIPPM_OK;
 }
 

@@ -299,6 +299,7 @@ class Engine:
         self.wt = [ActBuf(hp, 2 * d, self.dtype, self.device) for d in self.L.d_in]
         self.wb = [None] + [ActBuf(2 * d, hp, self.dtype, self.device) for d in self.L.d_in[1:]]
         self.launches = 0
+        self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
 
     # -- parameters -----------------------------------------------------------
     def set_params(self, items, normalizer) -> None:
@@ -344,10 +345,10 @@ class Engine:
                 _lib.call("dippm_pack", _p(w), 2 * d, L.hp, 0, self.wb[i].view(), s)
         self.launches += 1 + len(L.d_in) + len(L.d_in) - 1
 
-    def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8) -> None:
+    def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale: float = 1.0) -> None:
         """numerics.adam_step over all 15 tensors (one launch), then repack."""
         self.t += 1
-        _lib.call("dippm_adam", _p(self.params), _p(self.m), _p(self.v), _p(self.grads), self.L.total, self.t,
+        _lib.call("dippm_adam", _p(self.params), _p(self.m), _p(self.v), _p(self.grads), grad_scale, self.L.total, self.t,
                   lr, beta1, beta2, eps, _stream())
         self.launches += 1
         self.refresh()
@@ -355,7 +356,11 @@ class Engine:
     # -- kernels --------------------------------------------------------------
     def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1):
         args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits)
+        if self.gemm_hook is not None:
+            self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
+        if self.gemm_hook is not None:
+            self.gemm_hook("post", 2.0 * M * N * K)
         self.launches += 1
 
     def forward(self, b: Batch, ws: Workspace, mask_mode: int = 0, dropout_p: float = 0.0, seed: int = 0,

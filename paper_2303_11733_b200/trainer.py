@@ -1,0 +1,93 @@
+"""Batched training step — the public throughput API for DIPPM training on B200.
+
+`BatchTrainer.step_host(...)` is the end-to-end call a user makes with a
+collated batch in host memory: H2D of the batch, K1 CSR build, train-mode
+forward (device dropout masks), Huber loss, full backward, optional
+data-parallel gradient all-reduce, fused Adam + repack, and a D2H read of the
+loss.  `step_resident(batch)` is the same step for a batch already in HBM.
+
+The objective per step is the reference's batch objective (gnn.py:383-405:
+mean over the batch of the per-graph Huber loss) with train-mode dropout;
+Adam follows numerics.py:93-114 on fp64 masters.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .device import Batch, Engine, Workspace, build_batch_csr
+
+
+class BatchTrainer:
+    def __init__(self, model, precision: str = "bf16", lr: float = 2.754e-5, seed: int = 0, dropout: bool = True,
+                 huber_delta: float = 1.0, allreduce=None, world_size: int = 1, device=None, backend: str = "tc"):
+        self.model = model
+        self.engine = Engine(model.hidden, precision, device, backend)
+        self.engine.set_params(model.param_items(), model.normalizer)
+        self.lr, self.seed, self.delta = lr, seed, huber_delta
+        self.dropout_p = model.dropout_p if dropout else 0.0
+        self.allreduce = allreduce
+        self.world_size = world_size
+        self.steps = 0
+        self.ws = None
+        self._stage = None
+        self._loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+
+    def reserve(self, max_nodes: int, max_graphs: int, max_edges: int | None = None) -> None:
+        """Preallocate the workspace (and host-batch staging) for batches up to this size."""
+        self.ws = Workspace(self.engine, max_nodes, max_graphs, train=True)
+        e = max_edges if max_edges is not None else 2 * max_nodes
+        d = self.engine.device
+        self._stage = {
+            "x": torch.empty(max_nodes, dev.FEATURE_WIDTH, dtype=torch.float32, device=d),
+            "src": torch.empty(e, dtype=torch.int64, device=d), "dst": torch.empty(e, dtype=torch.int64, device=d),
+            "gp": torch.empty(max_graphs + 1, dtype=torch.int32, device=d),
+            "fs": torch.empty(max_graphs, dev.STATIC_WIDTH, dtype=torch.float32, device=d),
+            "y": torch.empty(max_graphs, 3, dtype=torch.float32, device=d),
+        }
+
+    def _ensure(self, b: Batch) -> None:
+        if self.ws is None or b.N > self.ws.N or b.G > self.ws.G:
+            self.reserve(max(b.N, 1), b.G)
+
+    def step_resident(self, b: Batch) -> None:
+        """One training step on a device-resident batch (no host synchronisation)."""
+        self._ensure(b)
+        eng, ws = self.engine, self.ws
+        build_batch_csr(b)
+        self.steps += 1
+        mode = 2 if self.dropout_p > 0 else 0
+        eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 1000003 + self.steps,
+                    predict=False)
+        eng.loss(b, ws, self.delta)
+        eng.backward(b, ws, use_masks=mode != 0)
+        if self.allreduce is not None:
+            self.allreduce(eng.grads)          # sum of per-rank batch means
+        eng.adam_step(self.lr, grad_scale=1.0 / self.world_size)
+
+    def step_host(self, x, src, dst, graph_ptr, fs, y) -> float:
+        """End-to-end step from host (ideally pinned) buffers; returns the batch loss."""
+        t = [torch.as_tensor(a) for a in (x, src, dst, graph_ptr, fs, y)]
+        G, N, E = t[3].numel() - 1, t[0].shape[0], t[1].numel()
+        if self._stage is None or N > self._stage["x"].shape[0] or E > self._stage["src"].numel() \
+                or G + 1 > self._stage["gp"].numel():
+            self.reserve(max(N, self.ws.N if self.ws else 0), max(G, self.ws.G if self.ws else 0), max_edges=2 * E)
+        s = self._stage
+        xs, ss, ds_, gs, fss, ys = s["x"][:N], s["src"][:E], s["dst"][:E], s["gp"][:G + 1], s["fs"][:G], s["y"][:G]
+        for d_, h in zip((xs, ss, ds_, gs, fss, ys), t):
+            d_.copy_(h, non_blocking=True)
+        b = Batch(G=G, N=N, E=E, x=xs, src=ss, dst=ds_, graph_ptr=gs, fs=fss, y=ys,
+                  h2d_bytes=sum(a.numel() * a.element_size() for a in t))
+        self.step_resident(b)
+        self._loss_host.copy_(self.ws.loss[:1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(self._loss_host[0])
+
+    def sync_model(self):
+        """Copy the device fp64 masters back into the host model's live arrays."""
+        final = self.engine.get_params()
+        for name, arr in self.model.param_items():
+            arr[...] = final[name]
+        return self.model
