@@ -28,9 +28,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 from pathlib import Path
 
@@ -47,8 +45,8 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200, help="timed steps (~5 epochs of the 41-batch corpus)")
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
     p.add_argument("--graphs", type=int, default=10508)
@@ -57,6 +55,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=6, help="CPU baseline sample: steps of one batch each")
+    p.add_argument("--clock-ms", type=int, default=10, help="NVML sampling interval during timing")
+    p.add_argument("--no-clocks", action="store_true")
     return p.parse_args()
 
 
@@ -72,44 +72,62 @@ def peaks():
 # clocks (nvidia-smi sampled during the timed region)
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled in-process through NVML (pynvml) on a
+    background thread during the timed region.  (Spawning `nvidia-smi -lms`
+    instead was measured to stall the GPU work it is observing.)"""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, gpu_index: int, interval_ms: int = 50):
+        self.gpu, self.interval = gpu_index, interval_ms
+        self.samples, self.active, self.stop_flag, self.thread, self.h = [], False, False, None, None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=self.file, stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import threading
+
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - report "not sampled" instead of failing the bench
+            self.h = None
+            return
+
+        def loop():
+            while not self.stop_flag:
+                if self.active:
+                    try:
+                        c = self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM)
+                        r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                        self.samples.append((c, r))
+                    except Exception:  # noqa: BLE001
+                        pass
+                time.sleep(self.interval / 1000.0)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def wait_first_sample(self):
+        pass
+
+    def mark(self):
+        self.samples.clear()
+        self.active = True
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        self.proc.wait(timeout=5)
-        self.file.flush()
-        rows = [r.split(", ") for r in Path(self.file.name).read_text().strip().splitlines() if r.strip()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, smax, reasons = [], None, set()
-        for r in rows:
-            try:
-                sm.append(float(r[1]))
-                smax = float(r[2])
-                for n, v in zip(names, r[5:9]):
-                    if v.strip().lower() == "active":
-                        reasons.add(n)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.active = False
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml not sampled"]}
+        reasons = sorted({name for _, r in self.samples for bit, name in self.REASONS.items() if r & bit})
+        sm = [c for c, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "nvml in-process"}
 
 
 # ---------------------------------------------------------------------------
@@ -300,14 +318,16 @@ def main():
     def step(i):
         trainer.step_resident(resident[i % nb])
 
+    sampler = ClockSampler(local, args.clock_ms)
+    if not args.no_clocks:
+        sampler.start()
+        sampler.wait_first_sample()
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
+    sampler.mark()
     l0 = lib.dippm_launch_count()
     t_wall = time.perf_counter()
     start = torch.cuda.Event(enable_timing=True)

@@ -99,24 +99,22 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
                              int32_t width, const int32_t* rowptr, const int32_t* col,
                              const float* inv_deg, void* stream);
 
-/* K2 backward — gnn.py:227,232: given dA = dz @ [W_self; W_neigh]^T as fp32
- * [N, 2*width] (row stride ld_da), computes
- *   dh[u]  = dA[u, :width] + sum_{v in out(u)} inv_deg[v] * dA[v, width:]
- *   dz[u]  = dh[u] * (h_prev[u] > 0)          (ReLU mask of the layer below)
- * writes dz into dz_out, and per-block column partial sums of dz into
- * colsum_partial [dippm_colsum_blocks(N), width] (bias gradient, gnn.py:230,
- * reduced deterministically by dippm_reduce_rows). */
+/* K2 backward — gnn.py:161-162, 227-232.  B = [dz | g] is [N, 2*width]
+ * (row stride B.ld) with dz in the left half; writes g = agg^T dz into the
+ * right half (g[u] = sum_{u->v} dz[v] / deg v, via the transposed CSR), so the
+ * input gradient dh_prev = [dz | g] @ [W_self | W_neigh]^T is one GATE GEMM.
+ * Also writes per-block column partial sums of dz into colsum_partial
+ * [dippm_colsum_blocks(N), width] (bias gradient gnn.py:230, reduced by
+ * dippm_reduce_rows).  write_agg = 0 computes the partial sums only. */
 int32_t dippm_colsum_blocks(int64_t num_nodes);
-int32_t dippm_sage_backward_gather(const float* dA, int64_t ld_da, int32_t width, dippm_act_t h_prev,
-                                   dippm_act_t dz_out, int64_t num_nodes, const int32_t* t_rowptr,
-                                   const int32_t* t_col, const float* inv_deg, float* colsum_partial,
-                                   void* stream);
-
-/* Readout backward — gnn.py:224,227: dz3[v] = dr[g(v)] / N_g * (h3[v] > 0),
- * dr = du[:, :width] with du [G, ld_du] fp32; plus column partial sums. */
-int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t num_graphs,
-                               int32_t width, dippm_act_t h3, dippm_act_t dz_out, int64_t num_nodes,
+int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t num_nodes, int32_t write_agg,
+                               const int32_t* t_rowptr, const int32_t* t_col, const float* inv_deg,
                                float* colsum_partial, void* stream);
+
+/* Readout backward — gnn.py:224,227: dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0),
+ * du [G, ld_du] fp32. */
+int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t num_graphs,
+                               int32_t width, dippm_act_t h3, dippm_act_t dz_out, int64_t num_nodes, void* stream);
 
 /* out[c] = scale * sum_{r<rows} in[r*ld + c] in fixed row order (fp32 in, fp64 accumulate). */
 int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t cols, double scale,
@@ -131,7 +129,9 @@ int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t col
  *   WGRAD:  C_s[M,N] fp32 partials of A^T-style products with both operands
  *           MN-major: C = dz^T @ [h | m] split over row chunks s — gnn.py:228-229
  * Operand "major": 0 = K-major ([rows, K] row-major), 1 = MN-major ([K, rows]). */
-enum dippm_gemm_kind { DIPPM_GEMM_FWD = 0, DIPPM_GEMM_STORE = 1, DIPPM_GEMM_WGRAD = 2 };
+enum dippm_gemm_kind { DIPPM_GEMM_FWD = 0, DIPPM_GEMM_STORE = 1, DIPPM_GEMM_WGRAD = 2, DIPPM_GEMM_GATE = 3 };
+/*   GATE:   out = (gate > 0) * gate_scale * (A @ B^T)  — dgrad fused with the ReLU (+dropout)
+ *           mask of the layer below: gnn.py:227,232 / 293-298, A = [dz | agg^T dz].          */
 
 typedef struct dippm_gemm_args {
   int64_t kind;
@@ -146,6 +146,13 @@ typedef struct dippm_gemm_args {
   float* c;            /* STORE: [M, ldc]; WGRAD: [splits, M, ldc] */
   int64_t ldc;
   int64_t splits;      /* WGRAD split count (>=1); others 1 */
+  dippm_act_t gate;    /* GATE: out = gate > 0 ? acc * gate_scale : 0 (ReLU' of the layer below, */
+  double gate_scale;   /*       times the inverted-dropout keep scale where one applies)          */
+  int64_t drop_mode;   /* FWD dropout after ReLU: 0 none, 1 multiply mask, 2 generate mask (hash) */
+  float* mask;         /* [M, ldm] fp32 dropout mask (read in mode 1, written in mode 2)         */
+  int64_t ldm;
+  double drop_p;
+  uint64_t seed;
 } dippm_gemm_args_t;
 
 /* Split count the tensor-core WGRAD would like for this problem. */
@@ -157,58 +164,65 @@ int32_t dippm_splitk_reduce_t(const float* in, int32_t splits, int64_t M, int64_
                               int64_t ldo, void* stream);
 
 /* ---------------------------------------------------------------------------
- * K4 — readout + static features: u[g] = [ mean_{v in g} h3[v] , (fs[g]-fs_mean)/fs_std ]
- * gnn.py:214-215, normalize_fs gnn.py:96-97.  u: [G, width+5] fp32.
+ * K4 — readout + static features (gnn.py:214-215, normalize_fs gnn.py:96-97):
+ *   u[g] = [ mean_{v in g} h3[v] , (fs[g] - fs_mean) / fs_std , 0 ... ]
+ * u: [G, u.ld] activation view in the head's operand dtype, u.ld >= width + 5
+ * (zero padded so fc1 runs as a K-aligned tensor-core GEMM).
  * norm: device double[16] = y_mean[3], y_std[3], fs_mean[5], fs_std[5]. */
 int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t num_graphs, int32_t width,
-                          const float* fs_raw, const double* norm, float* u, void* stream);
+                          const float* fs_raw, const double* norm, dippm_act_t u, void* stream);
 
 /* ---------------------------------------------------------------------------
- * K5 — FC head, gnn.py:265-284: fc1 (width+5 -> width) ReLU (+dropout),
- * fc2 (width -> width) ReLU (+dropout), fc3 (width -> 3).
- * head_w: device fp32, packed [fc1.w (width+5)*width | fc1.b | fc2.w | fc2.b | fc3.w | fc3.b].
- * cache: device fp32 [4, G, width] = a1, x2, a2, x3 (pre-activations and layer inputs).
- * masks: device fp32 [2, G, width]; mask_mode 0 = none (eval), 1 = use given
- * masks (host-drawn PCG64, numerics.py:45-55), 2 = generate (counter hash, seed).
- * out_norm: [G,3] fp32 normalised outputs.  If y_pred (device double [G,3]) is
- * non-NULL, also de-normalises (gnn.py:93-94) and writes MIG codes
- * (mig.py:32-45) from y_pred[:,1] into mig (int8 [G]). */
-int32_t dippm_head_forward(const float* u, int64_t num_graphs, int32_t width, const float* head_w,
-                           float* cache, float* masks, int32_t mask_mode, float dropout_p, uint64_t seed,
-                           float* out_norm, const double* norm, double* y_pred, int8_t* mig,
-                           int32_t* nonfinite, void* stream);
+ * K5 — FC head, gnn.py:265-284.  fc1/fc2 (and their gradients) are dippm_gemm
+ * calls: FWD with bias + ReLU + dropout epilogue, GATE / STORE / WGRAD for the
+ * backward.  fc3 (width -> 3) and the output stage are:
+ * dippm_fc3_forward: out_norm[g] = x3[g] @ w3 + b3 (normalised, [G,3] fp32);
+ * if y_pred != NULL also de-normalises (gnn.py:93-94, fp64) and writes the
+ * MIG code of y_pred[g,1] (mig.py:32-45) into mig[g]; *nonfinite set on NaN/Inf. */
+int32_t dippm_fc3_forward(dippm_act_t x3, int64_t num_graphs, int32_t width, const float* w3, const float* b3,
+                          float* out_norm, const double* norm, double* y_pred, int8_t* mig, int32_t* nonfinite,
+                          void* stream);
+
+/* fc3 backward fused with the fc2 ReLU/dropout gate (gnn.py:293-298):
+ *   grad_w3 = x3^T dout, grad_b3 = sum dout, d2 = (dout @ w3^T) * (x3 > 0) * keep_scale,
+ *   grad_b2 = column sums of d2.  keep_scale = 1/(1-p) in train mode with dropout, else 1. */
+int32_t dippm_fc3_backward(dippm_act_t x3, int64_t num_graphs, int32_t width, const float* w3, const float* dout,
+                           float keep_scale, float* grad_w3, float* grad_b3, dippm_act_t d2, float* grad_b2,
+                           void* stream);
+
+/* Column sums of an activation view (fixed order): out[c] = sum_r a[r, c]. */
+int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, void* stream);
 
 /* Huber loss + gradient, numerics.py:58-73, averaged over the batch
- * (gnn.py:398-404): dout[g] = grad_g / G.  y_raw [G,3] fp32 targets are
- * normalised on device (gnn.py:90-91).  loss_out: device double [4] =
- * {mean loss, sum APE latency, memory, energy} (APE uses de-normalised
+ * (gnn.py:398-404): dout[g] = grad_g / G (dout may be NULL).  y_raw [G,3] fp32
+ * targets are normalised on device (gnn.py:90-91).  loss_out: device double[4]
+ * = {mean loss, sum APE latency, memory, energy} (APE on de-normalised
  * outputs, gnn.py:458-459). */
 int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t num_graphs, const double* norm,
                     double delta, float* dout, double* loss_out, void* stream);
 
-/* Head backward, gnn.py:287-299: writes fc grads into grads_head (same
- * packing as head_w) and du [G, width+5] fp32 (input gradient). */
-int32_t dippm_head_backward(const float* u, int64_t num_graphs, int32_t width, const float* head_w,
-                            const float* cache, const float* masks, int32_t use_masks, const float* dout,
-                            float* grads_head, float* du, float* scratch, void* stream);
-size_t dippm_head_scratch_floats(int64_t num_graphs, int32_t width);
-
 /* ---------------------------------------------------------------------------
- * K8 — bias-corrected Adam, numerics.py:93-114, same op order, on fp64
- * master parameters (fp32 gradients, multiplied by grad_scale first — 1/world
- * size after a data-parallel sum), one launch for all 15 tensors. */
-int32_t dippm_adam(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
-                   int64_t t, double lr, double beta1, double beta2, double eps, void* stream);
+ * K8 — bias-corrected Adam (numerics.py:93-114, same op order) on fp64 master
+ * parameters, fused with the refresh of every compute copy the GEMMs read.
+ * grads (fp32) are multiplied by grad_scale first (1/world after a data-
+ * parallel sum).  do_adam = 0 only refreshes the copies.  p32 (fp32 [n]) gets
+ * the updated parameters; each segment copies params[src_off .. + rows*cols)
+ * (row-major [rows, cols]) into dst at (r, dst_col_off + c) in dst's dtype
+ * (bf16, or tf32 hi/lo planes).  One launch for all 15 tensors. */
+#define DIPPM_MAX_PACK_SEGS 12
+typedef struct dippm_pack_seg {
+  int64_t src_off;
+  int64_t rows, cols;
+  int64_t dst_col_off;
+  dippm_act_t dst;
+} dippm_pack_seg_t;
+int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
+                        int64_t t, double lr, double beta1, double beta2, double eps, int32_t do_adam, float* p32,
+                        const dippm_pack_seg_t* segs, int32_t nsegs, void* stream);
 
-/* Pack fp64 master weights into compute copies.
- *  w [rows, cols] fp64 row-major  ->  dst view (bf16 or tf32 hi/lo or f32);
- *  transpose != 0 writes dst[c, r] (K-major W^T for the forward GEMM). */
+/* Pack a fp64 matrix into a compute copy (tests / single-layer API):
+ *  w [rows, cols] fp64 row-major -> dst view; transpose != 0 writes dst[c, r]. */
 int32_t dippm_pack(const double* w, int64_t rows, int64_t cols, int32_t transpose, dippm_act_t dst, void* stream);
-
-/* Batch assembly from a device-resident dataset (bench / training epochs):
- * gathers graphs ids[0..G) into contiguous rows. */
-int32_t dippm_gather_rows(const float* src, const int64_t* src_row, int64_t rows, int32_t cols, float* dst,
-                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libdippm_b200.so"
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 DT_F32, DT_BF16, DT_TF32X3 = 0, 1, 2
-GEMM_FWD, GEMM_STORE, GEMM_WGRAD = 0, 1, 2
+GEMM_FWD, GEMM_STORE, GEMM_WGRAD, GEMM_GATE = 0, 1, 2, 3
 
 
 class DeviceUnavailable(DippmError):
@@ -40,10 +40,20 @@ class GemmArgs(C.Structure):
         ("a", Act), ("a_mn_major", C.c_int64), ("b", Act), ("b_mn_major", C.c_int64),
         ("bias", C.c_void_p), ("relu", C.c_int64), ("out", Act),
         ("c", C.c_void_p), ("ldc", C.c_int64), ("splits", C.c_int64),
+        ("gate", Act), ("gate_scale", C.c_double), ("drop_mode", C.c_int64), ("mask", C.c_void_p),
+        ("ldm", C.c_int64), ("drop_p", C.c_double), ("seed", C.c_uint64),
     ]
 
 
 P, I32, I64, U64, F32, F64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_size_t
+
+class PackSeg(C.Structure):
+    """dippm_pack_seg_t: one fp64-master -> compute-copy segment refreshed by dippm_adam_pack."""
+    _fields_ = [("src_off", C.c_int64), ("rows", C.c_int64), ("cols", C.c_int64), ("dst_col_off", C.c_int64),
+                ("dst", Act)]
+
+
+MAX_PACK_SEGS = 12
 
 # name -> (restype, argtypes); must match include/dippm_b200.h
 SIGNATURES = {
@@ -57,20 +67,19 @@ SIGNATURES = {
     "dippm_build_csr": (I32, [P, P, I64, I64, P, P, P, P, P, P, P, P, SZ, P]),
     "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
     "dippm_colsum_blocks": (I32, [I64]),
-    "dippm_sage_backward_gather": (I32, [P, I64, I32, Act, Act, I64, P, P, P, P, P]),
-    "dippm_readout_backward": (I32, [P, I64, P, I64, I32, Act, Act, I64, P, P]),
+    "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P]),
+    "dippm_readout_backward": (I32, [P, I64, P, I64, I32, Act, Act, I64, P]),
     "dippm_reduce_rows": (I32, [P, I64, I64, I32, F64, P, P]),
     "dippm_wgrad_splits": (I32, [I64, I64, I64]),
     "dippm_gemm": (I32, [C.POINTER(GemmArgs), I32, P]),
     "dippm_splitk_reduce_t": (I32, [P, I32, I64, I64, F64, P, I64, P]),
-    "dippm_pool_concat": (I32, [Act, P, I64, I32, P, P, P, P]),
-    "dippm_head_forward": (I32, [P, I64, I32, P, P, P, I32, F32, U64, P, P, P, P, P, P]),
+    "dippm_pool_concat": (I32, [Act, P, I64, I32, P, P, Act, P]),
+    "dippm_fc3_forward": (I32, [Act, I64, I32, P, P, P, P, P, P, P, P]),
+    "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
+    "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),
     "dippm_huber": (I32, [P, P, I64, P, F64, P, P, P]),
-    "dippm_head_backward": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
-    "dippm_head_scratch_floats": (SZ, [I64, I32]),
-    "dippm_adam": (I32, [P, P, P, P, F64, I64, I64, F64, F64, F64, F64, P]),
+    "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),
     "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
-    "dippm_gather_rows": (I32, [P, P, I64, I32, P, P]),
 }
 
 _lib = None

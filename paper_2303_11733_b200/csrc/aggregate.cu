@@ -64,98 +64,116 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m,
   }
 }
 
-// Backward gather (mode 0) / readout backward (mode 1) with fused ReLU mask and
-// per-block column partial sums of the produced dz (bias gradient).
-template <int kMode>
-__global__ void __launch_bounds__(kAggThreads) k_dz(const float* __restrict__ dA, int64_t ld_da, int width,
-                                                     ActView gate, ActView dz, int64_t N,
-                                                     const int* __restrict__ t_rowptr, const int* __restrict__ t_col,
-                                                     const float* __restrict__ inv_deg,
-                                                     const int* __restrict__ graph_ptr, int64_t G,
-                                                     float* __restrict__ colsum_partial) {
+// Transposed aggregation for the backward pass (gnn.py:161-162, 232): with
+// B = [dz | g] ([N, 2*width], dz already in the left half),
+//   g[u] = sum_{u->v} dz[v] / deg(v)          (agg^T dz, via the transposed CSR)
+// so that dh_prev = [dz | g] @ [W_self | W_neigh]^T is ONE GEMM (dgrad with the
+// ReLU gate fused in its epilogue).  Also emits per-block column partial sums
+// of dz (bias gradient, gnn.py:230).  write_agg = 0: partial sums only.
+__global__ void __launch_bounds__(kAggThreads) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
+                                                             const int* __restrict__ t_rowptr,
+                                                             const int* __restrict__ t_col,
+                                                             const float* __restrict__ inv_deg,
+                                                             float* __restrict__ colsum_partial) {
   extern __shared__ float s_part[];  // [groups][width]
   const int chunks = width >> 3;
-  const int groups = kAggThreads / chunks;  // >= 1 (width <= 2048)
+  const int groups = kAggThreads / chunks;
   const int grp = threadIdx.x / chunks, ch = threadIdx.x % chunks;
   const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
   const int64_t r1 = (N < r0 + kColsumRows) ? N : r0 + kColsumRows;
-  float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (grp < groups) {
     const int c = ch * 8;
-    int g = 0;
-    if (kMode == 1) {  // graph of the first row handled by this thread (binary search)
-      int lo = 0, hi = (int)G;
-      int64_t rr = r0 + grp;
-      while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (graph_ptr[mid] <= rr) lo = mid; else hi = mid;
-      }
-      g = lo;
-    }
+    float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t row = r0 + grp; row < r1; row += groups) {
       float v[8];
-      if (kMode == 0) {
-        const float4* p = reinterpret_cast<const float4*>(dA + row * ld_da + c);
-        float4 a0 = p[0], a1 = p[1];
-        v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
-        v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+      act_load8(B, row, c, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) part[k] += v[k];
+      if (write_agg) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const int b = t_rowptr[row], e = t_rowptr[row + 1];
         for (int j = b; j < e; ++j) {
           const int tv = t_col[j];
           const float w = inv_deg[tv];
-          const float4* q = reinterpret_cast<const float4*>(dA + (int64_t)tv * ld_da + width + c);
-          float4 b0 = q[0], b1 = q[1];
-          v[0] += w * b0.x; v[1] += w * b0.y; v[2] += w * b0.z; v[3] += w * b0.w;
-          v[4] += w * b1.x; v[5] += w * b1.y; v[6] += w * b1.z; v[7] += w * b1.w;
+          float x[8];
+          act_load8(B, tv, c, x);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = fmaf(w, x[k], acc[k]);
         }
-      } else {
-        while (graph_ptr[g + 1] <= row) ++g;
-        const float inv_n = 1.0f / (float)(graph_ptr[g + 1] - graph_ptr[g]);
-        const float* p = dA + (int64_t)g * ld_da + c;  // du rows (ld = width + 5) are not 16B aligned
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(p + k) * inv_n;
+        act_store8(B, row, width + c, acc);
       }
-      float hg[8];
-      act_load8(gate, row, c, hg);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        v[k] = hg[k] > 0.f ? v[k] : 0.f;  // relu'(z) with z>0 <=> h>0 (gnn.py:227)
-        part[k] += v[k];
-      }
-      act_store8(dz, row, c, v);
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_part[grp * width + c + k] = part[k];
   }
   __syncthreads();
   for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < groups; ++q) s += s_part[q * width + c];
-    colsum_partial[(int64_t)blockIdx.x * width + c] = s;
+    float t = 0.f;
+    for (int q = 0; q < groups; ++q) t += s_part[q * width + c];
+    colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
 }
 
-__global__ void k_reduce_rows(const float* __restrict__ in, int64_t rows, int64_t ld, int cols, double scale,
-                              float* __restrict__ out) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  double s = 0.0;
-  for (int64_t r = 0; r < rows; ++r) s += (double)in[r * ld + c];
-  out[c] = (float)(s * scale);
+// Readout backward (gnn.py:224, 227): dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0).
+__global__ void __launch_bounds__(kAggThreads) k_readout_backward(const float* __restrict__ du, int64_t ld_du,
+                                                                  int width, ActView gate, ActView dz, int64_t N,
+                                                                  const int* __restrict__ graph_ptr, int64_t G) {
+  const int chunks = width >> 3;
+  const int groups = kAggThreads / chunks;
+  const int grp = threadIdx.x / chunks, ch = threadIdx.x % chunks;
+  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
+  const int64_t r1 = (N < r0 + kColsumRows) ? N : r0 + kColsumRows;
+  if (grp >= groups || r0 + grp >= r1) return;
+  const int c = ch * 8;
+  int lo = 0, hi = (int)G;  // graph of the first row handled by this thread
+  const int64_t rr = r0 + grp;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (graph_ptr[mid] <= rr) lo = mid; else hi = mid;
+  }
+  int g = lo;
+  for (int64_t row = rr; row < r1; row += groups) {
+    while (graph_ptr[g + 1] <= row) ++g;
+    const float inv_n = 1.0f / (float)(graph_ptr[g + 1] - graph_ptr[g]);
+    const float* p = du + (int64_t)g * ld_du + c;
+    float v[8], hg[8];
+    act_load8(gate, row, c, hg);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = hg[k] > 0.f ? __ldg(p + k) * inv_n : 0.f;  // relu'(z): z>0 <=> h>0
+    act_store8(dz, row, c, v);
+  }
 }
 
-// K4: one block per graph.
+// Deterministic column reduction: out[c] = scale * sum_r in[r*ld + c].
+// 32 columns x 32 row-lanes per block, fixed-order fp64 accumulation.
+__global__ void __launch_bounds__(1024) k_reduce_rows(const float* __restrict__ in, int64_t rows, int64_t ld,
+                                                      int cols, double scale, float* __restrict__ out) {
+  __shared__ double s[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  double acc = 0.0;
+  if (c < cols)
+    for (int64_t r = ty; r < rows; r += 32) acc += (double)in[r * ld + c];
+  s[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    double t = 0.0;
+    for (int q = 0; q < 32; ++q) t += s[q][tx];
+    out[c] = (float)(t * scale);
+  }
+}
+
+// K4: one block per graph; u = [mean_g h3 | (fs - mu)/sigma | 0 ...] in the
+// head's operand dtype, row stride u.ld (>= width + 5, zero padded).
 __global__ void __launch_bounds__(kAggThreads) k_pool_concat(ActView h, const int* __restrict__ graph_ptr,
                                                              int width, const float* __restrict__ fs_raw,
-                                                             const double* __restrict__ norm,
-                                                             float* __restrict__ u) {
+                                                             const double* __restrict__ norm, ActView u) {
   extern __shared__ float s_part[];
   const int g = blockIdx.x;
   const int chunks = width >> 3;
   const int groups = kAggThreads / chunks;
   const int grp = threadIdx.x / chunks, ch = threadIdx.x % chunks;
   const int64_t r0 = graph_ptr[g], r1 = graph_ptr[g + 1];
-  const int ldu = width + kStaticWidth;
   if (grp < groups) {
     float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t row = r0 + grp; row < r1; row += groups) {
@@ -170,15 +188,18 @@ __global__ void __launch_bounds__(kAggThreads) k_pool_concat(ActView h, const in
   __syncthreads();
   const float inv_n = 1.0f / (float)(r1 - r0);
   for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < groups; ++q) s += s_part[q * width + c];
-    u[(int64_t)g * ldu + c] = s * inv_n;
+    float t = 0.f;
+    for (int q = 0; q < groups; ++q) t += s_part[q * width + c];
+    act_store(u, g, c, t * inv_n);
   }
-  if (threadIdx.x < kStaticWidth) {
-    const int k = threadIdx.x;
-    const double* fs_mean = norm + 6;
-    const double* fs_std = norm + 11;
-    u[(int64_t)g * ldu + width + k] = (float)(((double)fs_raw[g * kStaticWidth + k] - fs_mean[k]) / fs_std[k]);
+  for (int k = threadIdx.x; k < u.ld - width; k += blockDim.x) {
+    float v = 0.f;
+    if (k < kStaticWidth) {
+      const double* fs_mean = norm + 6;
+      const double* fs_std = norm + 11;
+      v = (float)(((double)fs_raw[g * kStaticWidth + k] - fs_mean[k]) / fs_std[k]);
+    }
+    act_store(u, g, width + k, v);
   }
 }
 
@@ -203,46 +224,41 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
   return DIPPM_OK;
 }
 
-int32_t dippm_sage_backward_gather(const float* dA, int64_t ld_da, int32_t width, dippm_act_t h_prev,
-                                   dippm_act_t dz_out, int64_t N, const int32_t* t_rowptr, const int32_t* t_col,
-                                   const float* inv_deg, float* colsum_partial, void* stream) {
-  DIPPM_ARG_CHECK(N >= 1 && width % 8 == 0 && width / 8 <= kAggThreads, "sage_backward_gather: bad width %d", width);
+int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
+                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+  DIPPM_ARG_CHECK(N >= 1 && width % 8 == 0 && width / 8 <= kAggThreads, "sage_aggregate_t: bad width %d", width);
   const int groups = kAggThreads / (width / 8);
   size_t smem = (size_t)groups * width * sizeof(float);
-  k_dz<0><<<dippm_colsum_blocks(N), kAggThreads, smem, (cudaStream_t)stream>>>(
-      dA, ld_da, width, make_view(h_prev), make_view(dz_out), N, t_rowptr, t_col, inv_deg, nullptr, 0,
-      colsum_partial);
-  DIPPM_LAUNCH_CHECK("k_dz<gather>");
+  k_aggregate_t<<<dippm_colsum_blocks(N), kAggThreads, smem, (cudaStream_t)stream>>>(
+      make_view(B), width, N, write_agg, t_rowptr, t_col, inv_deg, colsum_partial);
+  DIPPM_LAUNCH_CHECK("k_aggregate_t");
   return DIPPM_OK;
 }
 
 int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t G, int32_t width,
-                               dippm_act_t h3, dippm_act_t dz_out, int64_t N, float* colsum_partial, void* stream) {
+                               dippm_act_t h3, dippm_act_t dz_out, int64_t N, void* stream) {
   DIPPM_ARG_CHECK(N >= 1 && G >= 1 && width % 8 == 0 && width / 8 <= kAggThreads, "readout_backward: bad args");
-  const int groups = kAggThreads / (width / 8);
-  size_t smem = (size_t)groups * width * sizeof(float);
-  k_dz<1><<<dippm_colsum_blocks(N), kAggThreads, smem, (cudaStream_t)stream>>>(
-      du, ld_du, width, make_view(h3), make_view(dz_out), N, nullptr, nullptr, nullptr, graph_ptr, G,
-      colsum_partial);
-  DIPPM_LAUNCH_CHECK("k_dz<readout>");
+  k_readout_backward<<<dippm_colsum_blocks(N), kAggThreads, 0, (cudaStream_t)stream>>>(
+      du, ld_du, width, make_view(h3), make_view(dz_out), N, graph_ptr, G);
+  DIPPM_LAUNCH_CHECK("k_readout_backward");
   return DIPPM_OK;
 }
 
 int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t cols, double scale, float* out,
                           void* stream) {
   DIPPM_ARG_CHECK(rows >= 0 && cols >= 1, "reduce_rows: bad shape");
-  k_reduce_rows<<<ceil_div_i(cols, 128), 128, 0, (cudaStream_t)stream>>>(in, rows, ld, cols, scale, out);
+  k_reduce_rows<<<ceil_div_i(cols, 32), 1024, 0, (cudaStream_t)stream>>>(in, rows, ld, cols, scale, out);
   DIPPM_LAUNCH_CHECK("k_reduce_rows");
   return DIPPM_OK;
 }
 
 int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, int32_t width, const float* fs_raw,
-                          const double* norm, float* u, void* stream) {
-  DIPPM_ARG_CHECK(G >= 1 && width % 8 == 0 && width / 8 <= kAggThreads, "pool_concat: bad args");
+                          const double* norm, dippm_act_t u, void* stream) {
+  DIPPM_ARG_CHECK(G >= 1 && width % 8 == 0 && width / 8 <= kAggThreads && u.ld >= width + 5, "pool_concat: bad args");
   const int groups = kAggThreads / (width / 8);
   size_t smem = (size_t)groups * width * sizeof(float);
   k_pool_concat<<<(unsigned)G, kAggThreads, smem, (cudaStream_t)stream>>>(make_view(h), graph_ptr, width, fs_raw,
-                                                                         norm, u);
+                                                                         norm, make_view(u));
   DIPPM_LAUNCH_CHECK("k_pool_concat");
   return DIPPM_OK;
 }

@@ -50,30 +50,52 @@ __global__ void k_mig_codes(const double* mem, int64_t stride, int64_t n, int8_t
   codes[i] = (int8_t)mig_rule(a);
 }
 
-// numerics.py:93-114 in the same operation order (t already incremented).
-__global__ void k_adam(double* __restrict__ p, double* __restrict__ m, double* __restrict__ v,
-                       const float* __restrict__ g, double gscale, int64_t n, double lr, double b1, double b2, double eps,
-                       double bc1, double bc2) {
+struct PackSegs {
+  int n;
+  struct Seg {
+    int64_t src_off, rows, cols, dst_col_off;
+    ActView dst;
+  } s[DIPPM_MAX_PACK_SEGS];
+};
+
+// numerics.py:93-114 in the same operation order (t already incremented),
+// fused with the refresh of the fp32 copy and of every GEMM operand copy.
+__global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, double* __restrict__ m,
+                                                   double* __restrict__ v, const float* __restrict__ g,
+                                                   double gscale, int64_t n, double lr, double b1, double b2,
+                                                   double eps, double bc1, double bc2, int do_adam,
+                                                   float* __restrict__ p32, PackSegs segs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    double gi = (double)g[i] * gscale;
-    double mi = m[i] * b1;
-    mi += (1.0 - b1) * gi;
-    double tmp = gi * gi;
-    tmp *= 1.0 - b2;
-    double vi = v[i] * b2;
-    vi += tmp;
-    double denom = vi / bc2;
-    denom = sqrt(denom);
-    denom += eps;
-    double step = mi / bc1;
-    step /= denom;
-    step *= -lr;
-    step += p[i];
-    m[i] = mi;
-    v[i] = vi;
-    p[i] = step;
+    double val = p[i];
+    if (do_adam) {
+      double gi = (double)g[i] * gscale;
+      double mi = m[i] * b1;
+      mi += (1.0 - b1) * gi;
+      double tmp = gi * gi;
+      tmp *= 1.0 - b2;
+      double vi = v[i] * b2;
+      vi += tmp;
+      double denom = vi / bc2;
+      denom = sqrt(denom);
+      denom += eps;
+      double step = mi / bc1;
+      step /= denom;
+      step *= -lr;
+      step += val;
+      m[i] = mi;
+      v[i] = vi;
+      p[i] = step;
+      val = step;
+    }
+    const float f = (float)val;
+    p32[i] = f;
+    for (int k = 0; k < segs.n; ++k) {
+      const auto& sg = segs.s[k];
+      const int64_t j = i - sg.src_off;
+      if (j >= 0 && j < sg.rows * sg.cols) act_store(sg.dst, j / sg.cols, sg.dst_col_off + j % sg.cols, f);
+    }
   }
 }
 
@@ -95,14 +117,6 @@ __global__ void k_pack(const double* __restrict__ w, int64_t rows, int64_t cols,
       if (r < rows && c < cols) act_store(dst, r, c, tile[i][threadIdx.x]);
     }
   }
-}
-
-__global__ void k_gather_rows(const float* __restrict__ src, const int64_t* __restrict__ src_row, int64_t rows,
-                              int cols, float* __restrict__ dst) {
-  int64_t r = blockIdx.x;
-  if (r >= rows) return;
-  const float* s = src + src_row[r] * cols;
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) dst[r * cols + c] = s[c];
 }
 
 }  // namespace dippm
@@ -138,17 +152,30 @@ int32_t dippm_mig_codes(const double* mem_mb, int64_t stride, int64_t count, int
   return DIPPM_OK;
 }
 
-int32_t dippm_adam(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n, int64_t t,
-                   double lr,
-                   double beta1, double beta2, double eps, void* stream) {
-  DIPPM_ARG_CHECK(n >= 0 && t >= 1, "dippm_adam: bad n/t");
+int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
+                        int64_t t, double lr, double beta1, double beta2, double eps, int32_t do_adam, float* p32,
+                        const dippm_pack_seg_t* segs, int32_t nsegs, void* stream) {
+  DIPPM_ARG_CHECK(n >= 0 && (t >= 1 || !do_adam), "adam_pack: bad n/t");
+  DIPPM_ARG_CHECK(nsegs >= 0 && nsegs <= DIPPM_MAX_PACK_SEGS, "adam_pack: %d segments (max %d)", nsegs,
+                  DIPPM_MAX_PACK_SEGS);
   if (n == 0) return DIPPM_OK;
-  double bc1 = 1.0 - pow(beta1, (double)t);
-  double bc2 = 1.0 - pow(beta2, (double)t);
-  int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 4 * num_sms());
-  k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1, beta2, eps,
-                                                    bc1, bc2);
-  DIPPM_LAUNCH_CHECK("k_adam");
+  PackSegs ps{};
+  ps.n = nsegs;
+  for (int k = 0; k < nsegs; ++k) {
+    DIPPM_ARG_CHECK(segs[k].src_off >= 0 && segs[k].src_off + segs[k].rows * segs[k].cols <= n,
+                    "adam_pack: segment %d out of range", k);
+    ps.s[k].src_off = segs[k].src_off;
+    ps.s[k].rows = segs[k].rows;
+    ps.s[k].cols = segs[k].cols;
+    ps.s[k].dst_col_off = segs[k].dst_col_off;
+    ps.s[k].dst = make_view(segs[k].dst);
+  }
+  double bc1 = do_adam ? 1.0 - pow(beta1, (double)t) : 1.0;
+  double bc2 = do_adam ? 1.0 - pow(beta2, (double)t) : 1.0;
+  int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 8 * num_sms());
+  k_adam_pack<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1, beta2, eps,
+                                                        bc1, bc2, do_adam, p32, ps);
+  DIPPM_LAUNCH_CHECK("k_adam_pack");
   return DIPPM_OK;
 }
 
@@ -157,14 +184,6 @@ int32_t dippm_pack(const double* w, int64_t rows, int64_t cols, int32_t transpos
   dim3 grid(ceil_div_i(cols, 32), ceil_div_i(rows, 32));
   k_pack<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(w, rows, cols, transpose, make_view(dst));
   DIPPM_LAUNCH_CHECK("k_pack");
-  return DIPPM_OK;
-}
-
-int32_t dippm_gather_rows(const float* src, const int64_t* src_row, int64_t rows, int32_t cols, float* dst,
-                          void* stream) {
-  if (rows == 0) return DIPPM_OK;
-  k_gather_rows<<<(unsigned)rows, 128, 0, (cudaStream_t)stream>>>(src, src_row, rows, cols, dst);
-  DIPPM_LAUNCH_CHECK("k_gather_rows");
   return DIPPM_OK;
 }
 

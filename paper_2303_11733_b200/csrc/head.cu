@@ -1,10 +1,12 @@
-// K5/K6 — FC head forward/backward, Huber loss, de-normalisation + MIG pick,
-// and the SIMT fp32 GEMM that carries the head (M = #graphs, tiny next to the
-// SAGE GEMMs: ~0.2% of the FLOPs) and serves as the parity anchor backend for
-// the tensor-core kernels.
+// K5/K6 — FC head pieces that are not GEMMs, Huber loss, and the SIMT fp32
+// GEMM backend (parity anchor for the tensor-core kernels, selected with
+// backend = 1 in dippm_gemm).
 //
 // Head (gnn.py:265-284): a1 = u@W1+b1; x2 = relu(a1)*mask1; a2 = x2@W2+b2;
-// x3 = relu(a2)*mask2; out = x3@W3+b3.  Backward gnn.py:287-299.
+// x3 = relu(a2)*mask2; out = x3@W3+b3.  fc1/fc2 and their gradients run as
+// tcgen05 GEMMs (dippm_gemm FWD / GATE / STORE / WGRAD); fc3 (3 outputs),
+// its backward fused with the fc2 ReLU/dropout gate, the de-normalisation
+// and the MIG pick run here.
 #include <cmath>
 
 #include "common.cuh"
@@ -29,19 +31,19 @@ __device__ __forceinline__ float op_load(const Operand& o, int64_t r, int64_t c)
 }
 
 struct Epi {
-  float alpha;
-  const float* bias;      // [N]
-  float* pre;             // store pre-activation (ld = ldc)
+  int kind;               // DIPPM_GEMM_*
+  const float* bias;
   int relu;
-  const float* mask;      // multiply by mask(m,n) (ld = ldc)
-  int mask_gen;           // generate inverted-dropout mask into `mask_out`
-  float* mask_out;
+  int drop_mode;
+  float* mask;
+  int64_t ldm;
   float p;
   uint64_t seed;
-  const float* gate;      // zero where gate(m,n) <= 0 (ld = ldc)
-  float* c;               // fp32 output
+  ActView gate;
+  float gate_scale;
+  float* c;               // fp32 output (STORE / WGRAD)
   int64_t ldc;
-  ActView out;            // alternative output view (when c == nullptr)
+  ActView out;            // FWD / GATE output view
 };
 
 constexpr int kTM = 64, kTN = 64, kTK = 16;
@@ -86,21 +88,23 @@ __global__ void __launch_bounds__(256) k_simt_gemm(Operand A, Operand B, int64_t
     for (int j = 0; j < 4; ++j) {
       int64_t n = n0 + tx * 4 + j;
       if (n >= N) continue;
-      float v = acc[i][j] * e.alpha;
-      if (e.bias) v += e.bias[n];
-      int64_t idx = m * e.ldc + n;
-      if (e.pre) e.pre[idx] = v;
-      if (e.relu) v = fmaxf(v, 0.f);
-      if (e.mask_gen) {
-        float mk = (uniform_hash(e.seed, (uint64_t)idx) >= e.p) ? 1.0f / (1.0f - e.p) : 0.f;
-        e.mask_out[idx] = mk;
-        v *= mk;
-      } else if (e.mask) {
-        v *= e.mask[idx];
+      float v = acc[i][j];
+      if (e.kind == DIPPM_GEMM_FWD) {
+        if (e.bias) v += e.bias[n];
+        if (e.relu) v = fmaxf(v, 0.f);
+        if (e.drop_mode == 1) {
+          v *= e.mask[m * e.ldm + n];
+        } else if (e.drop_mode == 2) {
+          float mk = uniform_hash(e.seed, (uint64_t)(m * e.ldm + n)) >= e.p ? 1.0f / (1.0f - e.p) : 0.f;
+          e.mask[m * e.ldm + n] = mk;
+          v *= mk;
+        }
+        act_store(e.out, m, n, v);
+      } else if (e.kind == DIPPM_GEMM_GATE) {
+        act_store(e.out, m, n, act_load(e.gate, m, n) > 0.f ? v * e.gate_scale : 0.f);
+      } else {
+        e.c[m * e.ldc + n] = v;
       }
-      if (e.gate) v = e.gate[idx] > 0.f ? v : 0.f;
-      if (e.c) e.c[idx] = v;
-      else act_store(e.out, m, n, v);
     }
   }
 }
@@ -113,29 +117,18 @@ static int launch_simt(const Operand& A, const Operand& B, int64_t M, int64_t N,
   return DIPPM_OK;
 }
 
-static Epi epi_plain(float* c, int64_t ldc) {
-  Epi e{};
-  e.alpha = 1.f;
-  e.c = c;
-  e.ldc = ldc;
-  return e;
-}
-
-static Operand dense(const float* p, int64_t sr, int64_t sc) {
-  Operand o{p, sr, sc, 0, DIPPM_DT_F32};
-  return o;
-}
-
-// fc3 (width -> 3) + optional de-normalisation and MIG pick: one warp per graph.
-__global__ void k_fc3(const float* __restrict__ x3, int64_t G, int width, const float* __restrict__ w3,
-                      const float* __restrict__ b3, float* __restrict__ out, const double* __restrict__ norm,
-                      double* __restrict__ y_pred, int8_t* __restrict__ mig, int* nonfinite) {
+// ---------------------------------------------------------------------------
+// fc3 (width -> 3) + de-normalisation (gnn.py:93-94) + MIG pick (mig.py:32-45):
+// one warp per graph.
+__global__ void k_fc3(ActView x3, int64_t G, int width, const float* __restrict__ w3, const float* __restrict__ b3,
+                      float* __restrict__ out, const double* __restrict__ norm, double* __restrict__ y_pred,
+                      int8_t* __restrict__ mig, int* nonfinite) {
   int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (g >= G) return;
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
   for (int j = lane; j < width; j += 32) {
-    float x = x3[g * width + j];
+    float x = act_load(x3, g, j);
     s0 = fmaf(x, w3[j * 3 + 0], s0);
     s1 = fmaf(x, w3[j * 3 + 1], s1);
     s2 = fmaf(x, w3[j * 3 + 2], s2);
@@ -150,7 +143,7 @@ __global__ void k_fc3(const float* __restrict__ x3, int64_t G, int width, const 
     float o3[3] = {s0 + b3[0], s1 + b3[1], s2 + b3[2]};
     for (int k = 0; k < 3; ++k) out[g * 3 + k] = o3[k];
     if (y_pred) {
-      for (int k = 0; k < 3; ++k) y_pred[g * 3 + k] = (double)o3[k] * norm[3 + k] + norm[k];  // gnn.py:93-94
+      for (int k = 0; k < 3; ++k) y_pred[g * 3 + k] = (double)o3[k] * norm[3 + k] + norm[k];
       double mem = y_pred[g * 3 + 1];
       if (!isfinite(mem)) {
         atomicExch(nonfinite, 1);
@@ -159,6 +152,75 @@ __global__ void k_fc3(const float* __restrict__ x3, int64_t G, int width, const 
         mig[g] = (int8_t)mig_rule(mem);
       }
     }
+  }
+}
+
+// fc3 backward fused with the fc2 ReLU/dropout gate (gnn.py:293-298):
+//   dW3[j,k] = sum_g x3[g,j] d3[g,k];  db3[k] = sum_g d3[g,k]
+//   d2[g,j]  = (sum_k d3[g,k] W3[j,k]) * (x3[g,j] > 0 ? keep_scale : 0)
+//   db2[j]   = sum_g d2[g,j]
+// Block: 32 columns x 8 graph groups; fixed-order reductions (deterministic).
+__global__ void __launch_bounds__(256) k_fc3_backward(ActView x3, int64_t G, int width, const float* __restrict__ w3,
+                                                      const float* __restrict__ d3, float keep_scale,
+                                                      float* __restrict__ gw3, float* __restrict__ gb3, ActView d2,
+                                                      float* __restrict__ gb2) {
+  __shared__ float s[8][32][5];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, ab = 0.f;
+  if (j < width) {
+    const float w0 = w3[j * 3 + 0], w1 = w3[j * 3 + 1], w2 = w3[j * 3 + 2];
+    for (int64_t g = ty; g < G; g += 8) {
+      const float x = act_load(x3, g, j);
+      const float e0 = d3[g * 3 + 0], e1 = d3[g * 3 + 1], e2 = d3[g * 3 + 2];
+      a0 = fmaf(x, e0, a0);
+      a1 = fmaf(x, e1, a1);
+      a2 = fmaf(x, e2, a2);
+      const float dx = e0 * w0 + e1 * w1 + e2 * w2;
+      const float dv = x > 0.f ? dx * keep_scale : 0.f;
+      act_store(d2, g, j, dv);
+      ab += dv;
+    }
+  }
+  s[ty][tx][0] = a0;
+  s[ty][tx][1] = a1;
+  s[ty][tx][2] = a2;
+  s[ty][tx][3] = ab;
+  __syncthreads();
+  if (ty == 0 && j < width) {
+    float r0 = 0.f, r1 = 0.f, r2 = 0.f, rb = 0.f;
+    for (int q = 0; q < 8; ++q) {
+      r0 += s[q][tx][0];
+      r1 += s[q][tx][1];
+      r2 += s[q][tx][2];
+      rb += s[q][tx][3];
+    }
+    gw3[j * 3 + 0] = r0;
+    gw3[j * 3 + 1] = r1;
+    gw3[j * 3 + 2] = r2;
+    gb2[j] = rb;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    float b = 0.f;
+    for (int64_t g = 0; g < G; ++g) b += d3[g * 3 + threadIdx.x];
+    gb3[threadIdx.x] = b;
+  }
+}
+
+// Column sums of an activation view [rows, cols] (fixed order): 32 columns x 8 row groups per block.
+__global__ void __launch_bounds__(256) k_colsum_act(ActView a, int64_t rows, int cols, float* __restrict__ out) {
+  __shared__ float s[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  float acc = 0.f;
+  if (c < cols)
+    for (int64_t r = ty; r < rows; r += 8) acc += act_load(a, r, c);
+  s[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float t = 0.f;
+    for (int q = 0; q < 8; ++q) t += s[q][tx];
+    out[c] = t;
   }
 }
 
@@ -178,7 +240,7 @@ __global__ void k_huber(const float* __restrict__ out, const float* __restrict__
       bool quad = a <= delta;
       le += quad ? 0.5 * r * r : delta * (a - 0.5 * delta);
       double gr = quad ? r : delta * (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0));
-      dout[g * 3 + k] = (float)(gr / 3.0 / (double)G);
+      if (dout) dout[g * 3 + k] = (float)(gr / 3.0 / (double)G);
       double den = pred * norm[3 + k] + norm[k];
       ape[k] += fabs(den - y) / fabs(y);
     }
@@ -198,68 +260,37 @@ __global__ void k_huber(const float* __restrict__ out, const float* __restrict__
   }
 }
 
-__global__ void k_colsum(const float* __restrict__ d, int64_t rows, int cols, float* __restrict__ out) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s = 0.f;
-  for (int64_t r = 0; r < rows; ++r) s += d[r * cols + c];
-  out[c] = s;
-}
-
-struct HeadOffsets {
-  int64_t w1, b1, w2, b2, w3, b3, total;
-};
-static HeadOffsets head_offsets(int width) {
-  HeadOffsets o;
-  int64_t in1 = width + kStaticWidth;
-  o.w1 = 0;
-  o.b1 = o.w1 + in1 * width;
-  o.w2 = o.b1 + width;
-  o.b2 = o.w2 + (int64_t)width * width;
-  o.w3 = o.b2 + width;
-  o.b3 = o.w3 + (int64_t)width * 3;
-  o.total = o.b3 + 3;
-  return o;
-}
-
 }  // namespace dippm
 
 using namespace dippm;
 
 extern "C" {
 
-int32_t dippm_head_forward(const float* u, int64_t G, int32_t width, const float* head_w, float* cache, float* masks,
-                           int32_t mask_mode, float dropout_p, uint64_t seed, float* out_norm, const double* norm,
-                           double* y_pred, int8_t* mig, int32_t* nonfinite, void* stream) {
-  DIPPM_ARG_CHECK(G >= 1 && width >= 1, "head_forward: bad shape");
-  DIPPM_ARG_CHECK(mask_mode >= 0 && mask_mode <= 2, "head_forward: bad mask_mode");
-  DIPPM_ARG_CHECK(mask_mode == 0 || masks, "head_forward: masks buffer required in train mode");
-  cudaStream_t s = (cudaStream_t)stream;
-  HeadOffsets o = head_offsets(width);
-  const int64_t in1 = width + kStaticWidth;
-  const int64_t GW = G * width;
-  float *a1 = cache, *x2 = cache + GW, *a2 = cache + 2 * GW, *x3 = cache + 3 * GW;
-  for (int layer = 0; layer < 2; ++layer) {
-    const float* x = layer == 0 ? u : x2;
-    int64_t K = layer == 0 ? in1 : width;
-    Epi e = epi_plain(layer == 0 ? x2 : x3, width);
-    e.bias = head_w + (layer == 0 ? o.b1 : o.b2);
-    e.pre = layer == 0 ? a1 : a2;
-    e.relu = 1;
-    float* mk = masks ? masks + layer * GW : nullptr;
-    if (mask_mode == 1) e.mask = mk;
-    if (mask_mode == 2) {
-      e.mask_gen = 1;
-      e.mask_out = mk;
-      e.p = dropout_p;
-      e.seed = seed * 2 + layer;
-    }
-    int st = launch_simt(dense(x, K, 1), dense(head_w + (layer == 0 ? o.w1 : o.w2), width, 1), G, width, K, e, s);
-    if (st) return st;
-  }
-  k_fc3<<<ceil_div_i(G * 32, 256), 256, 0, s>>>(x3, G, width, head_w + o.w3, head_w + o.b3, out_norm, norm, y_pred,
-                                              mig, nonfinite);
+int32_t dippm_fc3_forward(dippm_act_t x3, int64_t G, int32_t width, const float* w3, const float* b3, float* out_norm,
+                          const double* norm, double* y_pred, int8_t* mig, int32_t* nonfinite, void* stream) {
+  DIPPM_ARG_CHECK(G >= 1 && width >= 1, "fc3_forward: bad shape");
+  DIPPM_ARG_CHECK(!y_pred || (mig && nonfinite && norm), "fc3_forward: y_pred needs norm, mig, nonfinite");
+  k_fc3<<<ceil_div_i(G * 32, 256), 256, 0, (cudaStream_t)stream>>>(make_view(x3), G, width, w3, b3, out_norm, norm,
+                                                                  y_pred, mig, nonfinite);
   DIPPM_LAUNCH_CHECK("k_fc3");
+  return DIPPM_OK;
+}
+
+int32_t dippm_fc3_backward(dippm_act_t x3, int64_t G, int32_t width, const float* w3, const float* dout,
+                           float keep_scale, float* grad_w3, float* grad_b3, dippm_act_t d2, float* grad_b2,
+                           void* stream) {
+  DIPPM_ARG_CHECK(G >= 1 && width >= 1, "fc3_backward: bad shape");
+  k_fc3_backward<<<ceil_div_i(width, 32), 256, 0, (cudaStream_t)stream>>>(make_view(x3), G, width, w3, dout,
+                                                                          keep_scale, grad_w3, grad_b3,
+                                                                          make_view(d2), grad_b2);
+  DIPPM_LAUNCH_CHECK("k_fc3_backward");
+  return DIPPM_OK;
+}
+
+int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, void* stream) {
+  DIPPM_ARG_CHECK(rows >= 1 && cols >= 1, "colsum_act: bad shape");
+  k_colsum_act<<<ceil_div_i(cols, 32), 256, 0, (cudaStream_t)stream>>>(make_view(a), rows, cols, out);
+  DIPPM_LAUNCH_CHECK("k_colsum_act");
   return DIPPM_OK;
 }
 
@@ -268,52 +299,6 @@ int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t G, const 
   DIPPM_ARG_CHECK(G >= 1 && delta > 0, "huber: bad args");
   k_huber<<<1, 256, 0, (cudaStream_t)stream>>>(out_norm, y_raw, G, norm, delta, dout, loss_out);
   DIPPM_LAUNCH_CHECK("k_huber");
-  return DIPPM_OK;
-}
-
-size_t dippm_head_scratch_floats(int64_t G, int32_t width) { return (size_t)(2 * G * width); }
-
-int32_t dippm_head_backward(const float* u, int64_t G, int32_t width, const float* head_w, const float* cache,
-                            const float* masks, int32_t use_masks, const float* dout, float* grads_head, float* du,
-                            float* scratch, void* stream) {
-  DIPPM_ARG_CHECK(G >= 1 && width >= 1, "head_backward: bad shape");
-  cudaStream_t s = (cudaStream_t)stream;
-  HeadOffsets o = head_offsets(width);
-  const int64_t in1 = width + kStaticWidth;
-  const int64_t GW = G * width;
-  const float *a1 = cache, *x2 = cache + GW, *a2 = cache + 2 * GW, *x3 = cache + 3 * GW;
-  float* d2 = scratch;       // [G, width]
-  float* d1 = scratch + GW;  // [G, width]
-  int st;
-  // fc3: dW3 = x3^T d3, db3 = sum d3, then d2 = (d3 @ W3^T) * mask2 * (a2 > 0)
-  st = launch_simt(dense(x3, 1, width), dense(dout, 3, 1), width, 3, G, epi_plain(grads_head + o.w3, 3), s);
-  if (st) return st;
-  k_colsum<<<1, 32, 0, s>>>(dout, G, 3, grads_head + o.b3);
-  {
-    Epi e = epi_plain(d2, width);
-    if (use_masks) e.mask = masks + GW;
-    e.gate = a2;
-    st = launch_simt(dense(dout, 3, 1), dense(head_w + o.w3, 1, 3), G, width, 3, e, s);
-    if (st) return st;
-  }
-  // fc2
-  st = launch_simt(dense(x2, 1, width), dense(d2, width, 1), width, width, G, epi_plain(grads_head + o.w2, width), s);
-  if (st) return st;
-  k_colsum<<<ceil_div_i(width, 128), 128, 0, s>>>(d2, G, width, grads_head + o.b2);
-  {
-    Epi e = epi_plain(d1, width);
-    if (use_masks) e.mask = masks;
-    e.gate = a1;
-    st = launch_simt(dense(d2, width, 1), dense(head_w + o.w2, 1, width), G, width, width, e, s);
-    if (st) return st;
-  }
-  // fc1
-  st = launch_simt(dense(u, 1, in1), dense(d1, width, 1), in1, width, G, epi_plain(grads_head + o.w1, width), s);
-  if (st) return st;
-  k_colsum<<<ceil_div_i(width, 128), 128, 0, s>>>(d1, G, width, grads_head + o.b1);
-  st = launch_simt(dense(d1, width, 1), dense(head_w + o.w1, 1, width), G, in1, width, epi_plain(du, in1), s);
-  if (st) return st;
-  DIPPM_LAUNCH_CHECK_N(3, "head_backward");
   return DIPPM_OK;
 }
 
@@ -338,30 +323,35 @@ int32_t dippm_gemm_simt_impl(const dippm_gemm_args_t* a, cudaStream_t s) {
   };
   Operand A = operand(a->a, (int)a->a_mn_major, false);
   Operand B = operand(a->b, (int)a->b_mn_major, true);
-  if (a->kind == DIPPM_GEMM_FWD) {
-    Epi e{};
-    e.alpha = 1.f;
-    e.bias = a->bias;
-    e.relu = (int)a->relu;
-    e.out = make_view(a->out);
-    return launch_simt(A, B, a->M, a->N, a->K, e, s);
-  }
-  if (a->kind == DIPPM_GEMM_STORE) return launch_simt(A, B, a->M, a->N, a->K, epi_plain(a->c, a->ldc), s);
-  // WGRAD: reduction over K split in `splits` chunks of whole 64-row blocks.
+  Epi e{};
+  e.kind = (int)a->kind;
+  e.bias = a->bias;
+  e.relu = (int)a->relu;
+  e.drop_mode = (int)a->drop_mode;
+  e.mask = a->mask;
+  e.ldm = a->ldm;
+  e.p = (float)a->drop_p;
+  e.seed = a->seed;
+  e.gate = make_view(a->gate);
+  e.gate_scale = (float)a->gate_scale;
+  e.c = a->c;
+  e.ldc = a->ldc;
+  e.out = make_view(a->out);
+  if (a->kind != DIPPM_GEMM_WGRAD) return launch_simt(A, B, a->M, a->N, a->K, e, s);
+  // WGRAD: reduction over K split in `splits` contiguous chunks.
   int64_t splits = a->splits < 1 ? 1 : a->splits;
-  int64_t kb = ceil_div_i(a->K, 64);
-  int64_t per = (kb + splits - 1) / splits;
   for (int64_t sp = 0; sp < splits; ++sp) {
-    int64_t k0 = sp * per * 64, k1 = std::min<int64_t>(a->K, (sp + 1) * per * 64);
-    float* c = a->c + sp * a->M * a->ldc;
+    int64_t k0 = sp * a->K / splits, k1 = (sp + 1) * a->K / splits;
+    Epi es = e;
+    es.c = a->c + sp * a->M * a->ldc;
     if (k1 <= k0) {
-      DIPPM_CUDA_CHECK(cudaMemsetAsync(c, 0, sizeof(float) * a->M * a->ldc, s));
+      DIPPM_CUDA_CHECK(cudaMemsetAsync(es.c, 0, sizeof(float) * a->M * a->ldc, s));
       continue;
     }
     Operand As = A, Bs = B;
     As.p = (const char*)A.p + k0 * A.sc * (A.dtype == DIPPM_DT_BF16 ? 2 : 4);
     Bs.p = (const char*)B.p + k0 * B.sr * (B.dtype == DIPPM_DT_BF16 ? 2 : 4);
-    int st = launch_simt(As, Bs, a->M, a->N, k1 - k0, epi_plain(c, a->ldc), s);
+    int st = launch_simt(As, Bs, a->M, a->N, k1 - k0, es, s);
     if (st) return st;
   }
   return DIPPM_OK;

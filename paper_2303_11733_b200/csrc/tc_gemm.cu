@@ -28,7 +28,7 @@ namespace tc {
 
 constexpr int kThreads = 192;
 constexpr int kBM = 128;
-enum { EPI_FWD = 0, EPI_STORE = 1, EPI_PARTIAL = 2 };
+enum { EPI_FWD = 0, EPI_STORE = 1, EPI_PARTIAL = 2, EPI_GATE = 3, EPI_FWD_DROP = 4 };
 
 struct Params {
   int64_t M, N, K;
@@ -39,6 +39,13 @@ struct Params {
   ActView out;
   float* c;
   int64_t ldc;
+  ActView gate;      // EPI_GATE: out = gate > 0 ? acc * gate_scale : 0
+  float gate_scale;
+  int drop_mode;     // EPI_FWD dropout: 0 none, 1 multiply mask[], 2 generate into mask[]
+  float* mask;
+  int64_t ldm;
+  float drop_p;
+  uint64_t seed;
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -288,15 +295,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
         if (row < p.M) {
           const int n = n0 + ch * 32;
-          if constexpr (kEpi == EPI_FWD) {
+          if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
+            float bv[32];
+            if (p.bias) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + g);
+                bv[4 * g] = b4.x; bv[4 * g + 1] = b4.y; bv[4 * g + 2] = b4.z; bv[4 * g + 3] = b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) bv[i] = 0.f;
+            }
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               float v[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                float x = __uint_as_float(raw[g * 8 + i]) + __ldg(p.bias + n + g * 8 + i);
+                const float x = __uint_as_float(raw[g * 8 + i]) + bv[g * 8 + i];
                 v[i] = p.relu ? fmaxf(x, 0.f) : x;
               }
+              if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
+#pragma unroll 1
+                for (int i = 0; i < 8; ++i) {
+                  const int64_t idx = row * p.ldm + n + g * 8 + i;
+                  if (p.drop_mode == 1) {
+                    v[i] *= p.mask[idx];
+                  } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
+                    const float mk = uniform_hash(p.seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
+                    p.mask[idx] = mk;
+                    v[i] *= mk;
+                  }
+                }
+              }
+              act_store8(p.out, row, n + g * 8, v);
+            }
+          } else if constexpr (kEpi == EPI_GATE) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float v[8], gt[8];
+              act_load8(p.gate, row, n + g * 8, gt);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = gt[i] > 0.f ? __uint_as_float(raw[g * 8 + i]) * p.gate_scale : 0.f;
               act_store8(p.out, row, n + g * 8, v);
             }
           } else {
@@ -397,6 +437,13 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.out = make_view(a->out);
   p.c = a->c;
   p.ldc = a->ldc;
+  p.gate = make_view(a->gate);
+  p.gate_scale = (float)a->gate_scale;
+  p.drop_mode = (int)a->drop_mode;
+  p.mask = a->mask;
+  p.ldm = a->ldm;
+  p.drop_p = (float)a->drop_p;
+  p.seed = a->seed;
   const int total = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::min(total, num_sms());
   kern<<<grid, kThreads, Cf::kSmemBytes, s>>>(ma, mb, p);
@@ -404,19 +451,27 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   return DIPPM_OK;
 }
 
-template <int kFmt, bool kMN, int kEpi>
+// BN choice: wide tiles when M supplies enough tiles to fill the GPU, narrower
+// ones for short problems (the FC head, M = #graphs) so more CTAs run.
+template <int kFmt, bool kAMN, bool kBMN, int kEpi>
 static int run_bn(const dippm_gemm_args_t* a, cudaStream_t s) {
-  if (a->N % 256 == 0) return run<kFmt, kMN, kMN, 256, kEpi>(a, s);
-  if (a->N % 128 == 0) return run<kFmt, kMN, kMN, 128, kEpi>(a, s);
-  return run<kFmt, kMN, kMN, 64, kEpi>(a, s);
+  const int64_t m_tiles = ceil_div_i(a->M, kBM);
+  const bool narrow = kEpi != EPI_PARTIAL && m_tiles * (a->N / 256) < num_sms() / 2;
+  if (a->N % 256 == 0 && !narrow) return run<kFmt, kAMN, kBMN, 256, kEpi>(a, s);
+  if (a->N % 128 == 0 && !(narrow && m_tiles * (a->N / 128) < num_sms() / 2))
+    return run<kFmt, kAMN, kBMN, 128, kEpi>(a, s);
+  return run<kFmt, kAMN, kBMN, 64, kEpi>(a, s);
 }
 
 template <int kFmt>
 static int dispatch(const dippm_gemm_args_t* a, cudaStream_t s) {
   switch (a->kind) {
-    case DIPPM_GEMM_FWD: return run_bn<kFmt, false, EPI_FWD>(a, s);
-    case DIPPM_GEMM_STORE: return run_bn<kFmt, false, EPI_STORE>(a, s);
-    default: return run_bn<kFmt, true, EPI_PARTIAL>(a, s);
+    case DIPPM_GEMM_FWD:
+      if (a->drop_mode) return run_bn<kFmt, false, true, EPI_FWD_DROP>(a, s);  // head fc1/fc2 in train mode
+      return a->b_mn_major ? run_bn<kFmt, false, true, EPI_FWD>(a, s) : run_bn<kFmt, false, false, EPI_FWD>(a, s);
+    case DIPPM_GEMM_GATE: return run_bn<kFmt, false, false, EPI_GATE>(a, s);
+    case DIPPM_GEMM_STORE: return run_bn<kFmt, false, false, EPI_STORE>(a, s);
+    default: return run_bn<kFmt, true, true, EPI_PARTIAL>(a, s);
   }
 }
 
@@ -445,9 +500,14 @@ extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void*
   DIPPM_ARG_CHECK(a->a.dtype == DIPPM_DT_BF16 || a->a.dtype == DIPPM_DT_TF32X3,
                   "gemm: tensor-core path needs bf16 or tf32x3 operands");
   DIPPM_ARG_CHECK(a->N % 64 == 0, "gemm: N=%lld must be a multiple of 64", (long long)a->N);
+  DIPPM_ARG_CHECK(a->kind >= DIPPM_GEMM_FWD && a->kind <= DIPPM_GEMM_GATE, "gemm: bad kind %lld",
+                  (long long)a->kind);
   const bool mn = a->kind == DIPPM_GEMM_WGRAD;
-  DIPPM_ARG_CHECK(mn == (a->a_mn_major != 0) && mn == (a->b_mn_major != 0),
-                  "gemm: FWD/STORE take K-major operands, WGRAD MN-major");
+  DIPPM_ARG_CHECK(mn == (a->a_mn_major != 0) && (mn == (a->b_mn_major != 0) || a->kind == DIPPM_GEMM_FWD),
+                  "gemm: FWD takes K-major A (B either), STORE/GATE K-major, WGRAD MN-major");
+  DIPPM_ARG_CHECK(a->drop_mode == 0 || (a->mask && a->kind == DIPPM_GEMM_FWD && a->b_mn_major && a->drop_p >= 0 &&
+                                        a->drop_p < 1),
+                  "gemm: dropout needs FWD with MN-major B, a mask buffer and 0 <= p < 1");
   const int bk = a->a.dtype == DIPPM_DT_BF16 ? 64 : 32;
   DIPPM_ARG_CHECK(mn || a->K % bk == 0, "gemm: K=%lld must be a multiple of %d", (long long)a->K, bk);
   if (a->a.dtype == DIPPM_DT_BF16) return tc::dispatch<1>(a, s);

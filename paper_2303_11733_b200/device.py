@@ -7,16 +7,19 @@ host buffers only; every FLOP runs in libdippm_b200.so.
 HBM layout (hidden H padded to Hp = ceil64(H); padded weights are zero and
 stay exactly zero under Adam, so results equal the unpadded network):
   params  fp64 [P]   master weights, reference order gnn.py:488-491, with
-                     sage{l}.w_self/w_neigh adjacent -> W_cat_l [2 d_l, Hp]
+                     sage{l}.w_self/w_neigh adjacent -> W_cat_l [2 d_l, Hp];
+                     fc1.w padded to [Hp+64, Hp] (fs rows at Hp..Hp+4)
   m, v    fp64 [P]   Adam moments (numerics.py:76-90)
-  grads   fp32 [P]   same offsets
-  p32     fp32 [P]   compute copy (biases, FC head)
-  wt[l]   [Hp, 2 d_l]   K-major W_cat^T, forward B operand (bf16 / tf32 hi|lo)
-  wb[l]   [2 d_l, Hp]   K-major W_cat, dgrad B operand (layers 2, 3)
+  grads   fp32 [P]   same offsets;  p32 fp32 [P] compute copy (biases, fc3)
+  Wf[l]   [2 d_l, Hp]  W_cat natural layout: forward B operand, MN-major
+  Wd[l]   [Hp, 2Hp]    [W_self | W_neigh] rows: dgrad B operand, K-major (l=2,3)
+  W1h     [Hp+64, Hp], W2h [Hp, Hp]: head operands (FWD MN-major, dgrad K-major)
+  (all GEMM copies in the compute dtype, refreshed inside the Adam kernel)
 Per batch (N nodes, G graphs):
-  A1 [N, 64]  = [X | agg X]         A2 [N, 2Hp] = [h1 | agg h1]
-  A3 [N, 2Hp] = [h2 | agg h2]       H3 [N, Hp]  = h3
-  u  [G, Hp+5] = [mean_g h3 | fs_norm]
+  A1 [N, 64]  = [X | agg X]        A2 [N, 2Hp] = [h1 | agg h1]
+  A3 [N, 2Hp] = [h2 | agg h2]      H3 [N, Hp]  = h3
+  u  [G, Hp+64] = [mean_g h3 | fs_norm | 0]   x2, x3 [G, Hp] head activations
+  backward: Bl [N, 2Hp] = [dz_l | agg^T dz_l]  (two ping-pong buffers)
 Node rows of a graph are contiguous (graph_ptr), edges carry global ids.
 """
 
@@ -28,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Act, GemmArgs, DT_BF16, DT_F32, DT_TF32X3, GEMM_FWD, GEMM_STORE, GEMM_WGRAD
+from ._lib import Act, GemmArgs, DT_BF16, DT_F32, DT_TF32X3, GEMM_FWD, GEMM_GATE, GEMM_STORE, GEMM_WGRAD
 from .errors import EmptyGraph, ShapeMismatch
 
 FEATURE_WIDTH = 32   # featurize.py:38
@@ -94,7 +97,8 @@ class Layout:
         shapes = []
         for i, d in enumerate(self.d_in, start=1):
             shapes += [(f"sage{i}.w_self", (d, hp)), (f"sage{i}.w_neigh", (d, hp)), (f"sage{i}.bias", (hp,))]
-        shapes += [("fc1.w", (hp + STATIC_WIDTH, hp)), ("fc1.b", (hp,)), ("fc2.w", (hp, hp)), ("fc2.b", (hp,)),
+        self.u_width = hp + 64  # [r | fs | 0]: K of fc1 aligned to the tensor-core k-block
+        shapes += [("fc1.w", (self.u_width, hp)), ("fc1.b", (hp,)), ("fc2.w", (hp, hp)), ("fc2.b", (hp,)),
                    ("fc3.w", (hp, 3)), ("fc3.b", (3,))]
         self.shapes = dict(shapes)
         self.offsets = {}
@@ -246,37 +250,41 @@ def build_batch_csr(b: Batch) -> Batch:
 # engine
 
 class Workspace:
-    """Per-batch activation / gradient buffers (sized for N nodes, G graphs)."""
+    """Per-batch activation / gradient buffers (sized for up to N nodes, G graphs)."""
 
     def __init__(self, eng: "Engine", N: int, G: int, train: bool):
         dev, dt, hp = eng.device, eng.dtype, eng.L.hp
         f32 = dict(dtype=torch.float32, device=dev)
+        lib = _lib.load()
         self.N, self.G = N, G
         self.A = [ActBuf(N, 2 * FEATURE_WIDTH, dt, dev), ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
         self.H3 = ActBuf(N, hp, dt, dev)
-        self.u = torch.empty(G, hp + STATIC_WIDTH, **f32)
-        self.cache = torch.empty(4, G, hp, **f32)
+        self.u = ActBuf(G, eng.L.u_width, dt, dev)
+        self.x2 = ActBuf(G, hp, dt, dev)
+        self.x3 = ActBuf(G, hp, dt, dev)
         self.masks = torch.ones(2, G, hp, **f32)
         self.out = torch.empty(G, 3, **f32)
         self.y_pred = torch.empty(G, 3, dtype=torch.float64, device=dev)
         self.mig = torch.empty(G, dtype=torch.int8, device=dev)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.loss = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.train = train
         if train:
             self.dout = torch.empty(G, 3, **f32)
-            self.du = torch.empty(G, hp + STATIC_WIDTH, **f32)
-            self.head_scratch = torch.empty(_lib.load().dippm_head_scratch_floats(G, hp), **f32)
-            self.dA = torch.empty(N, 2 * hp, **f32)
-            self.dz = [ActBuf(N, hp, dt, dev), ActBuf(N, hp, dt, dev)]
-            self.colsum = torch.empty(_lib.load().dippm_colsum_blocks(N), hp, **f32)
-            lib = _lib.load()
-            s_max = max(lib.dippm_wgrad_splits(hp, 2 * d, N) for d in eng.L.d_in)
+            self.d2 = ActBuf(G, hp, dt, dev)
+            self.d1 = ActBuf(G, hp, dt, dev)
+            self.du = torch.empty(G, hp, **f32)
+            self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+            self.colsum = torch.empty(lib.dippm_colsum_blocks(N), hp, **f32)
             self.splits = [lib.dippm_wgrad_splits(hp, 2 * d, N) for d in eng.L.d_in]
-            self.splitk = torch.empty(s_max * hp * 2 * hp, **f32)
+            self.head_splits = [lib.dippm_wgrad_splits(hp, hp, G), lib.dippm_wgrad_splits(hp, eng.L.u_width, G)]
+            widest = max(max(s * 2 * d for s, d in zip(self.splits, eng.L.d_in)),
+                         self.head_splits[0] * hp, self.head_splits[1] * eng.L.u_width)
+            self.splitk = torch.empty(widest * hp, **f32)
 
 
 class Engine:
-    """Device-resident DIPPM GraphSAGE network (weights, Adam state, packs)."""
+    """Device-resident DIPPM GraphSAGE network (weights, Adam state, GEMM operand copies)."""
 
     def __init__(self, hidden: int, precision: str = "fp32", device=None, backend: str = "tc"):
         if precision not in PRECISIONS:
@@ -284,9 +292,9 @@ class Engine:
         if backend not in BACKENDS:
             raise ValueError(f"backend must be one of {sorted(BACKENDS)}, got {backend!r}")
         self.device = require_device(device)
-        self.L = Layout(hidden)
+        self.L = L = Layout(hidden)
         self.precision, self.dtype, self.backend = precision, PRECISIONS[precision], BACKENDS[backend]
-        n = self.L.total
+        n = L.total
         f64 = dict(dtype=torch.float64, device=self.device)
         self.params = torch.zeros(n, **f64)
         self.m = torch.zeros(n, **f64)
@@ -295,9 +303,20 @@ class Engine:
         self.p32 = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.norm = torch.zeros(16, **f64)
         self.t = 0
-        hp = self.L.hp
-        self.wt = [ActBuf(hp, 2 * d, self.dtype, self.device) for d in self.L.d_in]
-        self.wb = [None] + [ActBuf(2 * d, hp, self.dtype, self.device) for d in self.L.d_in[1:]]
+        hp, dt, d = L.hp, self.dtype, self.device
+        self.Wf = [ActBuf(2 * di, hp, dt, d) for di in L.d_in]
+        self.Wd = [None] + [ActBuf(di, 2 * hp, dt, d) for di in L.d_in[1:]]
+        self.W1h = ActBuf(L.u_width, hp, dt, d)
+        self.W2h = ActBuf(hp, hp, dt, d)
+        segs = []
+        for i, di in enumerate(L.d_in):
+            segs.append(_lib.PackSeg(L.offsets[f"sage{i + 1}.w_self"], 2 * di, hp, 0, self.Wf[i].view()))
+            if i > 0:
+                segs.append(_lib.PackSeg(L.offsets[f"sage{i + 1}.w_self"], di, hp, 0, self.Wd[i].view()))
+                segs.append(_lib.PackSeg(L.offsets[f"sage{i + 1}.w_neigh"], di, hp, hp, self.Wd[i].view()))
+        segs.append(_lib.PackSeg(L.offsets["fc1.w"], L.u_width, hp, 0, self.W1h.view()))
+        segs.append(_lib.PackSeg(L.offsets["fc2.w"], hp, hp, 0, self.W2h.view()))
+        self._segs = (_lib.PackSeg * len(segs))(*segs)
         self.launches = 0
         self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
 
@@ -322,40 +341,42 @@ class Engine:
         self.v.zero_()
         self.t = 0
 
-    def get_params(self) -> dict:
-        host = self.params.cpu().numpy()
-        return {name: self.L.unpad(name, host[off:off + int(np.prod(self.L.shapes[name]))].reshape(self.L.shapes[name]))
+    def _unpack(self, flat: np.ndarray) -> dict:
+        return {name: self.L.unpad(name, flat[off:off + int(np.prod(self.L.shapes[name]))].reshape(self.L.shapes[name]))
                 for name, off in self.L.offsets.items()}
+
+    def get_params(self) -> dict:
+        return self._unpack(self.params.cpu().numpy())
 
     def get_grads(self) -> dict:
-        host = self.grads.double().cpu().numpy()
-        return {name: self.L.unpad(name, host[off:off + int(np.prod(self.L.shapes[name]))].reshape(self.L.shapes[name]))
-                for name, off in self.L.offsets.items()}
+        return self._unpack(self.grads.double().cpu().numpy())
+
+    def _adam_pack(self, do_adam: int, lr=0.0, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale=1.0) -> None:
+        _lib.call("dippm_adam_pack", _p(self.params), _p(self.m), _p(self.v), _p(self.grads), grad_scale,
+                  self.L.total, self.t, lr, beta1, beta2, eps, do_adam, _p(self.p32), self._segs, len(self._segs),
+                  _stream())
+        self.launches += 1
 
     def refresh(self) -> None:
-        """Pack fp64 masters into the fp32 copy and the GEMM operand layouts."""
-        s = _stream()
-        L = self.L
-        n = L.total
-        _lib.call("dippm_pack", _p(self.params), 1, n, 0, Act(self.p32.data_ptr(), n, 0, DT_F32), s)
-        for i, d in enumerate(L.d_in):
-            w = self.params[L.offsets[f"sage{i + 1}.w_self"]:]
-            _lib.call("dippm_pack", _p(w), 2 * d, L.hp, 1, self.wt[i].view(), s)
-            if i > 0:
-                _lib.call("dippm_pack", _p(w), 2 * d, L.hp, 0, self.wb[i].view(), s)
-        self.launches += 1 + len(L.d_in) + len(L.d_in) - 1
+        """Refresh the fp32 copy and every GEMM operand copy from the fp64 masters."""
+        self._adam_pack(0)
 
     def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale: float = 1.0) -> None:
-        """numerics.adam_step over all 15 tensors (one launch), then repack."""
+        """numerics.adam_step over all 15 tensors + operand refresh: one launch."""
         self.t += 1
-        _lib.call("dippm_adam", _p(self.params), _p(self.m), _p(self.v), _p(self.grads), grad_scale, self.L.total, self.t,
-                  lr, beta1, beta2, eps, _stream())
-        self.launches += 1
-        self.refresh()
+        self._adam_pack(1, lr, beta1, beta2, eps, grad_scale)
+
+    def _f32(self, name: str) -> int:
+        return self.p32.data_ptr() + 4 * self.L.offsets[name]
+
+    def _g32(self, name: str) -> int:
+        return self.grads.data_ptr() + 4 * self.L.offsets[name]
 
     # -- kernels --------------------------------------------------------------
-    def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1):
-        args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits)
+    def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1,
+              gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0):
+        args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits, gate, gate_scale,
+                        drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1))
         if self.gemm_hook is not None:
             self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
@@ -363,13 +384,17 @@ class Engine:
             self.gemm_hook("post", 2.0 * M * N * K)
         self.launches += 1
 
+    def _wgrad(self, dz: Act, x: Act, rows: int, width: int, splits: int, ws: Workspace, out_name: str) -> None:
+        """grads[out_name] (as [width, Hp]) = x^T @ dz over `rows` rows: split-K tcgen05 + fixed-order reduce."""
+        hp = self.L.hp
+        self._gemm(GEMM_WGRAD, hp, width, rows, dz, 1, x, 1, c=_p(ws.splitk), ldc=width, splits=splits)
+        _lib.call("dippm_splitk_reduce_t", _p(ws.splitk), splits, hp, width, 1.0, self._g32(out_name), hp, _stream())
+
     def forward(self, b: Batch, ws: Workspace, mask_mode: int = 0, dropout_p: float = 0.0, seed: int = 0,
                 predict: bool = True) -> None:
-        """Eval (mask_mode 0) or train-mode forward: K2 -> K3 x3, K4, K5."""
+        """Eval (mask_mode 0) or train-mode forward (1: masks in ws.masks, 2: generated):
+        K2 aggregation -> K3 GEMM x3, K4 pooling, K5 head (2 GEMMs + fc3)."""
         s, L, hp = _stream(), self.L, self.L.hp
-        P32 = self.p32
-        bias = lambda i: P32.data_ptr() + 4 * L.offsets[f"sage{i}.bias"]  # noqa: E731
-        # layer 1: A1 = [X | agg X]
         _lib.call("dippm_sage_aggregate", f32_act(b.x), ws.A[0].view(FEATURE_WIDTH), ws.A[0].view(0), b.N,
                   FEATURE_WIDTH, _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
         outs = [ws.A[1].view(0), ws.A[2].view(0), ws.H3.view(0)]
@@ -377,46 +402,50 @@ class Engine:
             if i > 0:
                 _lib.call("dippm_sage_aggregate", ws.A[i].view(0), ws.A[i].view(hp), NULL_ACT, b.N, hp,
                           _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
-            self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.wt[i].view(), 0,
-                       bias=bias(i + 1), relu=1, out=outs[i])
+            self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.Wf[i].view(), 1,
+                       bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i])
         _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
-                  _p(ws.u), s)
-        _lib.call("dippm_head_forward", _p(ws.u), b.G, hp, P32.data_ptr() + 4 * L.head_off, _p(ws.cache),
-                  _p(ws.masks), mask_mode, float(dropout_p), int(seed) & (2**64 - 1), _p(ws.out), _p(self.norm),
-                  _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None, _p(ws.nonfinite), s)
-        self.launches += 3 + 2 + 5
+                  ws.u.view(), s)
+        drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
+        for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
+            self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,
+                       out=out.view(), drop_mode=drop, mask=ws.masks[j].data_ptr(), ldm=hp, drop_p=dropout_p,
+                       seed=seed * 2 + j)
+        _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
+                  _p(self.norm), _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None,
+                  _p(ws.nonfinite), s)
+        self.launches += 3 + 1 + 1
 
     def loss(self, b: Batch, ws: Workspace, delta: float = 1.0) -> None:
-        _lib.call("dippm_huber", _p(ws.out), _p(b.y), b.G, _p(self.norm), float(delta), _p(ws.dout), _p(ws.loss),
-                  _stream())
+        _lib.call("dippm_huber", _p(ws.out), _p(b.y), b.G, _p(self.norm), float(delta),
+                  _p(ws.dout) if ws.train else None, _p(ws.loss), _stream())
         self.launches += 1
 
-    def backward(self, b: Batch, ws: Workspace, use_masks: bool) -> None:
-        """Head backward, readout backward, 3 x (WGRAD, DGRAD, transposed gather)."""
+    def backward(self, b: Batch, ws: Workspace, keep_scale: float = 1.0) -> None:
+        """Head backward (fc3 fused kernel, fc2/fc1 tcgen05 WGRAD/GATE/STORE), readout
+        backward, then per SAGE layer: agg^T + bias, WGRAD, gated dgrad GEMM."""
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
-        G32 = self.grads.data_ptr()
-        off = lambda name: G32 + 4 * L.offsets[name]  # noqa: E731
         lib = _lib.load()
         nblk = lib.dippm_colsum_blocks(N)
-        _lib.call("dippm_head_backward", _p(ws.u), b.G, hp, self.p32.data_ptr() + 4 * L.head_off, _p(ws.cache),
-                  _p(ws.masks), int(use_masks), _p(ws.dout), off("fc1.w"), _p(ws.du), _p(ws.head_scratch), s)
-        _lib.call("dippm_readout_backward", _p(ws.du), hp + STATIC_WIDTH, _p(b.graph_ptr), b.G, hp, ws.H3.view(0),
-                  ws.dz[0].view(), N, _p(ws.colsum), s)
-        _lib.call("dippm_reduce_rows", _p(ws.colsum), nblk, hp, hp, 1.0, off("sage3.bias"), s)
+        _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout), float(keep_scale),
+                  self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
+        self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws.head_splits[0], ws, "fc2.w")
+        self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
+                   gate=ws.x2.view(), gate_scale=keep_scale)
+        _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
+        self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws.head_splits[1], ws, "fc1.w")
+        self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
+        _lib.call("dippm_readout_backward", _p(ws.du), hp, _p(b.graph_ptr), b.G, hp, ws.H3.view(0),
+                  ws.B[0].view(0), N, s)
         cur = 0
         for i in (2, 1, 0):
-            width = 2 * L.d_in[i]
-            dz = ws.dz[cur]
-            S = ws.splits[i]
-            self._gemm(GEMM_WGRAD, hp, width, N, dz.view(), 1, ws.A[i].view(0), 1, c=_p(ws.splitk), ldc=width,
-                       splits=S)
-            _lib.call("dippm_splitk_reduce_t", _p(ws.splitk), S, hp, width, 1.0, off(f"sage{i + 1}.w_self"), hp, s)
-            if i == 0:
-                break
-            self._gemm(GEMM_STORE, N, width, hp, dz.view(), 0, self.wb[i].view(), 0, c=_p(ws.dA), ldc=width)
-            nxt = ws.dz[1 - cur]
-            _lib.call("dippm_sage_backward_gather", _p(ws.dA), width, hp, ws.A[i].view(0), nxt.view(), N,
-                      _p(b.t_rowptr), _p(b.t_col), _p(b.inv_deg), _p(ws.colsum), s)
-            _lib.call("dippm_reduce_rows", _p(ws.colsum), nblk, hp, hp, 1.0, off(f"sage{i}.bias"), s)
-            cur = 1 - cur
-        self.launches += 3 + 11 + 3 * 2 - 1
+            B = ws.B[cur]
+            _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
+                      _p(b.inv_deg), _p(ws.colsum), s)
+            _lib.call("dippm_reduce_rows", _p(ws.colsum), nblk, hp, hp, 1.0, self._g32(f"sage{i + 1}.bias"), s)
+            self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws.splits[i], ws, f"sage{i + 1}.w_self")
+            if i > 0:
+                self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
+                           out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0)
+                cur = 1 - cur
+        self.launches += 5 + 3 * 2

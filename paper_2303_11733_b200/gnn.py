@@ -276,8 +276,8 @@ def readout_mean(z: np.ndarray) -> np.ndarray:
     gp = torch.tensor([0, n], dtype=torch.int32, device=device)
     fs = torch.zeros(1, STATIC_WIDTH, dtype=torch.float32, device=device)
     norm = torch.tensor([0.0] * 6 + [0.0] * 5 + [1.0] * 5, dtype=torch.float64, device=device)
-    u = torch.empty(1, dp + STATIC_WIDTH, dtype=torch.float32, device=device)
-    _lib.call("dippm_pool_concat", f32_act(zt), gp.data_ptr(), 1, dp, fs.data_ptr(), norm.data_ptr(), u.data_ptr(),
+    u = torch.empty(1, dp + 8, dtype=torch.float32, device=device)
+    _lib.call("dippm_pool_concat", f32_act(zt), gp.data_ptr(), 1, dp, fs.data_ptr(), norm.data_ptr(), f32_act(u),
               dev._stream())
     return u[0, :d].double().cpu().numpy()
 
@@ -347,7 +347,7 @@ def backward(model, records, huber_delta: float = 1.0, precision: str = "fp32"):
     b, ws = _run_forward(eng, [r.encoding for r in records], [r.fs for r in records],
                          [r.target for r in records], train_buffers=True)
     eng.loss(b, ws, huber_delta)
-    eng.backward(b, ws, use_masks=False)
+    eng.backward(b, ws)
     return float(ws.loss[0].item()), eng.get_grads()
 
 
@@ -372,6 +372,7 @@ def _fit(train_records, val_records, config: TrainConfig):
     n = len(train_records)
     B = config.batch_size
     dropout = model.dropout_p > 0.0
+    keep = 1.0 / (1.0 - model.dropout_p) if dropout else 1.0
 
     if B == 1:
         batches = [upload_batch(*_records_arrays([r.encoding], [r.fs], [r.target]), device=eng.device)
@@ -394,7 +395,7 @@ def _fit(train_records, val_records, config: TrainConfig):
                 eng.forward(b, ws1, mask_mode=1 if dropout else 0, predict=False)
                 eng.loss(b, ws1, config.huber_delta)
                 acc.add_(ws1.loss)
-                eng.backward(b, ws1, use_masks=dropout)
+                eng.backward(b, ws1, keep_scale=keep)
                 eng.adam_step(config.lr)
         else:
             for s0 in range(0, n, B):
@@ -408,7 +409,7 @@ def _fit(train_records, val_records, config: TrainConfig):
                             seed=config.seed * 1000003 + step, predict=False)
                 eng.loss(b, ws, config.huber_delta)
                 acc.add_(ws.loss * torch.tensor([b.G, 1, 1, 1], dtype=torch.float64, device=eng.device))
-                eng.backward(b, ws, use_masks=dropout)
+                eng.backward(b, ws, keep_scale=keep)
                 eng.adam_step(config.lr)
         a = acc.cpu().numpy()
         if not np.all(np.isfinite(a)):

@@ -62,7 +62,7 @@ class BatchTrainer:
         eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 1000003 + self.steps,
                     predict=False)
         eng.loss(b, ws, self.delta)
-        eng.backward(b, ws, use_masks=mode != 0)
+        eng.backward(b, ws, keep_scale=1.0 / (1.0 - self.dropout_p) if mode else 1.0)
         if self.allreduce is not None:
             self.allreduce(eng.grads)          # sum of per-rank batch means
         eng.adam_step(self.lr, grad_scale=1.0 / self.world_size)

@@ -171,17 +171,134 @@ def test_pool_concat_and_mig_codes(golden):
     h = rng.normal(size=(gp[-1], 64)).astype(np.float32)
     fs = rng.normal(size=(G, 5)).astype(np.float32)
     norm = np.concatenate([np.zeros(6), rng.normal(size=5), rng.uniform(0.5, 2, 5)])
-    u = torch.empty(G, 69, device="cuda")
+    u = torch.full((G, 128), float("nan"), device="cuda")
     keep = [torch.from_numpy(a).cuda() for a in (h, gp, fs, norm)]  # hold the buffers across the launch
     _lib.call("dippm_pool_concat", dev.f32_act(keep[0]), keep[1].data_ptr(), G, 64, keep[2].data_ptr(),
-              keep[3].data_ptr(), u.data_ptr(), dev._stream())
+              keep[3].data_ptr(), dev.f32_act(u), dev._stream())
     got = u.cpu().numpy()
     for g in range(G):
         assert np.allclose(got[g, :64], h[gp[g]:gp[g + 1]].astype(np.float64).mean(0), atol=1e-6)
-        assert np.allclose(got[g, 64:], (fs[g] - norm[6:11]) / norm[11:16], atol=1e-6)
+        assert np.allclose(got[g, 64:69], (fs[g] - norm[6:11]) / norm[11:16], atol=1e-6)
+        assert np.all(got[g, 69:] == 0)
     alphas = torch.from_numpy(golden["mig_alpha"]).cuda()
     codes = torch.empty(len(alphas), dtype=torch.int8, device="cuda")
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("dippm_mig_codes", alphas.data_ptr(), 1, len(alphas), codes.data_ptr(), flag.data_ptr(), dev._stream())
     assert codes.cpu().numpy().tolist() == golden["mig_code"].tolist()
     assert int(flag.item()) == 0
+
+
+def _gemm(kind, M, N, K, a, a_mn, b, b_mn, backend=0, **kw):
+    f = dict(bias=None, relu=0, out=dev.NULL_ACT, c=None, ldc=0, splits=1, gate=dev.NULL_ACT, gate_scale=1.0,
+             drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0)
+    f.update(kw)
+    args = _lib.GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, f["bias"], f["relu"], f["out"], f["c"], f["ldc"],
+                         f["splits"], f["gate"], f["gate_scale"], f["drop_mode"], f["mask"], f["ldm"], f["drop_p"],
+                         f["seed"])
+    _lib.check(_lib.load().dippm_gemm(args, backend, dev._stream()))
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,N,K", [(1000, 512, 1024), (256, 512, 576), (3, 64, 64)])
+def test_fwd_mn_major_b_with_dropout(prec, M, N, K):
+    """Forward GEMM reading W in its natural [K, N] layout (MN-major B) with the
+    bias + ReLU + inverted-dropout epilogue; mode 2 writes the mask it used, mode 1
+    re-applies a given mask; tensor-core and SIMT backends agree."""
+    rng = np.random.default_rng(K + M)
+    dt = dev.PRECISIONS[prec]
+    A, a64, _ = _rand_act(M, K, dt, rng)
+    W, w64, _ = _rand_act(K, N, dt, rng, 0.05)
+    bias = torch.from_numpy(rng.normal(size=N).astype(np.float32)).cuda()
+    ref = np.maximum(a64 @ w64 + bias.double().cpu().numpy(), 0)
+    p = 0.3
+    outs = {}
+    for backend in (0, 1):
+        out = ActBuf(M, N, dev.DT_F32, "cuda")
+        mask = torch.full((M, N), -1.0, device="cuda")
+        _gemm(_lib.GEMM_FWD, M, N, K, A.view(), 0, W.view(), 1, backend, bias=bias.data_ptr(), relu=1,
+              out=out.view(), drop_mode=2, mask=mask.data_ptr(), ldm=N, drop_p=p, seed=1234)
+        mk = mask.cpu().numpy()
+        assert set(np.unique(mk)) <= {0.0, np.float32(1 / (1 - p))}
+        assert abs((mk == 0).mean() - p) < 0.05 or M * N < 1000
+        got = out.t.double().cpu().numpy()
+        assert np.max(np.abs(got - ref * mk)) <= 1e-5 * np.abs(ref).max() / (1 - p)
+        outs[backend] = mk
+        # mode 1 reproduces the same result from the stored mask
+        out2 = ActBuf(M, N, dev.DT_F32, "cuda")
+        _gemm(_lib.GEMM_FWD, M, N, K, A.view(), 0, W.view(), 1, backend, bias=bias.data_ptr(), relu=1,
+              out=out2.view(), drop_mode=1, mask=mask.data_ptr(), ldm=N)
+        assert torch.equal(out.t, out2.t)
+    assert np.array_equal(outs[0], outs[1])  # same counter-hash stream on both backends
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_gate_gemm(prec):
+    """dgrad GEMM with the ReLU/dropout gate epilogue: out = (gate>0) * s * (A @ B^T)."""
+    rng = np.random.default_rng(5)
+    dt = dev.PRECISIONS[prec]
+    M, N, K = 2000, 512, 1024
+    A, a64, _ = _rand_act(M, K, dt, rng)
+    B, b64, _ = _rand_act(N, K, dt, rng, 0.05)
+    gate, g64, _ = _rand_act(M, N, dt, rng)
+    ref = np.where(g64 > 0, 1.25 * (a64 @ b64.T), 0.0)
+    for backend in (0, 1):
+        out = ActBuf(M, N, dev.DT_F32, "cuda")
+        _gemm(_lib.GEMM_GATE, M, N, K, A.view(), 0, B.view(), 0, backend, out=out.view(), gate=gate.view(),
+              gate_scale=1.25)
+        assert np.max(np.abs(out.t.double().cpu().numpy() - ref)) <= 1e-5 * np.abs(ref).max()
+
+
+def test_aggregate_t_and_reduce_rows():
+    """agg^T dz into the right half + column partial sums; reduce_rows is exact in fixed order."""
+    rng = np.random.default_rng(9)
+    N, W = 3000, 64
+    src = rng.integers(0, N, 5000)
+    dst = rng.integers(0, N, 5000)
+    b = upload_batch(np.zeros((N, 32), np.float32), src, dst, np.array([0, N], np.int32),
+                     np.zeros((1, 5), np.float32))
+    dz = rng.normal(size=(N, W)).astype(np.float32)
+    B = torch.zeros(N, 2 * W, device="cuda")
+    B[:, :W] = torch.from_numpy(dz).cuda()
+    nblk = _lib.load().dippm_colsum_blocks(N)
+    part = torch.empty(nblk, W, device="cuda")
+    _lib.call("dippm_sage_aggregate_t", dev.f32_act(B), W, N, 1, b.t_rowptr.data_ptr(), b.t_col.data_ptr(),
+              b.inv_deg.data_ptr(), part.data_ptr(), dev._stream())
+    agg = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist())))
+    assert np.allclose(B[:, W:].cpu().numpy(), agg.T @ dz.astype(np.float64), rtol=1e-5, atol=1e-5)
+    out = torch.empty(W, device="cuda")
+    _lib.call("dippm_reduce_rows", part.data_ptr(), nblk, W, W, 1.0, out.data_ptr(), dev._stream())
+    assert np.allclose(out.cpu().numpy(), dz.astype(np.float64).sum(0), rtol=1e-5, atol=1e-4)
+    out2 = torch.empty(W, device="cuda")
+    _lib.call("dippm_reduce_rows", part.data_ptr(), nblk, W, W, 1.0, out2.data_ptr(), dev._stream())
+    assert torch.equal(out, out2)
+
+
+def test_fc3_forward_backward():
+    rng = np.random.default_rng(2)
+    G, W = 300, 128
+    x3 = np.maximum(rng.normal(size=(G, W)), 0).astype(np.float32)
+    w3 = rng.normal(size=(W, 3)).astype(np.float32)
+    b3 = rng.normal(size=3).astype(np.float32)
+    d3 = rng.normal(size=(G, 3)).astype(np.float32)
+    t = {k: torch.from_numpy(v).cuda() for k, v in dict(x3=x3, w3=w3, b3=b3, d3=d3).items()}
+    out = torch.empty(G, 3, device="cuda")
+    norm = torch.tensor([1.0, 2.0, 3.0, 2.0, 3.0, 4.0] + [0.0] * 10, dtype=torch.float64, device="cuda")
+    y = torch.empty(G, 3, dtype=torch.float64, device="cuda")
+    mig = torch.empty(G, dtype=torch.int8, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("dippm_fc3_forward", dev.f32_act(t["x3"]), G, W, t["w3"].data_ptr(), t["b3"].data_ptr(),
+              out.data_ptr(), norm.data_ptr(), y.data_ptr(), mig.data_ptr(), nf.data_ptr(), dev._stream())
+    ref = x3.astype(np.float64) @ w3 + b3
+    assert np.allclose(out.cpu().numpy(), ref, atol=1e-4)
+    assert np.allclose(y.cpu().numpy(), ref * [2, 3, 4] + [1, 2, 3], atol=1e-3)
+    gw3 = torch.empty(W, 3, device="cuda")
+    gb3 = torch.empty(3, device="cuda")
+    gb2 = torch.empty(W, device="cuda")
+    d2 = torch.empty(G, W, device="cuda")
+    _lib.call("dippm_fc3_backward", dev.f32_act(t["x3"]), G, W, t["w3"].data_ptr(), t["d3"].data_ptr(), 2.0,
+              gw3.data_ptr(), gb3.data_ptr(), dev.f32_act(d2), gb2.data_ptr(), dev._stream())
+    d2_ref = np.where(x3 > 0, 2.0 * (d3.astype(np.float64) @ w3.T), 0)
+    assert np.allclose(gw3.cpu().numpy(), x3.T.astype(np.float64) @ d3, atol=1e-3)
+    assert np.allclose(gb3.cpu().numpy(), d3.sum(0), atol=1e-4)
+    assert np.allclose(d2.cpu().numpy(), d2_ref, atol=1e-4)
+    assert np.allclose(gb2.cpu().numpy(), d2_ref.sum(0), atol=1e-3)
