@@ -54,9 +54,12 @@ def parse_args():
     p.add_argument("--hidden", type=int, default=512)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=6, help="CPU baseline sample: steps of one batch each")
+    p.add_argument("--cpu-steps", type=int, default=16, help="CPU baseline sample: steps of one batch each")
     p.add_argument("--clock-ms", type=int, default=10, help="NVML sampling interval during timing")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--no-infer", action="store_true", help="skip the configs[2] inference sweep")
+    p.add_argument("--infer-batch", type=int, default=4096)
+    p.add_argument("--infer-steps", type=int, default=20)
     return p.parse_args()
 
 
@@ -255,6 +258,65 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def inference_sweep(args, rank, world, lib):
+    """configs[2]: batched predict (CSR + forward + de-normalise + MIG pick) on
+    4096-graph batches, bf16 and fp32, sharded over ranks (no collective);
+    graphs/s over all ranks, max-over-ranks device time.  The 1M-graph sweep is
+    ~256 such batches; a bounded number of steps is timed (inputs resident)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_11733_b200 import gnn
+    from paper_2303_11733_b200.device import Engine, Workspace, build_batch_csr, upload_batch
+    from paper_2303_11733_b200.synth import make_dataset
+
+    ds = make_dataset(2 * args.infer_batch, seed=3 + rank)
+    norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    model = gnn.create_model(hidden=args.hidden, seed=0, normalizer=norm)
+    batches = [upload_batch(*ds.collate(np.arange(i * args.infer_batch, (i + 1) * args.infer_batch)),
+                            device="cuda", build_csr=False) for i in range(2)]
+    out = {"workload": f"configs[2]: predict + MIG, batch {args.infer_batch}/rank, hidden {args.hidden}",
+           "scaling": "weak"}
+    for prec in ("bf16", "fp32"):
+        eng = Engine(args.hidden, prec)
+        eng.set_params(model.param_items(), norm)
+        ws = Workspace(eng, max(b.N for b in batches), args.infer_batch, train=False)
+
+        def step(i):
+            b = batches[i % 2]
+            build_batch_csr(b)
+            eng.forward(b, ws, predict=True)
+
+        timer = GemmTimer()
+        for i in range(3):
+            step(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.infer_steps):
+            step(i)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        eng.gemm_hook = timer
+        for i in range(args.infer_steps):
+            step(i)
+        eng.gemm_hook = None
+        g_flops, g_ms, _ = timer.summary()
+        graphs = args.infer_steps * args.infer_batch * world
+        out[prec] = {"graphs_per_s": graphs / (ms / 1000.0), "ms_per_batch": ms / args.infer_steps,
+                     "gemm_tflops": g_flops / (g_ms / 1000.0) / 1e12,
+                     "gemm_share": g_ms / ms}
+        del ws, eng
+        torch.cuda.empty_cache()
+    return out
+
+
 class GemmTimer:
     """CUDA-event pairs around each tensor-core GEMM launch (on the launching stream)."""
 
@@ -306,8 +368,9 @@ def main():
 
     norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
     model = gnn.create_model(hidden=args.hidden, seed=0, normalizer=norm)
+    from paper_2303_11733_b200.dist import allreduce_sum
     trainer = BatchTrainer(model, precision=args.dtype, lr=gnn.DEFAULT_LEARNING_RATE, seed=11,
-                           allreduce=(lambda t: dist.all_reduce(t)) if world > 1 else None, world_size=world)
+                           allreduce=allreduce_sum if world > 1 else None, world_size=world, rank=rank)
     eng = trainer.engine
     # resident epoch: every batch collated in HBM before timing (CSR is rebuilt each step)
     resident = [upload_batch(*b, device=eng.device, build_csr=False) for b in batches_host]
@@ -389,6 +452,10 @@ def main():
         e2e = {"value": graphs / (ems / 1000.0), "unit": "graphs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 8}
 
+    infer = None
+    if not args.no_infer:
+        infer = inference_sweep(args, rank, world, lib)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = host_cores()
@@ -409,7 +476,7 @@ def main():
                              "gemm_share_of_step": (g_ms / args.steps) / (ms / args.steps),
                              "gemm_launches_per_step": g_n / args.steps,
                              "algorithmic_tflop_per_step": g_flops / args.steps / 1e12},
-                "cpu_baseline": cpu, "clocks": clocks, "wall_s_timed_region": wall}
+                "cpu_baseline": cpu, "clocks": clocks, "wall_s_timed_region": wall, "inference": infer}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

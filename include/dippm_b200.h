@@ -199,7 +199,9 @@ int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, 
  * = {mean loss, sum APE latency, memory, energy} (APE on de-normalised
  * outputs, gnn.py:458-459). */
 int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t num_graphs, const double* norm,
-                    double delta, float* dout, double* loss_out, void* stream);
+                    double delta, double grad_den, float* dout, double* loss_out, void* stream);
+/*   grad_den: denominator of dout (<= 0: num_graphs).  Data-parallel training passes the
+ *   GLOBAL batch size so the all-reduced sum of per-rank gradients is the global mean. */
 
 /* ---------------------------------------------------------------------------
  * K8 — bias-corrected Adam (numerics.py:93-114, same op order) on fp64 master

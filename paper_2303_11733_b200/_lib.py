@@ -77,7 +77,7 @@ SIGNATURES = {
     "dippm_fc3_forward": (I32, [Act, I64, I32, P, P, P, P, P, P, P, P]),
     "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),
-    "dippm_huber": (I32, [P, P, I64, P, F64, P, P, P]),
+    "dippm_huber": (I32, [P, P, I64, P, F64, F64, P, P, P]),
     "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),
     "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
 }

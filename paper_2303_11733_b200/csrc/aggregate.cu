@@ -18,48 +18,81 @@ constexpr int kAggThreads = 256;
 constexpr int kAggColCap = 2048;   // neighbour ids staged in shared memory per block
 constexpr int kColsumRows = 64;    // rows per block for column partial sums
 
-// Block handles a contiguous row range; lanes are grouped L per row
-// (L = min(32, width/8)), each lane owning 8-column chunks.
+// Both aggregation kernels stage the block's slice of the CSR (row pointers,
+// neighbour ids, 1/deg weights) in shared memory first, so the per-row work is
+// only independent 128-bit feature-row loads (no dependent index loads on the
+// critical path), and each lane keeps CPL 8-column chunks x 2 neighbours in
+// flight.  A warp covers one row when width/8 >= 32 (hidden 512: 2 chunks per
+// lane), or 32/L rows for narrow layers (layer 1, width 32).
+constexpr int kRowsPerBlock = 64;
+
+template <int CPL>
+__device__ __forceinline__ void load_chunks(const ActView& a, int64_t r, int c0, int stride, float (&x)[CPL][8]) {
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) act_load8(a, r, c0 + q * stride, x[q]);
+}
+
+// Forward: m[v] = (1/deg v) * sum_{u->v} h[u]; optionally self_out[v] = h[v].
+template <int CPL>
 __global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m, ActView self_out, int64_t N,
                                                            int width, const int* __restrict__ rowptr,
                                                            const int* __restrict__ col,
-                                                           const float* __restrict__ inv_deg, int rows_per_block) {
+                                                           const float* __restrict__ inv_deg) {
+  __shared__ int s_ptr[kRowsPerBlock + 1];
+  __shared__ float s_w[kRowsPerBlock];
   __shared__ int s_col[kAggColCap];
-  const int chunks = width >> 3;
-  const int L = chunks >= 32 ? 32 : chunks;
-  const int gpw = 32 / L;  // rows per warp per step
+  const int L = (width >> 3) / CPL;  // lanes per row
+  const int gpw = 32 / L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / L, sub = lane % L;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = (N < r0 + rows_per_block) ? N : r0 + rows_per_block;
-  if (r0 >= N) return;
-  const int cbeg = rowptr[r0], cend = rowptr[r1];
-  const bool staged = (cend - cbeg) <= kAggColCap;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int cbeg = rowptr[r0];
+  for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = rowptr[r0 + i] - cbeg;
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_w[i] = inv_deg[r0 + i];
+  const int ncol = rowptr[r0 + nrows] - cbeg;
+  const bool staged = ncol <= kAggColCap;
   if (staged)
-    for (int i = threadIdx.x; i < cend - cbeg; i += blockDim.x) s_col[i] = col[cbeg + i];
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) s_col[i] = col[cbeg + i];
   __syncthreads();
-  const int rows_per_step = (kAggThreads / 32) * gpw;
-  for (int64_t row = r0 + warp * gpw + grp; row < r1; row += rows_per_step) {
-    if (grp >= gpw) break;
-    const int b = rowptr[row], e = rowptr[row + 1];
-    const float w = inv_deg[row];
-    for (int c = sub * 8; c < width; c += L * 8) {
-      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int j = b; j < e; ++j) {
-        const int u = staged ? s_col[j - cbeg] : col[j];
-        float x[8];
-        act_load8(h, u, c, x);
+  if (grp >= gpw) return;
+  const int c0 = sub * 8, stride = L * 8;
+  for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
+    const int64_t row = r0 + lr;
+    const int b = s_ptr[lr], e = s_ptr[lr + 1];
+    float acc[CPL][8] = {};
+    int j = b;
+    for (; j + 1 < e; j += 2) {
+      const int u0 = staged ? s_col[j] : col[cbeg + j];
+      const int u1 = staged ? s_col[j + 1] : col[cbeg + j + 1];
+      float x0[CPL][8], x1[CPL][8];
+      load_chunks<CPL>(h, u0, c0, stride, x0);
+      load_chunks<CPL>(h, u1, c0, stride, x1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += x[k];
-      }
+      for (int q = 0; q < CPL; ++q)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] *= w;
-      act_store8(m, row, c, acc);
-      if (self_out.base) {
-        float x[8];
-        act_load8(h, row, c, x);
-        act_store8(self_out, row, c, x);
-      }
+        for (int k = 0; k < 8; ++k) acc[q][k] += x0[q][k] + x1[q][k];
+    }
+    if (j < e) {
+      float x0[CPL][8];
+      load_chunks<CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x0);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[q][k] += x0[q][k];
+    }
+    const float w = s_w[lr];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[q][k] *= w;
+      act_store8(m, row, c0 + q * stride, acc[q]);
+    }
+    if (self_out.base) {
+      float x[CPL][8];
+      load_chunks<CPL>(h, row, c0, stride, x);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) act_store8(self_out, row, c0 + q * stride, x[q]);
     }
   }
 }
@@ -69,47 +102,90 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m,
 //   g[u] = sum_{u->v} dz[v] / deg(v)          (agg^T dz, via the transposed CSR)
 // so that dh_prev = [dz | g] @ [W_self | W_neigh]^T is ONE GEMM (dgrad with the
 // ReLU gate fused in its epilogue).  Also emits per-block column partial sums
-// of dz (bias gradient, gnn.py:230).  write_agg = 0: partial sums only.
+// of dz (bias gradient, gnn.py:230), reduced over the block's warps in a fixed
+// order.  write_agg = 0: partial sums only.
+template <int CPL>
 __global__ void __launch_bounds__(kAggThreads) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
                                                              const int* __restrict__ t_rowptr,
                                                              const int* __restrict__ t_col,
                                                              const float* __restrict__ inv_deg,
                                                              float* __restrict__ colsum_partial) {
-  extern __shared__ float s_part[];  // [groups][width]
-  const int chunks = width >> 3;
-  const int groups = kAggThreads / chunks;
-  const int grp = threadIdx.x / chunks, ch = threadIdx.x % chunks;
-  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
-  const int64_t r1 = (N < r0 + kColsumRows) ? N : r0 + kColsumRows;
-  if (grp < groups) {
-    const int c = ch * 8;
-    float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t row = r0 + grp; row < r1; row += groups) {
-      float v[8];
-      act_load8(B, row, c, v);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) part[k] += v[k];
-      if (write_agg) {
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const int b = t_rowptr[row], e = t_rowptr[row + 1];
-        for (int j = b; j < e; ++j) {
-          const int tv = t_col[j];
-          const float w = inv_deg[tv];
-          float x[8];
-          act_load8(B, tv, c, x);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] = fmaf(w, x[k], acc[k]);
-        }
-        act_store8(B, row, width + c, acc);
+  extern __shared__ float s_part[];  // [8 warps * gpw][width]
+  __shared__ int s_ptr[kRowsPerBlock + 1];
+  __shared__ int s_col[kAggColCap];
+  __shared__ float s_cw[kAggColCap];
+  const int L = (width >> 3) / CPL;
+  const int gpw = 32 / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / L, sub = lane % L;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int cbeg = t_rowptr[r0];
+  const int ncol = t_rowptr[r0 + nrows] - cbeg;
+  const bool staged = ncol <= kAggColCap;
+  if (write_agg) {
+    for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
+    if (staged)
+      for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
+        const int v = t_col[cbeg + i];
+        s_col[i] = v;
+        s_cw[i] = inv_deg[v];
       }
-    }
+    __syncthreads();
+  }
+  const int c0 = sub * 8, stride = L * 8;
+  float part[CPL][8] = {};
+  if (grp < gpw) {
+    for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
+      const int64_t row = r0 + lr;
+      float own[CPL][8];
+      load_chunks<CPL>(B, row, c0, stride, own);
+      if (write_agg) {
+        const int b = s_ptr[lr], e = s_ptr[lr + 1];
+        float acc[CPL][8] = {};
+        int j = b;
+        for (; j + 1 < e; j += 2) {
+          const int v0 = staged ? s_col[j] : t_col[cbeg + j];
+          const int v1 = staged ? s_col[j + 1] : t_col[cbeg + j + 1];
+          const float w0 = staged ? s_cw[j] : inv_deg[v0];
+          const float w1 = staged ? s_cw[j + 1] : inv_deg[v1];
+          float x0[CPL][8], x1[CPL][8];
+          load_chunks<CPL>(B, v0, c0, stride, x0);
+          load_chunks<CPL>(B, v1, c0, stride, x1);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_part[grp * width + c + k] = part[k];
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[q][k] = fmaf(w1, x1[q][k], fmaf(w0, x0[q][k], acc[q][k]));
+        }
+        if (j < e) {
+          const int v0 = staged ? s_col[j] : t_col[cbeg + j];
+          const float w0 = staged ? s_cw[j] : inv_deg[v0];
+          float x0[CPL][8];
+          load_chunks<CPL>(B, v0, c0, stride, x0);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[q][k] = fmaf(w0, x0[q][k], acc[q][k]);
+        }
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) act_store8(B, row, width + c0 + q * stride, acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[q][k] += own[q][k];
+    }
+    const int slot = warp * gpw + grp;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_part[slot * width + c0 + q * stride + k] = part[q][k];
   }
   __syncthreads();
+  const int slots = (kAggThreads / 32) * gpw;
   for (int c = threadIdx.x; c < width; c += blockDim.x) {
     float t = 0.f;
-    for (int q = 0; q < groups; ++q) t += s_part[q * width + c];
+    for (int q = 0; q < slots; ++q) t += s_part[q * width + c];
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
 }
@@ -209,28 +285,52 @@ using namespace dippm;
 
 extern "C" {
 
-int32_t dippm_colsum_blocks(int64_t num_nodes) { return ceil_div_i(num_nodes, kColsumRows); }
+int32_t dippm_colsum_blocks(int64_t num_nodes) { return ceil_div_i(num_nodes, kRowsPerBlock); }
+
+static int cpl_for(int width) {
+  const int chunks = width / 8;
+  return chunks >= 128 ? 4 : (chunks >= 64 ? 2 : 1);
+}
 
 int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_out, int64_t N, int32_t width,
                              const int32_t* rowptr, const int32_t* col, const float* inv_deg, void* stream) {
   DIPPM_ARG_CHECK(N >= 1 && width >= 8 && width % 8 == 0, "sage_aggregate: width %d must be a multiple of 8", width);
-  const int chunks = width / 8;
-  const int L = chunks >= 32 ? 32 : chunks;
-  const int gpw = 32 / L;
-  const int rows_per_block = (kAggThreads / 32) * gpw * 4;
-  k_aggregate<<<ceil_div_i(N, rows_per_block), kAggThreads, 0, (cudaStream_t)stream>>>(
-      make_view(h), make_view(m_out), make_view(self_out), N, width, rowptr, col, inv_deg, rows_per_block);
+  const int cpl = cpl_for(width);
+  DIPPM_ARG_CHECK((width / 8) % cpl == 0 && (width / 8) / cpl <= 32 && 32 % ((width / 8) / cpl) == 0,
+                  "sage_aggregate: unsupported width %d", width);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = ceil_div_i(N, kRowsPerBlock);
+  ActView hv = make_view(h), mv = make_view(m_out), sv = make_view(self_out);
+  if (cpl == 4) k_aggregate<4><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
+  else if (cpl == 2) k_aggregate<2><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
+  else k_aggregate<1><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
   DIPPM_LAUNCH_CHECK("k_aggregate");
   return DIPPM_OK;
 }
 
 int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
                                const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
-  DIPPM_ARG_CHECK(N >= 1 && width % 8 == 0 && width / 8 <= kAggThreads, "sage_aggregate_t: bad width %d", width);
-  const int groups = kAggThreads / (width / 8);
-  size_t smem = (size_t)groups * width * sizeof(float);
-  k_aggregate_t<<<dippm_colsum_blocks(N), kAggThreads, smem, (cudaStream_t)stream>>>(
-      make_view(B), width, N, write_agg, t_rowptr, t_col, inv_deg, colsum_partial);
+  DIPPM_ARG_CHECK(N >= 1 && width >= 8 && width % 8 == 0, "sage_aggregate_t: bad width %d", width);
+  const int cpl = cpl_for(width);
+  const int L = (width / 8) / cpl;
+  DIPPM_ARG_CHECK((width / 8) % cpl == 0 && L <= 32 && 32 % L == 0, "sage_aggregate_t: unsupported width %d", width);
+  const size_t smem = (size_t)(kAggThreads / 32) * (32 / L) * width * sizeof(float);
+  DIPPM_ARG_CHECK(smem <= 160 * 1024, "sage_aggregate_t: width %d too large", width);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = ceil_div_i(N, kRowsPerBlock);
+  ActView bv = make_view(B);
+#define DIPPM_AGGT(C)                                                                                      \
+  do {                                                                                                     \
+    if (smem > 48 * 1024)                                                                                  \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            (int)smem));                                                   \
+    k_aggregate_t<C><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
+                                                    colsum_partial);                                       \
+  } while (0)
+  if (cpl == 4) DIPPM_AGGT(4);
+  else if (cpl == 2) DIPPM_AGGT(2);
+  else DIPPM_AGGT(1);
+#undef DIPPM_AGGT
   DIPPM_LAUNCH_CHECK("k_aggregate_t");
   return DIPPM_OK;
 }

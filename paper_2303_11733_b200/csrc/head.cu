@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) k_colsum_act(ActView a, int64_t rows, int
 
 // numerics.py:58-73 per graph, mean over the batch (gnn.py:402-404).
 __global__ void k_huber(const float* __restrict__ out, const float* __restrict__ y_raw, int64_t G,
-                        const double* __restrict__ norm, double delta, float* __restrict__ dout,
+                        const double* __restrict__ norm, double delta, double grad_den, float* __restrict__ dout,
                         double* __restrict__ loss_out) {
   __shared__ double s_loss[256], s_ape[3][256];
   double l = 0.0, ape[3] = {0, 0, 0};
@@ -240,7 +240,7 @@ __global__ void k_huber(const float* __restrict__ out, const float* __restrict__
       bool quad = a <= delta;
       le += quad ? 0.5 * r * r : delta * (a - 0.5 * delta);
       double gr = quad ? r : delta * (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0));
-      if (dout) dout[g * 3 + k] = (float)(gr / 3.0 / (double)G);
+      if (dout) dout[g * 3 + k] = (float)(gr / 3.0 / grad_den);
       double den = pred * norm[3 + k] + norm[k];
       ape[k] += fabs(den - y) / fabs(y);
     }
@@ -295,9 +295,10 @@ int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, 
 }
 
 int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t G, const double* norm, double delta,
-                    float* dout, double* loss_out, void* stream) {
+                    double grad_den, float* dout, double* loss_out, void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && delta > 0, "huber: bad args");
-  k_huber<<<1, 256, 0, (cudaStream_t)stream>>>(out_norm, y_raw, G, norm, delta, dout, loss_out);
+  k_huber<<<1, 256, 0, (cudaStream_t)stream>>>(out_norm, y_raw, G, norm, delta, grad_den > 0 ? grad_den : (double)G,
+                                               dout, loss_out);
   DIPPM_LAUNCH_CHECK("k_huber");
   return DIPPM_OK;
 }

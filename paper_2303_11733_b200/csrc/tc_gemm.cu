@@ -142,6 +142,53 @@ __host__ __device__ constexpr uint32_t make_idesc(int fmt, bool a_mn, bool b_mn,
          ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// GATE epilogue helpers: 32 gate values (the layer-below activation, in the
+// GEMM's operand dtype) -> a 32-bit (gate > 0) mask.  Loads are issued one
+// chunk ahead and decoded after the next chunk's math (latency hiding).
+// tf32x3: the sign of v = hi + lo is the sign of hi unless hi == 0 (|v| below
+// the tf32 grid, essentially exact zeros), where the lo plane decides.
+template <int kFmt>
+__device__ __forceinline__ void gate_issue(const ActView& g, int64_t row, int n, uint4 (&r)[8]) {
+  if constexpr (kFmt == 1) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(g.base) + row * g.ld + n);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __ldg(p + i);
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(g.base) + row * g.ld + n);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = __ldg(p + i);
+  }
+}
+template <int kFmt>
+__device__ __forceinline__ uint32_t gate_mask(const ActView& g, int64_t row, int n, const uint4 (&r)[8]) {
+  uint32_t m = 0;
+  if constexpr (kFmt == 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;  // bf16 > 0: sign clear, not zero
+        m |= (uint32_t)(!(lo & 0x8000u) && (lo & 0x7FFFu)) << (i * 8 + j * 2);
+        m |= (uint32_t)(!(hi & 0x8000u) && (hi & 0x7FFFu)) << (i * 8 + j * 2 + 1);
+      }
+    }
+  } else {
+    const float* lo_plane = reinterpret_cast<const float*>(g.base) + g.plane_stride + row * g.ld + n;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool pos = (int32_t)w[j] > 0;
+        if (w[j] == 0u || w[j] == 0x80000000u) pos = lo_plane[i * 4 + j] > 0.f;
+        m |= (uint32_t)pos << (i * 4 + j);
+      }
+    }
+  }
+  return m;
+}
+
 template <int kFmt, int kBN>
 struct Cfg {
   static constexpr int kElem = kFmt == 1 ? 2 : 4;
@@ -286,9 +333,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int split = t / tiles_mn, r = t % tiles_mn;
       const int m0 = (r / p.n_tiles) * kBM, n0 = (r % p.n_tiles) * kBN;
       const uint32_t acc = local & 1, use = local >> 1;
+      const int64_t row = (int64_t)m0 + q * 32 + lane;
+      if constexpr (kEpi == EPI_GATE) {
+        // The gate (activation of the layer below) is streamed one 32-column
+        // chunk ahead: chunk 0 is fetched while the MMAs are still running.
+        uint4 graw[8];
+        if (row < p.M) gate_issue<kFmt>(p.gate, row, n0, graw);
+        mbar_wait(&tfull[acc], use & 1);
+        tc_fence_after();
+        uint32_t gm = row < p.M ? gate_mask<kFmt>(p.gate, row, n0, graw) : 0u;
+#pragma unroll 1
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+          const bool more = ch + 1 < kBN / 32 && row < p.M;
+          if (more) gate_issue<kFmt>(p.gate, row, n0 + (ch + 1) * 32, graw);
+          uint32_t raw[32];
+          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
+          if (row < p.M) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                v[i] = (gm >> (g * 8 + i)) & 1u ? __uint_as_float(raw[g * 8 + i]) * p.gate_scale : 0.f;
+              act_store8(p.out, row, n0 + ch * 32 + g * 8, v);
+            }
+          }
+          if (more) gm = gate_mask<kFmt>(p.gate, row, n0 + (ch + 1) * 32, graw);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      const int64_t row = (int64_t)m0 + q * 32 + lane;
 #pragma unroll 1
       for (int ch = 0; ch < kBN / 32; ++ch) {
         uint32_t raw[32];
@@ -328,15 +405,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
                 }
               }
-              act_store8(p.out, row, n + g * 8, v);
-            }
-          } else if constexpr (kEpi == EPI_GATE) {
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              float v[8], gt[8];
-              act_load8(p.gate, row, n + g * 8, gt);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = gt[i] > 0.f ? __uint_as_float(raw[g * 8 + i]) * p.gate_scale : 0.f;
               act_store8(p.out, row, n + g * 8, v);
             }
           } else {

@@ -416,8 +416,9 @@ class Engine:
                   _p(ws.nonfinite), s)
         self.launches += 3 + 1 + 1
 
-    def loss(self, b: Batch, ws: Workspace, delta: float = 1.0) -> None:
-        _lib.call("dippm_huber", _p(ws.out), _p(b.y), b.G, _p(self.norm), float(delta),
+    def loss(self, b: Batch, ws: Workspace, delta: float = 1.0, grad_den: float = 0.0) -> None:
+        """Huber loss + dout (numerics.py:58-73); grad_den = global batch size under DP (0: this batch)."""
+        _lib.call("dippm_huber", _p(ws.out), _p(b.y), b.G, _p(self.norm), float(delta), float(grad_den),
                   _p(ws.dout) if ws.train else None, _p(ws.loss), _stream())
         self.launches += 1
 

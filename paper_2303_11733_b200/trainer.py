@@ -22,14 +22,15 @@ from .device import Batch, Engine, Workspace, build_batch_csr
 
 class BatchTrainer:
     def __init__(self, model, precision: str = "bf16", lr: float = 2.754e-5, seed: int = 0, dropout: bool = True,
-                 huber_delta: float = 1.0, allreduce=None, world_size: int = 1, device=None, backend: str = "tc"):
+                 huber_delta: float = 1.0, allreduce=None, world_size: int = 1, rank: int = 0, device=None,
+                 backend: str = "tc"):
         self.model = model
         self.engine = Engine(model.hidden, precision, device, backend)
         self.engine.set_params(model.param_items(), model.normalizer)
         self.lr, self.seed, self.delta = lr, seed, huber_delta
         self.dropout_p = model.dropout_p if dropout else 0.0
         self.allreduce = allreduce
-        self.world_size = world_size
+        self.world_size, self.rank = world_size, rank
         self.steps = 0
         self.ws = None
         self._stage = None
@@ -52,20 +53,27 @@ class BatchTrainer:
         if self.ws is None or b.N > self.ws.N or b.G > self.ws.G:
             self.reserve(max(b.N, 1), b.G)
 
-    def step_resident(self, b: Batch) -> None:
-        """One training step on a device-resident batch (no host synchronisation)."""
+    def step_resident(self, b: Batch, global_graphs: int | None = None) -> None:
+        """One training step on a device-resident batch (no host synchronisation).
+
+        Data parallel: the gradient denominator is the global batch
+        (`global_graphs`, default G x world), so the all-reduced SUM of the
+        per-rank gradients is the global batch mean (gnn.py:402-404)."""
         self._ensure(b)
         eng, ws = self.engine, self.ws
         build_batch_csr(b)
         self.steps += 1
         mode = 2 if self.dropout_p > 0 else 0
-        eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 1000003 + self.steps,
-                    predict=False)
-        eng.loss(b, ws, self.delta)
+        eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p,
+                    seed=(self.seed * 1000003 + self.steps) * 131 + self.rank, predict=False)
+        den = 0.0
+        if self.allreduce is not None:
+            den = float(global_graphs if global_graphs else b.G * self.world_size)
+        eng.loss(b, ws, self.delta, grad_den=den)
         eng.backward(b, ws, keep_scale=1.0 / (1.0 - self.dropout_p) if mode else 1.0)
         if self.allreduce is not None:
-            self.allreduce(eng.grads)          # sum of per-rank batch means
-        eng.adam_step(self.lr, grad_scale=1.0 / self.world_size)
+            self.allreduce(eng.grads)          # the one exchange: sum of per-rank gradient shares
+        eng.adam_step(self.lr)
 
     def step_host(self, x, src, dst, graph_ptr, fs, y) -> float:
         """End-to-end step from host (ideally pinned) buffers; returns the batch loss."""
