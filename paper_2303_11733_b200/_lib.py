@@ -65,6 +65,8 @@ SIGNATURES = {
     "dippm_mig_codes": (I32, [P, I64, I64, P, P, P]),
     "dippm_csr_workspace_bytes": (SZ, [I64, I64]),
     "dippm_build_csr": (I32, [P, P, I64, I64, P, P, P, P, P, P, P, P, SZ, P]),
+    "dippm_csr_grouped_workspace_bytes": (SZ, [I64, I64]),
+    "dippm_build_csr_grouped": (I32, [P, P, P, P, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
     "dippm_colsum_blocks": (I32, [I64]),
     "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P]),

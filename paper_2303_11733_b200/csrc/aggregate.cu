@@ -26,18 +26,19 @@ constexpr int kColsumRows = 64;    // rows per block for column partial sums
 // lane), or 32/L rows for narrow layers (layer 1, width 32).
 constexpr int kRowsPerBlock = 64;
 
-template <int CPL>
+template <int DT, int CPL>
 __device__ __forceinline__ void load_chunks(const ActView& a, int64_t r, int c0, int stride, float (&x)[CPL][8]) {
 #pragma unroll
-  for (int q = 0; q < CPL; ++q) act_load8(a, r, c0 + q * stride, x[q]);
+  for (int q = 0; q < CPL; ++q) act_load8_t<DT>(a, r, c0 + q * stride, x[q]);
 }
 
 // Forward: m[v] = (1/deg v) * sum_{u->v} h[u]; optionally self_out[v] = h[v].
-template <int CPL>
-__global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m, ActView self_out, int64_t N,
-                                                           int width, const int* __restrict__ rowptr,
-                                                           const int* __restrict__ col,
-                                                           const float* __restrict__ inv_deg) {
+// DTI: dtype of h (fp32 X for layer 1, the compute dtype after), DTO: of m.
+template <int DTI, int DTO, int CPL>
+__global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView m, ActView self_out, int64_t N,
+                                                              int width, const int* __restrict__ rowptr,
+                                                              const int* __restrict__ col,
+                                                              const float* __restrict__ inv_deg) {
   __shared__ int s_ptr[kRowsPerBlock + 1];
   __shared__ float s_w[kRowsPerBlock];
   __shared__ int s_col[kAggColCap];
@@ -61,38 +62,26 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m,
     const int64_t row = r0 + lr;
     const int b = s_ptr[lr], e = s_ptr[lr + 1];
     float acc[CPL][8] = {};
-    int j = b;
-    for (; j + 1 < e; j += 2) {
-      const int u0 = staged ? s_col[j] : col[cbeg + j];
-      const int u1 = staged ? s_col[j + 1] : col[cbeg + j + 1];
-      float x0[CPL][8], x1[CPL][8];
-      load_chunks<CPL>(h, u0, c0, stride, x0);
-      load_chunks<CPL>(h, u1, c0, stride, x1);
+    for (int j = b; j < e; ++j) {
+      float x[CPL][8];
+      load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[q][k] += x0[q][k] + x1[q][k];
-    }
-    if (j < e) {
-      float x0[CPL][8];
-      load_chunks<CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x0);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[q][k] += x0[q][k];
+        for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
     }
     const float w = s_w[lr];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[q][k] *= w;
-      act_store8(m, row, c0 + q * stride, acc[q]);
+      act_store8_t<DTO>(m, row, c0 + q * stride, acc[q]);
     }
     if (self_out.base) {
       float x[CPL][8];
-      load_chunks<CPL>(h, row, c0, stride, x);
+      load_chunks<DTI, CPL>(h, row, c0, stride, x);
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) act_store8(self_out, row, c0 + q * stride, x[q]);
+      for (int q = 0; q < CPL; ++q) act_store8_t<DTO>(self_out, row, c0 + q * stride, x[q]);
     }
   }
 }
@@ -102,14 +91,14 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate(ActView h, ActView m,
 //   g[u] = sum_{u->v} dz[v] / deg(v)          (agg^T dz, via the transposed CSR)
 // so that dh_prev = [dz | g] @ [W_self | W_neigh]^T is ONE GEMM (dgrad with the
 // ReLU gate fused in its epilogue).  Also emits per-block column partial sums
-// of dz (bias gradient, gnn.py:230), reduced over the block's warps in a fixed
-// order.  write_agg = 0: partial sums only.
-template <int CPL>
-__global__ void __launch_bounds__(kAggThreads) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
-                                                             const int* __restrict__ t_rowptr,
-                                                             const int* __restrict__ t_col,
-                                                             const float* __restrict__ inv_deg,
-                                                             float* __restrict__ colsum_partial) {
+// of dz (bias gradient, gnn.py:230), reduced over the block's row slots in a
+// fixed order.  write_agg = 0: partial sums only.
+template <int DT, int CPL>
+__global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
+                                                                const int* __restrict__ t_rowptr,
+                                                                const int* __restrict__ t_col,
+                                                                const float* __restrict__ inv_deg,
+                                                                float* __restrict__ colsum_partial) {
   extern __shared__ float s_part[];  // [8 warps * gpw][width]
   __shared__ int s_ptr[kRowsPerBlock + 1];
   __shared__ int s_col[kAggColCap];
@@ -139,36 +128,22 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate_t(ActView B, int widt
     for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
       const int64_t row = r0 + lr;
       float own[CPL][8];
-      load_chunks<CPL>(B, row, c0, stride, own);
+      load_chunks<DT, CPL>(B, row, c0, stride, own);
       if (write_agg) {
         const int b = s_ptr[lr], e = s_ptr[lr + 1];
         float acc[CPL][8] = {};
-        int j = b;
-        for (; j + 1 < e; j += 2) {
+        for (int j = b; j < e; ++j) {
           const int v0 = staged ? s_col[j] : t_col[cbeg + j];
-          const int v1 = staged ? s_col[j + 1] : t_col[cbeg + j + 1];
           const float w0 = staged ? s_cw[j] : inv_deg[v0];
-          const float w1 = staged ? s_cw[j + 1] : inv_deg[v1];
-          float x0[CPL][8], x1[CPL][8];
-          load_chunks<CPL>(B, v0, c0, stride, x0);
-          load_chunks<CPL>(B, v1, c0, stride, x1);
+          float x[CPL][8];
+          load_chunks<DT, CPL>(B, v0, c0, stride, x);
 #pragma unroll
           for (int q = 0; q < CPL; ++q)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc[q][k] = fmaf(w1, x1[q][k], fmaf(w0, x0[q][k], acc[q][k]));
-        }
-        if (j < e) {
-          const int v0 = staged ? s_col[j] : t_col[cbeg + j];
-          const float w0 = staged ? s_cw[j] : inv_deg[v0];
-          float x0[CPL][8];
-          load_chunks<CPL>(B, v0, c0, stride, x0);
-#pragma unroll
-          for (int q = 0; q < CPL; ++q)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[q][k] = fmaf(w0, x0[q][k], acc[q][k]);
+            for (int k = 0; k < 8; ++k) acc[q][k] = fmaf(w0, x[q][k], acc[q][k]);
         }
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) act_store8(B, row, width + c0 + q * stride, acc[q]);
+        for (int q = 0; q < CPL; ++q) act_store8_t<DT>(B, row, width + c0 + q * stride, acc[q]);
       }
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -298,12 +273,25 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
   const int cpl = cpl_for(width);
   DIPPM_ARG_CHECK((width / 8) % cpl == 0 && (width / 8) / cpl <= 32 && 32 % ((width / 8) / cpl) == 0,
                   "sage_aggregate: unsupported width %d", width);
+  DIPPM_ARG_CHECK(!self_out.data || self_out.dtype == m_out.dtype, "sage_aggregate: self_out dtype");
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = ceil_div_i(N, kRowsPerBlock);
   ActView hv = make_view(h), mv = make_view(m_out), sv = make_view(self_out);
-  if (cpl == 4) k_aggregate<4><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
-  else if (cpl == 2) k_aggregate<2><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
-  else k_aggregate<1><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg);
+#define DIPPM_AGG(DI, DO, C) k_aggregate<DI, DO, C><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg)
+#define DIPPM_AGG_C(DI, DO) \
+  do { if (cpl == 4) DIPPM_AGG(DI, DO, 4); else if (cpl == 2) DIPPM_AGG(DI, DO, 2); else DIPPM_AGG(DI, DO, 1); } while (0)
+#define DIPPM_AGG_O(DI)                                                   \
+  do {                                                                    \
+    if (m_out.dtype == DIPPM_DT_BF16) DIPPM_AGG_C(DI, DIPPM_DT_BF16);     \
+    else if (m_out.dtype == DIPPM_DT_TF32X3) DIPPM_AGG_C(DI, DIPPM_DT_TF32X3); \
+    else DIPPM_AGG_C(DI, DIPPM_DT_F32);                                   \
+  } while (0)
+  if (h.dtype == DIPPM_DT_BF16) DIPPM_AGG_O(DIPPM_DT_BF16);
+  else if (h.dtype == DIPPM_DT_TF32X3) DIPPM_AGG_O(DIPPM_DT_TF32X3);
+  else DIPPM_AGG_O(DIPPM_DT_F32);
+#undef DIPPM_AGG_O
+#undef DIPPM_AGG_C
+#undef DIPPM_AGG
   DIPPM_LAUNCH_CHECK("k_aggregate");
   return DIPPM_OK;
 }
@@ -319,17 +307,20 @@ int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t 
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = ceil_div_i(N, kRowsPerBlock);
   ActView bv = make_view(B);
-#define DIPPM_AGGT(C)                                                                                      \
-  do {                                                                                                     \
-    if (smem > 48 * 1024)                                                                                  \
-      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                            (int)smem));                                                   \
-    k_aggregate_t<C><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
-                                                    colsum_partial);                                       \
+#define DIPPM_AGGT(D, C)                                                                                      \
+  do {                                                                                                        \
+    if (smem > 48 * 1024)                                                                                     \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            (int)smem));                                                      \
+    k_aggregate_t<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
+                                                       colsum_partial);                                       \
   } while (0)
-  if (cpl == 4) DIPPM_AGGT(4);
-  else if (cpl == 2) DIPPM_AGGT(2);
-  else DIPPM_AGGT(1);
+#define DIPPM_AGGT_C(D) \
+  do { if (cpl == 4) DIPPM_AGGT(D, 4); else if (cpl == 2) DIPPM_AGGT(D, 2); else DIPPM_AGGT(D, 1); } while (0)
+  if (B.dtype == DIPPM_DT_BF16) DIPPM_AGGT_C(DIPPM_DT_BF16);
+  else if (B.dtype == DIPPM_DT_TF32X3) DIPPM_AGGT_C(DIPPM_DT_TF32X3);
+  else DIPPM_AGGT_C(DIPPM_DT_F32);
+#undef DIPPM_AGGT_C
 #undef DIPPM_AGGT
   DIPPM_LAUNCH_CHECK("k_aggregate_t");
   return DIPPM_OK;

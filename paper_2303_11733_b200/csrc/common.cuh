@@ -48,13 +48,19 @@ int num_sms();
 
 // ---------------------------------------------------------------------------
 // Activation storage.  A "plane pair" holds an fp32 value v as two fp32 planes
-// (hi = v with the low 13 mantissa bits cleared, lo = v - hi) so the tensor
+// (hi = tf32(v), lo = tf32(v - hi), both round-to-nearest) so the tensor
 // cores' tf32 path can run the 3-pass split (hi*hi + hi*lo + lo*hi) at fp32
 // accuracy.  bf16 mode stores one bf16 plane.
 
-__device__ __forceinline__ float tf32_hi(float v) {
-  return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+// Round-to-nearest tf32 (cvt.rna): |v - hi| <= 2^-11 |v|; lo = rna(v - hi) is
+// itself exactly representable in tf32, so the tensor core reads both planes
+// without further rounding and each 3-pass product carries ~2^-22 relative error.
+__device__ __forceinline__ float tf32_rn(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
 }
+__device__ __forceinline__ float tf32_hi(float v) { return tf32_rn(v); }
 
 struct ActView {
   // Element (r, c) of plane p lives at base + p*plane_stride + r*ld + c.
@@ -81,7 +87,7 @@ __device__ __forceinline__ void act_store(const ActView& a, int64_t r, int64_t c
     float* p = reinterpret_cast<float*>(a.base) + r * a.ld + c;
     float hi = tf32_hi(v);
     p[0] = hi;
-    p[a.plane_stride] = v - hi;
+    p[a.plane_stride] = tf32_rn(v - hi);
   } else {
     reinterpret_cast<float*>(a.base)[r * a.ld + c] = v;
   }
@@ -127,7 +133,7 @@ __device__ __forceinline__ void act_store8(const ActView& a, int64_t r, int64_t 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       hi[i] = tf32_hi(v[i]);
-      lo[i] = v[i] - hi[i];
+      lo[i] = tf32_rn(v[i] - hi[i]);
     }
     reinterpret_cast<float4*>(p)[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
     reinterpret_cast<float4*>(p)[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
@@ -137,6 +143,63 @@ __device__ __forceinline__ void act_store8(const ActView& a, int64_t r, int64_t 
     float* p = reinterpret_cast<float*>(a.base) + r * a.ld + c;
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// Compile-time-dtype variants (memory-bound kernels specialise on the dtype so
+// the loads/stores carry no runtime branches and fewer live registers).
+template <int DT>
+__device__ __forceinline__ void act_load8_t(const ActView& a, int64_t r, int64_t c, float (&v)[8]) {
+  if constexpr (DT == DIPPM_DT_BF16) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(
+        reinterpret_cast<const __nv_bfloat16*>(a.base) + r * a.ld + c));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  } else {
+    const float* p = reinterpret_cast<const float*>(a.base) + r * a.ld + c;
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 x1 = __ldg(reinterpret_cast<const float4*>(p + 4));
+    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+    if constexpr (DT == DIPPM_DT_TF32X3) {
+      const float4 y0 = __ldg(reinterpret_cast<const float4*>(p + a.plane_stride));
+      const float4 y1 = __ldg(reinterpret_cast<const float4*>(p + a.plane_stride + 4));
+      v[0] += y0.x; v[1] += y0.y; v[2] += y0.z; v[3] += y0.w;
+      v[4] += y1.x; v[5] += y1.y; v[6] += y1.z; v[7] += y1.w;
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void act_store8_t(const ActView& a, int64_t r, int64_t c, const float (&v)[8]) {
+  if constexpr (DT == DIPPM_DT_BF16) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.base) + r * a.ld + c) = q;
+  } else {
+    float* p = reinterpret_cast<float*>(a.base) + r * a.ld + c;
+    if constexpr (DT == DIPPM_DT_TF32X3) {
+      float hi[8], lo[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        hi[i] = tf32_hi(v[i]);
+        lo[i] = tf32_rn(v[i] - hi[i]);
+      }
+      reinterpret_cast<float4*>(p)[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      reinterpret_cast<float4*>(p)[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      reinterpret_cast<float4*>(p + a.plane_stride)[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      reinterpret_cast<float4*>(p + a.plane_stride)[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+    } else {
+      reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
   }
 }
 

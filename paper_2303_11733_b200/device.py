@@ -172,6 +172,24 @@ class Batch:
     t_col: torch.Tensor | None = None
     bad: torch.Tensor | None = None
     h2d_bytes: int = 0
+    edge_ptr: torch.Tensor | None = None  # i64 [G+1] when edges are grouped by graph (fast CSR path)
+    max_nodes: int = 0                    # largest graph (nodes / edges) for the per-graph CSR kernel
+    max_edges: int = 0
+
+
+def group_edges(src, dst, graph_ptr):
+    """edge_ptr [G+1] if the edge list is a concatenation of per-graph edge lists
+    (what collation produces), else None.  Host-side, O(E)."""
+    src, dst, gp = np.asarray(src), np.asarray(dst), np.asarray(graph_ptr, dtype=np.int64)
+    G = len(gp) - 1
+    if len(dst) == 0:
+        return np.zeros(G + 1, np.int64)
+    gd = np.searchsorted(gp, dst, side="right") - 1
+    if np.any(np.diff(gd) < 0) or np.any(np.searchsorted(gp, src, side="right") - 1 != gd):
+        return None
+    ep = np.zeros(G + 1, np.int64)
+    np.cumsum(np.bincount(gd, minlength=G), out=ep[1:])
+    return ep
 
 
 def collate_host(encodings, fs_vectors, targets=None):
@@ -209,7 +227,7 @@ def collate_host(encodings, fs_vectors, targets=None):
     return x, src, dst, graph_ptr, fs, y
 
 
-def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=True) -> Batch:
+def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=True, edge_ptr=None) -> Batch:
     """Pinned host -> device copies of a collated batch, then K1 CSR on device."""
     dev = torch.device(device)
 
@@ -217,17 +235,31 @@ def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=Tr
         t = torch.from_numpy(np.ascontiguousarray(a))
         return t.pin_memory().to(dev, non_blocking=True) if t.numel() else t.to(dev)
 
+    if edge_ptr is None:
+        edge_ptr = group_edges(src, dst, graph_ptr)
     arrays = [x, src, dst, graph_ptr, fs] + ([y] if y is not None else [])
     b = Batch(G=int(len(graph_ptr) - 1), N=int(graph_ptr[-1]), E=int(len(src)), x=h2d(x), src=h2d(src),
               dst=h2d(dst), graph_ptr=h2d(graph_ptr), fs=h2d(fs), y=None if y is None else h2d(y),
               h2d_bytes=int(sum(np.asarray(a).nbytes for a in arrays)))
+    if edge_ptr is not None:
+        b.edge_ptr = h2d(np.asarray(edge_ptr, np.int64))
+        b.max_nodes = int(np.diff(np.asarray(graph_ptr)).max())
+        b.max_edges = int(np.diff(edge_ptr).max()) if len(edge_ptr) > 1 else 0
+        b.h2d_bytes += int(np.asarray(edge_ptr).nbytes)
     if build_csr:
         build_batch_csr(b)
     return b
 
 
-def build_batch_csr(b: Batch) -> Batch:
-    """K1: deterministic CSR + transposed CSR of the batch (gnn.py:130-137)."""
+GROUPED_MAX_EDGES = 16384  # per-graph limit of the shared-memory CSR kernel (padded to a power of 2)
+GROUPED_MAX_GRAPHS = 8192
+
+
+def build_batch_csr(b: Batch, grouped: bool | None = None) -> Batch:
+    """K1: deterministic CSR + transposed CSR of the batch (gnn.py:130-137).
+
+    Uses the per-graph shared-memory kernel when the batch is grouped by graph
+    (3 launches), else the global path; both give bit-identical output."""
     dev = b.x.device
     N, E = b.N, b.E
     i32 = dict(dtype=torch.int32, device=dev)
@@ -237,8 +269,18 @@ def build_batch_csr(b: Batch) -> Batch:
     b.inv_deg = torch.empty(N, dtype=torch.float32, device=dev)
     b.t_rowptr = torch.empty(N + 1, **i32)
     b.t_col = torch.empty(max(E, 1), **i32)
-    b.bad = torch.zeros(1, **i32)
+    b.bad = torch.empty(1, **i32)
     lib = _lib.load()
+    if grouped is None:
+        grouped = (b.edge_ptr is not None and b.G <= GROUPED_MAX_GRAPHS and b.max_edges <= GROUPED_MAX_EDGES
+                   and b.max_nodes <= GROUPED_MAX_EDGES)
+    if grouped:
+        ws_bytes = lib.dippm_csr_grouped_workspace_bytes(b.G, E)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        _lib.call("dippm_build_csr_grouped", _p(b.src), _p(b.dst), _p(b.graph_ptr), _p(b.edge_ptr), b.G, N, E,
+                  b.max_nodes, b.max_edges, _p(b.rowptr), _p(b.col), _p(b.deg), _p(b.inv_deg), _p(b.t_rowptr),
+                  _p(b.t_col), _p(b.bad), _p(ws), ws_bytes, _stream())
+        return b
     ws_bytes = lib.dippm_csr_workspace_bytes(N, E)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.call("dippm_build_csr", _p(b.src), _p(b.dst), E, N, _p(b.rowptr), _p(b.col), _p(b.deg), _p(b.inv_deg),

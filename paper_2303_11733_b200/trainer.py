@@ -47,6 +47,7 @@ class BatchTrainer:
             "gp": torch.empty(max_graphs + 1, dtype=torch.int32, device=d),
             "fs": torch.empty(max_graphs, dev.STATIC_WIDTH, dtype=torch.float32, device=d),
             "y": torch.empty(max_graphs, 3, dtype=torch.float32, device=d),
+            "ep": torch.empty(max_graphs + 1, dtype=torch.int64, device=d),
         }
 
     def _ensure(self, b: Batch) -> None:
@@ -75,19 +76,30 @@ class BatchTrainer:
             self.allreduce(eng.grads)          # the one exchange: sum of per-rank gradient shares
         eng.adam_step(self.lr)
 
-    def step_host(self, x, src, dst, graph_ptr, fs, y) -> float:
-        """End-to-end step from host (ideally pinned) buffers; returns the batch loss."""
-        t = [torch.as_tensor(a) for a in (x, src, dst, graph_ptr, fs, y)]
+    def step_host(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None) -> float:
+        """End-to-end step from host (ideally pinned) buffers; returns the batch loss.
+
+        edge_ptr [G+1] (edges grouped by graph, as collation produces) enables the
+        per-graph CSR kernel; if omitted it is derived on the host when possible."""
+        if edge_ptr is None:
+            edge_ptr = dev.group_edges(np.asarray(src), np.asarray(dst), np.asarray(graph_ptr))
+        arrays = [x, src, dst, graph_ptr, fs, y] + ([edge_ptr] if edge_ptr is not None else [])
+        t = [torch.as_tensor(a) for a in arrays]
         G, N, E = t[3].numel() - 1, t[0].shape[0], t[1].numel()
         if self._stage is None or N > self._stage["x"].shape[0] or E > self._stage["src"].numel() \
                 or G + 1 > self._stage["gp"].numel():
             self.reserve(max(N, self.ws.N if self.ws else 0), max(G, self.ws.G if self.ws else 0), max_edges=2 * E)
         s = self._stage
-        xs, ss, ds_, gs, fss, ys = s["x"][:N], s["src"][:E], s["dst"][:E], s["gp"][:G + 1], s["fs"][:G], s["y"][:G]
-        for d_, h in zip((xs, ss, ds_, gs, fss, ys), t):
+        views = [s["x"][:N], s["src"][:E], s["dst"][:E], s["gp"][:G + 1], s["fs"][:G], s["y"][:G], s["ep"][:G + 1]]
+        for d_, h in zip(views, t):
             d_.copy_(h, non_blocking=True)
-        b = Batch(G=G, N=N, E=E, x=xs, src=ss, dst=ds_, graph_ptr=gs, fs=fss, y=ys,
+        b = Batch(G=G, N=N, E=E, x=views[0], src=views[1], dst=views[2], graph_ptr=views[3], fs=views[4], y=views[5],
                   h2d_bytes=sum(a.numel() * a.element_size() for a in t))
+        if edge_ptr is not None:
+            ep = np.asarray(edge_ptr)
+            gp = np.asarray(graph_ptr)
+            b.edge_ptr, b.max_nodes = views[6], int(np.diff(gp).max())
+            b.max_edges = int(np.diff(ep).max()) if len(ep) > 1 else 0
         self.step_resident(b)
         self._loss_host.copy_(self.ws.loss[:1], non_blocking=True)
         torch.cuda.current_stream().synchronize()
