@@ -10,7 +10,8 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; the fp32
 //               accumulator (128 x BN) lives in TMEM, double-buffered so the
 //               epilogue of tile i overlaps the MMAs of tile i+1;
-//   warps 2-5   epilogue: tcgen05.ld (32x32b.x32) -> bias/ReLU -> store.
+//   warps 2-9   epilogue (two warps per TMEM lane quarter, alternate 32-column
+//               chunks): tcgen05.ld (32x32b.x32) -> bias/ReLU/gate -> smem -> TMA store.
 // Operand precision:
 //   bf16  kind::f16, one pass;
 //   tf32x3 kind::tf32 on hi/lo planes, 3 passes (hi*hi + hi*lo + lo*hi) so
@@ -26,7 +27,7 @@
 namespace dippm {
 namespace tc {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 64 + 256;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kBM = 128;
 enum { EPI_FWD = 0, EPI_STORE = 1, EPI_PARTIAL = 2, EPI_GATE = 3, EPI_FWD_DROP = 4 };
 
@@ -189,6 +190,81 @@ __device__ __forceinline__ uint32_t gate_mask(const ActView& g, int64_t row, int
   return m;
 }
 
+// Activation-writing epilogues stage each warp's 32 rows x 32 columns in shared
+// memory and hand them to the TMA engine (cp.async.bulk.tensor store): fully
+// coalesced, asynchronous, and rows beyond M are clipped by the tensor map.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+// Each of the 8 epilogue warps owns 4 KB of staging: two 2 KB slots for bf16
+// output (one TMA store stays in flight while the next chunk is computed), one
+// slot for fp32, and for tf32 hi/lo the two planes go through the slot in turn.
+constexpr int kEpiWarps = 8;
+constexpr int kStageWarpBytes = 4096;
+
+__device__ __forceinline__ void stage_wait(int lane, int pending) {
+  if (lane == 0) {
+    if (pending == 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void stage_issue(const CUtensorMap* map, const uint8_t* stg, int lane, int x, int y, int z) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(map, stg, x, y, z);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtensorMap* map, int64_t dtype, int lane,
+                                                const float (&v)[32], int x, int y, int chunk) {
+  if (dtype == DIPPM_DT_BF16) {
+    uint8_t* stg = stg_base + (chunk & 1) * 2048;
+    stage_wait(lane, 1);  // the slot's previous store has been read
+    uint4* d = reinterpret_cast<uint4*>(stg + lane * 64);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint4 q;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[k * 8 + 2 * i], v[k * 8 + 2 * i + 1]);
+      d[k] = q;
+    }
+    stage_issue(map, stg, lane, x, y, 0);
+  } else if (dtype == DIPPM_DT_TF32X3) {
+    float4* d = reinterpret_cast<float4*>(stg_base + lane * 128);
+    float lo[32];
+    stage_wait(lane, 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float hi[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        hi[i] = tf32_hi(v[4 * k + i]);
+        lo[4 * k + i] = tf32_rn(v[4 * k + i] - hi[i]);
+      }
+      d[k] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    }
+    stage_issue(map, stg_base, lane, x, y, 0);
+    stage_wait(lane, 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k] = make_float4(lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
+    stage_issue(map, stg_base, lane, x, y, 1);
+  } else {
+    float4* d = reinterpret_cast<float4*>(stg_base + lane * 128);
+    stage_wait(lane, 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    stage_issue(map, stg_base, lane, x, y, 0);
+  }
+}
+
 template <int kFmt, int kBN>
 struct Cfg {
   static constexpr int kElem = kFmt == 1 ? 2 : 4;
@@ -200,16 +276,19 @@ struct Cfg {
   static constexpr int kStageBytes = kPlanes * (kATile + kBTile);
   static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
   static constexpr int kTmemCols = 2 * kBN;     // double-buffered accumulator
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kEpiStage = kEpiWarps * kStageWarpBytes;  // TMA-store staging of the epilogue warps
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiStage + 1024 + 256;
 };
 
 template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, Params p) {
   using C = Cfg<kFmt, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* epi_stage = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + C::kEpiStage);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -223,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -327,7 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4 =====
-    const int q = warp & 3;
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;  // two warps per quarter split the column chunks
     uint32_t local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int split = t / tiles_mn, r = t % tiles_mn;
@@ -338,27 +418,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The gate (activation of the layer below) is streamed one 32-column
         // chunk ahead: chunk 0 is fetched while the MMAs are still running.
         uint4 graw[8];
-        if (row < p.M) gate_issue<kFmt>(p.gate, row, n0, graw);
+        if (row < p.M) gate_issue<kFmt>(p.gate, row, n0 + half * 32, graw);
         mbar_wait(&tfull[acc], use & 1);
         tc_fence_after();
-        uint32_t gm = row < p.M ? gate_mask<kFmt>(p.gate, row, n0, graw) : 0u;
+        uint32_t gm = row < p.M ? gate_mask<kFmt>(p.gate, row, n0 + half * 32, graw) : 0u;
 #pragma unroll 1
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          const bool more = ch + 1 < kBN / 32 && row < p.M;
-          if (more) gate_issue<kFmt>(p.gate, row, n0 + (ch + 1) * 32, graw);
+        for (int ch = half; ch < kBN / 32; ch += 2) {
+          const bool more = ch + 2 < kBN / 32 && row < p.M;
+          if (more) gate_issue<kFmt>(p.gate, row, n0 + (ch + 2) * 32, graw);
           uint32_t raw[32];
           tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
-          if (row < p.M) {
+          float v[32];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              float v[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                v[i] = (gm >> (g * 8 + i)) & 1u ? __uint_as_float(raw[g * 8 + i]) * p.gate_scale : 0.f;
-              act_store8(p.out, row, n0 + ch * 32 + g * 8, v);
-            }
-          }
-          if (more) gm = gate_mask<kFmt>(p.gate, row, n0 + (ch + 1) * 32, graw);
+          for (int i = 0; i < 32; ++i) v[i] = (gm >> i) & 1u ? __uint_as_float(raw[i]) * p.gate_scale : 0.f;
+          epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n0 + ch * 32,
+                          m0 + q * 32, local * (kBN / 64) + (ch >> 1));
+          if (more) gm = gate_mask<kFmt>(p.gate, row, n0 + (ch + 2) * 32, graw);
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -367,47 +442,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int ch = 0; ch < kBN / 32; ++ch) {
+      for (int ch = half; ch < kBN / 32; ch += 2) {
         uint32_t raw[32];
         tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
-        if (row < p.M) {
-          const int n = n0 + ch * 32;
-          if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
-            float bv[32];
-            if (p.bias) {
+        const int n = n0 + ch * 32;
+        if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
+          float v[32];
+          if (p.bias) {
 #pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + g);
-                bv[4 * g] = b4.x; bv[4 * g + 1] = b4.y; bv[4 * g + 2] = b4.z; bv[4 * g + 3] = b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) bv[i] = 0.f;
-            }
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              float v[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float x = __uint_as_float(raw[g * 8 + i]) + bv[g * 8 + i];
-                v[i] = p.relu ? fmaxf(x, 0.f) : x;
-              }
-              if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
-#pragma unroll 1
-                for (int i = 0; i < 8; ++i) {
-                  const int64_t idx = row * p.ldm + n + g * 8 + i;
-                  if (p.drop_mode == 1) {
-                    v[i] *= p.mask[idx];
-                  } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
-                    const float mk = uniform_hash(p.seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
-                    p.mask[idx] = mk;
-                    v[i] *= mk;
-                  }
-                }
-              }
-              act_store8(p.out, row, n + g * 8, v);
+            for (int g = 0; g < 8; ++g) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + g);
+              v[4 * g] = b4.x; v[4 * g + 1] = b4.y; v[4 * g + 2] = b4.z; v[4 * g + 3] = b4.w;
             }
           } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(raw[i]) + v[i];
+            v[i] = p.relu ? fmaxf(x, 0.f) : x;
+          }
+          if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
+            if (row < p.M) {
+#pragma unroll 1
+              for (int i = 0; i < 32; ++i) {
+                const int64_t idx = row * p.ldm + n + i;
+                if (p.drop_mode == 1) {
+                  v[i] *= p.mask[idx];
+                } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
+                  const float mk = uniform_hash(p.seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
+                  p.mask[idx] = mk;
+                  v[i] *= mk;
+                }
+              }
+            }
+          }
+          epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
+                          local * (kBN / 64) + (ch >> 1));
+        } else if (row < p.M) {
+          {
             float* dst = p.c + (kEpi == EPI_PARTIAL ? (int64_t)split * p.M * p.ldc : 0) + row * p.ldc + n;
 #pragma unroll
             for (int g = 0; g < 8; ++g)
@@ -420,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores drained
   }
   tc_fence_before();
   __syncthreads();
@@ -445,7 +520,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D map over (cols, rows, plane) of a row-major operand; box = one 128-byte
 // swizzle row of columns by box_rows rows.
 static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows,
-                    bool atom32 = false) {
+                    bool atom32 = false, bool no_swizzle = false) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -460,7 +535,8 @@ static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, v.dtype == DIPPM_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   3, v.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                             : (atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r, (long long)rows,
@@ -479,7 +555,7 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes));
     attr_set = true;
   }
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   int st;
   // A logical (M x K); B logical (N x K).
   if (!kAMN) st = make_map(&ma, a->a, a->M, a->K, Cf::kBK, kBM);
@@ -514,7 +590,13 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.seed = a->seed;
   const int total = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::min(total, num_sms());
-  kern<<<grid, kThreads, Cf::kSmemBytes, s>>>(ma, mb, p);
+  if (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP || kEpi == EPI_GATE) {
+    st = make_map(&mc, a->out, a->M, a->N, 32, 32, false, true);  // epilogue TMA-store target
+    if (st) return st;
+  } else {
+    mc = ma;  // unused
+  }
+  kern<<<grid, kThreads, Cf::kSmemBytes, s>>>(ma, mb, mc, p);
   DIPPM_LAUNCH_CHECK("k_tc_gemm");
   return DIPPM_OK;
 }

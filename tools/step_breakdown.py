@@ -48,7 +48,8 @@ class GemmWrap:
         e0.record()
         r = orig_gemm(args, backend, stream)
         e1.record()
-        records.append((f"{gemm_kind[args.kind]} M{args.M} N{args.N} K{args.K}", e0, e1))
+        m = "G" if args.M <= 8192 and args.kind != 2 else ("N" if args.kind != 2 else "H")
+        records.append((f"{gemm_kind[args.kind]} M={m} N{args.N} K{'rows' if args.K > 8192 else args.K}", e0, e1))
         return r
 
 
