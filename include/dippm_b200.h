@@ -123,7 +123,18 @@ int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t num_nodes, 
                                const int32_t* t_rowptr, const int32_t* t_col, const float* inv_deg,
                                float* colsum_partial, void* stream);
 
-/* Readout backward — gnn.py:224,227: dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0),
+/* Layer-3 variant with the readout backward fused in (gnn.py:224, 227): dz3 is
+ * formed on the fly as dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0), written to
+ * B's left half, while agg^T dz3 goes to the right half and the bias partial
+ * sums to colsum_partial.  node_graph [N] maps node -> graph (dippm_node_graph). */
+int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t* graph_ptr,
+                                  const int32_t* node_graph, dippm_act_t h3, dippm_act_t B, int32_t width,
+                                  int64_t num_nodes, const int32_t* t_rowptr, const int32_t* t_col,
+                                  const float* inv_deg, float* colsum_partial, void* stream);
+/* node_graph[v] = g for v in [graph_ptr[g], graph_ptr[g+1]). */
+int32_t dippm_node_graph(const int32_t* graph_ptr, int64_t num_graphs, int32_t* node_graph, void* stream);
+
+/* Readout backward alone — gnn.py:224,227: dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0),
  * du [G, ld_du] fp32. */
 int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t num_graphs,
                                int32_t width, dippm_act_t h3, dippm_act_t dz_out, int64_t num_nodes, void* stream);

@@ -93,12 +93,24 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
 // ReLU gate fused in its epilogue).  Also emits per-block column partial sums
 // of dz (bias gradient, gnn.py:230), reduced over the block's row slots in a
 // fixed order.  write_agg = 0: partial sums only.
-template <int DT, int CPL>
+// kReadout: layer 3 — dz3 is not materialised yet; it is formed on the fly from
+// the readout gradient (gnn.py:224, 227): dz3[v] = du[g(v)] / N_g * (h3[v] > 0),
+// written into B's left half while g = agg^T dz3 goes to the right half.  All
+// neighbours of v lie in v's graph, so one graph id per row suffices.
+struct ReadoutArgs {
+  const float* du;          // [G, ld_du] fp32 (dr = du[:, :width])
+  int64_t ld_du;
+  const int* graph_ptr;     // [G+1]
+  const int* node_graph;    // [N]
+  ActView h3;               // ReLU gate
+};
+
+template <int DT, int CPL, bool kReadout>
 __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
                                                                 const int* __restrict__ t_rowptr,
                                                                 const int* __restrict__ t_col,
                                                                 const float* __restrict__ inv_deg,
-                                                                float* __restrict__ colsum_partial) {
+                                                                float* __restrict__ colsum_partial, ReadoutArgs ro) {
   extern __shared__ float s_part[];  // [8 warps * gpw][width]
   __shared__ int s_ptr[kRowsPerBlock + 1];
   __shared__ int s_col[kAggColCap];
@@ -128,7 +140,29 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
     for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
       const int64_t row = r0 + lr;
       float own[CPL][8];
-      load_chunks<DT, CPL>(B, row, c0, stride, own);
+      float dr[CPL][8];  // readout: du[g(row)] / N_g (shared by the row and its neighbours)
+      if constexpr (kReadout) {
+        const int g = ro.node_graph[row];
+        const float inv_n = 1.0f / (float)(ro.graph_ptr[g + 1] - ro.graph_ptr[g]);
+        const float* dp = ro.du + (int64_t)g * ro.ld_du;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride));
+          const float4 b2 = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride + 4));
+          dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
+          dr[q][4] = b2.x * inv_n; dr[q][5] = b2.y * inv_n; dr[q][6] = b2.z * inv_n; dr[q][7] = b2.w * inv_n;
+        }
+        float hg[CPL][8];
+        load_chunks<DT, CPL>(ro.h3, row, c0, stride, hg);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) own[q][k] = hg[q][k] > 0.f ? dr[q][k] : 0.f;
+          act_store8_t<DT>(B, row, c0 + q * stride, own[q]);
+        }
+      } else {
+        load_chunks<DT, CPL>(B, row, c0, stride, own);
+      }
       if (write_agg) {
         const int b = s_ptr[lr], e = s_ptr[lr + 1];
         float acc[CPL][8] = {};
@@ -136,7 +170,15 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
           const int v0 = staged ? s_col[j] : t_col[cbeg + j];
           const float w0 = staged ? s_cw[j] : inv_deg[v0];
           float x[CPL][8];
-          load_chunks<DT, CPL>(B, v0, c0, stride, x);
+          if constexpr (kReadout) {
+            load_chunks<DT, CPL>(ro.h3, v0, c0, stride, x);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) x[q][k] = x[q][k] > 0.f ? dr[q][k] : 0.f;
+          } else {
+            load_chunks<DT, CPL>(B, v0, c0, stride, x);
+          }
 #pragma unroll
           for (int q = 0; q < CPL; ++q)
 #pragma unroll
@@ -202,10 +244,18 @@ __global__ void __launch_bounds__(1024) k_reduce_rows(const float* __restrict__ 
   __shared__ double s[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
-  double acc = 0.0;
-  if (c < cols)
-    for (int64_t r = ty; r < rows; r += 32) acc += (double)in[r * ld + c];
-  s[ty][tx] = acc;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains: 4 loads in flight
+  if (c < cols) {
+    int64_t r = ty;
+    for (; r + 96 < rows; r += 128) {
+      a0 += (double)in[r * ld + c];
+      a1 += (double)in[(r + 32) * ld + c];
+      a2 += (double)in[(r + 64) * ld + c];
+      a3 += (double)in[(r + 96) * ld + c];
+    }
+    for (; r < rows; r += 32) a0 += (double)in[r * ld + c];
+  }
+  s[ty][tx] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (ty == 0 && c < cols) {
     double t = 0.0;
@@ -214,33 +264,44 @@ __global__ void __launch_bounds__(1024) k_reduce_rows(const float* __restrict__ 
   }
 }
 
-// K4: one block per graph; u = [mean_g h3 | (fs - mu)/sigma | 0 ...] in the
-// head's operand dtype, row stride u.ld (>= width + 5, zero padded).
-__global__ void __launch_bounds__(kAggThreads) k_pool_concat(ActView h, const int* __restrict__ graph_ptr,
-                                                             int width, const float* __restrict__ fs_raw,
-                                                             const double* __restrict__ norm, ActView u) {
-  extern __shared__ float s_part[];
+// K4: one block per graph (16 warps); a warp reads a whole h3 row with
+// 128-bit loads (CPL chunks of 8 columns per lane), rows strided over the warps,
+// then a fixed-order smem reduction over warps.  u = [mean_g h3 | (fs-mu)/sigma | 0]
+// in the head's operand dtype, row stride u.ld (>= width + 5, zero padded).
+constexpr int kPoolThreads = 512;
+template <int DT, int CPL>
+__global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const int* __restrict__ graph_ptr,
+                                                              int width, const float* __restrict__ fs_raw,
+                                                              const double* __restrict__ norm, ActView u) {
+  extern __shared__ float s_part[];  // [slots][width]
   const int g = blockIdx.x;
-  const int chunks = width >> 3;
-  const int groups = kAggThreads / chunks;
-  const int grp = threadIdx.x / chunks, ch = threadIdx.x % chunks;
+  const int L = (width >> 3) / CPL, gpw = 32 / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / L, sub = lane % L;
+  const int slots = (kPoolThreads / 32) * gpw;
   const int64_t r0 = graph_ptr[g], r1 = graph_ptr[g + 1];
-  if (grp < groups) {
-    float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t row = r0 + grp; row < r1; row += groups) {
-      float x[8];
-      act_load8(h, row, ch * 8, x);
+  const int c0 = sub * 8, stride = L * 8;
+  if (grp < gpw) {
+    float part[CPL][8] = {};
+    for (int64_t row = r0 + warp * gpw + grp; row < r1; row += slots) {
+      float x[CPL][8];
+      load_chunks<DT, CPL>(h, row, c0, stride, x);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) part[k] += x[k];
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[q][k] += x[q][k];
     }
+    const int slot = warp * gpw + grp;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_part[grp * width + ch * 8 + k] = part[k];
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_part[slot * width + c0 + q * stride + k] = part[q][k];
   }
   __syncthreads();
   const float inv_n = 1.0f / (float)(r1 - r0);
   for (int c = threadIdx.x; c < width; c += blockDim.x) {
     float t = 0.f;
-    for (int q = 0; q < groups; ++q) t += s_part[q * width + c];
+    for (int q = 0; q < slots; ++q) t += s_part[q * width + c];
     act_store(u, g, c, t * inv_n);
   }
   for (int k = threadIdx.x; k < u.ld - width; k += blockDim.x) {
@@ -252,6 +313,12 @@ __global__ void __launch_bounds__(kAggThreads) k_pool_concat(ActView h, const in
     }
     act_store(u, g, width + k, v);
   }
+}
+
+// node -> graph id (for kernels that need g(v) per row).
+__global__ void k_node_graph(const int* __restrict__ graph_ptr, int* __restrict__ node_graph) {
+  const int g = blockIdx.x;
+  for (int v = graph_ptr[g] + threadIdx.x; v < graph_ptr[g + 1]; v += blockDim.x) node_graph[v] = g;
 }
 
 }  // namespace dippm
@@ -296,34 +363,51 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
   return DIPPM_OK;
 }
 
-int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
-                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
+                              const int32_t* t_col, const float* inv_deg, float* colsum_partial, ReadoutArgs ro,
+                              bool readout, cudaStream_t s) {
   DIPPM_ARG_CHECK(N >= 1 && width >= 8 && width % 8 == 0, "sage_aggregate_t: bad width %d", width);
   const int cpl = cpl_for(width);
   const int L = (width / 8) / cpl;
   DIPPM_ARG_CHECK((width / 8) % cpl == 0 && L <= 32 && 32 % L == 0, "sage_aggregate_t: unsupported width %d", width);
   const size_t smem = (size_t)(kAggThreads / 32) * (32 / L) * width * sizeof(float);
   DIPPM_ARG_CHECK(smem <= 160 * 1024, "sage_aggregate_t: width %d too large", width);
-  cudaStream_t s = (cudaStream_t)stream;
   const int grid = ceil_div_i(N, kRowsPerBlock);
   ActView bv = make_view(B);
-#define DIPPM_AGGT(D, C)                                                                                      \
-  do {                                                                                                        \
-    if (smem > 48 * 1024)                                                                                     \
-      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                            (int)smem));                                                      \
-    k_aggregate_t<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
-                                                       colsum_partial);                                       \
+#define DIPPM_AGGT(D, C, R)                                                                                      \
+  do {                                                                                                           \
+    if (smem > 48 * 1024)                                                                                        \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            (int)smem));                                                         \
+    k_aggregate_t<D, C, R><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
+                                                          colsum_partial, ro);                                   \
   } while (0)
-#define DIPPM_AGGT_C(D) \
-  do { if (cpl == 4) DIPPM_AGGT(D, 4); else if (cpl == 2) DIPPM_AGGT(D, 2); else DIPPM_AGGT(D, 1); } while (0)
-  if (B.dtype == DIPPM_DT_BF16) DIPPM_AGGT_C(DIPPM_DT_BF16);
-  else if (B.dtype == DIPPM_DT_TF32X3) DIPPM_AGGT_C(DIPPM_DT_TF32X3);
-  else DIPPM_AGGT_C(DIPPM_DT_F32);
+#define DIPPM_AGGT_C(D, R) \
+  do { if (cpl == 4) DIPPM_AGGT(D, 4, R); else if (cpl == 2) DIPPM_AGGT(D, 2, R); else DIPPM_AGGT(D, 1, R); } while (0)
+#define DIPPM_AGGT_R(D) do { if (readout) DIPPM_AGGT_C(D, true); else DIPPM_AGGT_C(D, false); } while (0)
+  if (B.dtype == DIPPM_DT_BF16) DIPPM_AGGT_R(DIPPM_DT_BF16);
+  else if (B.dtype == DIPPM_DT_TF32X3) DIPPM_AGGT_R(DIPPM_DT_TF32X3);
+  else DIPPM_AGGT_R(DIPPM_DT_F32);
+#undef DIPPM_AGGT_R
 #undef DIPPM_AGGT_C
 #undef DIPPM_AGGT
   DIPPM_LAUNCH_CHECK("k_aggregate_t");
   return DIPPM_OK;
+}
+
+int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
+                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+  ReadoutArgs ro{};
+  return launch_aggregate_t(B, width, N, write_agg, t_rowptr, t_col, inv_deg, colsum_partial, ro, false,
+                            (cudaStream_t)stream);
+}
+
+int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t* graph_ptr, const int32_t* node_graph,
+                                  dippm_act_t h3, dippm_act_t B, int32_t width, int64_t N, const int32_t* t_rowptr,
+                                  const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+  DIPPM_ARG_CHECK(h3.dtype == B.dtype && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
+  ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3)};
+  return launch_aggregate_t(B, width, N, 1, t_rowptr, t_col, inv_deg, colsum_partial, ro, true, (cudaStream_t)stream);
 }
 
 int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t G, int32_t width,
@@ -345,12 +429,36 @@ int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t col
 
 int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, int32_t width, const float* fs_raw,
                           const double* norm, dippm_act_t u, void* stream) {
-  DIPPM_ARG_CHECK(G >= 1 && width % 8 == 0 && width / 8 <= kAggThreads && u.ld >= width + 5, "pool_concat: bad args");
-  const int groups = kAggThreads / (width / 8);
-  size_t smem = (size_t)groups * width * sizeof(float);
-  k_pool_concat<<<(unsigned)G, kAggThreads, smem, (cudaStream_t)stream>>>(make_view(h), graph_ptr, width, fs_raw,
-                                                                         norm, make_view(u));
+  DIPPM_ARG_CHECK(G >= 1 && width >= 8 && width % 8 == 0 && u.ld >= width + 5, "pool_concat: bad args");
+  const int cpl = cpl_for(width);
+  const int L = (width / 8) / cpl;
+  DIPPM_ARG_CHECK((width / 8) % cpl == 0 && L <= 32 && 32 % L == 0, "pool_concat: unsupported width %d", width);
+  const size_t smem = (size_t)(kPoolThreads / 32) * (32 / L) * width * sizeof(float);
+  DIPPM_ARG_CHECK(smem <= 160 * 1024, "pool_concat: width %d too large", width);
+  cudaStream_t s = (cudaStream_t)stream;
+  ActView hv = make_view(h), uv = make_view(u);
+#define DIPPM_POOL(D, C)                                                                                         \
+  do {                                                                                                           \
+    if (smem > 48 * 1024)                                                                                        \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_pool_concat<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                            (int)smem));                                                         \
+    k_pool_concat<D, C><<<(unsigned)G, kPoolThreads, smem, s>>>(hv, graph_ptr, width, fs_raw, norm, uv);         \
+  } while (0)
+#define DIPPM_POOL_C(D) \
+  do { if (cpl == 4) DIPPM_POOL(D, 4); else if (cpl == 2) DIPPM_POOL(D, 2); else DIPPM_POOL(D, 1); } while (0)
+  if (h.dtype == DIPPM_DT_BF16) DIPPM_POOL_C(DIPPM_DT_BF16);
+  else if (h.dtype == DIPPM_DT_TF32X3) DIPPM_POOL_C(DIPPM_DT_TF32X3);
+  else DIPPM_POOL_C(DIPPM_DT_F32);
+#undef DIPPM_POOL_C
+#undef DIPPM_POOL
   DIPPM_LAUNCH_CHECK("k_pool_concat");
+  return DIPPM_OK;
+}
+
+int32_t dippm_node_graph(const int32_t* graph_ptr, int64_t G, int32_t* node_graph, void* stream) {
+  DIPPM_ARG_CHECK(G >= 1, "node_graph: no graphs");
+  k_node_graph<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(graph_ptr, node_graph);
+  DIPPM_LAUNCH_CHECK("k_node_graph");
   return DIPPM_OK;
 }
 

@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
     for (int k = 0; k < segs.n; ++k) {
       const auto& sg = segs.s[k];
       const int64_t j = i - sg.src_off;
-      if (j >= 0 && j < sg.rows * sg.cols) act_store(sg.dst, j / sg.cols, sg.dst_col_off + j % sg.cols, f);
+      if (j >= 0 && j < sg.rows * sg.cols) {  // 32-bit div/mod: segments are < 2^31 elements
+        const uint32_t jj = (uint32_t)j, cc = (uint32_t)sg.cols;
+        act_store(sg.dst, jj / cc, sg.dst_col_off + jj % cc, f);
+      }
     }
   }
 }

@@ -175,6 +175,7 @@ class Batch:
     edge_ptr: torch.Tensor | None = None  # i64 [G+1] when edges are grouped by graph (fast CSR path)
     max_nodes: int = 0                    # largest graph (nodes / edges) for the per-graph CSR kernel
     max_edges: int = 0
+    node_graph: torch.Tensor | None = None  # i32 [N] node -> graph id
 
 
 def group_edges(src, dst, graph_ptr):
@@ -270,6 +271,8 @@ def build_batch_csr(b: Batch, grouped: bool | None = None) -> Batch:
     b.t_rowptr = torch.empty(N + 1, **i32)
     b.t_col = torch.empty(max(E, 1), **i32)
     b.bad = torch.empty(1, **i32)
+    b.node_graph = torch.empty(max(N, 1), **i32)
+    _lib.call("dippm_node_graph", _p(b.graph_ptr), b.G, _p(b.node_graph), _stream())
     lib = _lib.load()
     if grouped is None:
         grouped = (b.edge_ptr is not None and b.G <= GROUPED_MAX_GRAPHS and b.max_edges <= GROUPED_MAX_EDGES
@@ -478,13 +481,16 @@ class Engine:
         _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
         self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws.head_splits[1], ws, "fc1.w")
         self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
-        _lib.call("dippm_readout_backward", _p(ws.du), hp, _p(b.graph_ptr), b.G, hp, ws.H3.view(0),
-                  ws.B[0].view(0), N, s)
         cur = 0
         for i in (2, 1, 0):
             B = ws.B[cur]
-            _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
-                      _p(b.inv_deg), _p(ws.colsum), s)
+            if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
+                _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
+                          ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr), _p(b.t_col), _p(b.inv_deg),
+                          _p(ws.colsum), s)
+            else:
+                _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
+                          _p(b.inv_deg), _p(ws.colsum), s)
             _lib.call("dippm_reduce_rows", _p(ws.colsum), nblk, hp, hp, 1.0, self._g32(f"sage{i + 1}.bias"), s)
             self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws.splits[i], ws, f"sage{i + 1}.w_self")
             if i > 0:
