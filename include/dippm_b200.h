@@ -176,6 +176,7 @@ typedef struct dippm_gemm_args {
   int64_t ldm;
   double drop_p;
   uint64_t seed;
+  const int64_t* seed_dev; /* nullable device step counter mixed into the dropout seed (graph replays) */
 } dippm_gemm_args_t;
 
 /* Split count the tensor-core WGRAD would like for this problem. */
@@ -242,8 +243,11 @@ typedef struct dippm_pack_seg {
   dippm_act_t dst;
 } dippm_pack_seg_t;
 int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
-                        int64_t t, double lr, double beta1, double beta2, double eps, int32_t do_adam, float* p32,
-                        const dippm_pack_seg_t* segs, int32_t nsegs, void* stream);
+                        int64_t t, const int64_t* t_dev, double lr, double beta1, double beta2, double eps,
+                        int32_t do_adam, float* p32, const dippm_pack_seg_t* segs, int32_t nsegs, void* stream);
+/*   t_dev (nullable): device step counter; when given it overrides t (CUDA-graph replays). */
+/* t_dev[0] += 1 on the stream (the per-step counter a captured training step replays). */
+int32_t dippm_step_counter(int64_t* t_dev, void* stream);
 
 /* Pack a fp64 matrix into a compute copy (tests / single-layer API):
  *  w [rows, cols] fp64 row-major -> dst view; transpose != 0 writes dst[c, r]. */

@@ -41,7 +41,7 @@ class GemmArgs(C.Structure):
         ("bias", C.c_void_p), ("relu", C.c_int64), ("out", Act),
         ("c", C.c_void_p), ("ldc", C.c_int64), ("splits", C.c_int64),
         ("gate", Act), ("gate_scale", C.c_double), ("drop_mode", C.c_int64), ("mask", C.c_void_p),
-        ("ldm", C.c_int64), ("drop_p", C.c_double), ("seed", C.c_uint64),
+        ("ldm", C.c_int64), ("drop_p", C.c_double), ("seed", C.c_uint64), ("seed_dev", C.c_void_p),
     ]
 
 
@@ -82,7 +82,8 @@ SIGNATURES = {
     "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),
     "dippm_huber": (I32, [P, P, I64, P, F64, F64, P, P, P]),
-    "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),
+    "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, P, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),
+    "dippm_step_counter": (I32, [P, P]),
     "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
 }
 

@@ -63,10 +63,15 @@ struct PackSegs {
 __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, double* __restrict__ m,
                                                    double* __restrict__ v, const float* __restrict__ g,
                                                    double gscale, int64_t n, double lr, double b1, double b2,
-                                                   double eps, double bc1, double bc2, int do_adam,
+                                                   double eps, double bc1, double bc2, const int64_t* t_dev, int do_adam,
                                                    float* __restrict__ p32, PackSegs segs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (t_dev && do_adam) {  // step count on the device (CUDA-graph replays): bias corrections from it
+    const double t = (double)t_dev[0];
+    bc1 = 1.0 - pow(b1, t);
+    bc2 = 1.0 - pow(b2, t);
+  }
   for (; i < n; i += stride) {
     double val = p[i];
     if (do_adam) {
@@ -101,6 +106,8 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
     }
   }
 }
+
+__global__ void k_step_counter(int64_t* t) { t[0] += 1; }
 
 __global__ void k_pack(const double* __restrict__ w, int64_t rows, int64_t cols, int transpose, ActView dst) {
   // 32x32 tile transpose through shared memory when transpose != 0.
@@ -156,9 +163,9 @@ int32_t dippm_mig_codes(const double* mem_mb, int64_t stride, int64_t count, int
 }
 
 int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads, double grad_scale, int64_t n,
-                        int64_t t, double lr, double beta1, double beta2, double eps, int32_t do_adam, float* p32,
-                        const dippm_pack_seg_t* segs, int32_t nsegs, void* stream) {
-  DIPPM_ARG_CHECK(n >= 0 && (t >= 1 || !do_adam), "adam_pack: bad n/t");
+                        int64_t t, const int64_t* t_dev, double lr, double beta1, double beta2, double eps,
+                        int32_t do_adam, float* p32, const dippm_pack_seg_t* segs, int32_t nsegs, void* stream) {
+  DIPPM_ARG_CHECK(n >= 0 && (t >= 1 || t_dev || !do_adam), "adam_pack: bad n/t");
   DIPPM_ARG_CHECK(nsegs >= 0 && nsegs <= DIPPM_MAX_PACK_SEGS, "adam_pack: %d segments (max %d)", nsegs,
                   DIPPM_MAX_PACK_SEGS);
   if (n == 0) return DIPPM_OK;
@@ -173,12 +180,18 @@ int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads
     ps.s[k].dst_col_off = segs[k].dst_col_off;
     ps.s[k].dst = make_view(segs[k].dst);
   }
-  double bc1 = do_adam ? 1.0 - pow(beta1, (double)t) : 1.0;
-  double bc2 = do_adam ? 1.0 - pow(beta2, (double)t) : 1.0;
+  double bc1 = do_adam && t >= 1 ? 1.0 - pow(beta1, (double)t) : 1.0;
+  double bc2 = do_adam && t >= 1 ? 1.0 - pow(beta2, (double)t) : 1.0;
   int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 8 * num_sms());
   k_adam_pack<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1, beta2, eps,
-                                                        bc1, bc2, do_adam, p32, ps);
+                                                        bc1, bc2, t_dev, do_adam, p32, ps);
   DIPPM_LAUNCH_CHECK("k_adam_pack");
+  return DIPPM_OK;
+}
+
+int32_t dippm_step_counter(int64_t* t_dev, void* stream) {
+  k_step_counter<<<1, 1, 0, (cudaStream_t)stream>>>(t_dev);
+  DIPPM_LAUNCH_CHECK("k_step_counter");
   return DIPPM_OK;
 }
 

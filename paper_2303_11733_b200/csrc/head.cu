@@ -333,6 +333,12 @@ int32_t dippm_gemm_simt_impl(const dippm_gemm_args_t* a, cudaStream_t s) {
   e.ldm = a->ldm;
   e.p = (float)a->drop_p;
   e.seed = a->seed;
+  if (a->seed_dev) {  // host copy of the device counter is not available here: the SIMT anchor is eager-only
+    int64_t t = 0;
+    cudaMemcpyAsync(&t, a->seed_dev, sizeof(t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    e.seed ^= (uint64_t)t * 0x9E3779B97F4A7C15ull;
+  }
   e.gate = make_view(a->gate);
   e.gate_scale = (float)a->gate_scale;
   e.c = a->c;

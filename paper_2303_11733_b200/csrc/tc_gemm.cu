@@ -47,6 +47,7 @@ struct Params {
   int64_t ldm;
   float drop_p;
   uint64_t seed;
+  const int64_t* seed_dev;
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[i] = p.relu ? fmaxf(x, 0.f) : x;
           }
           if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
+            const uint64_t seed = p.seed ^ (p.seed_dev ? (uint64_t)p.seed_dev[0] * 0x9E3779B97F4A7C15ull : 0ull);
             if (row < p.M) {
 #pragma unroll 1
               for (int i = 0; i < 32; ++i) {
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.drop_mode == 1) {
                   v[i] *= p.mask[idx];
                 } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
-                  const float mk = uniform_hash(p.seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
+                  const float mk = uniform_hash(seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
                   p.mask[idx] = mk;
                   v[i] *= mk;
                 }
@@ -588,6 +590,7 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.ldm = a->ldm;
   p.drop_p = (float)a->drop_p;
   p.seed = a->seed;
+  p.seed_dev = a->seed_dev;
   const int total = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::min(total, num_sms());
   if (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP || kEpi == EPI_GATE) {

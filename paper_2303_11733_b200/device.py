@@ -347,7 +347,7 @@ class Engine:
         self.grads = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.p32 = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.norm = torch.zeros(16, **f64)
-        self.t = 0
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)  # Adam step count (graph-safe)
         hp, dt, d = L.hp, self.dtype, self.device
         self.Wf = [ActBuf(2 * di, hp, dt, d) for di in L.d_in]
         self.Wd = [None] + [ActBuf(di, 2 * hp, dt, d) for di in L.d_in[1:]]
@@ -384,7 +384,12 @@ class Engine:
     def reset_adam(self) -> None:
         self.m.zero_()
         self.v.zero_()
-        self.t = 0
+        self.t_dev.zero_()
+
+    @property
+    def t(self) -> int:
+        """Adam step count (lives on the device so captured steps advance it)."""
+        return int(self.t_dev.item())
 
     def _unpack(self, flat: np.ndarray) -> dict:
         return {name: self.L.unpad(name, flat[off:off + int(np.prod(self.L.shapes[name]))].reshape(self.L.shapes[name]))
@@ -398,8 +403,8 @@ class Engine:
 
     def _adam_pack(self, do_adam: int, lr=0.0, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale=1.0) -> None:
         _lib.call("dippm_adam_pack", _p(self.params), _p(self.m), _p(self.v), _p(self.grads), grad_scale,
-                  self.L.total, self.t, lr, beta1, beta2, eps, do_adam, _p(self.p32), self._segs, len(self._segs),
-                  _stream())
+                  self.L.total, 0, _p(self.t_dev), lr, beta1, beta2, eps, do_adam, _p(self.p32), self._segs,
+                  len(self._segs), _stream())
         self.launches += 1
 
     def refresh(self) -> None:
@@ -407,8 +412,8 @@ class Engine:
         self._adam_pack(0)
 
     def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale: float = 1.0) -> None:
-        """numerics.adam_step over all 15 tensors + operand refresh: one launch."""
-        self.t += 1
+        """numerics.adam_step over all 15 tensors + operand refresh (t += 1 on the device first)."""
+        _lib.call("dippm_step_counter", _p(self.t_dev), _stream())
         self._adam_pack(1, lr, beta1, beta2, eps, grad_scale)
 
     def _f32(self, name: str) -> int:
@@ -419,9 +424,9 @@ class Engine:
 
     # -- kernels --------------------------------------------------------------
     def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1,
-              gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0):
+              gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None):
         args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits, gate, gate_scale,
-                        drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1))
+                        drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1), seed_dev)
         if self.gemm_hook is not None:
             self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
@@ -455,7 +460,7 @@ class Engine:
         for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
             self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,
                        out=out.view(), drop_mode=drop, mask=ws.masks[j].data_ptr(), ldm=hp, drop_p=dropout_p,
-                       seed=seed * 2 + j)
+                       seed=seed * 2 + j, seed_dev=_p(self.t_dev) if drop == 2 else None)
         _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
                   _p(self.norm), _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None,
                   _p(ws.nonfinite), s)

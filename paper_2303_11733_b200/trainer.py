@@ -23,7 +23,7 @@ from .device import Batch, Engine, Workspace, build_batch_csr
 class BatchTrainer:
     def __init__(self, model, precision: str = "bf16", lr: float = 2.754e-5, seed: int = 0, dropout: bool = True,
                  huber_delta: float = 1.0, allreduce=None, world_size: int = 1, rank: int = 0, device=None,
-                 backend: str = "tc"):
+                 backend: str = "tc", use_graphs: bool = False):
         self.model = model
         self.engine = Engine(model.hidden, precision, device, backend)
         self.engine.set_params(model.param_items(), model.normalizer)
@@ -31,7 +31,11 @@ class BatchTrainer:
         self.dropout_p = model.dropout_p if dropout else 0.0
         self.allreduce = allreduce
         self.world_size, self.rank = world_size, rank
+        self.use_graphs = use_graphs
+        self._graphs, self._keep, self._warm = {}, [], False
+        self._pool = torch.cuda.graph_pool_handle() if use_graphs else None
         self.steps = 0
+        self.replayed_launches = 0  # kernels launched by graph replays (not seen by dippm_launch_count)
         self.ws = None
         self._stage = None
         self._loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
@@ -39,6 +43,8 @@ class BatchTrainer:
     def reserve(self, max_nodes: int, max_graphs: int, max_edges: int | None = None) -> None:
         """Preallocate the workspace (and host-batch staging) for batches up to this size."""
         self.ws = Workspace(self.engine, max_nodes, max_graphs, train=True)
+        self._graphs.clear()  # captured steps point into the old workspace
+        self._keep.clear()
         e = max_edges if max_edges is not None else 2 * max_nodes
         d = self.engine.device
         self._stage = {
@@ -61,12 +67,44 @@ class BatchTrainer:
         (`global_graphs`, default G x world), so the all-reduced SUM of the
         per-rank gradients is the global batch mean (gnn.py:402-404)."""
         self._ensure(b)
+        self.steps += 1
+        if not self.use_graphs:
+            self._step(b, global_graphs)
+            return
+        # CUDA graphs: the trainer's first step runs eagerly (module load, kernel
+        # attributes); afterwards each resident batch's step is captured once
+        # and replayed.  Step-dependent values (Adam's t, the dropout stream)
+        # live on the device, so replays advance them.
+        hit = self._graphs.get(id(b))
+        if hit is None:
+            if not self._warm:
+                self._step(b, global_graphs)
+                self._warm = True
+                return
+            hit = self.capture(b, global_graphs)
+        hit[0].replay()
+        self.replayed_launches += hit[1]
+
+    def capture(self, b: Batch, global_graphs: int | None = None):
+        """Record (without executing) the training step on resident batch `b` as a CUDA graph."""
+        if id(b) in self._graphs:
+            return self._graphs[id(b)]
+        self._ensure(b)
+        g = torch.cuda.CUDAGraph()
+        lib = dev._lib.load()
+        l0 = lib.dippm_launch_count()
+        with torch.cuda.graph(g, pool=self._pool):
+            self._step(b, global_graphs)
+        hit = self._graphs[id(b)] = (g, lib.dippm_launch_count() - l0)
+        self._keep.append(b)  # captured pointers must stay alive
+        return hit
+
+    def _step(self, b: Batch, global_graphs: int | None) -> None:
         eng, ws = self.engine, self.ws
         build_batch_csr(b)
-        self.steps += 1
         mode = 2 if self.dropout_p > 0 else 0
-        eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p,
-                    seed=(self.seed * 1000003 + self.steps) * 131 + self.rank, predict=False)
+        eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 131 + self.rank,
+                    predict=False)
         den = 0.0
         if self.allreduce is not None:
             den = float(global_graphs if global_graphs else b.G * self.world_size)
@@ -100,7 +138,9 @@ class BatchTrainer:
             gp = np.asarray(graph_ptr)
             b.edge_ptr, b.max_nodes = views[6], int(np.diff(gp).max())
             b.max_edges = int(np.diff(ep).max()) if len(ep) > 1 else 0
-        self.step_resident(b)
+        self._ensure(b)
+        self.steps += 1
+        self._step(b, None)  # ragged shapes: host batches run eagerly
         self._loss_host.copy_(self.ws.loss[:1], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return float(self._loss_host[0])

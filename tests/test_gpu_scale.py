@@ -132,3 +132,22 @@ def test_batched_training_step_matches_backward_and_adam(cfg1):
         big = np.abs(grads[k]) > 1e-3 * np.abs(grads[k]).max()
         assert np.mean(np.sign(upd[big]) == np.sign(ref_upd[big])) > 0.999, k
         assert np.allclose(upd[big], ref_upd[big], rtol=1e-3, atol=1e-7), k
+
+
+def test_cuda_graph_replay_equals_eager_steps(cfg1):
+    """Captured-and-replayed training steps (dropout on, bf16) are bit-identical to
+    eager steps: Adam's t and the dropout stream advance on the device."""
+    ds, _, model = cfg1
+    finals = []
+    for graphs in (False, True):
+        tr = BatchTrainer(model, precision="bf16", lr=1e-3, dropout=True, use_graphs=graphs)
+        b = upload_batch(*ds.collate(np.arange(64)), device="cuda", build_csr=False)
+        losses = []
+        for _ in range(4):
+            tr.step_resident(b)
+            losses.append(float(tr.ws.loss[0]))
+        assert tr.engine.t == 4
+        finals.append((tr.engine.params.cpu().numpy(), losses))
+    assert np.array_equal(finals[0][0], finals[1][0])
+    assert finals[0][1] == finals[1][1]
+    assert len(set(finals[0][1])) == 4  # the steps really differ (masks and params move)
