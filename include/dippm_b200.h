@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 1
+#define DIPPM_ABI_VERSION 2
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -149,8 +149,12 @@ int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t col
  *   FWD:    out = act(A @ B^T + bias)   A [M,K] (= [h | m]), B [N,K] packed W^T
  *           — gnn.py:207-209 (z = h@W_self + m@W_neigh + bias; h = relu(z))
  *   STORE:  C[M,N] fp32 = A @ B^T        — dgrad, gnn.py:232 (dz @ W^T)
- *   WGRAD:  C_s[M,N] fp32 partials of A^T-style products with both operands
- *           MN-major: C = dz^T @ [h | m] split over row chunks s — gnn.py:228-229
+ *   WGRAD:  C[M,N] fp32 = A^T-style product with both operands MN-major, the reduction
+ *           (over node rows) split in `splits` chunks — gnn.py:228-229
+ *           ([h | m]^T @ dz = [dW_self; dW_neigh]).  With tile_sync != NULL the kernel
+ *           reduces the split partials itself (fixed split order, fp64 sums, see
+ *           tile_sync) and writes out = out_scale * C into `out` (F32 view); with
+ *           tile_sync == NULL it only writes the partials C_s to c.
  * Operand "major": 0 = K-major ([rows, K] row-major), 1 = MN-major ([K, rows]). */
 enum dippm_gemm_kind { DIPPM_GEMM_FWD = 0, DIPPM_GEMM_STORE = 1, DIPPM_GEMM_WGRAD = 2, DIPPM_GEMM_GATE = 3 };
 /*   GATE:   out = (gate > 0) * gate_scale * (A @ B^T)  — dgrad fused with the ReLU (+dropout)
@@ -166,7 +170,7 @@ typedef struct dippm_gemm_args {
   const float* bias;   /* FWD: [N] fp32 */
   int64_t relu;        /* FWD */
   dippm_act_t out;     /* FWD output view */
-  float* c;            /* STORE: [M, ldc]; WGRAD: [splits, M, ldc] */
+  float* c;            /* STORE: [M, ldc]; WGRAD: [splits, M, ldc] partials (unused if splits == 1 and fused) */
   int64_t ldc;
   int64_t splits;      /* WGRAD split count (>=1); others 1 */
   dippm_act_t gate;    /* GATE: out = gate > 0 ? acc * gate_scale : 0 (ReLU' of the layer below, */
@@ -177,10 +181,20 @@ typedef struct dippm_gemm_args {
   double drop_p;
   uint64_t seed;
   const int64_t* seed_dev; /* nullable device step counter mixed into the dropout seed (graph replays) */
+  uint32_t* relu_bits;       /* FWD (optional): bit c%32 of word [r*bits_ld + c/32] = (stored out[r,c] > 0) */
+  const uint32_t* gate_bits; /* GATE (optional): use these bits instead of reading `gate` values          */
+                             /* (relu_bits / gate_bits: tensor-core backend; the SIMT anchor gates on values) */
+  int64_t bits_ld;           /* words per row of relu_bits / gate_bits (>= N/32)                           */
+  int64_t cta_pair;          /* 0 auto, 1 force 1-CTA 128-row tiles, 2 force cta_group::2 256-row tiles   */
+  int32_t* tile_sync;        /* WGRAD fused reduce: device int32[dippm_wgrad_sync_ints(M, N)], zeroed once  */
+                             /* by the caller; every launch leaves it zero again (graph-replay safe)      */
+  double out_scale;          /* WGRAD fused reduce: out = out_scale * sum_s C_s                            */
 } dippm_gemm_args_t;
 
 /* Split count the tensor-core WGRAD would like for this problem. */
 int32_t dippm_wgrad_splits(int64_t M, int64_t N, int64_t K);
+/* Size (int32 elements) of the WGRAD tile_sync counter array for an M x N output. */
+int64_t dippm_wgrad_sync_ints(int64_t M, int64_t N);
 int32_t dippm_gemm(const dippm_gemm_args_t* args, int32_t backend, void* stream);
 
 /* out[j*ldo + i] = scale * sum_s in[s*M*N + i*N + j]  (split-K reduce + transpose; fixed order) */

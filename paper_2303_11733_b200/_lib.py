@@ -33,6 +33,9 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
+ABI_VERSION = 2  # DIPPM_ABI_VERSION in include/dippm_b200.h
+
+
 class GemmArgs(C.Structure):
     """dippm_gemm_args_t."""
     _fields_ = [
@@ -42,6 +45,8 @@ class GemmArgs(C.Structure):
         ("c", C.c_void_p), ("ldc", C.c_int64), ("splits", C.c_int64),
         ("gate", Act), ("gate_scale", C.c_double), ("drop_mode", C.c_int64), ("mask", C.c_void_p),
         ("ldm", C.c_int64), ("drop_p", C.c_double), ("seed", C.c_uint64), ("seed_dev", C.c_void_p),
+        ("relu_bits", C.c_void_p), ("gate_bits", C.c_void_p), ("bits_ld", C.c_int64), ("cta_pair", C.c_int64),
+        ("tile_sync", C.c_void_p), ("out_scale", C.c_double),
     ]
 
 
@@ -75,6 +80,7 @@ SIGNATURES = {
     "dippm_node_graph": (I32, [P, I64, P, P]),
     "dippm_reduce_rows": (I32, [P, I64, I64, I32, F64, P, P]),
     "dippm_wgrad_splits": (I32, [I64, I64, I64]),
+    "dippm_wgrad_sync_ints": (I64, [I64, I64]),
     "dippm_gemm": (I32, [C.POINTER(GemmArgs), I32, P]),
     "dippm_splitk_reduce_t": (I32, [P, I32, I64, I64, F64, P, I64, P]),
     "dippm_pool_concat": (I32, [Act, P, I64, I32, P, P, Act, P]),
@@ -103,6 +109,8 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.dippm_abi_version() != ABI_VERSION:
+        raise DeviceUnavailable(f"{LIB_PATH.name} has ABI {lib.dippm_abi_version()}, expected {ABI_VERSION}; rebuild it")
     _lib = lib
     return lib
 

@@ -109,6 +109,17 @@ __global__ void __launch_bounds__(256) k_simt_gemm(Operand A, Operand B, int64_t
   }
 }
 
+// out[i*ldo + j] = scale * sum_s in[s*M*ldc + i*ldc + j] (fixed split order, fp64 sums)
+__global__ void k_splitk_reduce(const float* __restrict__ in, int64_t splits, int64_t M, int64_t N, int64_t ldc,
+                                double scale, float* __restrict__ out, int64_t ldo) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * N) return;
+  const int64_t i = idx / N, j = idx % N;
+  double a = 0.0;
+  for (int64_t s = 0; s < splits; ++s) a += (double)in[s * M * ldc + i * ldc + j];
+  out[i * ldo + j] = (float)(a * scale);
+}
+
 static int launch_simt(const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, const Epi& e,
                        cudaStream_t s) {
   dim3 grid(ceil_div_i(N, kTN), ceil_div_i(M, kTM));
@@ -347,6 +358,18 @@ int32_t dippm_gemm_simt_impl(const dippm_gemm_args_t* a, cudaStream_t s) {
   if (a->kind != DIPPM_GEMM_WGRAD) return launch_simt(A, B, a->M, a->N, a->K, e, s);
   // WGRAD: reduction over K split in `splits` contiguous chunks.
   int64_t splits = a->splits < 1 ? 1 : a->splits;
+  const bool fused = a->tile_sync != nullptr;
+  if (fused && !a->c) {  // no workspace (single split): compute into out, then scale in place
+    DIPPM_ARG_CHECK(splits == 1 && a->out.data, "gemm WGRAD: fused reduce needs out and (splits > 1) c");
+    e.c = reinterpret_cast<float*>(a->out.data);
+    e.ldc = a->out.ld;
+    int st = launch_simt(A, B, a->M, a->N, a->K, e, s);
+    if (st) return st;
+    k_splitk_reduce<<<ceil_div_i(a->M * a->N, 256), 256, 0, s>>>(e.c, 1, a->M, a->N, e.ldc, a->out_scale, e.c,
+                                                                 e.ldc);
+    DIPPM_LAUNCH_CHECK("k_splitk_reduce");
+    return DIPPM_OK;
+  }
   for (int64_t sp = 0; sp < splits; ++sp) {
     int64_t k0 = sp * a->K / splits, k1 = (sp + 1) * a->K / splits;
     Epi es = e;
@@ -360,6 +383,12 @@ int32_t dippm_gemm_simt_impl(const dippm_gemm_args_t* a, cudaStream_t s) {
     Bs.p = (const char*)B.p + k0 * B.sr * (B.dtype == DIPPM_DT_BF16 ? 2 : 4);
     int st = launch_simt(As, Bs, a->M, a->N, k1 - k0, es, s);
     if (st) return st;
+  }
+  if (fused) {
+    DIPPM_ARG_CHECK(a->out.data != nullptr, "gemm WGRAD: fused reduce needs an out view");
+    k_splitk_reduce<<<ceil_div_i(a->M * a->N, 256), 256, 0, s>>>(a->c, splits, a->M, a->N, a->ldc, a->out_scale,
+                                                                 reinterpret_cast<float*>(a->out.data), a->out.ld);
+    DIPPM_LAUNCH_CHECK("k_splitk_reduce");
   }
   return DIPPM_OK;
 }

@@ -48,6 +48,17 @@ struct Params {
   float drop_p;
   uint64_t seed;
   const int64_t* seed_dev;
+  uint32_t* relu_bits;        // FWD: optional 1-bit (out > 0) mask, bits_ld words per row
+  const uint32_t* gate_bits;  // GATE: optional 1-bit gate instead of gate values
+  int64_t bits_ld;
+  // WGRAD output: reduce_mode 0 = partials to c only; 1 = fused reduce, every split CTA
+  // reduces a row slice once all splits of its tile have landed (all tiles co-resident);
+  // 2 = fused reduce by the last split to arrive; 3 = single split, write wout directly.
+  int reduce_mode;
+  float* wout;
+  int64_t ldo;
+  double out_scale;
+  int* sync;
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -266,14 +277,16 @@ __device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtenso
   }
 }
 
-template <int kFmt, int kBN>
+template <int kFmt, int kBN, int kCta>
 struct Cfg {
   static constexpr int kElem = kFmt == 1 ? 2 : 4;
   static constexpr int kBK = 128 / kElem;       // one 128-byte swizzle row of K (or of MN) per k-block
   static constexpr int kUK = 32 / kElem;        // K per tcgen05.mma (16 bf16 / 8 tf32)
   static constexpr int kPlanes = kFmt == 1 ? 1 : 2;
+  static constexpr int kBNl = kBN / kCta;       // B rows (N) held by each CTA of the pair
+  static constexpr int kTileM = kBM * kCta;     // output rows per (cluster) tile
   static constexpr int kATile = kBM * 128;      // bytes per plane
-  static constexpr int kBTile = kBN * 128;
+  static constexpr int kBTile = kBNl * 128;
   static constexpr int kStageBytes = kPlanes * (kATile + kBTile);
   static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
   static constexpr int kTmemCols = 2 * kBN;     // double-buffered accumulator
@@ -281,11 +294,105 @@ struct Cfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiStage + 1024 + 256;
 };
 
-template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi>
+// ---- CTA-pair (cta_group::2) plumbing -------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load whose completion is signalled on the leader CTA's mbarrier (2-SM mode)
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
+                                                 int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+template <int kFmt>
+__device__ __forceinline__ void umma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (kFmt == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+}
+// commit: arrive on the barrier at this offset in both CTAs of the pair once the MMAs retire
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Fixed-order split-K reduction of one CTA's 128-row tile slice: out = scale * sum_s C_s
+// (fp64 sums, split order 0..S-1, independent of which CTA reduces, so results are
+// deterministic).  Partials are read through L2 (ld.global.cg).
+template <int kBN>
+__device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, int n0, int r0, int r1, int tid) {
+  constexpr int kC4 = kBN / 4;
+  const int64_t plane = p.M * p.ldc;
+  for (int idx = tid; idx < (r1 - r0) * kC4; idx += kEpiWarps * 32) {
+    const int64_t r = m0 + r0 + idx / kC4;
+    const int c = n0 + (idx % kC4) * 4;
+    const float* src = p.c + r * p.ldc + c;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int s = 0;
+    for (; s + 8 <= p.splits; s += 8) {  // 8 loads in flight, summed in split order
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src + (s + j) * plane));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a0 += v[j].x; a1 += v[j].y; a2 += v[j].z; a3 += v[j].w;
+      }
+    }
+    for (; s < p.splits; ++s) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * plane));
+      a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+    }
+    const double sc = p.out_scale;
+    *reinterpret_cast<float4*>(p.wout + r * p.ldo + c) =
+        make_float4((float)(a0 * sc), (float)(a1 * sc), (float)(a2 * sc), (float)(a3 * sc));
+  }
+}
+
+// One persistent kernel for both tile shapes.  kCta == 2: a cluster of two
+// CTAs on one TPC computes a 256 x kBN tile with cta_group::2 MMAs issued by the
+// even CTA; each CTA stages its own 128 A rows and half of the kBN B rows, so
+// per-SM operand traffic from L2 drops by a third against the 1-CTA 128 x kBN
+// tile (the 1-CTA kernel is L2-bandwidth-bound; profiles/README.md).
+template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi, int kCta>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, Params p) {
-  using C = Cfg<kFmt, kBN>;
+  using C = Cfg<kFmt, kBN, kCta>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + C::kStages * C::kStageBytes;
@@ -296,6 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = kCta == 2 ? cluster_rank() : 0u;
+  const int cid = blockIdx.x / kCta, ncl = gridDim.x / kCta;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -303,19 +412,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 32 * kEpiWarps);
+      mbar_init(&tempty[b], kEpiWarps * kCta);  // one arrival per epilogue warp of each CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "r"(C::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kCta == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCta == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
@@ -325,11 +441,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs; completion signalled on the leader's barrier) =====
+      const uint32_t full_leader0 = kCta == 2 ? mapa(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         const int split = t / tiles_mn, r = t % tiles_mn;
-        const int m0 = (r / p.n_tiles) * kBM, n0 = (r % p.n_tiles) * kBN;
+        const int m0 = (r / p.n_tiles) * C::kTileM + (int)rank * kBM;
+        const int n0 = (r % p.n_tiles) * kBN + (int)rank * C::kBNl;
         const int kb0 = (int)((int64_t)split * kb_total / p.splits);
         const int kb1 = (int)((int64_t)(split + 1) * kb_total / p.splits);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -337,32 +455,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
           uint8_t* sa = smem + s * C::kStageBytes;
           uint8_t* sb = sa + C::kPlanes * C::kATile;
-          mbar_expect_tx(&full[s], C::kStageBytes);
+          if (rank == 0) mbar_expect_tx(&full[s], C::kStageBytes * kCta);
+          const uint32_t fb = full_leader0 + s * 8;
           const int k0 = kb * C::kBK;
 #pragma unroll
           for (int pl = 0; pl < C::kPlanes; ++pl) {
+            auto load = [&](void* dst, const CUtensorMap* map, int x, int y) {
+              if constexpr (kCta == 2) tma_load_3d_pair(dst, map, fb, x, y, pl);
+              else tma_load_3d(dst, map, &full[s], x, y, pl);
+            };
             if constexpr (!kAMN) {
-              tma_load_3d(sa + pl * C::kATile, &tmA, &full[s], k0, m0, pl);
+              load(sa + pl * C::kATile, &tmA, k0, m0);
             } else {
 #pragma unroll
-              for (int c = 0; c < kBM / C::kBK; ++c)
-                tma_load_3d(sa + pl * C::kATile + c * C::kBK * 128, &tmA, &full[s], m0 + c * C::kBK, k0, pl);
+              for (int c = 0; c < kBM / C::kBK; ++c) load(sa + pl * C::kATile + c * C::kBK * 128, &tmA, m0 + c * C::kBK, k0);
             }
             if constexpr (!kBMN) {
-              tma_load_3d(sb + pl * C::kBTile, &tmB, &full[s], k0, n0, pl);
+              load(sb + pl * C::kBTile, &tmB, k0, n0);
             } else {
 #pragma unroll
-              for (int c = 0; c < kBN / C::kBK; ++c)
-                tma_load_3d(sb + pl * C::kBTile + c * C::kBK * 128, &tmB, &full[s], n0 + c * C::kBK, k0, pl);
+              for (int c = 0; c < C::kBNl / C::kBK; ++c)
+                load(sb + pl * C::kBTile + c * C::kBK * 128, &tmB, n0 + c * C::kBK, k0);
             }
           }
         }
       }
+      // tail: every MMA commit aimed at this CTA's empty barriers has landed before exit
+      for (int i = 0; i < C::kStages; ++i, ++it) mbar_wait(&empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (one thread) =====
-      constexpr uint32_t idesc = make_idesc(kFmt, kAMN, kBMN, kBM, kBN);
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (one thread of the leader CTA) =====
+      constexpr uint32_t idesc = make_idesc(kFmt, kAMN, kBMN, C::kTileM, kBN);
       constexpr uint32_t a_lbo = kAMN ? C::kBK * 128 : 16, b_lbo = kBMN ? C::kBK * 128 : 16;
       constexpr uint32_t a_step = kAMN ? C::kUK * 128 : 32, b_step = kBMN ? C::kUK * 128 : 32;
       // 32-bit MN-major operands use the 128B swizzle with 32-byte atoms
@@ -371,8 +495,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr bool a32 = kAMN && kFmt == 2, b32 = kBMN && kFmt == 2;
       constexpr uint64_t a_lay = a32 ? 1 : 2, b_lay = b32 ? 1 : 2;
       constexpr uint32_t a_sbo = a32 ? 512 : 1024, b_sbo = b32 ? 512 : 1024;
+      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+        if constexpr (kCta == 2) umma_pair<kFmt>(d, a, b, idesc, acc);
+        else umma<kFmt>(d, a, b, idesc, acc);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (kCta == 2) umma_commit_pair(bar);
+        else umma_commit(bar);
+      };
       uint32_t it = 0, local = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      for (int t = cid; t < total; t += ncl, ++local) {
         const int split = t / tiles_mn;
         const int kb0 = (int)((int64_t)split * kb_total / p.splits);
         const int kb1 = (int)((int64_t)(split + 1) * kb_total / p.splits);
@@ -391,31 +523,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < C::kBK / C::kUK; ++j) {
             const uint64_t a_hi = sdesc(sa + j * a_step, a_lbo, a_sbo, a_lay);
             const uint64_t b_hi = sdesc(sb + j * b_step, b_lbo, b_sbo, b_lay);
-            umma<kFmt>(d, a_hi, b_hi, idesc, first ? 0u : 1u);
+            mma(d, a_hi, b_hi, first ? 0u : 1u);
             first = 0;
             if constexpr (C::kPlanes == 2) {
               const uint64_t a_lo = sdesc(sa + C::kATile + j * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t b_lo = sdesc(sb + C::kBTile + j * b_step, b_lbo, b_sbo, b_lay);
-              umma<kFmt>(d, a_hi, b_lo, idesc, 1u);
-              umma<kFmt>(d, a_lo, b_hi, idesc, 1u);
+              mma(d, a_hi, b_lo, 1u);
+              mma(d, a_lo, b_hi, 1u);
             }
           }
-          umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
+          commit(&empty[s]);  // frees the smem slot (in both CTAs) when these MMAs retire
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        commit(&tfull[acc]);  // accumulator ready for the epilogue(s)
       }
     }
   } else {
-    // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4 =====
+    // ===== epilogue warps 2..9: TMEM lane quarter = warp % 4 =====
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;  // two warps per quarter split the column chunks
+    const uint32_t tempty_leader0 = kCta == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    auto release = [&](uint32_t acc) {  // this warp is done reading accumulator `acc`
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (kCta == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
+    };
     uint32_t local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+    for (int t = cid; t < total; t += ncl, ++local) {
       const int split = t / tiles_mn, r = t % tiles_mn;
-      const int m0 = (r / p.n_tiles) * kBM, n0 = (r % p.n_tiles) * kBN;
+      const int m0 = (r / p.n_tiles) * C::kTileM + (int)rank * kBM, n0 = (r % p.n_tiles) * kBN;
       const uint32_t acc = local & 1, use = local >> 1;
       const int64_t row = (int64_t)m0 + q * 32 + lane;
       if constexpr (kEpi == EPI_GATE) {
+        if (p.gate_bits) {
+          // 1-bit ReLU' masks written by the forward epilogue: one word per 32 columns.
+          uint32_t gw[kBN / 64];
+#pragma unroll
+          for (int i = 0; i < kBN / 64; ++i)
+            gw[i] = row < p.M ? __ldg(p.gate_bits + row * p.bits_ld + (n0 >> 5) + half + 2 * i) : 0u;
+          mbar_wait(&tfull[acc], use & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int i = 0; i < kBN / 64; ++i) {
+            const int ch = half + 2 * i;
+            uint32_t raw[32];
+            tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = (gw[i] >> j) & 1u ? __uint_as_float(raw[j]) * p.gate_scale : 0.f;
+            epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n0 + ch * 32,
+                            m0 + q * 32, local * (kBN / 64) + i);
+          }
+          release(acc);
+          continue;
+        }
         // The gate (activation of the layer below) is streamed one 32-column
         // chunk ahead: chunk 0 is fetched while the MMAs are still running.
         uint4 graw[8];
@@ -436,8 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           m0 + q * 32, local * (kBN / 64) + (ch >> 1));
           if (more) gm = gate_mask<kFmt>(p.gate, row, n0 + (ch + 2) * 32, graw);
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release(acc);
         continue;
       }
       mbar_wait(&tfull[acc], use & 1);
@@ -480,10 +642,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          if (p.relu_bits && row < p.M) {  // 1-bit ReLU' (and dropout) mask for the backward GATE epilogue
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bits |= (uint32_t)(v[i] > 0.f) << i;
+            p.relu_bits[row * p.bits_ld + (n >> 5)] = bits;
+          }
           epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
                           local * (kBN / 64) + (ch >> 1));
         } else if (row < p.M) {
-          {
+          if (kEpi == EPI_PARTIAL && p.reduce_mode == 3) {  // single split: final output, scaled
+            float* dst = p.wout + row * p.ldo + n;
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              reinterpret_cast<float4*>(dst)[g] =
+                  make_float4(__uint_as_float(raw[4 * g]) * p.out_scale, __uint_as_float(raw[4 * g + 1]) * p.out_scale,
+                              __uint_as_float(raw[4 * g + 2]) * p.out_scale,
+                              __uint_as_float(raw[4 * g + 3]) * p.out_scale);
+          } else {
             float* dst = p.c + (kEpi == EPI_PARTIAL ? (int64_t)split * p.M * p.ldc : 0) + row * p.ldc + n;
 #pragma unroll
             for (int g = 0; g < 8; ++g)
@@ -493,16 +669,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      release(acc);
+      if constexpr (kEpi == EPI_PARTIAL) {
+        if (p.reduce_mode == 1 || p.reduce_mode == 2) {
+          // ---- fused split-K reduction (replaces a separate reduce kernel) ----
+          const int tid = threadIdx.x - 64;
+          int* arrive = p.sync + r * kCta + rank;
+          int* depart = arrive + tiles_mn * kCta;
+          uint32_t* s_flag = tslot + 1;
+          epi_sync();  // this CTA's partial rows are all written
+          if (tid == 0) {
+            __threadfence();
+            const int old = atomicAdd(arrive, 1);
+            uint32_t go = 1;
+            if (p.reduce_mode == 1) {
+              uint32_t spins = 0;
+              uint64_t t0 = 0;
+              while (ld_acquire(arrive) < p.splits) {
+                if (++spins == 64) t0 = globaltimer();
+                if (spins > 64 && (spins & 255) == 0 && globaltimer() - t0 > 2000000000ull) __trap();
+              }
+            } else {
+              go = old == p.splits - 1;
+              if (go) __threadfence();
+            }
+            *s_flag = go;
+          }
+          epi_sync();
+          const int rows_valid = (int)(p.M - m0 < kBM ? p.M - m0 : kBM);
+          if (*s_flag && rows_valid > 0) {
+            const int r0 = p.reduce_mode == 1 ? (int)((int64_t)split * rows_valid / p.splits) : 0;
+            const int r1 = p.reduce_mode == 1 ? (int)((int64_t)(split + 1) * rows_valid / p.splits) : rows_valid;
+            reduce_rows_slice<kBN>(p, m0, n0, r0, r1, tid);
+          }
+          if (p.reduce_mode == 1) {
+            epi_sync();
+            if (tid == 0 && atomicAdd(depart, 1) == p.splits - 1) {  // every split is past its spin
+              *arrive = 0;
+              *depart = 0;
+            }
+          } else if (tid == 0 && *s_flag) {
+            *arrive = 0;  // the last arriver: all splits have arrived
+          }
+        }
+      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores drained
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCta == 2) cluster_sync_all();  // both CTAs done with TMEM and with remote barriers
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::kTmemCols));
+    if constexpr (kCta == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::kTmemCols));
   }
 }
 
@@ -548,10 +770,10 @@ static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_
   return DIPPM_OK;
 }
 
-template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi>
+template <int kFmt, bool kAMN, bool kBMN, int kBN, int kEpi, int kCta>
 static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
-  using Cf = Cfg<kFmt, kBN>;
-  auto kern = k_tc_gemm<kFmt, kAMN, kBMN, kBN, kEpi>;
+  using Cf = Cfg<kFmt, kBN, kCta>;
+  auto kern = k_tc_gemm<kFmt, kAMN, kBMN, kBN, kEpi, kCta>;
   static bool attr_set = false;
   if (!attr_set) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes));
@@ -559,11 +781,11 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   }
   CUtensorMap ma, mb, mc;
   int st;
-  // A logical (M x K); B logical (N x K).
+  // A logical (M x K); B logical (N x K).  Boxes are per CTA (B: kBN / kCta rows).
   if (!kAMN) st = make_map(&ma, a->a, a->M, a->K, Cf::kBK, kBM);
   else st = make_map(&ma, a->a, a->K, a->M, Cf::kBK, Cf::kBK, kFmt == 2);
   if (st) return st;
-  if (!kBMN) st = make_map(&mb, a->b, a->N, a->K, Cf::kBK, kBN);
+  if (!kBMN) st = make_map(&mb, a->b, a->N, a->K, Cf::kBK, Cf::kBNl);
   else st = make_map(&mb, a->b, a->K, a->N, Cf::kBK, Cf::kBK, kFmt == 2);
   if (st) return st;
   Params p{};
@@ -576,7 +798,7 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
     set_error("gemm: %d splits exceed %d k-blocks (use dippm_wgrad_splits)", p.splits, kb_total);
     return DIPPM_ERR_ARG;
   }
-  p.m_tiles = ceil_div_i(a->M, kBM);
+  p.m_tiles = ceil_div_i(a->M, Cf::kTileM);
   p.n_tiles = (int)(a->N / kBN);
   p.bias = a->bias;
   p.relu = (int)a->relu;
@@ -591,29 +813,67 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.drop_p = (float)a->drop_p;
   p.seed = a->seed;
   p.seed_dev = a->seed_dev;
+  p.relu_bits = a->relu_bits;
+  p.gate_bits = a->gate_bits;
+  p.bits_ld = a->bits_ld;
   const int total = p.m_tiles * p.n_tiles * p.splits;
-  const int grid = std::min(total, num_sms());
+  const int clusters = std::min(total, num_sms() / kCta);
+  p.reduce_mode = 0;
+  if (kEpi == EPI_PARTIAL && a->tile_sync) {
+    if (a->out.dtype != DIPPM_DT_F32 || !a->out.data || (p.splits > 1 && !a->c)) {
+      set_error("gemm WGRAD fused reduce: needs an F32 out view and (splits > 1) a partial workspace c");
+      return DIPPM_ERR_ARG;
+    }
+    p.reduce_mode = p.splits == 1 ? 3 : (total <= clusters ? 1 : 2);
+    p.wout = reinterpret_cast<float*>(a->out.data);
+    p.ldo = a->out.ld;
+    p.out_scale = a->out_scale;
+    p.sync = a->tile_sync;
+  }
   if (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP || kEpi == EPI_GATE) {
     st = make_map(&mc, a->out, a->M, a->N, 32, 32, false, true);  // epilogue TMA-store target
     if (st) return st;
   } else {
     mc = ma;  // unused
   }
-  kern<<<grid, kThreads, Cf::kSmemBytes, s>>>(ma, mb, mc, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * kCta);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cf::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kCta == 2 ? 1 : 0;
+  DIPPM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p));
   DIPPM_LAUNCH_CHECK("k_tc_gemm");
   return DIPPM_OK;
 }
 
-// BN choice: wide tiles when M supplies enough tiles to fill the GPU, narrower
-// ones for short problems (the FC head, M = #graphs) so more CTAs run.
+// Tile choice: 256 x 256 CTA-pair tiles when M is large (the SAGE layers,
+// M = nodes), 1-CTA 128 x BN tiles otherwise; narrower BN for short problems
+// (the FC head, M = #graphs) so more CTAs run.
 template <int kFmt, bool kAMN, bool kBMN, int kEpi>
 static int run_bn(const dippm_gemm_args_t* a, cudaStream_t s) {
   const int64_t m_tiles = ceil_div_i(a->M, kBM);
+  const bool pair_ok = a->N % 256 == 0;
+  const int64_t splits = kEpi == EPI_PARTIAL ? std::max<int64_t>(1, a->splits) : 1;
+  const bool pair = a->cta_pair == 2 ? pair_ok
+                                     : (a->cta_pair != 1 && pair_ok && a->M > kBM &&
+                                        4 * m_tiles * (a->N / 256) * splits >= 3 * num_sms());
+  if (a->cta_pair == 2 && !pair_ok) {
+    set_error("gemm: cta_pair=2 needs N %% 256 == 0 (N=%lld)", (long long)a->N);
+    return DIPPM_ERR_ARG;
+  }
+  if (pair) return run<kFmt, kAMN, kBMN, 256, kEpi, 2>(a, s);
   const bool narrow = kEpi != EPI_PARTIAL && m_tiles * (a->N / 256) < num_sms() / 2;
-  if (a->N % 256 == 0 && !narrow) return run<kFmt, kAMN, kBMN, 256, kEpi>(a, s);
+  if (a->N % 256 == 0 && !narrow) return run<kFmt, kAMN, kBMN, 256, kEpi, 1>(a, s);
   if (a->N % 128 == 0 && !(narrow && m_tiles * (a->N / 128) < num_sms() / 2))
-    return run<kFmt, kAMN, kBMN, 128, kEpi>(a, s);
-  return run<kFmt, kAMN, kBMN, 64, kEpi>(a, s);
+    return run<kFmt, kAMN, kBMN, 128, kEpi, 1>(a, s);
+  return run<kFmt, kAMN, kBMN, 64, kEpi, 1>(a, s);
 }
 
 template <int kFmt>
@@ -641,6 +901,10 @@ extern "C" int32_t dippm_wgrad_splits(int64_t M, int64_t N, int64_t K) {
   const int kb_total = ceil_div_i(K, 64);  // bf16 k-block; tf32 uses 32-row blocks (twice as many)
   int want = (int)std::max<int64_t>(1, num_sms() / std::max<int64_t>(1, tiles));
   return std::min(want, kb_total);  // every split owns >= 1 k-block for both k-block sizes
+}
+
+extern "C" int64_t dippm_wgrad_sync_ints(int64_t M, int64_t N) {
+  return 2 * (int64_t)ceil_div_i(M, tc::kBM) * ceil_div_i(N, 64);  // arrive + depart per (tile, CTA)
 }
 
 extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void* stream) {

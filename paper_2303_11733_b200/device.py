@@ -320,12 +320,20 @@ class Workspace:
             self.d1 = ActBuf(G, hp, dt, dev)
             self.du = torch.empty(G, hp, **f32)
             self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+            # 1-bit ReLU' masks of h1, h2 (and of the head's x2, dropout included) written by the
+            # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
+            self.relu_bits = torch.empty(2, N, hp // 32, dtype=torch.int32, device=dev)
+            self.head_bits = torch.empty(G, hp // 32, dtype=torch.int32, device=dev)
             self.colsum = torch.empty(lib.dippm_colsum_blocks(N), hp, **f32)
-            self.splits = [lib.dippm_wgrad_splits(hp, 2 * d, N) for d in eng.L.d_in]
-            self.head_splits = [lib.dippm_wgrad_splits(hp, hp, G), lib.dippm_wgrad_splits(hp, eng.L.u_width, G)]
+            # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
+            # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
+            self.splits = [lib.dippm_wgrad_splits(2 * d, hp, N) for d in eng.L.d_in]
+            self.head_splits = [lib.dippm_wgrad_splits(hp, hp, G), lib.dippm_wgrad_splits(eng.L.u_width, hp, G)]
             widest = max(max(s * 2 * d for s, d in zip(self.splits, eng.L.d_in)),
                          self.head_splits[0] * hp, self.head_splits[1] * eng.L.u_width)
             self.splitk = torch.empty(widest * hp, **f32)
+            sync = max(lib.dippm_wgrad_sync_ints(w, hp) for w in [2 * d for d in eng.L.d_in] + [eng.L.u_width])
+            self.tile_sync = torch.zeros(sync, dtype=torch.int32, device=dev)
 
 
 class Engine:
@@ -363,6 +371,7 @@ class Engine:
         segs.append(_lib.PackSeg(L.offsets["fc2.w"], hp, hp, 0, self.W2h.view()))
         self._segs = (_lib.PackSeg * len(segs))(*segs)
         self.launches = 0
+        self.cta_pair = 0       # GEMM tile policy passed to the library: 0 auto, 1 single-CTA, 2 CTA pair
         self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
 
     # -- parameters -----------------------------------------------------------
@@ -424,9 +433,11 @@ class Engine:
 
     # -- kernels --------------------------------------------------------------
     def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1,
-              gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None):
+              gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None,
+              relu_bits=None, gate_bits=None, bits_ld=0, tile_sync=None, out_scale=1.0):
         args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits, gate, gate_scale,
-                        drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1), seed_dev)
+                        drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1), seed_dev, relu_bits, gate_bits,
+                        bits_ld, self.cta_pair, tile_sync, out_scale)
         if self.gemm_hook is not None:
             self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
@@ -435,10 +446,11 @@ class Engine:
         self.launches += 1
 
     def _wgrad(self, dz: Act, x: Act, rows: int, width: int, splits: int, ws: Workspace, out_name: str) -> None:
-        """grads[out_name] (as [width, Hp]) = x^T @ dz over `rows` rows: split-K tcgen05 + fixed-order reduce."""
+        """grads[out_name] (as [width, Hp]) = x^T @ dz over `rows` rows (gnn.py:228-229, 296):
+        one split-K tcgen05 launch that also reduces its partials in fixed split order."""
         hp = self.L.hp
-        self._gemm(GEMM_WGRAD, hp, width, rows, dz, 1, x, 1, c=_p(ws.splitk), ldc=width, splits=splits)
-        _lib.call("dippm_splitk_reduce_t", _p(ws.splitk), splits, hp, width, 1.0, self._g32(out_name), hp, _stream())
+        self._gemm(GEMM_WGRAD, width, hp, rows, x, 1, dz, 1, out=Act(self._g32(out_name), hp, 0, DT_F32),
+                   c=_p(ws.splitk), ldc=hp, splits=splits, tile_sync=_p(ws.tile_sync), out_scale=1.0)
 
     def forward(self, b: Batch, ws: Workspace, mask_mode: int = 0, dropout_p: float = 0.0, seed: int = 0,
                 predict: bool = True) -> None:
@@ -448,19 +460,22 @@ class Engine:
         _lib.call("dippm_sage_aggregate", f32_act(b.x), ws.A[0].view(FEATURE_WIDTH), ws.A[0].view(0), b.N,
                   FEATURE_WIDTH, _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
         outs = [ws.A[1].view(0), ws.A[2].view(0), ws.H3.view(0)]
+        bits = ws.relu_bits if ws.train else None
         for i in range(3):
             if i > 0:
                 _lib.call("dippm_sage_aggregate", ws.A[i].view(0), ws.A[i].view(hp), NULL_ACT, b.N, hp,
                           _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
             self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.Wf[i].view(), 1,
-                       bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i])
+                       bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i],
+                       relu_bits=_p(bits[i]) if bits is not None and i < 2 else None, bits_ld=hp // 32)
         _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
                   ws.u.view(), s)
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
         for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
             self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,
                        out=out.view(), drop_mode=drop, mask=ws.masks[j].data_ptr(), ldm=hp, drop_p=dropout_p,
-                       seed=seed * 2 + j, seed_dev=_p(self.t_dev) if drop == 2 else None)
+                       seed=seed * 2 + j, seed_dev=_p(self.t_dev) if drop == 2 else None,
+                       relu_bits=_p(ws.head_bits) if ws.train and j == 0 else None, bits_ld=hp // 32)
         _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
                   _p(self.norm), _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None,
                   _p(ws.nonfinite), s)
@@ -482,7 +497,7 @@ class Engine:
                   self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
         self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws.head_splits[0], ws, "fc2.w")
         self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
-                   gate=ws.x2.view(), gate_scale=keep_scale)
+                   gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=hp // 32)
         _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
         self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws.head_splits[1], ws, "fc1.w")
         self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
@@ -500,6 +515,7 @@ class Engine:
             self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws.splits[i], ws, f"sage{i + 1}.w_self")
             if i > 0:
                 self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
-                           out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0)
+                           out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
+                           gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=hp // 32)
                 cur = 1 - cur
         self.launches += 5 + 3 * 2

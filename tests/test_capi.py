@@ -26,7 +26,7 @@ def test_every_declared_symbol_is_exported_and_bound():
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
-    assert lib.dippm_abi_version() == 1
+    assert lib.dippm_abi_version() == _lib.ABI_VERSION
 
 
 def test_header_is_plain_c():

@@ -190,11 +190,13 @@ def test_pool_concat_and_mig_codes(golden):
 
 def _gemm(kind, M, N, K, a, a_mn, b, b_mn, backend=0, **kw):
     f = dict(bias=None, relu=0, out=dev.NULL_ACT, c=None, ldc=0, splits=1, gate=dev.NULL_ACT, gate_scale=1.0,
-             drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0)
+             drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None, relu_bits=None, gate_bits=None,
+             bits_ld=0, cta_pair=0, tile_sync=None, out_scale=1.0)
     f.update(kw)
     args = _lib.GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, f["bias"], f["relu"], f["out"], f["c"], f["ldc"],
                          f["splits"], f["gate"], f["gate_scale"], f["drop_mode"], f["mask"], f["ldm"], f["drop_p"],
-                         f["seed"])
+                         f["seed"], f["seed_dev"], f["relu_bits"], f["gate_bits"], f["bits_ld"], f["cta_pair"],
+                         f["tile_sync"], f["out_scale"])
     _lib.check(_lib.load().dippm_gemm(args, backend, dev._stream()))
 
 
@@ -341,3 +343,94 @@ def test_grouped_csr_equals_global_path(golden, case):
         assert np.array_equal(f, s)
     # an edge crossing graphs is rejected by the grouped kernel
     assert group_edges(np.array([0, 5]), np.array([1, 1]), np.array([0, 3, 6])) is None
+
+
+def _bits_of(x):
+    """[M, N] bool -> [M, N/32] int32 words, bit c%32 of word c/32."""
+    b = x.reshape(x.shape[0], -1, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)
+    return b.sum(-1).astype(np.uint32).view(np.int32)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("M", [612, 3001, 20000])
+def test_cta_pair_tiles_equal_single_cta(prec, M):
+    """cta_group::2 256x256 tiles (incl. a last pair whose second CTA is wholly past M)
+    give the same results as 1-CTA tiles for every GEMM kind; FWD's 1-bit ReLU mask
+    equals (out > 0) and GATE on those bits equals GATE on the activation values."""
+    rng = np.random.default_rng(M)
+    dt = dev.PRECISIONS[prec]
+    N, K = 512, 1024
+    A, a64, _ = _rand_act(M, K, dt, rng)
+    Wn, wn64, _ = _rand_act(K, N, dt, rng, 0.05)   # natural [K, N] weights: MN-major B
+    Wk, wk64, _ = _rand_act(N, K, dt, rng, 0.05)   # [N, K]: K-major B
+    bias = torch.from_numpy(rng.normal(size=N).astype(np.float32)).cuda()
+    ref_fwd = np.maximum(a64 @ wn64 + bias.double().cpu().numpy(), 0)
+    tol = 1e-5 * np.abs(ref_fwd).max()
+    res = {}
+    for pair in (1, 2):
+        out = ActBuf(M, N, dt, "cuda")
+        bits = torch.full((M, N // 32), -1, dtype=torch.int32, device="cuda")
+        _gemm(_lib.GEMM_FWD, M, N, K, A.view(), 0, Wn.view(), 1, bias=bias.data_ptr(), relu=1, out=out.view(),
+              relu_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair)
+        h = out.to_float().double().cpu().numpy()
+        assert np.max(np.abs(h - ref_fwd)) <= (2e-2 if prec == "bf16" else 1e-5) * np.abs(ref_fwd).max()
+        assert np.array_equal(bits.cpu().numpy(), _bits_of(h > 0)), pair
+        # GATE: values vs bits
+        g_val = ActBuf(M, N, dev.DT_F32, "cuda")
+        g_bit = ActBuf(M, N, dev.DT_F32, "cuda")
+        _gemm(_lib.GEMM_GATE, M, N, K, A.view(), 0, Wk.view(), 0, out=g_val.view(), gate=out.view(),
+              gate_scale=1.5, cta_pair=pair)
+        _gemm(_lib.GEMM_GATE, M, N, K, A.view(), 0, Wk.view(), 0, out=g_bit.view(), gate=dev.NULL_ACT,
+              gate_scale=1.5, gate_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair)
+        assert torch.equal(g_val.t, g_bit.t)
+        ref_gate = np.where(h > 0, 1.5 * (a64 @ wk64.T), 0.0)
+        assert np.max(np.abs(g_val.t.double().cpu().numpy() - ref_gate)) <= 1e-5 * np.abs(ref_gate).max()
+        # STORE
+        c = torch.full((M, N), float("nan"), device="cuda")
+        _gemm(_lib.GEMM_STORE, M, N, K, A.view(), 0, Wk.view(), 0, c=c.data_ptr(), ldc=N, cta_pair=pair)
+        # WGRAD (MN-major both): C[N=512 features, K=1024] over M rows
+        S = _lib.load().dippm_wgrad_splits(N, K, M)
+        ws = torch.full((S, N, K), float("nan"), device="cuda")
+        dz, dz64, _ = (out, h, None)
+        _gemm(_lib.GEMM_WGRAD, N, K, M, dz.view(), 1, A.view(), 1, c=ws.data_ptr(), ldc=K, splits=S, cta_pair=pair)
+        wg = torch.empty(K, N, device="cuda")
+        _lib.call("dippm_splitk_reduce_t", ws.data_ptr(), S, N, K, 1.0, wg.data_ptr(), N, dev._stream())
+        ref_w = a64.T @ h
+        assert np.max(np.abs(wg.double().cpu().numpy() - ref_w)) <= 1e-5 * (np.abs(a64).T @ np.abs(h)).max()
+        res[pair] = (out.t.clone(), g_val.t.clone(), c.clone(), wg.clone())
+    for x1, x2 in zip(res[1], res[2]):  # same per-element k order: expected bit-identical
+        x1, x2 = x1.double(), x2.double()
+        assert torch.allclose(x1, x2, rtol=0, atol=1e-6 * float(x1.abs().max())), float((x1 - x2).abs().max())
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("R,M,N,splits", [(76800, 1024, 512, 0), (76800, 64, 512, 0), (3000, 576, 512, 0),
+                                          (5000, 1024, 512, 1), (20000, 1024, 512, 20), (300, 512, 512, 3)])
+def test_wgrad_fused_reduce(prec, R, M, N, splits):
+    """WGRAD with the in-kernel split-K reduction (tile_sync): every reduce mode
+    (slice-parallel, last-arriver, single split) equals the separate fixed-order
+    reduce of the same partials bit for bit, and matches fp64; the counters are
+    left zero (the launch can be replayed)."""
+    rng = np.random.default_rng(R + M)
+    dt = dev.PRECISIONS[prec]
+    X, x64, _ = _rand_act(R, M, dt, rng)
+    dz, dz64, _ = _rand_act(R, N, dt, rng)
+    lib = _lib.load()
+    S = splits or lib.dippm_wgrad_splits(M, N, R)
+    sync = torch.zeros(lib.dippm_wgrad_sync_ints(M, N), dtype=torch.int32, device="cuda")
+    ref = x64.T @ dz64
+    scale_ref = (np.abs(x64).T @ np.abs(dz64)).max()
+    for backend in (0, 1):
+        ws = torch.full((S, M, N), float("nan"), device="cuda")
+        out = torch.full((M, N), float("nan"), device="cuda")
+        for rep in range(2):
+            _gemm(_lib.GEMM_WGRAD, M, N, R, X.view(), 1, dz.view(), 1, backend, out=dev.f32_act(out),
+                  c=ws.data_ptr(), ldc=N, splits=S, tile_sync=sync.data_ptr(), out_scale=0.5)
+            assert int(sync.abs().sum()) == 0
+        got = out.double().cpu().numpy()
+        assert np.max(np.abs(got - 0.5 * ref)) <= 1e-5 * scale_ref, (backend, np.max(np.abs(got - 0.5 * ref)))
+        if S > 1:
+            sep = ws[0].double()
+            for k in range(1, S):  # fp64 sum of the same partials in split order
+                sep += ws[k].double()
+            assert torch.equal(out, (sep * 0.5).float()), backend

@@ -52,20 +52,45 @@ for prec in ("bf16", "fp32"):
 
     def g(kind, a, amn, b, bmn, Mm, Nn, Kk, **kw):
         f = dict(bias=None, relu=0, out=dev.NULL_ACT, c=None, ldc=0, splits=1, gate=dev.NULL_ACT, gate_scale=1.0,
-                 drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0)
+                 drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, relu_bits=None, gate_bits=None, bits_ld=0,
+                 cta_pair=0, tile_sync=None, out_scale=1.0)
         f.update(kw)
         args = _lib.GemmArgs(kind, Mm, Nn, Kk, a, amn, b, bmn, f["bias"], f["relu"], f["out"], f["c"], f["ldc"],
                              f["splits"], f["gate"], f["gate_scale"], f["drop_mode"], f["mask"], f["ldm"],
-                             f["drop_p"], f["seed"])
+                             f["drop_p"], f["seed"], None, f["relu_bits"], f["gate_bits"], f["bits_ld"],
+                             f["cta_pair"], f["tile_sync"], f["out_scale"])
         return lambda: _lib.check(lib.dippm_gemm(args, 0, dev._stream()))
 
-    cases = {
-        "fwd  A:K B:K  ": g(0, A.view(), 0, Wk.view(), 0, M, N, K, bias=bias.data_ptr(), relu=1, out=out.view()),
-        "fwd  A:K B:MN ": g(0, A.view(), 0, Wmn.view(), 1, M, N, K, bias=bias.data_ptr(), relu=1, out=out.view()),
-        "gate A:K B:K  ": g(3, A.view(), 0, Wk.view(), 0, M, N, K, out=out.view(), gate=gate.view()),
-        "store(N=1024) ": g(1, dz.view(), 0, Wmn.view(), 0, M, K, N, c=c.data_ptr(), ldc=K),
-        "wgrad MN/MN   ": g(2, dz.view(), 1, A.view(), 1, N, K, M, c=ws.data_ptr(), ldc=K, splits=S),
-    }
+    bits = torch.zeros(M, N // 32, dtype=torch.int32, device="cuda")
+    Sf = lib.dippm_wgrad_splits(K, N, M)
+    sync = torch.zeros(lib.dippm_wgrad_sync_ints(K, N), dtype=torch.int32, device="cuda")
+    wout = torch.empty(K, N, device="cuda")
+    X1 = act(M, 64, dt)
+    S1 = lib.dippm_wgrad_splits(64, N, M)
+    wout1 = torch.empty(64, N, device="cuda")
+    cases = {}
+    for pair in (1, 2):
+        cases.update({
+            f"fwd  A:K B:K  pair{pair}": g(0, A.view(), 0, Wk.view(), 0, M, N, K, bias=bias.data_ptr(), relu=1,
+                                           out=out.view(), cta_pair=pair),
+            f"fwd  A:K B:MN pair{pair}": g(0, A.view(), 0, Wmn.view(), 1, M, N, K, bias=bias.data_ptr(), relu=1,
+                                           out=out.view(), cta_pair=pair),
+            f"fwd +bits     pair{pair}": g(0, A.view(), 0, Wmn.view(), 1, M, N, K, bias=bias.data_ptr(), relu=1,
+                                           out=out.view(), relu_bits=bits.data_ptr(), bits_ld=N // 32,
+                                           cta_pair=pair),
+            f"gate values   pair{pair}": g(3, A.view(), 0, Wk.view(), 0, M, N, K, out=out.view(), gate=gate.view(),
+                                           cta_pair=pair),
+            f"gate bits     pair{pair}": g(3, A.view(), 0, Wk.view(), 0, M, N, K, out=out.view(),
+                                           gate_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair),
+            f"store(N=1024) pair{pair}": g(1, dz.view(), 0, Wmn.view(), 0, M, K, N, c=c.data_ptr(), ldc=K,
+                                           cta_pair=pair),
+            f"wgrad MN/MN   pair{pair}": g(2, dz.view(), 1, A.view(), 1, N, K, M, c=ws.data_ptr(), ldc=K, splits=S,
+                                           cta_pair=pair),
+            f"wgrad fused   pair{pair}": g(2, A.view(), 1, dz.view(), 1, K, N, M, c=ws.data_ptr(), ldc=N, splits=Sf,
+                                           out=dev.f32_act(wout), tile_sync=sync.data_ptr(), cta_pair=pair),
+            f"wgrad fused l1 (M=64)   ": g(2, X1.view(), 1, dz.view(), 1, 64, N, M, c=ws.data_ptr(), ldc=N, splits=S1,
+                                           out=dev.f32_act(wout1), tile_sync=sync.data_ptr(), cta_pair=pair),
+        })
     for name, fn in cases.items():
         ms = timeit(fn)
         print(f"{prec} {name} {ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s")

@@ -1,0 +1,6 @@
+set -x
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q -k "cta_pair or wgrad" 2>&1 | tail -5
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 200 python tools/gemm_bench.py 2>&1 | grep bf16
+timeout 300 python tools/step_breakdown.py bf16 2>&1 | tail -30
+timeout 500 python bench.py --no-cpu-baseline 2>&1 | tail -1
