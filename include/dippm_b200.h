@@ -115,13 +115,20 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
  * (row stride B.ld) with dz in the left half; writes g = agg^T dz into the
  * right half (g[u] = sum_{u->v} dz[v] / deg v, via the transposed CSR), so the
  * input gradient dh_prev = [dz | g] @ [W_self | W_neigh]^T is one GATE GEMM.
- * Also writes per-block column partial sums of dz into colsum_partial
- * [dippm_colsum_blocks(N), width] (bias gradient gnn.py:230, reduced by
- * dippm_reduce_rows).  write_agg = 0 computes the partial sums only. */
+ * Also reduces the columns of dz (bias gradient gnn.py:230): per-block partial
+ * sums go to colsum_partial [dippm_colsum_rows(N), width]; with bias_grad !=
+ * NULL the kernel finishes the reduction itself (two fixed-order levels, last
+ * block of each group / last group, fp64 sums) and writes bias_grad [width];
+ * sync is device int32[dippm_colsum_sync_ints(N)], zeroed once by the caller
+ * and left zero by every launch.  With bias_grad == NULL only the first
+ * dippm_colsum_blocks(N) partial rows are written (reduce with
+ * dippm_reduce_rows).  write_agg = 0 computes the column sums only. */
 int32_t dippm_colsum_blocks(int64_t num_nodes);
+int32_t dippm_colsum_rows(int64_t num_nodes);
+int32_t dippm_colsum_sync_ints(int64_t num_nodes);
 int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t num_nodes, int32_t write_agg,
                                const int32_t* t_rowptr, const int32_t* t_col, const float* inv_deg,
-                               float* colsum_partial, void* stream);
+                               float* colsum_partial, float* bias_grad, int32_t* sync, void* stream);
 
 /* Layer-3 variant with the readout backward fused in (gnn.py:224, 227): dz3 is
  * formed on the fly as dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0), written to
@@ -130,7 +137,8 @@ int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t num_nodes, 
 int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t* graph_ptr,
                                   const int32_t* node_graph, dippm_act_t h3, dippm_act_t B, int32_t width,
                                   int64_t num_nodes, const int32_t* t_rowptr, const int32_t* t_col,
-                                  const float* inv_deg, float* colsum_partial, void* stream);
+                                  const float* inv_deg, float* colsum_partial, float* bias_grad, int32_t* sync,
+                                  void* stream);
 /* node_graph[v] = g for v in [graph_ptr[g], graph_ptr[g+1]). */
 int32_t dippm_node_graph(const int32_t* graph_ptr, int64_t num_graphs, int32_t* node_graph, void* stream);
 

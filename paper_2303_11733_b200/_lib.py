@@ -74,9 +74,11 @@ SIGNATURES = {
     "dippm_build_csr_grouped": (I32, [P, P, P, P, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
     "dippm_colsum_blocks": (I32, [I64]),
-    "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P]),
+    "dippm_colsum_rows": (I32, [I64]),
+    "dippm_colsum_sync_ints": (I32, [I64]),
+    "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P, P, P]),
     "dippm_readout_backward": (I32, [P, I64, P, I64, I32, Act, Act, I64, P]),
-    "dippm_readout_aggregate_t": (I32, [P, I64, P, P, Act, Act, I32, I64, P, P, P, P, P]),
+    "dippm_readout_aggregate_t": (I32, [P, I64, P, P, Act, Act, I32, I64, P, P, P, P, P, P, P]),
     "dippm_node_graph": (I32, [P, I64, P, P]),
     "dippm_reduce_rows": (I32, [P, I64, I64, I32, F64, P, P]),
     "dippm_wgrad_splits": (I32, [I64, I64, I64]),

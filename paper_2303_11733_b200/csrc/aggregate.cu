@@ -10,6 +10,8 @@
 // 16-byte aligned and processed 8 columns per lane with 128-bit loads.  All
 // reductions run in a fixed order (no float atomics): results are
 // bit-reproducible run to run.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dippm {
@@ -17,6 +19,9 @@ namespace dippm {
 constexpr int kAggThreads = 256;
 constexpr int kAggColCap = 2048;   // neighbour ids staged in shared memory per block
 constexpr int kColsumRows = 64;    // rows per block for column partial sums
+constexpr int kColsumGroup = 64;   // block partials folded per level-2 partial (fused bias-gradient reduce)
+
+__host__ __device__ inline int colsum_groups(int nblk) { return (nblk + kColsumGroup - 1) / kColsumGroup; }
 
 // Both aggregation kernels stage the block's slice of the CSR (row pointers,
 // neighbour ids, 1/deg weights) in shared memory first, so the per-row work is
@@ -97,6 +102,44 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
 // the readout gradient (gnn.py:224, 227): dz3[v] = du[g(v)] / N_g * (h3[v] > 0),
 // written into B's left half while g = agg^T dz3 goes to the right half.  All
 // neighbours of v lie in v's graph, so one graph id per row suffices.
+// out[c] = sum_{r0 <= r < r1} x[r*width + c] for all c < width, by one block:
+// thread t owns 4 columns (float4) of one of `halves` row ranges, 8 L2 loads in
+// flight; the range sums are combined in range order through shared memory.
+// Fixed order throughout (fp64), so the result is deterministic.
+__device__ __forceinline__ void fold_rows_block(const float* x, int r0, int r1, int width, float* out,
+                                                double* s_fold /* [kAggThreads * 4] */) {
+  const int c4n = width >> 2;
+  const int halves = (int)blockDim.x / c4n;  // width 512: 2 row ranges of 128 column groups
+  const int t = threadIdx.x, h = t / c4n, c = (t % c4n) * 4;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  if (h < halves) {
+    const int n = r1 - r0;
+    const int lo = r0 + h * n / halves, hi = r0 + (h + 1) * n / halves;
+    int r = lo;
+    for (; r + 8 <= hi; r += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(reinterpret_cast<const float4*>(x + (int64_t)(r + k) * width + c));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a[0] += v[k].x; a[1] += v[k].y; a[2] += v[k].z; a[3] += v[k].w;
+      }
+    }
+    for (; r < hi; ++r) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(x + (int64_t)r * width + c));
+      a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s_fold[h * width + c + k] = a[k];
+  }
+  __syncthreads();
+  for (int cc = threadIdx.x; cc < width; cc += blockDim.x) {
+    double tot = 0.0;
+    for (int q = 0; q < halves; ++q) tot += s_fold[q * width + cc];
+    out[cc] = (float)tot;
+  }
+}
+
 struct ReadoutArgs {
   const float* du;          // [G, ld_du] fp32 (dr = du[:, :width])
   int64_t ld_du;
@@ -110,7 +153,8 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
                                                                 const int* __restrict__ t_rowptr,
                                                                 const int* __restrict__ t_col,
                                                                 const float* __restrict__ inv_deg,
-                                                                float* __restrict__ colsum_partial, ReadoutArgs ro) {
+                                                                float* __restrict__ colsum_partial, ReadoutArgs ro,
+                                                                float* __restrict__ bias_out, int* __restrict__ sync) {
   extern __shared__ float s_part[];  // [8 warps * gpw][width]
   __shared__ int s_ptr[kRowsPerBlock + 1];
   __shared__ int s_col[kAggColCap];
@@ -204,6 +248,37 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
     float t = 0.f;
     for (int q = 0; q < slots; ++q) t += s_part[q * width + c];
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
+  }
+  if (bias_out) {
+    // Fused bias-gradient reduction (gnn.py:230), two fixed-order levels: the last
+    // block of each group of kColsumGroup blocks folds the group's partials (in
+    // block order) into a level-2 row; the last group to finish folds those (in
+    // group order) into bias_out.  Counters return to zero for the next launch.
+    __shared__ int s_last;
+    const int nblk = (int)gridDim.x, ngroups = colsum_groups(nblk);
+    const int grp = blockIdx.x / kColsumGroup;
+    float* l2 = colsum_partial + (int64_t)nblk * width;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int gsize = min(kColsumGroup, nblk - grp * kColsumGroup);
+      s_last = atomicAdd(&sync[grp], 1) == gsize - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    const int b0 = grp * kColsumGroup, b1 = min(nblk, b0 + kColsumGroup);
+    double* s_fold = reinterpret_cast<double*>(s_part);  // the warp partials are no longer needed
+    fold_rows_block(colsum_partial, b0, b1, width, l2 + (int64_t)grp * width, s_fold);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sync[grp] = 0;
+      __threadfence();
+      s_last = atomicAdd(&sync[ngroups], 1) == ngroups - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    fold_rows_block(l2, 0, ngroups, width, bias_out, s_fold);
+    if (threadIdx.x == 0) sync[ngroups] = 0;
   }
 }
 
@@ -328,6 +403,11 @@ using namespace dippm;
 extern "C" {
 
 int32_t dippm_colsum_blocks(int64_t num_nodes) { return ceil_div_i(num_nodes, kRowsPerBlock); }
+int32_t dippm_colsum_rows(int64_t num_nodes) {
+  const int nblk = dippm_colsum_blocks(num_nodes);
+  return nblk + colsum_groups(nblk);
+}
+int32_t dippm_colsum_sync_ints(int64_t num_nodes) { return colsum_groups(dippm_colsum_blocks(num_nodes)) + 1; }
 
 static int cpl_for(int width) {
   const int chunks = width / 8;
@@ -365,13 +445,17 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
 
 static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, ReadoutArgs ro,
-                              bool readout, cudaStream_t s) {
+                              bool readout, float* bias_out, int32_t* sync, cudaStream_t s) {
+  DIPPM_ARG_CHECK(!bias_out || sync, "sage_aggregate_t: bias_grad needs the sync counters");
   DIPPM_ARG_CHECK(N >= 1 && width >= 8 && width % 8 == 0, "sage_aggregate_t: bad width %d", width);
   const int cpl = cpl_for(width);
   const int L = (width / 8) / cpl;
   DIPPM_ARG_CHECK((width / 8) % cpl == 0 && L <= 32 && 32 % L == 0, "sage_aggregate_t: unsupported width %d", width);
-  const size_t smem = (size_t)(kAggThreads / 32) * (32 / L) * width * sizeof(float);
+  size_t smem = (size_t)(kAggThreads / 32) * (32 / L) * width * sizeof(float);
   DIPPM_ARG_CHECK(smem <= 160 * 1024, "sage_aggregate_t: width %d too large", width);
+  DIPPM_ARG_CHECK(!bias_out || width / 4 <= kAggThreads, "sage_aggregate_t: fused bias reduce needs width <= %d",
+                  4 * kAggThreads);
+  if (bias_out) smem = std::max(smem, (size_t)kAggThreads * 4 * sizeof(double));  // fold scratch
   const int grid = ceil_div_i(N, kRowsPerBlock);
   ActView bv = make_view(B);
 #define DIPPM_AGGT(D, C, R)                                                                                      \
@@ -380,7 +464,7 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
       DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                             (int)smem));                                                         \
     k_aggregate_t<D, C, R><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
-                                                          colsum_partial, ro);                                   \
+                                                          colsum_partial, ro, bias_out, sync);                   \
   } while (0)
 #define DIPPM_AGGT_C(D, R) \
   do { if (cpl == 4) DIPPM_AGGT(D, 4, R); else if (cpl == 2) DIPPM_AGGT(D, 2, R); else DIPPM_AGGT(D, 1, R); } while (0)
@@ -396,18 +480,21 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
 }
 
 int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
-                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+                               const int32_t* t_col, const float* inv_deg, float* colsum_partial, float* bias_grad,
+                               int32_t* sync, void* stream) {
   ReadoutArgs ro{};
-  return launch_aggregate_t(B, width, N, write_agg, t_rowptr, t_col, inv_deg, colsum_partial, ro, false,
-                            (cudaStream_t)stream);
+  return launch_aggregate_t(B, width, N, write_agg, t_rowptr, t_col, inv_deg, colsum_partial, ro, false, bias_grad,
+                            sync, (cudaStream_t)stream);
 }
 
 int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t* graph_ptr, const int32_t* node_graph,
                                   dippm_act_t h3, dippm_act_t B, int32_t width, int64_t N, const int32_t* t_rowptr,
-                                  const int32_t* t_col, const float* inv_deg, float* colsum_partial, void* stream) {
+                                  const int32_t* t_col, const float* inv_deg, float* colsum_partial,
+                                  float* bias_grad, int32_t* sync, void* stream) {
   DIPPM_ARG_CHECK(h3.dtype == B.dtype && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
   ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3)};
-  return launch_aggregate_t(B, width, N, 1, t_rowptr, t_col, inv_deg, colsum_partial, ro, true, (cudaStream_t)stream);
+  return launch_aggregate_t(B, width, N, 1, t_rowptr, t_col, inv_deg, colsum_partial, ro, true, bias_grad, sync,
+                            (cudaStream_t)stream);
 }
 
 int32_t dippm_readout_backward(const float* du, int64_t ld_du, const int32_t* graph_ptr, int64_t G, int32_t width,

@@ -324,7 +324,8 @@ class Workspace:
             # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
             self.relu_bits = torch.empty(2, N, hp // 32, dtype=torch.int32, device=dev)
             self.head_bits = torch.empty(G, hp // 32, dtype=torch.int32, device=dev)
-            self.colsum = torch.empty(lib.dippm_colsum_blocks(N), hp, **f32)
+            self.colsum = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
+            self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
             # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
             # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
             self.splits = [lib.dippm_wgrad_splits(2 * d, hp, N) for d in eng.L.d_in]
@@ -491,8 +492,6 @@ class Engine:
         """Head backward (fc3 fused kernel, fc2/fc1 tcgen05 WGRAD/GATE/STORE), readout
         backward, then per SAGE layer: agg^T + bias, WGRAD, gated dgrad GEMM."""
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
-        lib = _lib.load()
-        nblk = lib.dippm_colsum_blocks(N)
         _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout), float(keep_scale),
                   self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
         self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws.head_splits[0], ws, "fc2.w")
@@ -504,18 +503,18 @@ class Engine:
         cur = 0
         for i in (2, 1, 0):
             B = ws.B[cur]
+            bias = self._g32(f"sage{i + 1}.bias")  # gnn.py:230, reduced inside the kernel
             if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
                           ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr), _p(b.t_col), _p(b.inv_deg),
-                          _p(ws.colsum), s)
+                          _p(ws.colsum), bias, _p(ws.colsum_sync), s)
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
-                          _p(b.inv_deg), _p(ws.colsum), s)
-            _lib.call("dippm_reduce_rows", _p(ws.colsum), nblk, hp, hp, 1.0, self._g32(f"sage{i + 1}.bias"), s)
+                          _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)
             self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws.splits[i], ws, f"sage{i + 1}.w_self")
             if i > 0:
                 self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
                            out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
                            gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=hp // 32)
                 cur = 1 - cur
-        self.launches += 5 + 3 * 2
+        self.launches += 5 + 3 * 2 - 3

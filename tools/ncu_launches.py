@@ -7,6 +7,9 @@ import sys
 def load(path):
     rows = [r for r in csv.reader(open(path)) if r and not r[0].startswith("==")]
     hdr = rows[0]
+    if "Metric Name" in hdr:  # several metrics per launch: keep the duration rows
+        mi = hdr.index("Metric Name")
+        rows = [hdr] + [r for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     out = []
     for r in rows[1:]:
