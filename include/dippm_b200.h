@@ -218,6 +218,11 @@ int32_t dippm_splitk_reduce_t(const float* in, int32_t splits, int64_t M, int64_
 int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t num_graphs, int32_t width,
                           const float* fs_raw, const double* norm, dippm_act_t u, void* stream);
 
+/* MLP baseline input (MlpModel.forward_norm gnn.py:253-255, normalize_fs gnn.py:96-97):
+ * u[g, c] = (fs_raw[g, c] - fs_mean[c]) / fs_std[c] for c < 5, 0 for 5 <= c < cols. */
+int32_t dippm_fs_normalize(const float* fs_raw, int64_t num_graphs, const double* norm, dippm_act_t u,
+                           int32_t cols, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K5 — FC head, gnn.py:265-284.  fc1/fc2 (and their gradients) are dippm_gemm
  * calls: FWD with bias + ReLU + dropout epilogue, GATE / STORE / WGRAD for the

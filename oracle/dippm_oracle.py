@@ -296,14 +296,16 @@ def mig_code(alpha_mb: float) -> int:
 
 
 def train_reference_protocol(records, epochs, seed=0, hidden=DEFAULT_HIDDEN, lr=DEFAULT_LEARNING_RATE,
-                             delta=1.0, shuffle=True, dropout_p=DEFAULT_DROPOUT, val_records=()):
+                             delta=1.0, shuffle=True, dropout_p=DEFAULT_DROPOUT, val_records=(), arch="sage"):
     """gnn.py:424-482: batch-size-1 Adam over records with PCG64 dropout masks
-    drawn in the reference order.  Returns (params, normaliser, history)."""
+    drawn in the reference order.  arch "mlp" = train_mlp (gnn.py:418-421).
+    Returns (params, normaliser, history)."""
     rng = np.random.default_rng(seed)
     targets = np.stack([r[4] for r in records])
     statics = np.stack([r[3] for r in records])
     norm = normalizer_fit(targets, statics)
-    params = init_params(hidden, rng)
+    mlp = arch == "mlp"
+    params = init_mlp_params(hidden, rng) if mlp else init_params(hidden, rng)
     preps = [(aggregation_matrix(n, e), np.asarray(X, dtype=np.float64)) for n, e, X, _, _ in records]
     fs_norm = [(r[3] - norm["fs_mean"]) / norm["fs_std"] for r in records]
     y_norm = [(r[4] - norm["y_mean"]) / norm["y_std"] for r in records]
@@ -321,12 +323,19 @@ def train_reference_protocol(records, epochs, seed=0, hidden=DEFAULT_HIDDEN, lr=
                 m2 = dropout_mask((hidden,), dropout_p, rng)
                 masks = (m1, m2)
             agg, X = preps[i]
-            out, cache = forward_norm(params, X, agg, fs_norm[i], masks)
+            if mlp:
+                out, cache = fc_forward(params, fs_norm[i], masks)
+            else:
+                out, cache = forward_norm(params, X, agg, fs_norm[i], masks)
             loss, dout = huber_loss(out, y_norm[i], delta)
             loss_sum += loss
             pred = out * norm["y_std"] + norm["y_mean"]
             ape += np.abs(pred - records[i][4]) / np.abs(records[i][4])
-            grads = backward_from(params, cache, dout, hidden)
+            if mlp:
+                grads = {}
+                fc_backward(params, cache, dout, grads)
+            else:
+                grads = backward_from(params, cache, dout, hidden)
             t += 1
             for k in params:
                 m, v = state[k]
@@ -336,7 +345,7 @@ def train_reference_protocol(records, epochs, seed=0, hidden=DEFAULT_HIDDEN, lr=
         if val_records:
             vl, va = 0.0, np.zeros(3)
             for vn, ve, vX, vfs, vy in val_records:
-                out = forward(params, norm, vn, ve, vX, vfs)
+                out = mlp_forward(params, norm, vfs) if mlp else forward(params, norm, vn, ve, vX, vfs)
                 loss, _ = huber_loss(out, (vy - norm["y_mean"]) / norm["y_std"], delta)
                 vl += loss
                 va += np.abs(out * norm["y_std"] + norm["y_mean"] - vy) / np.abs(vy)
@@ -344,3 +353,57 @@ def train_reference_protocol(records, epochs, seed=0, hidden=DEFAULT_HIDDEN, lr=
             entry["val_mape"] = float((va / len(val_records)).mean())
         history.append(entry)
     return params, norm, history
+
+
+# ---------------------------------------------------------------------------
+# MLP baseline (gnn.py:236-262, 322-324, 418-421) — static features only
+
+MLP_PARAM_NAMES = tuple(f"fc{i}.{p}" for i in (1, 2, 3) for p in ("w", "b"))
+
+
+def init_mlp_params(hidden: int, rng: np.random.Generator) -> dict:
+    """gnn.py:322-324 via _fc_stack gnn.py:174-175: fc1..3 w in draw order."""
+    p = {}
+    for i, (di, do) in enumerate([(STATIC_WIDTH, hidden), (hidden, hidden), (hidden, 3)], start=1):
+        p[f"fc{i}.w"] = glorot(rng, di, do)
+        p[f"fc{i}.b"] = np.zeros(do)
+    return p
+
+
+def mlp_forward(params, norm, fs_raw, masks=None):
+    """MlpModel.forward_norm gnn.py:253-255 after normalize_fs gnn.py:96-97."""
+    out, _ = fc_forward(params, (np.asarray(fs_raw, np.float64) - norm["fs_mean"]) / norm["fs_std"], masks)
+    return out
+
+
+def mlp_predict(params, norm, fs_raw):
+    return mlp_forward(params, norm, fs_raw) * norm["y_std"] + norm["y_mean"]
+
+
+def mlp_backward(params, norm, records, delta=1.0):
+    """gnn.backward (gnn.py:383-405) for an MlpModel: mean loss, mean grads (eval mode)."""
+    grads = {k: np.zeros_like(v) for k, v in params.items()}
+    total = 0.0
+    for _, _, _, fs_raw, y_raw in records:
+        fs_norm = (fs_raw - norm["fs_mean"]) / norm["fs_std"]
+        out, cache = fc_forward(params, fs_norm)
+        loss, dout = huber_loss(out, (y_raw - norm["y_mean"]) / norm["y_std"], delta)
+        total += loss
+        g = {}
+        fc_backward(params, cache, dout, g)
+        for k, v in g.items():
+            grads[k] += v
+    scale = 1.0 / len(records)
+    return total * scale, {k: v * scale for k, v in grads.items()}
+
+
+def mape(preds, actuals):
+    """dataset.mape (dataset.py:229-248): per-target mean |p - a| / |a| and their mean."""
+    p, a = np.asarray(preds, np.float64), np.asarray(actuals, np.float64)
+    if p.shape != a.shape or len(p) == 0:
+        raise ValueError("need matching, non-empty prediction / actual lists")
+    if np.any(a == 0.0):
+        raise ValueError("actual target contains a zero component")
+    per = (np.abs(p - a) / np.abs(a)).sum(axis=0) / len(p)
+    return {"latency": float(per[0]), "memory": float(per[1]), "energy": float(per[2]),
+            "overall": float(per.mean())}

@@ -390,6 +390,18 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const i
   }
 }
 
+// MLP baseline input (gnn.py:253-255 with normalize_fs :96-97): u[g] = [(fs-mu)/sigma | 0].
+__global__ void k_fs_normalize(const float* __restrict__ fs_raw, int64_t G, const double* __restrict__ norm,
+                               ActView u, int cols) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G * cols) return;
+  const int64_t g = i / cols;
+  const int c = (int)(i % cols);
+  float v = 0.f;
+  if (c < kStaticWidth) v = (float)(((double)fs_raw[g * kStaticWidth + c] - norm[6 + c]) / norm[11 + c]);
+  act_store(u, g, c, v);
+}
+
 // node -> graph id (for kernels that need g(v) per row).
 __global__ void k_node_graph(const int* __restrict__ graph_ptr, int* __restrict__ node_graph) {
   const int g = blockIdx.x;
@@ -539,6 +551,14 @@ int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, in
 #undef DIPPM_POOL_C
 #undef DIPPM_POOL
   DIPPM_LAUNCH_CHECK("k_pool_concat");
+  return DIPPM_OK;
+}
+
+int32_t dippm_fs_normalize(const float* fs_raw, int64_t G, const double* norm, dippm_act_t u, int32_t cols,
+                           void* stream) {
+  DIPPM_ARG_CHECK(G >= 1 && cols >= kStaticWidth && cols <= u.ld, "fs_normalize: bad shape");
+  k_fs_normalize<<<ceil_div_i(G * cols, 256), 256, 0, (cudaStream_t)stream>>>(fs_raw, G, norm, make_view(u), cols);
+  DIPPM_LAUNCH_CHECK("k_fs_normalize");
   return DIPPM_OK;
 }
 

@@ -87,17 +87,29 @@ def f32_act(t: torch.Tensor) -> Act:
 NULL_ACT = Act(None, 0, 0, 0)
 
 
-class Layout:
-    """Flat parameter layout with hidden padded to a multiple of 64."""
+ARCHS = ("sage", "mlp")
 
-    def __init__(self, hidden: int):
-        self.hidden = hidden
+
+class Layout:
+    """Flat parameter layout with hidden padded to a multiple of 64.
+
+    arch "sage": DippmModel (gnn.py:178-233), fc1 input u = [mean h3 | fs_norm | 0];
+    arch "mlp":  MlpModel (gnn.py:236-262), the static-features-only baseline,
+                 fc1 input u = [fs_norm | 0] (64 wide, K-aligned).
+    """
+
+    def __init__(self, hidden: int, arch: str = "sage"):
+        if arch not in ARCHS:
+            raise ValueError(f"arch must be one of {ARCHS}, got {arch!r}")
+        self.hidden, self.arch = hidden, arch
         self.hp = hp = -(-hidden // 64) * 64
-        self.d_in = [FEATURE_WIDTH, hp, hp]
+        self.d_in = [FEATURE_WIDTH, hp, hp] if arch == "sage" else []
         shapes = []
         for i, d in enumerate(self.d_in, start=1):
             shapes += [(f"sage{i}.w_self", (d, hp)), (f"sage{i}.w_neigh", (d, hp)), (f"sage{i}.bias", (hp,))]
-        self.u_width = hp + 64  # [r | fs | 0]: K of fc1 aligned to the tensor-core k-block
+        # [r | fs | 0] (sage) or [fs | 0] (mlp): K of fc1 aligned to the tensor-core k-block
+        self.u_width = hp + 64 if arch == "sage" else 64
+        self.fs_col = hp if arch == "sage" else 0
         shapes += [("fc1.w", (self.u_width, hp)), ("fc1.b", (hp,)), ("fc2.w", (hp, hp)), ("fc2.b", (hp,)),
                    ("fc3.w", (hp, 3)), ("fc3.b", (3,))]
         self.shapes = dict(shapes)
@@ -111,6 +123,9 @@ class Layout:
 
     def ref_shape(self, name: str):
         h = self.hidden
+        if self.arch == "mlp":
+            return {"fc1.w": (STATIC_WIDTH, h), "fc1.b": (h,), "fc2.w": (h, h), "fc2.b": (h,),
+                    "fc3.w": (h, 3), "fc3.b": (3,)}[name]
         return {
             "sage1.w_self": (FEATURE_WIDTH, h), "sage1.w_neigh": (FEATURE_WIDTH, h), "sage1.bias": (h,),
             "sage2.w_self": (h, h), "sage2.w_neigh": (h, h), "sage2.bias": (h,),
@@ -126,8 +141,9 @@ class Layout:
         if a.shape != self.ref_shape(name):
             raise ShapeMismatch(f"parameter {name}: shape {a.shape}, expected {self.ref_shape(name)}")
         if name == "fc1.w":
-            out[:h, :h] = a[:h]
-            out[hp:hp + STATIC_WIDTH, :h] = a[h:]
+            r = a.shape[0] - STATIC_WIDTH   # rows fed by the readout (0 for the MLP)
+            out[:r, :h] = a[:r]
+            out[self.fs_col:self.fs_col + STATIC_WIDTH, :h] = a[r:]
         elif a.ndim == 1:
             out[:a.shape[0]] = a
         else:
@@ -138,7 +154,8 @@ class Layout:
         h, hp = self.hidden, self.hp
         shp = self.ref_shape(name)
         if name == "fc1.w":
-            return np.concatenate([padded[:h, :h], padded[hp:hp + STATIC_WIDTH, :h]])
+            r = shp[0] - STATIC_WIDTH
+            return np.concatenate([padded[:r, :h], padded[self.fs_col:self.fs_col + STATIC_WIDTH, :h]])
         if len(shp) == 1:
             return padded[:shp[0]].copy()
         return padded[:shp[0], :shp[1]].copy()
@@ -302,8 +319,10 @@ class Workspace:
         f32 = dict(dtype=torch.float32, device=dev)
         lib = _lib.load()
         self.N, self.G = N, G
-        self.A = [ActBuf(N, 2 * FEATURE_WIDTH, dt, dev), ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
-        self.H3 = ActBuf(N, hp, dt, dev)
+        sage = eng.L.arch == "sage"
+        if sage:
+            self.A = [ActBuf(N, 2 * FEATURE_WIDTH, dt, dev), ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+            self.H3 = ActBuf(N, hp, dt, dev)
         self.u = ActBuf(G, eng.L.u_width, dt, dev)
         self.x2 = ActBuf(G, hp, dt, dev)
         self.x3 = ActBuf(G, hp, dt, dev)
@@ -318,20 +337,21 @@ class Workspace:
             self.dout = torch.empty(G, 3, **f32)
             self.d2 = ActBuf(G, hp, dt, dev)
             self.d1 = ActBuf(G, hp, dt, dev)
-            self.du = torch.empty(G, hp, **f32)
-            self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
-            # 1-bit ReLU' masks of h1, h2 (and of the head's x2, dropout included) written by the
-            # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
-            self.relu_bits = torch.empty(2, N, hp // 32, dtype=torch.int32, device=dev)
             self.head_bits = torch.empty(G, hp // 32, dtype=torch.int32, device=dev)
-            self.colsum = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
-            self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
+            if sage:
+                self.du = torch.empty(G, hp, **f32)
+                self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+                # 1-bit ReLU' masks of h1, h2 (and of the head's x2, dropout included) written by the
+                # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
+                self.relu_bits = torch.empty(2, N, hp // 32, dtype=torch.int32, device=dev)
+                self.colsum = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
+                self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
             # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
             # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
             self.splits = [lib.dippm_wgrad_splits(2 * d, hp, N) for d in eng.L.d_in]
             self.head_splits = [lib.dippm_wgrad_splits(hp, hp, G), lib.dippm_wgrad_splits(eng.L.u_width, hp, G)]
-            widest = max(max(s * 2 * d for s, d in zip(self.splits, eng.L.d_in)),
-                         self.head_splits[0] * hp, self.head_splits[1] * eng.L.u_width)
+            widest = max([s * 2 * d for s, d in zip(self.splits, eng.L.d_in)]
+                         + [self.head_splits[0] * hp, self.head_splits[1] * eng.L.u_width])
             self.splitk = torch.empty(widest * hp, **f32)
             sync = max(lib.dippm_wgrad_sync_ints(w, hp) for w in [2 * d for d in eng.L.d_in] + [eng.L.u_width])
             self.tile_sync = torch.zeros(sync, dtype=torch.int32, device=dev)
@@ -340,13 +360,14 @@ class Workspace:
 class Engine:
     """Device-resident DIPPM GraphSAGE network (weights, Adam state, GEMM operand copies)."""
 
-    def __init__(self, hidden: int, precision: str = "fp32", device=None, backend: str = "tc"):
+    def __init__(self, hidden: int, precision: str = "fp32", device=None, backend: str = "tc", arch: str = "sage"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
         if backend not in BACKENDS:
             raise ValueError(f"backend must be one of {sorted(BACKENDS)}, got {backend!r}")
         self.device = require_device(device)
-        self.L = L = Layout(hidden)
+        self.L = L = Layout(hidden, arch)
+        self.arch = arch
         self.precision, self.dtype, self.backend = precision, PRECISIONS[precision], BACKENDS[backend]
         n = L.total
         f64 = dict(dtype=torch.float64, device=self.device)
@@ -458,6 +479,11 @@ class Engine:
         """Eval (mask_mode 0) or train-mode forward (1: masks in ws.masks, 2: generated):
         K2 aggregation -> K3 GEMM x3, K4 pooling, K5 head (2 GEMMs + fc3)."""
         s, L, hp = _stream(), self.L, self.L.hp
+        if self.arch == "mlp":  # MlpModel.forward_norm (gnn.py:253-255): the head on [fs_norm | 0]
+            _lib.call("dippm_fs_normalize", _p(b.fs), b.G, _p(self.norm), ws.u.view(), L.u_width, s)
+            self.launches += 1
+            self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
+            return
         _lib.call("dippm_sage_aggregate", f32_act(b.x), ws.A[0].view(FEATURE_WIDTH), ws.A[0].view(0), b.N,
                   FEATURE_WIDTH, _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
         outs = [ws.A[1].view(0), ws.A[2].view(0), ws.H3.view(0)]
@@ -471,6 +497,13 @@ class Engine:
                        relu_bits=_p(bits[i]) if bits is not None and i < 2 else None, bits_ld=hp // 32)
         _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
                   ws.u.view(), s)
+        self.launches += 3 + 1
+        self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
+
+    def _head_forward(self, b: Batch, ws: Workspace, mask_mode: int, dropout_p: float, seed: int,
+                      predict: bool) -> None:
+        """K5: fc1/fc2 tcgen05 GEMMs (bias, ReLU, dropout epilogue) + fc3/de-normalise/MIG (gnn.py:265-284)."""
+        s, hp = _stream(), self.L.hp
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
         for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
             self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,
@@ -480,7 +513,7 @@ class Engine:
         _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
                   _p(self.norm), _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None,
                   _p(ws.nonfinite), s)
-        self.launches += 3 + 1 + 1
+        self.launches += 1
 
     def loss(self, b: Batch, ws: Workspace, delta: float = 1.0, grad_den: float = 0.0) -> None:
         """Huber loss + dout (numerics.py:58-73); grad_den = global batch size under DP (0: this batch)."""
@@ -499,6 +532,9 @@ class Engine:
                    gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=hp // 32)
         _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
         self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws.head_splits[1], ws, "fc1.w")
+        if self.arch == "mlp":  # no graph network below the head
+            self.launches += 2
+            return
         self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
         cur = 0
         for i in (2, 1, 0):

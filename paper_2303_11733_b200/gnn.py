@@ -152,10 +152,44 @@ class DippmModel:
         return items
 
 
+@dataclass
+class MlpModel:
+    """Baseline that regresses from the static features alone (gnn.py:236-262).
+
+    Same head as DippmModel but fc1 reads only the 5 normalised static
+    features; runs on the same tcgen05 head kernels (device arch "mlp")."""
+
+    fc: list
+    dropout_p: float
+    normalizer: Normalizer
+    hidden: int
+    vocab_version: str = VOCAB_VERSION
+
+    arch: ClassVar[str] = "mlp"
+
+    def param_items(self) -> list:
+        items = []
+        for i, layer in enumerate(self.fc, start=1):
+            items.append((f"fc{i}.w", layer.w))
+            items.append((f"fc{i}.b", layer.b))
+        return items
+
+
 def create_model(hidden: int = DEFAULT_HIDDEN, seed: int = 0, dropout_p: float = DEFAULT_DROPOUT,
                  normalizer: Normalizer | None = None) -> DippmModel:
     """Glorot-normal init in the reference draw order (gnn.py:302-319)."""
     return _new_sage_model(hidden, np.random.default_rng(seed), dropout_p, normalizer or Normalizer.identity())
+
+
+def create_mlp_model(hidden: int = DEFAULT_HIDDEN, seed: int = 0, dropout_p: float = DEFAULT_DROPOUT,
+                     normalizer: Normalizer | None = None) -> MlpModel:
+    """gnn.py:307-309: Glorot-normal fc1..fc3 in the reference draw order."""
+    return _new_mlp_model(hidden, np.random.default_rng(seed), dropout_p, normalizer or Normalizer.identity())
+
+
+def _new_mlp_model(hidden, rng, dropout_p, normalizer) -> MlpModel:
+    fc = _fc_stack(rng, [(STATIC_WIDTH, hidden), (hidden, hidden), (hidden, 3)])  # gnn.py:322-324
+    return MlpModel(fc=fc, dropout_p=dropout_p, normalizer=normalizer, hidden=hidden)
 
 
 def _new_sage_model(hidden, rng, dropout_p, normalizer) -> DippmModel:
@@ -171,13 +205,12 @@ def _new_sage_model(hidden, rng, dropout_p, normalizer) -> DippmModel:
 
 def _engine(model, precision: str = "fp32", device=None, backend: str = "tc") -> Engine:
     """Device engine for `model`, refreshed from the model's current host values."""
-    if getattr(model, "arch", "sage") != "sage":
-        raise ShapeMismatch(f"model arch {model.arch!r} has no graph network")
-    key = (precision, str(device), backend, int(model.hidden))
+    arch = getattr(model, "arch", "sage")
+    key = (precision, str(device), backend, int(model.hidden), arch)
     cache = model.__dict__.setdefault("_b200_engines", {})
     eng = cache.get(key)
     if eng is None:
-        eng = Engine(model.hidden, precision, device, backend)
+        eng = Engine(model.hidden, precision, device, backend, arch=arch)
         cache[key] = eng
     eng.set_params(model.param_items(), model.normalizer)
     return eng
@@ -190,7 +223,7 @@ def _records_arrays(encodings, fss, targets=None):
 
 def _run_forward(eng: Engine, encodings, fss, targets=None, mask_mode=0, masks=None, train_buffers=False):
     x, src, dst, gp, fs, y = _records_arrays(encodings, fss, targets)
-    b = upload_batch(x, src, dst, gp, fs, y, device=eng.device)
+    b = upload_batch(x, src, dst, gp, fs, y, device=eng.device, build_csr=eng.arch == "sage")
     ws = Workspace(eng, b.N, b.G, train=train_buffers)
     if masks is not None:
         ws.masks[:, :, :masks.shape[-1]].copy_(torch.from_numpy(masks.astype(np.float32)))
@@ -356,27 +389,33 @@ def backward(model, records, huber_delta: float = 1.0, precision: str = "fp32"):
 
 def train(train_records, val_records, config: TrainConfig):
     """Fit the graph network; returns the final-epoch model and history."""
-    return _fit(train_records, val_records, config)
+    return _fit(_new_sage_model, train_records, val_records, config)
 
 
-def _fit(train_records, val_records, config: TrainConfig):
+def train_mlp(train_records, val_records, config: TrainConfig):
+    """Fit the static-features-only baseline with the identical protocol (gnn.py:418-421)."""
+    return _fit(_new_mlp_model, train_records, val_records, config)
+
+
+def _fit(make_model, train_records, val_records, config: TrainConfig):
     if not train_records:
         raise EmptyDataset("training split is empty")
     rng = np.random.default_rng(config.seed)
     targets = np.stack([target_vector(r.target) for r in train_records])
     statics = np.stack([fs_vector(r.fs) for r in train_records])
     normalizer = Normalizer.fit(targets, statics)
-    model = _new_sage_model(config.hidden, rng, DEFAULT_DROPOUT, normalizer)
-    eng = Engine(config.hidden, config.precision, config.device, config.backend)
+    model = make_model(config.hidden, rng, DEFAULT_DROPOUT, normalizer)
+    eng = Engine(config.hidden, config.precision, config.device, config.backend, arch=model.arch)
     eng.set_params(model.param_items(), normalizer)
+    sage = model.arch == "sage"
     n = len(train_records)
     B = config.batch_size
     dropout = model.dropout_p > 0.0
     keep = 1.0 / (1.0 - model.dropout_p) if dropout else 1.0
 
     if B == 1:
-        batches = [upload_batch(*_records_arrays([r.encoding], [r.fs], [r.target]), device=eng.device)
-                   for r in train_records]
+        batches = [upload_batch(*_records_arrays([r.encoding], [r.fs], [r.target]), device=eng.device,
+                                build_csr=sage) for r in train_records]
     n_max = max(b.N for b in batches) if B == 1 else None
     ws1 = Workspace(eng, n_max, 1, train=True) if B == 1 else None
     ws_cache = {}
@@ -402,7 +441,7 @@ def _fit(train_records, val_records, config: TrainConfig):
                 idx = order[s0:s0 + B]
                 recs = [train_records[i] for i in idx]
                 b = upload_batch(*_records_arrays([r.encoding for r in recs], [r.fs for r in recs],
-                                                  [r.target for r in recs]), device=eng.device)
+                                                  [r.target for r in recs]), device=eng.device, build_csr=sage)
                 ws = _workspace(ws_cache, eng, b, train=True)
                 step += 1
                 eng.forward(b, ws, mask_mode=2 if dropout else 0, dropout_p=model.dropout_p,
@@ -441,7 +480,7 @@ def _evaluate(eng, records, delta, ws_cache, chunk=256):
     for s0 in range(0, len(records), chunk):
         recs = records[s0:s0 + chunk]
         b = upload_batch(*_records_arrays([r.encoding for r in recs], [r.fs for r in recs],
-                                          [r.target for r in recs]), device=eng.device)
+                                          [r.target for r in recs]), device=eng.device, build_csr=eng.arch == "sage")
         ws = _workspace(ws_cache, eng, b, train=True)
         eng.forward(b, ws, predict=False)
         eng.loss(b, ws, delta)
@@ -458,6 +497,7 @@ _SAGE_PARAM_NAMES = tuple(
     [f"sage{i}.{part}" for i in (1, 2, 3) for part in ("w_self", "w_neigh", "bias")]
     + [f"fc{i}.{part}" for i in (1, 2, 3) for part in ("w", "b")]
 )
+_MLP_PARAM_NAMES = tuple(f"fc{i}.{part}" for i in (1, 2, 3) for part in ("w", "b"))
 _VECTOR_SUFFIXES = (".bias", ".b")
 
 
@@ -507,8 +547,6 @@ def load_model(path):
     arch = doc.get("arch")
     if arch not in ("sage", "mlp"):
         raise IoFailure(f"unknown model arch {arch!r}")
-    if arch == "mlp":
-        raise IoFailure("MLP baseline models are not served by the B200 graph path")
     try:
         hidden = int(doc["hidden"])
         dropout_p = float(doc["dropout_p"])
@@ -518,7 +556,7 @@ def load_model(path):
                                 fs_mean=np.asarray(nd["fs_mean"], dtype=np.float64),
                                 fs_std=np.asarray(nd["fs_std"], dtype=np.float64))
         arrays = {}
-        for name in _SAGE_PARAM_NAMES:
+        for name in (_SAGE_PARAM_NAMES if arch == "sage" else _MLP_PARAM_NAMES):
             entry = doc["params"][name]
             rows, cols = int(entry["rows"]), int(entry["cols"])
             data = np.asarray(entry["data"], dtype=np.float64)
@@ -527,8 +565,10 @@ def load_model(path):
             arrays[name] = data if name.endswith(_VECTOR_SUFFIXES) else data.reshape(rows, cols)
     except (KeyError, TypeError, ValueError) as exc:
         raise IoFailure(f"model file {path} is incomplete: {exc}") from exc
+    fc = [AffineParams(w=arrays[f"fc{i}.w"], b=arrays[f"fc{i}.b"]) for i in (1, 2, 3)]
+    if arch == "mlp":
+        return MlpModel(fc=fc, dropout_p=dropout_p, normalizer=normalizer, hidden=hidden, vocab_version=version)
     sage = [SageLayerParams(w_self=arrays[f"sage{i}.w_self"], w_neigh=arrays[f"sage{i}.w_neigh"],
                             bias=arrays[f"sage{i}.bias"]) for i in (1, 2, 3)]
-    fc = [AffineParams(w=arrays[f"fc{i}.w"], b=arrays[f"fc{i}.b"]) for i in (1, 2, 3)]
     return DippmModel(sage=sage, fc=fc, dropout_p=dropout_p, normalizer=normalizer, hidden=hidden,
                       vocab_version=version)

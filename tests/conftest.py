@@ -7,6 +7,7 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 GOLDEN = Path(__file__).resolve().parent / "golden" / "golden_v1.npz"
+GOLDEN_NEXT = Path(__file__).resolve().parent / "golden" / "golden_next_v1.npz"
 
 
 def pytest_configure(config):
@@ -16,6 +17,11 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     return dict(np.load(GOLDEN))
+
+
+@pytest.fixture(scope="session")
+def golden_next():
+    return dict(np.load(GOLDEN_NEXT))
 
 
 def unpack_records(g, prefix="rec_"):

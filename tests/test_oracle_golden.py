@@ -105,3 +105,58 @@ def test_reference_protocol_training_matches(golden):
     assert np.allclose(got, golden["train_hist"], rtol=1e-10, atol=0)
     for k in O.SAGE_PARAM_NAMES:
         assert np.allclose(params[k], golden[f"train_param_{k}"], rtol=1e-10, atol=1e-14), k
+
+
+# ---- §8f rows: MLP baseline, MAPE (tests/golden/make_golden_next.py) ----
+
+MLP_TAGS = {"mlp32": (32, 11), "mlp512": (512, 0)}
+
+
+def mlp_params(gn, tag):
+    """Rebuild an MLP baseline from its seed (pins the reference draw order) + golden biases."""
+    hidden, seed = MLP_TAGS[tag]
+    params = O.init_mlp_params(hidden, np.random.default_rng(seed))
+    checksum = np.array([float(np.sum(params[k])) for k in O.MLP_PARAM_NAMES])
+    assert np.array_equal(checksum, gn[f"{tag}_param_checksum"]), "MLP init order / PCG64 stream changed"
+    for k in O.MLP_PARAM_NAMES:
+        if params[k].ndim == 1:
+            params[k] = gn[f"{tag}_bias_{k}"].copy()
+    return params
+
+
+@pytest.mark.parametrize("tag", sorted(MLP_TAGS))
+def test_mlp_forward_backward_match_reference(golden, golden_next, tag):
+    recs, norm = unpack_records(golden), _norm(golden)
+    params = mlp_params(golden_next, tag)
+    fwd = np.stack([O.mlp_forward(params, norm, r[3]) for r in recs])
+    assert np.allclose(fwd, golden_next[f"{tag}_forward"], rtol=1e-12, atol=1e-12)
+    pred = np.stack([O.mlp_predict(params, norm, r[3]) for r in recs])
+    assert np.allclose(pred, golden_next[f"{tag}_predict"], rtol=1e-12, atol=1e-9)
+    loss, grads = O.mlp_backward(params, norm, recs[:20])
+    assert abs(loss - float(golden_next[f"{tag}_backward_loss"])) <= 1e-12
+    for k, g in grads.items():
+        if f"{tag}_grad_{k}" in golden_next:
+            assert np.allclose(g, golden_next[f"{tag}_grad_{k}"], rtol=1e-10, atol=1e-14), k
+        else:
+            st = golden_next[f"{tag}_gradstat_{k}"]
+            assert np.isclose(np.linalg.norm(g), st[0], rtol=1e-10), k
+            assert np.allclose(g.ravel()[::97], golden_next[f"{tag}_gradsample_{k}"], rtol=1e-9, atol=1e-14), k
+
+
+def test_mape_matches_reference(golden, golden_next):
+    recs, norm = unpack_records(golden), _norm(golden)
+    params = mlp_params(golden_next, "mlp32")
+    preds = [O.mlp_predict(params, norm, r[3]) for r in recs]
+    m = O.mape(preds, [r[4] for r in recs])
+    got = [m["latency"], m["memory"], m["energy"], m["overall"]]
+    assert np.allclose(got, golden_next["mape_mlp32"], rtol=1e-12)
+
+
+def test_mlp_reference_protocol_training_matches(golden, golden_next):
+    recs = unpack_records(golden, "train_rec_")
+    params, _n, hist = O.train_reference_protocol(recs[:8], epochs=3, seed=123, hidden=16, val_records=recs[8:],
+                                                  arch="mlp")
+    got = np.array([[h["epoch"], h["train_loss"], h["train_mape"], h["val_loss"], h["val_mape"]] for h in hist])
+    assert np.allclose(got, golden_next["train_mlp_hist"], rtol=1e-10, atol=0)
+    for k in O.MLP_PARAM_NAMES:
+        assert np.allclose(params[k], golden_next[f"train_mlp_param_{k}"], rtol=1e-10, atol=1e-14), k
