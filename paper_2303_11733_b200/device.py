@@ -348,10 +348,11 @@ class Workspace:
                 self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
             # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
             # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
-            self.splits = [lib.dippm_wgrad_splits(2 * d, hp, N) for d in eng.L.d_in]
-            self.head_splits = [lib.dippm_wgrad_splits(hp, hp, G), lib.dippm_wgrad_splits(eng.L.u_width, hp, G)]
-            widest = max([s * 2 * d for s, d in zip(self.splits, eng.L.d_in)]
-                         + [self.head_splits[0] * hp, self.head_splits[1] * eng.L.u_width])
+            # split counts are chosen per call from the actual row count (<= these upper bounds)
+            big = 1 << 30
+            smax = [lib.dippm_wgrad_splits(2 * d, hp, big) for d in eng.L.d_in]
+            hmax = [lib.dippm_wgrad_splits(hp, hp, big), lib.dippm_wgrad_splits(eng.L.u_width, hp, big)]
+            widest = max([s * 2 * d for s, d in zip(smax, eng.L.d_in)] + [hmax[0] * hp, hmax[1] * eng.L.u_width])
             self.splitk = torch.empty(widest * hp, **f32)
             sync = max(lib.dippm_wgrad_sync_ints(w, hp) for w in [2 * d for d in eng.L.d_in] + [eng.L.u_width])
             self.tile_sync = torch.zeros(sync, dtype=torch.int32, device=dev)
@@ -467,10 +468,11 @@ class Engine:
             self.gemm_hook("post", 2.0 * M * N * K)
         self.launches += 1
 
-    def _wgrad(self, dz: Act, x: Act, rows: int, width: int, splits: int, ws: Workspace, out_name: str) -> None:
+    def _wgrad(self, dz: Act, x: Act, rows: int, width: int, ws: Workspace, out_name: str) -> None:
         """grads[out_name] (as [width, Hp]) = x^T @ dz over `rows` rows (gnn.py:228-229, 296):
         one split-K tcgen05 launch that also reduces its partials in fixed split order."""
         hp = self.L.hp
+        splits = _lib.load().dippm_wgrad_splits(width, hp, rows)
         self._gemm(GEMM_WGRAD, width, hp, rows, x, 1, dz, 1, out=Act(self._g32(out_name), hp, 0, DT_F32),
                    c=_p(ws.splitk), ldc=hp, splits=splits, tile_sync=_p(ws.tile_sync), out_scale=1.0)
 
@@ -527,11 +529,11 @@ class Engine:
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
         _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout), float(keep_scale),
                   self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
-        self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws.head_splits[0], ws, "fc2.w")
+        self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
         self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
                    gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=hp // 32)
         _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
-        self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws.head_splits[1], ws, "fc1.w")
+        self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
         if self.arch == "mlp":  # no graph network below the head
             self.launches += 2
             return
@@ -547,7 +549,7 @@ class Engine:
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
                           _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)
-            self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws.splits[i], ws, f"sage{i + 1}.w_self")
+            self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws, f"sage{i + 1}.w_self")
             if i > 0:
                 self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
                            out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,

@@ -37,8 +37,11 @@ class BatchTrainer:
         self.steps = 0
         self.replayed_launches = 0  # kernels launched by graph replays (not seen by dippm_launch_count)
         self.ws = None
-        self._stage = None
-        self._loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+        self._slots = []
+        self._slot_next = 0
+        self._copy_stream = torch.cuda.Stream() if torch.cuda.is_available() else None
+        self._loss_ring = [torch.zeros(1, dtype=torch.float64).pin_memory() for _ in range(64)]
+        self._loss_next = 0
 
     def reserve(self, max_nodes: int, max_graphs: int, max_edges: int | None = None) -> None:
         """Preallocate the workspace (and host-batch staging) for batches up to this size."""
@@ -47,14 +50,16 @@ class BatchTrainer:
         self._keep.clear()
         e = max_edges if max_edges is not None else 2 * max_nodes
         d = self.engine.device
-        self._stage = {
+        self._slots = [{  # two host-batch staging slots (double buffering for submit())
             "x": torch.empty(max_nodes, dev.FEATURE_WIDTH, dtype=torch.float32, device=d),
             "src": torch.empty(e, dtype=torch.int64, device=d), "dst": torch.empty(e, dtype=torch.int64, device=d),
             "gp": torch.empty(max_graphs + 1, dtype=torch.int32, device=d),
             "fs": torch.empty(max_graphs, dev.STATIC_WIDTH, dtype=torch.float32, device=d),
             "y": torch.empty(max_graphs, 3, dtype=torch.float32, device=d),
             "ep": torch.empty(max_graphs + 1, dtype=torch.int64, device=d),
-        }
+            "free": torch.cuda.Event(), "ready": torch.cuda.Event(),
+        } for _ in range(2)]
+        self._slot_next = 0
 
     def _ensure(self, b: Batch) -> None:
         if self.ws is None or b.N > self.ws.N or b.G > self.ws.G:
@@ -119,31 +124,56 @@ class BatchTrainer:
 
         edge_ptr [G+1] (edges grouped by graph, as collation produces) enables the
         per-graph CSR kernel; if omitted it is derived on the host when possible."""
+        return self.submit(x, src, dst, graph_ptr, fs, y, edge_ptr).loss()
+
+    def submit(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None) -> "StepHandle":
+        """Asynchronous end-to-end step from host buffers (pipelined `step_host`).
+
+        The batch is copied host->device on a side copy stream into one of two
+        staging slots while the previous step still computes; the step then
+        runs on the current stream and its loss is read back device->host into
+        pinned memory.  Returns a StepHandle whose .loss() waits for that read.
+        Steps stay in submission order (one compute stream), so the result is
+        the same as calling step_host repeatedly."""
         if edge_ptr is None:
             edge_ptr = dev.group_edges(np.asarray(src), np.asarray(dst), np.asarray(graph_ptr))
         arrays = [x, src, dst, graph_ptr, fs, y] + ([edge_ptr] if edge_ptr is not None else [])
         t = [torch.as_tensor(a) for a in arrays]
         G, N, E = t[3].numel() - 1, t[0].shape[0], t[1].numel()
-        if self._stage is None or N > self._stage["x"].shape[0] or E > self._stage["src"].numel() \
-                or G + 1 > self._stage["gp"].numel():
+        slots = self._slots
+        if not slots or N > slots[0]["x"].shape[0] or E > slots[0]["src"].numel() or G + 1 > slots[0]["gp"].numel():
+            torch.cuda.current_stream().synchronize()  # in-flight steps may still read the old slots
             self.reserve(max(N, self.ws.N if self.ws else 0), max(G, self.ws.G if self.ws else 0), max_edges=2 * E)
-        s = self._stage
-        views = [s["x"][:N], s["src"][:E], s["dst"][:E], s["gp"][:G + 1], s["fs"][:G], s["y"][:G], s["ep"][:G + 1]]
-        for d_, h in zip(views, t):
-            d_.copy_(h, non_blocking=True)
+            slots = self._slots
+        k = self._slot_next
+        self._slot_next = 1 - k
+        sl = slots[k]
+        compute = torch.cuda.current_stream()
+        with torch.cuda.stream(self._copy_stream):
+            self._copy_stream.wait_event(sl["free"])  # the step that last read this slot is done
+            views = [sl["x"][:N], sl["src"][:E], sl["dst"][:E], sl["gp"][:G + 1], sl["fs"][:G], sl["y"][:G],
+                     sl["ep"][:G + 1]]
+            for d_, h in zip(views, t):
+                d_.copy_(h, non_blocking=True)
+            sl["ready"].record(self._copy_stream)
+        compute.wait_event(sl["ready"])
         b = Batch(G=G, N=N, E=E, x=views[0], src=views[1], dst=views[2], graph_ptr=views[3], fs=views[4], y=views[5],
                   h2d_bytes=sum(a.numel() * a.element_size() for a in t))
         if edge_ptr is not None:
-            ep = np.asarray(edge_ptr)
-            gp = np.asarray(graph_ptr)
+            gp, ep = t[3].numpy(), np.asarray(edge_ptr)
             b.edge_ptr, b.max_nodes = views[6], int(np.diff(gp).max())
             b.max_edges = int(np.diff(ep).max()) if len(ep) > 1 else 0
         self._ensure(b)
         self.steps += 1
         self._step(b, None)  # ragged shapes: host batches run eagerly
-        self._loss_host.copy_(self.ws.loss[:1], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return float(self._loss_host[0])
+        sl["free"].record(compute)
+        j = self._loss_next
+        self._loss_next = (j + 1) % len(self._loss_ring)
+        host = self._loss_ring[j]
+        host.copy_(self.ws.loss[:1], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(compute)
+        return StepHandle(done, host)
 
     def sync_model(self):
         """Copy the device fp64 masters back into the host model's live arrays."""
@@ -151,3 +181,17 @@ class BatchTrainer:
         for name, arr in self.model.param_items():
             arr[...] = final[name]
         return self.model
+
+
+class StepHandle:
+    """Result of BatchTrainer.submit: .loss() waits for the step's loss read-back."""
+
+    def __init__(self, event, host):
+        self._event, self._host = event, host
+
+    def done(self) -> bool:
+        return self._event.query()
+
+    def loss(self) -> float:
+        self._event.synchronize()
+        return float(self._host[0])

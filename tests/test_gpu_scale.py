@@ -151,3 +151,33 @@ def test_cuda_graph_replay_equals_eager_steps(cfg1):
     assert np.array_equal(finals[0][0], finals[1][0])
     assert finals[0][1] == finals[1][1]
     assert len(set(finals[0][1])) == 4  # the steps really differ (masks and params move)
+
+
+def test_pipelined_host_steps_equal_sequential_and_resident(cfg1):
+    """BatchTrainer.submit (double-buffered H2D on a copy stream, loss read back per
+    step) gives bit-identical parameters and losses to synchronous step_host and
+    to step_resident on the same batches, including a batch larger than the
+    staging slots (forces a re-reserve mid-pipeline)."""
+    ds, _, model = cfg1
+    idx = [np.arange(0, 48), np.arange(48, 96), np.arange(96, 256), np.arange(10, 40)]
+    host = []
+    for ii in idx:
+        arrays = ds.collate(ii)
+        host.append([torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays])
+    runs = []
+    for mode in ("resident", "sync", "pipelined"):
+        tr = BatchTrainer(model, precision="bf16", lr=1e-3, dropout=True)
+        tr.reserve(int(host[0][3][-1]) + 1, 48)  # smaller than batch 2: re-reserve while steps are in flight
+        losses = []
+        if mode == "resident":
+            for h in host:
+                tr.step_resident(upload_batch(*[a.numpy() for a in h], device="cuda", build_csr=False))
+                losses.append(float(tr.ws.loss[0]))
+        elif mode == "sync":
+            losses = [tr.step_host(*h) for h in host]
+        else:
+            losses = [hd.loss() for hd in [tr.submit(*h) for h in host]]
+        runs.append((tr.engine.params.cpu().numpy(), losses))
+    for p, l in runs[1:]:
+        assert np.array_equal(p, runs[0][0])
+        assert l == runs[0][1]
