@@ -128,6 +128,19 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Issue only (no wait): the registers are valid after the next tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -239,6 +252,8 @@ __device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtenso
   if (dtype == DIPPM_DT_BF16) {
     uint8_t* stg = stg_base + (chunk & 1) * 2048;
     stage_wait(lane, 1);  // the slot's previous store has been read
+    // 64-byte rows in the TMA 64B-swizzle layout: 16-byte unit k of row r sits at
+    // unit k ^ ((r >> 1) & 3), so the 8 lanes of each store phase hit distinct banks.
     uint4* d = reinterpret_cast<uint4*>(stg + lane * 64);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -246,10 +261,11 @@ __device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtenso
       __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
 #pragma unroll
       for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[k * 8 + 2 * i], v[k * 8 + 2 * i + 1]);
-      d[k] = q;
+      d[k ^ ((lane >> 1) & 3)] = q;
     }
     stage_issue(map, stg, lane, x, y, 0);
   } else if (dtype == DIPPM_DT_TF32X3) {
+    // 128-byte rows in the TMA 128B-swizzle layout: unit k of row r at unit k ^ (r & 7).
     float4* d = reinterpret_cast<float4*>(stg_base + lane * 128);
     float lo[32];
     stage_wait(lane, 0);
@@ -261,18 +277,18 @@ __device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtenso
         hi[i] = tf32_hi(v[4 * k + i]);
         lo[4 * k + i] = tf32_rn(v[4 * k + i] - hi[i]);
       }
-      d[k] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      d[k ^ (lane & 7)] = make_float4(hi[0], hi[1], hi[2], hi[3]);
     }
     stage_issue(map, stg_base, lane, x, y, 0);
     stage_wait(lane, 0);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = make_float4(lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
+    for (int k = 0; k < 8; ++k) d[k ^ (lane & 7)] = make_float4(lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
     stage_issue(map, stg_base, lane, x, y, 1);
   } else {
     float4* d = reinterpret_cast<float4*>(stg_base + lane * 128);
     stage_wait(lane, 0);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    for (int k = 0; k < 8; ++k) d[k ^ (lane & 7)] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
     stage_issue(map, stg_base, lane, x, y, 0);
   }
 }
@@ -565,16 +581,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             gw[i] = row < p.M ? __ldg(p.gate_bits + row * p.bits_ld + (n0 >> 5) + half + 2 * i) : 0u;
           mbar_wait(&tfull[acc], use & 1);
           tc_fence_after();
+          const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBN;
+          uint32_t rawb[2][32];
+          tmem_ld32_issue(tq + half * 32, rawb[0]);
+          tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < kBN / 64; ++i) {
             const int ch = half + 2 * i;
-            uint32_t raw[32];
-            tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
+            if (i + 1 < kBN / 64) tmem_ld32_issue(tq + (ch + 2) * 32, rawb[(i + 1) & 1]);
+            uint32_t(&raw)[32] = rawb[i & 1];
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (gw[i] >> j) & 1u ? __uint_as_float(raw[j]) * p.gate_scale : 0.f;
             epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n0 + ch * 32,
                             m0 + q * 32, local * (kBN / 64) + i);
+            tmem_wait_ld();
           }
           release(acc);
           continue;
@@ -604,10 +625,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = half; ch < kBN / 32; ch += 2) {
-        uint32_t raw[32];
-        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * kBN + ch * 32, raw);
+      // TMEM reads run one chunk ahead: chunk i+1 is in flight while chunk i is processed.
+      const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBN;
+      uint32_t rawb[2][32];
+      tmem_ld32_issue(tq + half * 32, rawb[0]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < kBN / 64; ++i) {
+        const int ch = half + 2 * i;
+        if (i + 1 < kBN / 64) tmem_ld32_issue(tq + (ch + 2) * 32, rawb[(i + 1) & 1]);
+        uint32_t(&raw)[32] = rawb[i & 1];
         const int n = n0 + ch * 32;
         if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
           float v[32];
@@ -668,6 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               __uint_as_float(raw[4 * g + 2]), __uint_as_float(raw[4 * g + 3]));
           }
         }
+        tmem_wait_ld();  // chunk i+1 has landed
       }
       release(acc);
       if constexpr (kEpi == EPI_PARTIAL) {
@@ -744,7 +772,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D map over (cols, rows, plane) of a row-major operand; box = one 128-byte
 // swizzle row of columns by box_rows rows.
 static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows,
-                    bool atom32 = false, bool no_swizzle = false) {
+                    bool atom32 = false, bool store_map = false) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -759,8 +787,9 @@ static int make_map(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, v.dtype == DIPPM_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   3, v.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
-                             : (atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B),
+                  // epilogue store maps: 32-column boxes, 64 B rows (bf16) -> 64B swizzle, 128 B rows -> 128B
+                  store_map ? (elem == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B)
+                            : (atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r, (long long)rows,
