@@ -30,6 +30,24 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+HOST_LIB = PKG / "libdippm_host.so"
+HOST_SOURCES = ["featurize.cpp"]
+CXX = os.environ.get("CXX", "g++")
+
+
+def build_host(verbose: bool = False, force: bool = False) -> Path:
+    """libdippm_host.so: the native front end (graph JSON -> features), host C++17 only."""
+    srcs = [PKG / "hostsrc" / s for s in HOST_SOURCES]
+    deps = srcs + [ROOT / "include" / "dippm_host.h"]
+    if force or _stale(HOST_LIB, deps):
+        cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", "-Wno-unused-parameter", "-Wno-array-bounds",
+               "-I", str(ROOT / "include"), *map(str, srcs), "-o", str(HOST_LIB)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return HOST_LIB
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "dippm_b200.h"]
     objdir = PKG / "build"
@@ -49,6 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
+    build_host(verbose, force)
     return LIB
 
 

@@ -12,11 +12,23 @@ import pytest
 from paper_2303_11733_b200 import _lib, mig
 
 HEADER = Path(__file__).resolve().parents[1] / "include" / "dippm_b200.h"
+HOST_HEADER = Path(__file__).resolve().parents[1] / "include" / "dippm_host.h"
 
 
-def declared_functions():
-    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+def declared_functions(header=HEADER):
+    text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
     return sorted(set(re.findall(r"\b(dippm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_host_library_exports_every_declared_symbol():
+    from paper_2303_11733_b200 import featurize
+    lib = featurize._host()
+    names = declared_functions(HOST_HEADER)
+    assert len(names) >= 8
+    for name in names:
+        assert hasattr(lib, name), name
+    text = re.sub(r"/\*.*?\*/", "", HOST_HEADER.read_text(), flags=re.S)
+    assert 'extern "C"' in text and "std::" not in text and "torch" not in text
 
 
 def test_every_declared_symbol_is_exported_and_bound():
