@@ -40,7 +40,7 @@ def build_host(verbose: bool = False, force: bool = False) -> Path:
     srcs = [PKG / "hostsrc" / s for s in HOST_SOURCES]
     deps = srcs + [ROOT / "include" / "dippm_host.h"]
     if force or _stale(HOST_LIB, deps):
-        cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", "-Wno-unused-parameter", "-Wno-array-bounds",
+        cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", "-Wno-unused-parameter", "-Wno-array-bounds", "-Wno-stringop-overflow",
                "-I", str(ROOT / "include"), *map(str, srcs), "-o", str(HOST_LIB)]
         if verbose:
             print(" ".join(cmd))

@@ -195,11 +195,17 @@ def predict_documents(model, docs, batch_sizes=None, precision: str = "fp32", th
     """The `dippm predict` path (cli.py:148-172) for many documents at once:
     native featurisation, one device pass (gnn.predict_batch semantics).
     Returns (y float64 [G, 3] latency_ms / memory_mb / energy_j, MIG codes int8 [G], names)."""
+    fb = featurize_documents(docs, batch_sizes, threads)
+    y, mig = predict_featurized(model, fb, precision)
+    return y, mig, fb.names
+
+
+def predict_featurized(model, fb: FeaturizedBatch, precision: str = "fp32"):
+    """Device half of predict_documents: one forward over an already featurised batch."""
     import torch
 
     from . import gnn
     from .device import Workspace, upload_batch
-    fb = featurize_documents(docs, batch_sizes, threads)
     x, src, dst, gp, fs, ep = fb.collate()
     eng = gnn._engine(model, precision)
     b = upload_batch(x, src, dst, gp, fs, None, device=eng.device, build_csr=eng.arch == "sage", edge_ptr=ep)
@@ -208,4 +214,4 @@ def predict_documents(model, docs, batch_sizes=None, precision: str = "fp32", th
     torch.cuda.current_stream().synchronize()
     if int(ws.nonfinite.item()):
         raise E.NonFinite("memory prediction is not finite")
-    return ws.y_pred.cpu().numpy(), ws.mig.cpu().numpy(), fb.names
+    return ws.y_pred.cpu().numpy(), ws.mig.cpu().numpy()

@@ -18,8 +18,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cerrno>
 #include <queue>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <unordered_map>
 #include <unordered_set>
@@ -38,38 +40,33 @@ struct Fail {
 std::string I(int64_t v) { return std::to_string(v); }
 
 // ------------------------------------------------------------------ JSON
-struct J {
-  enum T { NUL, BOOL, INT, FLT, STR, ARR, OBJ } t = NUL;
+// A streaming parser specialised to the graph schema: one pass over the text
+// records exactly what parse_graph_json inspects (value types, ids, names,
+// inputs, known attributes, shapes) without building a document tree; every
+// other value is skipped with full syntax validation, so a syntax error
+// anywhere is a MalformedDocument exactly like json.loads failing first.
+enum VT : uint8_t { V_NUL, V_BOOL, V_INT, V_FLT, V_STR, V_ARR, V_OBJ };
+
+struct Scalar {
+  uint8_t t = V_NUL;
   bool b = false;
   int64_t i = 0;
   double f = 0.0;
-  std::string s;
-  std::vector<J> a;
-  std::vector<std::pair<std::string, J>> o;
-
-  const J* get(const char* key) const {  // last duplicate wins (Python dict semantics)
-    const J* r = nullptr;
-    for (const auto& kv : o)
-      if (kv.first == key) r = &kv.second;
-    return r;
-  }
-  bool is_int() const { return t == INT; }                 // isinstance(v, int) and not bool
-  bool is_num() const { return t == INT || t == FLT; }     // (int, float), not bool
-  double num() const { return t == INT ? (double)i : f; }  // float(v)
 };
 
-struct Parser {
+struct Cursor {
   const char* p;
   const char* e;
   int depth = 0;
+  std::string tmp;  // decoded string with escapes
+  Cursor(const char* b, const char* end) : p(b), e(end) {}
   [[noreturn]] void bad(const char* what) {
     fail(DIPPM_FEAT_MALFORMED_DOCUMENT, std::string("invalid JSON: ") + what);
   }
-  void ws() {
+  inline void ws() {
     while (p < e && (*p == ' ' || *p == '\t' || *p == '\n' || *p == '\r')) ++p;
   }
-  bool lit(const char* w) {
-    size_t n = strlen(w);
+  bool lit(const char* w, size_t n) {
     if ((size_t)(e - p) >= n && memcmp(p, w, n) == 0) {
       p += n;
       return true;
@@ -97,7 +94,7 @@ struct Parser {
     if (e - p < 4) bad("truncated \\u escape");
     uint32_t v = 0;
     for (int k = 0; k < 4; ++k) {
-      char c = *p++;
+      const char c = *p++;
       v <<= 4;
       if (c >= '0' && c <= '9') v |= (uint32_t)(c - '0');
       else if (c >= 'a' && c <= 'f') v |= (uint32_t)(c - 'a' + 10);
@@ -106,59 +103,68 @@ struct Parser {
     }
     return v;
   }
-  std::string str() {
-    ++p;  // opening quote
-    std::string out;
+  // string at *p == '"'; returns a view valid until the next string() call
+  std::string_view string() {
+    const char* s0 = ++p;
+    while (p < e) {  // fast path: no escapes
+      const unsigned char c = (unsigned char)*p;
+      if (c == '"') return std::string_view(s0, (size_t)(p++ - s0));
+      if (c == '\\') break;
+      if (c < 0x20) bad("control character in string");
+      ++p;
+    }
+    tmp.assign(s0, (size_t)(p - s0));
     while (true) {
       if (p >= e) bad("unterminated string");
-      unsigned char c = (unsigned char)*p++;
+      const unsigned char c = (unsigned char)*p++;
       if (c == '"') break;
       if (c < 0x20) bad("control character in string");
       if (c != '\\') {
-        out += (char)c;
+        tmp += (char)c;
         continue;
       }
       if (p >= e) bad("unterminated escape");
-      char x = *p++;
+      const char x = *p++;
       switch (x) {
-        case '"': out += '"'; break;
-        case '\\': out += '\\'; break;
-        case '/': out += '/'; break;
-        case 'b': out += '\b'; break;
-        case 'f': out += '\f'; break;
-        case 'n': out += '\n'; break;
-        case 'r': out += '\r'; break;
-        case 't': out += '\t'; break;
+        case '"': tmp += '"'; break;
+        case '\\': tmp += '\\'; break;
+        case '/': tmp += '/'; break;
+        case 'b': tmp += '\b'; break;
+        case 'f': tmp += '\f'; break;
+        case 'n': tmp += '\n'; break;
+        case 'r': tmp += '\r'; break;
+        case 't': tmp += '\t'; break;
         case 'u': {
           uint32_t cp = hex4();
           if (cp >= 0xD800 && cp < 0xDC00 && e - p >= 6 && p[0] == '\\' && p[1] == 'u') {
             const char* save = p;
             p += 2;
-            uint32_t lo = hex4();
+            const uint32_t lo = hex4();
             if (lo >= 0xDC00 && lo < 0xE000) cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
             else p = save;
           }
-          put_utf8(out, cp);
+          put_utf8(tmp, cp);
           break;
         }
         default: bad("bad escape");
       }
     }
-    return out;
+    return std::string_view(tmp);
   }
-  J number() {
+  Scalar number() {
     const char* s0 = p;
+    Scalar v;
     if (p < e && *p == '-') ++p;
-    if (p < e && *p == 'I') {  // -Infinity
-      if (!lit("Infinity")) bad("bad literal");
-      J v;
-      v.t = J::FLT;
+    if (p < e && *p == 'I') {
+      if (!lit("Infinity", 8)) bad("bad literal");
+      v.t = V_FLT;
       v.f = -INFINITY;
       return v;
     }
-    if (p >= e || !(*p >= '0' && *p <= '9')) bad("bad number");
+    if (p >= e || !(*p >= '0' && *p <= '9')) bad("bad value");
     if (*p == '0') ++p;
-    else while (p < e && *p >= '0' && *p <= '9') ++p;
+    else
+      while (p < e && *p >= '0' && *p <= '9') ++p;
     bool flt = false;
     if (p < e && *p == '.' && p + 1 < e && p[1] >= '0' && p[1] <= '9') {
       flt = true;
@@ -174,95 +180,150 @@ struct Parser {
         while (p < e && *p >= '0' && *p <= '9') ++p;
       }
     }
-    std::string tok(s0, p - s0);
-    J v;
+    const size_t n = (size_t)(p - s0);
+    if (!flt && n <= 18) {  // fits int64 without overflow checks
+      int64_t x = 0;
+      const char* q = s0;
+      const bool neg = *q == '-';
+      if (neg) ++q;
+      for (; q < p; ++q) x = x * 10 + (*q - '0');
+      v.t = V_INT;
+      v.i = neg ? -x : x;
+      return v;
+    }
+    char buf[64];
+    std::string big;
+    const char* z;
+    if (n < sizeof(buf)) {
+      memcpy(buf, s0, n);
+      buf[n] = 0;
+      z = buf;
+    } else {
+      big.assign(s0, n);
+      z = big.c_str();
+    }
     if (flt) {
-      v.t = J::FLT;
-      v.f = strtod(tok.c_str(), nullptr);  // correctly rounded, like Python's float()
+      v.t = V_FLT;
+      v.f = strtod(z, nullptr);  // correctly rounded, like Python's float()
     } else {
       errno = 0;
-      char* end = nullptr;
-      long long x = strtoll(tok.c_str(), &end, 10);
-      if (errno == ERANGE) fail(DIPPM_FEAT_UNSUPPORTED, "integer " + tok + " does not fit in 64 bits");
-      v.t = J::INT;
+      const long long x = strtoll(z, nullptr, 10);
+      if (errno == ERANGE) fail(DIPPM_FEAT_UNSUPPORTED, "integer " + std::string(z) + " does not fit in 64 bits");
+      v.t = V_INT;
       v.i = (int64_t)x;
     }
     return v;
   }
-  J value() {
-    if (++depth > 512) bad("nesting too deep");
+  // A scalar, or V_ARR / V_OBJ after skipping a container (validated).
+  Scalar value() {
     ws();
     if (p >= e) bad("unexpected end");
-    J v;
-    char c = *p;
-    if (c == '{') {
+    Scalar v;
+    switch (*p) {
+      case '{': skip_container(); v.t = V_OBJ; return v;
+      case '[': skip_container(); v.t = V_ARR; return v;
+      case '"': string(); v.t = V_STR; return v;
+      case 't': if (lit("true", 4)) { v.t = V_BOOL; v.b = true; return v; } break;
+      case 'f': if (lit("false", 5)) { v.t = V_BOOL; return v; } break;
+      case 'n': if (lit("null", 4)) return v; break;
+      case 'N': if (lit("NaN", 3)) { v.t = V_FLT; v.f = NAN; return v; } break;
+      case 'I': if (lit("Infinity", 8)) { v.t = V_FLT; v.f = INFINITY; return v; } break;
+      default: return number();
+    }
+    bad("bad literal");
+  }
+  void skip_container() {
+    if (++depth > 512) bad("nesting too deep");
+    const char open = *p++;
+    const char close = open == '{' ? '}' : ']';
+    ws();
+    if (p < e && *p == close) {
       ++p;
-      v.t = J::OBJ;
-      ws();
-      if (p < e && *p == '}') {
+      --depth;
+      return;
+    }
+    while (true) {
+      if (open == '{') {
+        ws();
+        if (p >= e || *p != '"') bad("expected key");
+        string();
+        ws();
+        if (p >= e || *p != ':') bad("expected ':'");
         ++p;
-      } else {
-        while (true) {
-          ws();
-          if (p >= e || *p != '"') bad("expected key");
-          std::string k = str();
-          ws();
-          if (p >= e || *p != ':') bad("expected ':'");
-          ++p;
-          J val = value();
-          v.o.emplace_back(std::move(k), std::move(val));
-          ws();
-          if (p < e && *p == ',') { ++p; continue; }
-          if (p < e && *p == '}') { ++p; break; }
-          bad("expected ',' or '}'");
-        }
       }
-    } else if (c == '[') {
-      ++p;
-      v.t = J::ARR;
+      value();
       ws();
-      if (p < e && *p == ']') {
+      if (p < e && *p == ',') {
         ++p;
-      } else {
-        while (true) {
-          v.a.push_back(value());
-          ws();
-          if (p < e && *p == ',') { ++p; continue; }
-          if (p < e && *p == ']') { ++p; break; }
-          bad("expected ',' or ']'");
-        }
+        continue;
       }
-    } else if (c == '"') {
-      v.t = J::STR;
-      v.s = str();
-    } else if (lit("true")) {
-      v.t = J::BOOL;
-      v.b = true;
-    } else if (lit("false")) {
-      v.t = J::BOOL;
-    } else if (lit("null")) {
-      v.t = J::NUL;
-    } else if (lit("NaN")) {
-      v.t = J::FLT;
-      v.f = NAN;
-    } else if (lit("Infinity")) {
-      v.t = J::FLT;
-      v.f = INFINITY;
-    } else {
-      v = number();
+      if (p < e && *p == close) {
+        ++p;
+        break;
+      }
+      bad("expected ',' or closing bracket");
     }
     --depth;
-    return v;
+  }
+  // Iterate an object's members: f(key) must consume the value.
+  template <class F>
+  void object(F&& f) {
+    ++p;
+    ws();
+    if (p < e && *p == '}') {
+      ++p;
+      return;
+    }
+    while (true) {
+      ws();
+      if (p >= e || *p != '"') bad("expected key");
+      const std::string key(string());
+      ws();
+      if (p >= e || *p != ':') bad("expected ':'");
+      ++p;
+      ws();
+      f(key);
+      ws();
+      if (p < e && *p == ',') {
+        ++p;
+        continue;
+      }
+      if (p < e && *p == '}') {
+        ++p;
+        return;
+      }
+      bad("expected ',' or '}'");
+    }
+  }
+  // Iterate an array's elements: f() must consume each element.
+  template <class F>
+  void array(F&& f) {
+    ++p;
+    ws();
+    if (p < e && *p == ']') {
+      ++p;
+      return;
+    }
+    while (true) {
+      ws();
+      f();
+      ws();
+      if (p < e && *p == ',') {
+        ++p;
+        continue;
+      }
+      if (p < e && *p == ']') {
+        ++p;
+        return;
+      }
+      bad("expected ',' or ']'");
+    }
+  }
+  bool peek(char c) {
+    ws();
+    return p < e && *p == c;
   }
 };
-
-J parse_json(const char* s, int64_t n) {
-  Parser P{s, s + n};
-  J v = P.value();
-  P.ws();
-  if (P.p != P.e) P.bad("extra data");
-  return v;
-}
 
 // ------------------------------------------------------------------ IR
 // Operator vocabulary, definition order = one-hot order (graph_ir.py:53-79).
@@ -345,72 +406,194 @@ void check_shape(const std::vector<int64_t>& s, int64_t id) {  // graph_ir.py:20
     if (d < 1) fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(id) + ": shape entry " + I(d) + " is not a positive integer");
 }
 
+// What one node entry of the document holds (last duplicate key wins).
+struct RawNode {
+  bool is_obj = false;
+  bool has_id = false;
+  Scalar id;
+  bool has_op = false;
+  uint8_t op_t = V_NUL;
+  std::string op;
+  bool has_inputs = false;
+  uint8_t inputs_t = V_NUL;
+  bool inputs_ok = true;  // every element an int (not bool)
+  std::vector<int64_t> inputs;
+  bool has_attrs = false;
+  uint8_t attrs_t = V_NUL;
+  std::vector<std::pair<std::string, Scalar>> attrs;  // final (deduplicated) entries
+  bool has_shape = false;
+  uint8_t shape_t = V_NUL;
+  std::vector<Scalar> shape;
+};
+
+void read_node(Cursor& c, RawNode& r) {
+  r.is_obj = true;
+  c.object([&](const std::string& key) {
+    if (key == "id") {
+      r.has_id = true;
+      r.id = c.value();
+    } else if (key == "op") {
+      r.has_op = true;
+      if (c.peek('"')) {
+        r.op_t = V_STR;
+        r.op = std::string(c.string());
+      } else {
+        r.op_t = c.value().t;
+        r.op.clear();
+      }
+    } else if (key == "inputs") {
+      r.has_inputs = true;
+      r.inputs.clear();
+      r.inputs_ok = true;
+      if (c.peek('[')) {
+        r.inputs_t = V_ARR;
+        c.array([&] {
+          const Scalar v = c.value();
+          if (v.t == V_INT) r.inputs.push_back(v.i);
+          else r.inputs_ok = false;
+        });
+      } else {
+        r.inputs_t = c.value().t;
+      }
+    } else if (key == "attrs") {
+      r.has_attrs = true;
+      r.attrs.clear();
+      if (c.peek('{')) {
+        r.attrs_t = V_OBJ;
+        c.object([&](const std::string& k) {
+          const Scalar v = c.value();
+          for (auto& kv : r.attrs)
+            if (kv.first == k) {
+              kv.second = v;
+              return;
+            }
+          r.attrs.emplace_back(k, v);
+        });
+      } else {
+        r.attrs_t = c.value().t;
+      }
+    } else if (key == "out_shape") {
+      r.has_shape = true;
+      r.shape.clear();
+      if (c.peek('[')) {
+        r.shape_t = V_ARR;
+        c.array([&] { r.shape.push_back(c.value()); });
+      } else {
+        r.shape_t = c.value().t;
+      }
+    } else {
+      c.value();
+    }
+  });
+}
+
 // parse_graph_json graph_ir.py:212-297
 Graph parse_graph(const char* text, int64_t len) {
-  J doc = parse_json(text, len);
-  if (doc.t != J::OBJ) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "top-level value must be an object");
-  const J* raw_nodes = doc.get("nodes");
-  if (!raw_nodes || raw_nodes->t != J::ARR || raw_nodes->a.empty())
-    fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"nodes\" must be a non-empty list");
-  const J* outputs = doc.get("outputs");
-  bool ok = outputs && outputs->t == J::ARR && !outputs->a.empty();
-  if (ok)
-    for (const J& o : outputs->a)
-      if (!(o.t == J::INT || o.t == J::BOOL)) ok = false;  // isinstance(o, int): bool is an int
-  if (!ok) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"outputs\" must be a non-empty list of node ids");
-  const J* batch = doc.get("batch");
-  if (!batch || batch->t != J::INT || batch->i < 1)
-    fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"batch\" must be a positive integer");
-  const J* name = doc.get("name");
-  if (name && name->t != J::STR) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"name\" must be a string");
+  Cursor c{text, text + len};
+  bool has_nodes = false, nodes_arr = false, has_outputs = false, outputs_arr = false, has_batch = false,
+       has_name = false;
+  std::vector<RawNode> raw;
+  std::vector<Scalar> outputs;
+  Scalar batch, name_v;
+  std::string name;
+  c.ws();
+  if (!c.peek('{')) {
+    c.value();  // a valid non-object document (or a syntax error)
+    c.ws();
+    if (c.p != c.e) c.bad("extra data");
+    fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "top-level value must be an object");
+  }
+  c.object([&](const std::string& key) {
+    if (key == "nodes") {
+      has_nodes = true;
+      raw.clear();
+      nodes_arr = c.peek('[');
+      if (nodes_arr) {
+        c.array([&] {
+          raw.emplace_back();
+          if (c.peek('{')) read_node(c, raw.back());
+          else c.value();
+        });
+      } else {
+        c.value();
+      }
+    } else if (key == "outputs") {
+      has_outputs = true;
+      outputs.clear();
+      outputs_arr = c.peek('[');
+      if (outputs_arr) c.array([&] { outputs.push_back(c.value()); });
+      else c.value();
+    } else if (key == "batch") {
+      has_batch = true;
+      batch = c.value();
+    } else if (key == "name") {
+      has_name = true;
+      if (c.peek('"')) {
+        name_v.t = V_STR;
+        name = std::string(c.string());
+      } else {
+        name_v = c.value();
+      }
+    } else {
+      c.value();
+    }
+  });
+  c.ws();
+  if (c.p != c.e) c.bad("extra data");
 
-  std::unordered_map<int64_t, size_t> by_id;  // id -> entry index (document order kept in `order_doc`)
+  if (!has_nodes || !nodes_arr || raw.empty())
+    fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"nodes\" must be a non-empty list");
+  bool ok = has_outputs && outputs_arr && !outputs.empty();
+  if (ok)
+    for (const Scalar& o : outputs)
+      if (!(o.t == V_INT || o.t == V_BOOL)) ok = false;  // isinstance(o, int): bool is an int
+  if (!ok) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"outputs\" must be a non-empty list of node ids");
+  if (!has_batch || batch.t != V_INT || batch.i < 1)
+    fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"batch\" must be a positive integer");
+  if (has_name && name_v.t != V_STR) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"name\" must be a string");
+
+  std::unordered_map<int64_t, size_t> by_id;
+  by_id.reserve(raw.size() * 2);
   std::vector<int64_t> order_doc;
+  order_doc.reserve(raw.size());
   std::vector<Node> entries;
-  for (const J& ent : raw_nodes->a) {
-    if (ent.t != J::OBJ) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "every node must be an object");
-    const J* idj = ent.get("id");
-    if (!idj || idj->t != J::INT || idj->i < 0)
+  entries.reserve(raw.size());
+  for (RawNode& r : raw) {
+    if (!r.is_obj) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "every node must be an object");
+    if (!r.has_id || r.id.t != V_INT || r.id.i < 0)
       fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node id must be a non-negative integer");
-    const int64_t nid = idj->i;
+    const int64_t nid = r.id.i;
     if (by_id.count(nid)) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "duplicate node id " + I(nid));
-    const J* op = ent.get("op");
-    if (!op || op->t != J::STR || op->s.empty())
+    if (!r.has_op || r.op_t != V_STR || r.op.empty())
       fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": missing operator name");
     Node n;
-    n.raw = op->s;
-    const J* ins = ent.get("inputs");
-    if (ins) {
-      bool good = ins->t == J::ARR;
-      if (good)
-        for (const J& x : ins->a)
-          if (x.t != J::INT) good = false;
-      if (!good) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": inputs must be a list of node ids");
-      for (const J& x : ins->a) n.inputs.push_back(x.i);
+    n.raw = std::move(r.op);
+    if (r.has_inputs) {
+      if (r.inputs_t != V_ARR || !r.inputs_ok)
+        fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": inputs must be a list of node ids");
+      n.inputs = std::move(r.inputs);
     }
-    const J* attrs = ent.get("attrs");
-    if (attrs) {
-      bool good = attrs->t == J::OBJ;
+    if (r.has_attrs) {
+      bool good = r.attrs_t == V_OBJ;
       if (good)
-        for (const auto& kv : attrs->o)
-          if (!kv.second.is_num()) good = false;
+        for (const auto& kv : r.attrs)
+          if (kv.second.t != V_INT && kv.second.t != V_FLT) good = false;
       if (!good) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": attrs must map names to numbers");
-      for (const auto& kv : attrs->o)
+      for (const auto& kv : r.attrs)
         for (int a = 0; a < 12; ++a)
-          if (kv.first == kAttrs[a]) {  // later duplicates overwrite (dict semantics)
+          if (kv.first == kAttrs[a]) {
             n.has_attr[a] = true;
-            n.attr[a] = kv.second.num();
-            n.attr_int[a] = kv.second.t == J::INT;
+            n.attr_int[a] = kv.second.t == V_INT;
             n.attr_i[a] = kv.second.i;
+            n.attr[a] = kv.second.t == V_INT ? (double)kv.second.i : kv.second.f;
           }
     }
-    const J* shp = ent.get("out_shape");
-    if (shp && shp->t != J::NUL) {
-      if (shp->t != J::ARR) fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": out_shape must be a list");
-      if (shp->a.size() < 1 || shp->a.size() > 4)
-        fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": shape rank " + I((int64_t)shp->a.size()) + " outside [1, 4]");
-      for (const J& d : shp->a) {
-        if (d.t != J::INT || d.i < 1)
+    if (r.has_shape && r.shape_t != V_NUL) {
+      if (r.shape_t != V_ARR) fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": out_shape must be a list");
+      if (r.shape.size() < 1 || r.shape.size() > 4)
+        fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": shape rank " + I((int64_t)r.shape.size()) + " outside [1, 4]");
+      for (const Scalar& d : r.shape) {
+        if (d.t != V_INT || d.i < 1)
           fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": shape entry is not a positive integer");
         n.shape.push_back(d.i);
       }
@@ -424,57 +607,68 @@ Graph parse_graph(const char* text, int64_t len) {
     for (int64_t src : entries[k].inputs)
       if (!by_id.count(src))
         fail(DIPPM_FEAT_DANGLING_REFERENCE, "node " + I(order_doc[k]) + " references missing input " + I(src));
-  for (const J& o : outputs->a) {
-    const int64_t oid = o.t == J::BOOL ? (int64_t)o.b : o.i;
+  for (const Scalar& o : outputs) {
+    const int64_t oid = o.t == V_BOOL ? (int64_t)o.b : o.i;
     if (!by_id.count(oid)) fail(DIPPM_FEAT_DANGLING_REFERENCE, "output id " + I(oid) + " does not exist");
   }
-  // _topological_order: Kahn over a min-heap of original ids, inputs counted with multiplicity
-  std::unordered_map<int64_t, std::vector<int64_t>> consumers;
-  std::unordered_map<int64_t, int64_t> pending;
-  for (size_t k = 0; k < entries.size(); ++k) {
-    pending[order_doc[k]] = (int64_t)entries[k].inputs.size();
-    for (int64_t src : entries[k].inputs) consumers[src].push_back(order_doc[k]);
+  // _topological_order: Kahn over a min-heap of original ids, inputs counted with multiplicity.
+  // Ids are renamed to entry indices for the bookkeeping; the heap orders by original id.
+  const size_t M = entries.size();
+  std::vector<int64_t> pending(M), cptr(M + 1, 0);
+  std::vector<size_t> cons;
+  for (size_t k = 0; k < M; ++k) {
+    pending[k] = (int64_t)entries[k].inputs.size();
+    for (int64_t src : entries[k].inputs) ++cptr[by_id[src] + 1];
   }
-  std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> heap;
-  for (int64_t nid : order_doc)
-    if (pending[nid] == 0) heap.push(nid);
-  std::vector<int64_t> order;
+  for (size_t k = 0; k < M; ++k) cptr[k + 1] += cptr[k];
+  cons.resize((size_t)cptr[M]);
+  {
+    std::vector<int64_t> fillp(cptr.begin(), cptr.end() - 1);
+    for (size_t k = 0; k < M; ++k)  // consumers in document order, like the reference's dict
+      for (int64_t src : entries[k].inputs) cons[(size_t)fillp[by_id[src]]++] = k;
+  }
+  std::priority_queue<std::pair<int64_t, size_t>, std::vector<std::pair<int64_t, size_t>>, std::greater<>> heap;
+  for (size_t k = 0; k < M; ++k)
+    if (pending[k] == 0) heap.push({order_doc[k], k});
+  std::vector<size_t> order;
+  order.reserve(M);
   while (!heap.empty()) {
-    const int64_t nid = heap.top();
+    const size_t k = heap.top().second;
     heap.pop();
-    order.push_back(nid);
-    auto it = consumers.find(nid);
-    if (it != consumers.end())
-      for (int64_t c : it->second)
-        if (--pending[c] == 0) heap.push(c);
+    order.push_back(k);
+    for (int64_t j = cptr[k]; j < cptr[k + 1]; ++j) {
+      const size_t cidx = cons[(size_t)j];
+      if (--pending[cidx] == 0) heap.push({order_doc[cidx], cidx});
+    }
   }
-  if (order.size() != entries.size()) {
+  if (order.size() != M) {
+    std::vector<char> done(M, 0);
+    for (size_t k : order) done[k] = 1;
     std::vector<int64_t> stuck;
-    std::unordered_set<int64_t> done(order.begin(), order.end());
-    for (int64_t nid : order_doc)
-      if (!done.count(nid)) stuck.push_back(nid);
+    for (size_t k = 0; k < M; ++k)
+      if (!done[k]) stuck.push_back(order_doc[k]);
     std::sort(stuck.begin(), stuck.end());
     fail(DIPPM_FEAT_CYCLIC_GRAPH, "nodes " + shape_str(stuck) + " form a dependency cycle");
   }
-  std::unordered_map<int64_t, int64_t> remap;
-  for (size_t k = 0; k < order.size(); ++k) remap[order[k]] = (int64_t)k;
+  std::vector<int64_t> remap(M);
+  for (size_t k = 0; k < M; ++k) remap[order[k]] = (int64_t)k;
   Graph g;
-  g.batch = batch->i;
-  g.name = name ? name->s : "";
-  g.nodes.reserve(order.size());
-  for (int64_t old : order) {
-    Node n = entries[by_id[old]];
-    for (auto& i : n.inputs) i = remap[i];
+  g.batch = batch.i;
+  g.name = std::move(name);
+  g.nodes.reserve(M);
+  for (size_t k : order) {
+    Node n = std::move(entries[k]);
+    for (auto& i : n.inputs) i = remap[by_id[i]];
     const std::string tail = op_tail(n.raw);
     n.kind = OTHER;
-    for (int k = 0; k < 16; ++k)
-      if (tail == kKinds[k]) n.kind = k;
+    for (int q = 0; q < 16; ++q)
+      if (tail == kKinds[q]) n.kind = q;
     n.is_op = true;
     for (const char* w : kNonOperator)
       if (tail == w) n.is_op = false;
     g.nodes.push_back(std::move(n));
   }
-  for (const J& o : outputs->a) g.outputs.push_back(remap[o.t == J::BOOL ? (int64_t)o.b : o.i]);
+  for (const Scalar& o : outputs) g.outputs.push_back(remap[by_id[o.t == V_BOOL ? (int64_t)o.b : o.i]]);
   return g;
 }
 

@@ -139,3 +139,65 @@ def make_dataset(num_graphs: int, seed: int = 0, n_lo: int = 270, n_hi: int = 33
     y = np.stack([latency, memory, energy], 1).astype(np.float32)
     return SynthDataset(n=n, node_ptr=node_ptr, x=x, edge_ptr=edge_ptr, src=src_g.astype(np.int64),
                         dst=dst_g.astype(np.int64), fs=fs, y=y)
+
+
+# ---------------------------------------------------------------------------
+# graph JSON documents (reference schema, graph_ir.py:8-27) for the end-to-end
+# predict path: native featuriser -> device forward -> MIG (configs[4])
+
+def _resnet_doc(n_ops: int, rng: np.random.Generator, name: str) -> str:
+    """A resnet-like model with about n_ops operator nodes: stem conv/bn/relu,
+    residual blocks (conv, batchnorm, relu, conv, batchnorm, add, relu) with an
+    occasional maxpool, a few constant inputs, then global pool, reshape, dense.
+    Non-source shapes are left out, so parsing runs shape inference."""
+    import json
+    batch = int(rng.choice([1, 2, 4, 8, 16, 32, 64]))
+    c = int(rng.choice([8, 16, 32, 64]))
+    hw = int(rng.choice([32, 64, 128, 224]))
+    nodes = [{"id": 0, "op": "input", "inputs": [], "attrs": {}, "out_shape": [batch, 3, hw, hw]}]
+
+    def add(op, inputs, attrs=None):
+        nodes.append({"id": len(nodes), "op": op, "inputs": inputs, "attrs": attrs or {}})
+        return len(nodes) - 1
+
+    conv = {"kernel_h": 3, "kernel_w": 3, "stride_h": 1, "stride_w": 1, "pad_h": 1, "pad_w": 1,
+            "dilation_h": 1, "dilation_w": 1, "groups": 1, "out_features": c, "has_bias": 0}
+    cur = add("nn.conv2d", [0], dict(conv))
+    cur = add("nn.batch_norm" if rng.random() < 0.5 else "batchnorm", [cur], {"epsilon": 1e-5})
+    cur = add("nn.relu", [cur])
+    ops = 3
+    size = hw
+    while ops + 10 < n_ops:
+        skip = cur
+        a = add("nn.conv2d", [cur], dict(conv))
+        a = add("batchnorm", [a], {"epsilon": 1e-5})
+        a = add("nn.relu", [a])
+        a = add("nn.conv2d", [a], dict(conv))
+        a = add("batchnorm", [a], {"epsilon": 1e-5})
+        if rng.random() < 0.2:  # a constant scale through dropped plumbing (edge contraction)
+            k = add("const", [])
+            nodes[k]["out_shape"] = [batch, c, size, size]
+            a = add("multiply", [a, k])
+            ops += 1
+        a = add("add", [a, skip])
+        cur = add("nn.relu", [a])
+        ops += 7
+        if size >= 4 and rng.random() < 0.1:
+            cur = add("nn.maxpool2d" if rng.random() < 0.5 else "maxpool2d", [cur],
+                      {"kernel_h": 2, "kernel_w": 2, "stride_h": 2, "stride_w": 2})
+            size //= 2
+            ops += 1
+    cur = add("global_avgpool2d", [cur])
+    cur = add("reshape", [cur])
+    cur = add("nn.dense", [cur], {"out_features": int(rng.integers(10, 1000)), "has_bias": 1})
+    return json.dumps({"name": name, "batch": batch, "outputs": [cur], "nodes": nodes})
+
+
+def make_graph_documents(count: int, seed: int = 5, n_lo: int = 12, n_hi: int = 5000, alpha: float = 1.5) -> list:
+    """`count` graph JSON documents with operator-node counts from a truncated
+    power law (N in [n_lo, n_hi], alpha 1.5)."""
+    rng = np.random.default_rng(seed)
+    u = rng.random(count)
+    a1 = 1.0 - alpha
+    n = ((n_hi ** a1 - n_lo ** a1) * u + n_lo ** a1) ** (1.0 / a1)
+    return [_resnet_doc(int(k), rng, f"synth-{seed}-{i}") for i, k in enumerate(n.astype(np.int64))]
