@@ -58,7 +58,8 @@ struct PackSegs {
   } s[DIPPM_MAX_PACK_SEGS];
 };
 
-// numerics.py:93-114 in the same operation order (t already incremented),
+// numerics.py:93-114 in the same operation order (t already incremented; the two bias
+// corrections are applied as multiplies by per-block reciprocals, fp64 throughout),
 // fused with the refresh of the fp32 copy and of every GEMM operand copy.
 __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, double* __restrict__ m,
                                                    double* __restrict__ v, const float* __restrict__ g,
@@ -68,10 +69,17 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (t_dev && do_adam) {  // step count on the device (CUDA-graph replays): bias corrections from it
-    const double t = (double)t_dev[0];
-    bc1 = 1.0 - pow(b1, t);
-    bc2 = 1.0 - pow(b2, t);
+    __shared__ double s_bc[2];  // one pow pair per block, not per thread
+    if (threadIdx.x == 0) {
+      const double t = (double)t_dev[0];
+      s_bc[0] = 1.0 - pow(b1, t);
+      s_bc[1] = 1.0 - pow(b2, t);
+    }
+    __syncthreads();
+    bc1 = s_bc[0];
+    bc2 = s_bc[1];
   }
+  const double inv_bc1 = 1.0 / bc1, inv_bc2 = 1.0 / bc2;
   for (; i < n; i += stride) {
     double val = p[i];
     if (do_adam) {
@@ -82,10 +90,10 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
       tmp *= 1.0 - b2;
       double vi = v[i] * b2;
       vi += tmp;
-      double denom = vi / bc2;
+      double denom = vi * inv_bc2;  // v / (1 - b2^t) as a multiply by the per-block reciprocal
       denom = sqrt(denom);
       denom += eps;
-      double step = mi / bc1;
+      double step = mi * inv_bc1;
       step /= denom;
       step *= -lr;
       step += val;
@@ -101,7 +109,12 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
       const int64_t j = i - sg.src_off;
       if (j >= 0 && j < sg.rows * sg.cols) {  // 32-bit div/mod: segments are < 2^31 elements
         const uint32_t jj = (uint32_t)j, cc = (uint32_t)sg.cols;
-        act_store(sg.dst, jj / cc, sg.dst_col_off + jj % cc, f);
+        if ((cc & (cc - 1)) == 0) {  // power-of-two widths (the padded hidden sizes): shifts
+          const int sh = __ffs(cc) - 1;
+          act_store(sg.dst, jj >> sh, sg.dst_col_off + (jj & (cc - 1)), f);
+        } else {
+          act_store(sg.dst, jj / cc, sg.dst_col_off + jj % cc, f);
+        }
       }
     }
   }

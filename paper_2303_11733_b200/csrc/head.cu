@@ -171,17 +171,41 @@ __global__ void k_fc3(ActView x3, int64_t G, int width, const float* __restrict_
 //   d2[g,j]  = (sum_k d3[g,k] W3[j,k]) * (x3[g,j] > 0 ? keep_scale : 0)
 //   db2[j]   = sum_g d2[g,j]
 // Block: 32 columns x 8 graph groups; fixed-order reductions (deterministic).
-__global__ void __launch_bounds__(256) k_fc3_backward(ActView x3, int64_t G, int width, const float* __restrict__ w3,
+constexpr int kFc3Groups = 32;  // row groups per block (warps): 32 columns x 32 row groups
+__global__ void __launch_bounds__(1024) k_fc3_backward(ActView x3, int64_t G, int width, const float* __restrict__ w3,
                                                       const float* __restrict__ d3, float keep_scale,
                                                       float* __restrict__ gw3, float* __restrict__ gb3, ActView d2,
                                                       float* __restrict__ gb2) {
-  __shared__ float s[8][32][5];
+  __shared__ float s[kFc3Groups][32][5];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, ab = 0.f;
   if (j < width) {
     const float w0 = w3[j * 3 + 0], w1 = w3[j * 3 + 1], w2 = w3[j * 3 + 2];
-    for (int64_t g = ty; g < G; g += 8) {
+    int64_t g = ty;
+    // 4 rows per step: all loads issued before the stores (d2 may alias nothing we read,
+    // but the compiler cannot know), so each thread keeps 4 row loads in flight.
+    for (; g + 3 * kFc3Groups < G; g += 4 * kFc3Groups) {
+      float x[4], e[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = act_load(x3, g + kFc3Groups * u, j);
+        e[u][0] = __ldg(d3 + (g + kFc3Groups * u) * 3 + 0);
+        e[u][1] = __ldg(d3 + (g + kFc3Groups * u) * 3 + 1);
+        e[u][2] = __ldg(d3 + (g + kFc3Groups * u) * 3 + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fmaf(x[u], e[u][0], a0);
+        a1 = fmaf(x[u], e[u][1], a1);
+        a2 = fmaf(x[u], e[u][2], a2);
+        const float dx = e[u][0] * w0 + e[u][1] * w1 + e[u][2] * w2;
+        const float dv = x[u] > 0.f ? dx * keep_scale : 0.f;
+        act_store(d2, g + kFc3Groups * u, j, dv);
+        ab += dv;
+      }
+    }
+    for (; g < G; g += kFc3Groups) {
       const float x = act_load(x3, g, j);
       const float e0 = d3[g * 3 + 0], e1 = d3[g * 3 + 1], e2 = d3[g * 3 + 2];
       a0 = fmaf(x, e0, a0);
@@ -200,7 +224,7 @@ __global__ void __launch_bounds__(256) k_fc3_backward(ActView x3, int64_t G, int
   __syncthreads();
   if (ty == 0 && j < width) {
     float r0 = 0.f, r1 = 0.f, r2 = 0.f, rb = 0.f;
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < kFc3Groups; ++q) {
       r0 += s[q][tx][0];
       r1 += s[q][tx][1];
       r2 += s[q][tx][2];
@@ -211,10 +235,24 @@ __global__ void __launch_bounds__(256) k_fc3_backward(ActView x3, int64_t G, int
     gw3[j * 3 + 2] = r2;
     gb2[j] = rb;
   }
-  if (blockIdx.x == 0 && threadIdx.x < 3) {
-    float b = 0.f;
-    for (int64_t g = 0; g < G; ++g) b += d3[g * 3 + threadIdx.x];
-    gb3[threadIdx.x] = b;
+  if (blockIdx.x == 0) {  // db3 = sum_g d3[g]: 1024 threads, fixed-order tree over thread partials
+    __shared__ float sb[3][1024];
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    for (int64_t g = threadIdx.x; g < G; g += blockDim.x) {
+      b0 += d3[g * 3 + 0];
+      b1 += d3[g * 3 + 1];
+      b2 += d3[g * 3 + 2];
+    }
+    sb[0][threadIdx.x] = b0;
+    sb[1][threadIdx.x] = b1;
+    sb[2][threadIdx.x] = b2;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w)
+        for (int k = 0; k < 3; ++k) sb[k][threadIdx.x] += sb[k][threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x < 3) gb3[threadIdx.x] = sb[threadIdx.x][0];
   }
 }
 
@@ -224,8 +262,18 @@ __global__ void __launch_bounds__(256) k_colsum_act(ActView a, int64_t rows, int
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
   float acc = 0.f;
-  if (c < cols)
-    for (int64_t r = ty; r < rows; r += 8) acc += act_load(a, r, c);
+  if (c < cols) {
+    int64_t r = ty;
+    for (; r + 24 < rows; r += 32) {  // 4 independent loads in flight, summed in row order
+      const float v0 = act_load(a, r, c), v1 = act_load(a, r + 8, c), v2 = act_load(a, r + 16, c),
+                  v3 = act_load(a, r + 24, c);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; r < rows; r += 8) acc += act_load(a, r, c);
+  }
   s[ty][tx] = acc;
   __syncthreads();
   if (ty == 0 && c < cols) {
@@ -291,7 +339,7 @@ int32_t dippm_fc3_backward(dippm_act_t x3, int64_t G, int32_t width, const float
                            float keep_scale, float* grad_w3, float* grad_b3, dippm_act_t d2, float* grad_b2,
                            void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && width >= 1, "fc3_backward: bad shape");
-  k_fc3_backward<<<ceil_div_i(width, 32), 256, 0, (cudaStream_t)stream>>>(make_view(x3), G, width, w3, dout,
+  k_fc3_backward<<<ceil_div_i(width, 32), 32 * kFc3Groups, 0, (cudaStream_t)stream>>>(make_view(x3), G, width, w3, dout,
                                                                           keep_scale, grad_w3, grad_b3,
                                                                           make_view(d2), grad_b2);
   DIPPM_LAUNCH_CHECK("k_fc3_backward");

@@ -656,15 +656,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
             const uint64_t seed = p.seed ^ (p.seed_dev ? (uint64_t)p.seed_dev[0] * 0x9E3779B97F4A7C15ull : 0ull);
             if (row < p.M) {
-#pragma unroll 1
-              for (int i = 0; i < 32; ++i) {
-                const int64_t idx = row * p.ldm + n + i;
-                if (p.drop_mode == 1) {
-                  v[i] *= p.mask[idx];
-                } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
-                  const float mk = uniform_hash(seed, (uint64_t)idx) >= p.drop_p ? 1.0f / (1.0f - p.drop_p) : 0.f;
-                  p.mask[idx] = mk;
+              if (p.drop_mode == 1) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 m4 = *reinterpret_cast<const float4*>(p.mask + row * p.ldm + n + i);
+                  v[i] *= m4.x; v[i + 1] *= m4.y; v[i + 2] *= m4.z; v[i + 3] *= m4.w;
+                }
+              } else {  // counter-hash stream (numerics.py:45-55 semantics, statistical parity)
+                const float keep = 1.0f / (1.0f - p.drop_p);
+#pragma unroll 8
+                for (int i = 0; i < 32; ++i) {
+                  const int64_t idx = row * p.ldm + n + i;
+                  const float mk = uniform_hash(seed, (uint64_t)idx) >= p.drop_p ? keep : 0.f;
                   v[i] *= mk;
+                }
+                if (p.mask) {  // optional record of the mask (the backward uses the 1-bit masks)
+#pragma unroll
+                  for (int i = 0; i < 32; i += 4) {
+                    float4 m4;
+                    m4.y = uniform_hash(seed, (uint64_t)(row * p.ldm + n + i + 1)) >= p.drop_p ? keep : 0.f;
+                    m4.z = uniform_hash(seed, (uint64_t)(row * p.ldm + n + i + 2)) >= p.drop_p ? keep : 0.f;
+                    m4.w = uniform_hash(seed, (uint64_t)(row * p.ldm + n + i + 3)) >= p.drop_p ? keep : 0.f;
+                    m4.x = uniform_hash(seed, (uint64_t)(row * p.ldm + n + i)) >= p.drop_p ? keep : 0.f;
+                    *reinterpret_cast<float4*>(p.mask + row * p.ldm + n + i) = m4;
+                  }
                 }
               }
             }
@@ -951,9 +966,9 @@ extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void*
   const bool mn = a->kind == DIPPM_GEMM_WGRAD;
   DIPPM_ARG_CHECK(mn == (a->a_mn_major != 0) && (mn == (a->b_mn_major != 0) || a->kind == DIPPM_GEMM_FWD),
                   "gemm: FWD takes K-major A (B either), STORE/GATE K-major, WGRAD MN-major");
-  DIPPM_ARG_CHECK(a->drop_mode == 0 || (a->mask && a->kind == DIPPM_GEMM_FWD && a->b_mn_major && a->drop_p >= 0 &&
-                                        a->drop_p < 1),
-                  "gemm: dropout needs FWD with MN-major B, a mask buffer and 0 <= p < 1");
+  DIPPM_ARG_CHECK(a->drop_mode == 0 || ((a->mask || a->drop_mode == 2) && a->kind == DIPPM_GEMM_FWD &&
+                                        a->b_mn_major && a->drop_p >= 0 && a->drop_p < 1 && a->ldm % 4 == 0),
+                  "gemm: dropout needs FWD with MN-major B, 0 <= p < 1, ldm %% 4 == 0 and (mode 1) a mask buffer");
   const int bk = a->a.dtype == DIPPM_DT_BF16 ? 64 : 32;
   DIPPM_ARG_CHECK(mn || a->K % bk == 0, "gemm: K=%lld must be a multiple of %d", (long long)a->K, bk);
   if (a->a.dtype == DIPPM_DT_BF16) return tc::dispatch<1>(a, s);

@@ -509,7 +509,10 @@ class Engine:
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
         for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
             self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,
-                       out=out.view(), drop_mode=drop, mask=ws.masks[j].data_ptr(), ldm=hp, drop_p=dropout_p,
+                       out=out.view(), drop_mode=drop, ldm=hp, drop_p=dropout_p,
+                       # generated masks (mode 2) are not recorded on the tensor-core path: the
+                       # backward gates on the 1-bit masks; the SIMT anchor records them
+                       mask=None if drop == 2 and self.backend == 0 else ws.masks[j].data_ptr(),
                        seed=seed * 2 + j, seed_dev=_p(self.t_dev) if drop == 2 else None,
                        relu_bits=_p(ws.head_bits) if ws.train and j == 0 else None, bits_ld=hp // 32)
         _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
