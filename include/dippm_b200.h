@@ -138,7 +138,9 @@ int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t*
                                   const int32_t* node_graph, dippm_act_t h3, dippm_act_t B, int32_t width,
                                   int64_t num_nodes, const int32_t* t_rowptr, const int32_t* t_col,
                                   const float* inv_deg, float* colsum_partial, float* bias_grad, int32_t* sync,
-                                  void* stream);
+                                  const uint32_t* h3_bits, int64_t bits_ld, void* stream);
+/*   h3_bits (optional): the layer-3 forward GEMM's 1-bit (h3 > 0) masks (dippm_gemm relu_bits
+ *   layout, bits_ld >= N); used instead of reading h3 for the ReLU gate. */
 /* node_graph[v] = g for v in [graph_ptr[g], graph_ptr[g+1]). */
 int32_t dippm_node_graph(const int32_t* graph_ptr, int64_t num_graphs, int32_t* node_graph, void* stream);
 
@@ -189,10 +191,10 @@ typedef struct dippm_gemm_args {
   double drop_p;
   uint64_t seed;
   const int64_t* seed_dev; /* nullable device step counter mixed into the dropout seed (graph replays) */
-  uint32_t* relu_bits;       /* FWD (optional): bit c%32 of word [r*bits_ld + c/32] = (stored out[r,c] > 0) */
+  uint32_t* relu_bits;       /* FWD (optional): bit c%32 of word [(c/32)*bits_ld + r] = (stored out[r,c] > 0) */
   const uint32_t* gate_bits; /* GATE (optional): use these bits instead of reading `gate` values          */
                              /* (relu_bits / gate_bits: tensor-core backend; the SIMT anchor gates on values) */
-  int64_t bits_ld;           /* words per row of relu_bits / gate_bits (>= N/32)                           */
+  int64_t bits_ld;           /* words per 32-column chunk of relu_bits / gate_bits (chunk-major, >= M)   */
   int64_t cta_pair;          /* 0 auto, 1 force 1-CTA 128-row tiles, 2 force cta_group::2 256-row tiles   */
   int32_t* tile_sync;        /* WGRAD fused reduce: device int32[dippm_wgrad_sync_ints(M, N)], zeroed once  */
                              /* by the caller; every launch leaves it zero again (graph-replay safe)      */

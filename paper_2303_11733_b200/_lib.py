@@ -78,7 +78,7 @@ SIGNATURES = {
     "dippm_colsum_sync_ints": (I32, [I64]),
     "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P, P, P]),
     "dippm_readout_backward": (I32, [P, I64, P, I64, I32, Act, Act, I64, P]),
-    "dippm_readout_aggregate_t": (I32, [P, I64, P, P, Act, Act, I32, I64, P, P, P, P, P, P, P]),
+    "dippm_readout_aggregate_t": (I32, [P, I64, P, P, Act, Act, I32, I64, P, P, P, P, P, P, P, I64, P]),
     "dippm_node_graph": (I32, [P, I64, P, P]),
     "dippm_fs_normalize": (I32, [P, I64, P, Act, I32, P]),
     "dippm_reduce_rows": (I32, [P, I64, I64, I32, F64, P, P]),

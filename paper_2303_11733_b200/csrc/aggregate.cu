@@ -145,11 +145,35 @@ struct ReadoutArgs {
   int64_t ld_du;
   const int* graph_ptr;     // [G+1]
   const int* node_graph;    // [N]
-  ActView h3;               // ReLU gate
+  ActView h3;               // ReLU gate (values), used when h3_bits is NULL
+  const uint32_t* h3_bits;  // 1-bit (h3 > 0) masks from the layer-3 forward epilogue, word [(c/32)*bits_ld + r]
+  int64_t bits_ld;
 };
 
+// ReLU'(z3) for 8 consecutive columns per chunk: from the forward's bit mask (4 bytes per 32
+// columns) when present, else by reading h3 (z > 0 <=> h > 0).
+template <int DT, int CPL>
+__device__ __forceinline__ void relu_gate(const ReadoutArgs& ro, int64_t r, int c0, int stride, bool (&gt)[CPL][8]) {
+  if (ro.h3_bits) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = c0 + q * stride;
+      const uint32_t w = __ldg(ro.h3_bits + (int64_t)(c >> 5) * ro.bits_ld + r) >> (c & 31);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) gt[q][k] = (w >> k) & 1u;
+    }
+  } else {
+    float hg[CPL][8];
+    load_chunks<DT, CPL>(ro.h3, r, c0, stride, hg);
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) gt[q][k] = hg[q][k] > 0.f;
+  }
+}
+
 template <int DT, int CPL, bool kReadout>
-__global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
+__global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
                                                                 const int* __restrict__ t_rowptr,
                                                                 const int* __restrict__ t_col,
                                                                 const float* __restrict__ inv_deg,
@@ -196,12 +220,12 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
           dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
           dr[q][4] = b2.x * inv_n; dr[q][5] = b2.y * inv_n; dr[q][6] = b2.z * inv_n; dr[q][7] = b2.w * inv_n;
         }
-        float hg[CPL][8];
-        load_chunks<DT, CPL>(ro.h3, row, c0, stride, hg);
+        bool gt[CPL][8];
+        relu_gate<DT, CPL>(ro, row, c0, stride, gt);
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) own[q][k] = hg[q][k] > 0.f ? dr[q][k] : 0.f;
+          for (int k = 0; k < 8; ++k) own[q][k] = gt[q][k] ? dr[q][k] : 0.f;
           act_store8_t<DT>(B, row, c0 + q * stride, own[q]);
         }
       } else {
@@ -215,11 +239,12 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_aggregate_t(ActView B, int w
           const float w0 = staged ? s_cw[j] : inv_deg[v0];
           float x[CPL][8];
           if constexpr (kReadout) {
-            load_chunks<DT, CPL>(ro.h3, v0, c0, stride, x);
+            bool gt[CPL][8];
+            relu_gate<DT, CPL>(ro, v0, c0, stride, gt);
 #pragma unroll
             for (int q = 0; q < CPL; ++q)
 #pragma unroll
-              for (int k = 0; k < 8; ++k) x[q][k] = x[q][k] > 0.f ? dr[q][k] : 0.f;
+              for (int k = 0; k < 8; ++k) x[q][k] = gt[q][k] ? dr[q][k] : 0.f;
           } else {
             load_chunks<DT, CPL>(B, v0, c0, stride, x);
           }
@@ -502,9 +527,11 @@ int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t 
 int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t* graph_ptr, const int32_t* node_graph,
                                   dippm_act_t h3, dippm_act_t B, int32_t width, int64_t N, const int32_t* t_rowptr,
                                   const int32_t* t_col, const float* inv_deg, float* colsum_partial,
-                                  float* bias_grad, int32_t* sync, void* stream) {
-  DIPPM_ARG_CHECK(h3.dtype == B.dtype && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
-  ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3)};
+                                  float* bias_grad, int32_t* sync, const uint32_t* h3_bits, int64_t bits_ld,
+                                  void* stream) {
+  DIPPM_ARG_CHECK((h3_bits || h3.dtype == B.dtype) && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
+  DIPPM_ARG_CHECK(!h3_bits || bits_ld >= N, "readout_aggregate_t: bits_ld %lld < rows", (long long)bits_ld);
+  ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3), h3_bits, bits_ld};
   return launch_aggregate_t(B, width, N, 1, t_rowptr, t_col, inv_deg, colsum_partial, ro, true, bias_grad, sync,
                             (cudaStream_t)stream);
 }

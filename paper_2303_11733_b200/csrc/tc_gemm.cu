@@ -48,7 +48,7 @@ struct Params {
   float drop_p;
   uint64_t seed;
   const int64_t* seed_dev;
-  uint32_t* relu_bits;        // FWD: optional 1-bit (out > 0) mask, bits_ld words per row
+  uint32_t* relu_bits;        // FWD: optional 1-bit (out > 0) mask, word [(c/32)*bits_ld + r] (chunk-major)
   const uint32_t* gate_bits;  // GATE: optional 1-bit gate instead of gate values
   int64_t bits_ld;
   // WGRAD output: reduce_mode 0 = partials to c only; 1 = fused reduce, every split CTA
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t gw[kBN / 64];
 #pragma unroll
           for (int i = 0; i < kBN / 64; ++i)
-            gw[i] = row < p.M ? __ldg(p.gate_bits + row * p.bits_ld + (n0 >> 5) + half + 2 * i) : 0u;
+            gw[i] = row < p.M ? __ldg(p.gate_bits + ((n0 >> 5) + half + 2 * i) * p.bits_ld + row) : 0u;
           mbar_wait(&tfull[acc], use & 1);
           tc_fence_after();
           const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBN;
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t bits = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) bits |= (uint32_t)(v[i] > 0.f) << i;
-            p.relu_bits[row * p.bits_ld + (n >> 5)] = bits;
+            p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;  // chunk-major: a warp stores 128 contiguous bytes
           }
           epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
                           local * (kBN / 64) + (ch >> 1));
@@ -907,6 +907,7 @@ static int run_bn(const dippm_gemm_args_t* a, cudaStream_t s) {
   const int64_t splits = kEpi == EPI_PARTIAL ? std::max<int64_t>(1, a->splits) : 1;
   const bool pair = a->cta_pair == 2 ? pair_ok
                                      : (a->cta_pair != 1 && pair_ok && a->M > kBM &&
+                                        (kEpi == EPI_PARTIAL || a->K > 128) &&  // short K: epilogue-bound, 1-CTA wins
                                         4 * m_tiles * (a->N / 256) * splits >= 3 * num_sms());
   if (a->cta_pair == 2 && !pair_ok) {
     set_error("gemm: cta_pair=2 needs N %% 256 == 0 (N=%lld)", (long long)a->N);

@@ -321,7 +321,15 @@ class Workspace:
         self.N, self.G = N, G
         sage = eng.L.arch == "sage"
         if sage:
-            self.A = [ActBuf(N, 2 * FEATURE_WIDTH, dt, dev), ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+            # A1 = [X | agg X | 1 | 0...]: the constant ones column (col 64) turns the layer-1 weight
+            # gradient GEMM into [dW_self; dW_neigh; db] in one pass (row 64 = sum_rows dz1 = the
+            # bias gradient, gnn.py:230, which lands on sage1.bias right after w_neigh in the layout)
+            self.A = [ActBuf(N, 4 * FEATURE_WIDTH, dt, dev), ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+            a1 = self.A[0].t
+            (a1[0] if dt == DT_TF32X3 else a1)[:, 2 * FEATURE_WIDTH:].zero_()
+            (a1[0] if dt == DT_TF32X3 else a1)[:, 2 * FEATURE_WIDTH] = 1.0
+            if dt == DT_TF32X3:
+                a1[1][:, 2 * FEATURE_WIDTH:].zero_()
             self.H3 = ActBuf(N, hp, dt, dev)
         self.u = ActBuf(G, eng.L.u_width, dt, dev)
         self.x2 = ActBuf(G, hp, dt, dev)
@@ -337,22 +345,24 @@ class Workspace:
             self.dout = torch.empty(G, 3, **f32)
             self.d2 = ActBuf(G, hp, dt, dev)
             self.d1 = ActBuf(G, hp, dt, dev)
-            self.head_bits = torch.empty(G, hp // 32, dtype=torch.int32, device=dev)
+            self.head_bits = torch.empty(hp // 32, G, dtype=torch.int32, device=dev)
             if sage:
                 self.du = torch.empty(G, hp, **f32)
                 self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
                 # 1-bit ReLU' masks of h1, h2 (and of the head's x2, dropout included) written by the
                 # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
-                self.relu_bits = torch.empty(2, N, hp // 32, dtype=torch.int32, device=dev)
+                # chunk-major [3, Hp/32, N]: word (c/32, r); a warp's 32 rows store/load 128 contiguous bytes
+                self.relu_bits = torch.empty(3, hp // 32, N, dtype=torch.int32, device=dev)  # h1, h2, h3
                 self.colsum = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
                 self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
             # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
             # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
             # split counts are chosen per call from the actual row count (<= these upper bounds)
             big = 1 << 30
-            smax = [lib.dippm_wgrad_splits(2 * d, hp, big) for d in eng.L.d_in]
+            wg_rows = [2 * d + (1 if i == 0 else 0) for i, d in enumerate(eng.L.d_in)]  # layer 1: + bias row
+            smax = [lib.dippm_wgrad_splits(w, hp, big) for w in wg_rows]
             hmax = [lib.dippm_wgrad_splits(hp, hp, big), lib.dippm_wgrad_splits(eng.L.u_width, hp, big)]
-            widest = max([s * 2 * d for s, d in zip(smax, eng.L.d_in)] + [hmax[0] * hp, hmax[1] * eng.L.u_width])
+            widest = max([s * w for s, w in zip(smax, wg_rows)] + [hmax[0] * hp, hmax[1] * eng.L.u_width])
             self.splitk = torch.empty(widest * hp, **f32)
             sync = max(lib.dippm_wgrad_sync_ints(w, hp) for w in [2 * d for d in eng.L.d_in] + [eng.L.u_width])
             self.tile_sync = torch.zeros(sync, dtype=torch.int32, device=dev)
@@ -496,7 +506,7 @@ class Engine:
                           _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
             self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.Wf[i].view(), 1,
                        bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i],
-                       relu_bits=_p(bits[i]) if bits is not None and i < 2 else None, bits_ld=hp // 32)
+                       relu_bits=_p(bits[i]) if bits is not None else None, bits_ld=ws.N)
         _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
                   ws.u.view(), s)
         self.launches += 3 + 1
@@ -514,7 +524,7 @@ class Engine:
                        # backward gates on the 1-bit masks; the SIMT anchor records them
                        mask=None if drop == 2 and self.backend == 0 else ws.masks[j].data_ptr(),
                        seed=seed * 2 + j, seed_dev=_p(self.t_dev) if drop == 2 else None,
-                       relu_bits=_p(ws.head_bits) if ws.train and j == 0 else None, bits_ld=hp // 32)
+                       relu_bits=_p(ws.head_bits) if ws.train and j == 0 else None, bits_ld=ws.G)
         _lib.call("dippm_fc3_forward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), self._f32("fc3.b"), _p(ws.out),
                   _p(self.norm), _p(ws.y_pred) if predict else None, _p(ws.mig) if predict else None,
                   _p(ws.nonfinite), s)
@@ -534,7 +544,7 @@ class Engine:
                   self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
         self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
         self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
-                   gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=hp // 32)
+                   gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=ws.G)
         _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
         self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
         if self.arch == "mlp":  # no graph network below the head
@@ -545,10 +555,13 @@ class Engine:
         for i in (2, 1, 0):
             B = ws.B[cur]
             bias = self._g32(f"sage{i + 1}.bias")  # gnn.py:230, reduced inside the kernel
+            if i == 0:  # layer 1: the bias gradient comes out of the WGRAD GEMM (ones column of A1)
+                self._wgrad(B.view(0), ws.A[0].view(0), N, 2 * L.d_in[0] + 1, ws, "sage1.w_self")
+                continue
             if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
                           ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr), _p(b.t_col), _p(b.inv_deg),
-                          _p(ws.colsum), bias, _p(ws.colsum_sync), s)
+                          _p(ws.colsum), bias, _p(ws.colsum_sync), _p(ws.relu_bits[2]), ws.N, s)
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
                           _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)
@@ -556,6 +569,6 @@ class Engine:
             if i > 0:
                 self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
                            out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
-                           gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=hp // 32)
+                           gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=ws.N)
                 cur = 1 - cur
-        self.launches += 5 + 3 * 2 - 3
+        self.launches += 5 + 3 * 2 - 3 - 1

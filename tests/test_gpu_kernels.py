@@ -358,9 +358,9 @@ def test_grouped_csr_equals_global_path(golden, case):
 
 
 def _bits_of(x):
-    """[M, N] bool -> [M, N/32] int32 words, bit c%32 of word c/32."""
+    """[M, N] bool -> chunk-major [N/32, M] int32 words: bit c%32 of word (c/32, r)."""
     b = x.reshape(x.shape[0], -1, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)
-    return b.sum(-1).astype(np.uint32).view(np.int32)
+    return np.ascontiguousarray(b.sum(-1).astype(np.uint32).view(np.int32).T)
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
@@ -381,9 +381,9 @@ def test_cta_pair_tiles_equal_single_cta(prec, M):
     res = {}
     for pair in (1, 2):
         out = ActBuf(M, N, dt, "cuda")
-        bits = torch.full((M, N // 32), -1, dtype=torch.int32, device="cuda")
+        bits = torch.full((N // 32, M), -1, dtype=torch.int32, device="cuda")
         _gemm(_lib.GEMM_FWD, M, N, K, A.view(), 0, Wn.view(), 1, bias=bias.data_ptr(), relu=1, out=out.view(),
-              relu_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair)
+              relu_bits=bits.data_ptr(), bits_ld=M, cta_pair=pair)
         h = out.to_float().double().cpu().numpy()
         assert np.max(np.abs(h - ref_fwd)) <= (2e-2 if prec == "bf16" else 1e-5) * np.abs(ref_fwd).max()
         assert np.array_equal(bits.cpu().numpy(), _bits_of(h > 0)), pair
@@ -393,7 +393,7 @@ def test_cta_pair_tiles_equal_single_cta(prec, M):
         _gemm(_lib.GEMM_GATE, M, N, K, A.view(), 0, Wk.view(), 0, out=g_val.view(), gate=out.view(),
               gate_scale=1.5, cta_pair=pair)
         _gemm(_lib.GEMM_GATE, M, N, K, A.view(), 0, Wk.view(), 0, out=g_bit.view(), gate=dev.NULL_ACT,
-              gate_scale=1.5, gate_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair)
+              gate_scale=1.5, gate_bits=bits.data_ptr(), bits_ld=M, cta_pair=pair)
         assert torch.equal(g_val.t, g_bit.t)
         ref_gate = np.where(h > 0, 1.5 * (a64 @ wk64.T), 0.0)
         assert np.max(np.abs(g_val.t.double().cpu().numpy() - ref_gate)) <= 1e-5 * np.abs(ref_gate).max()
@@ -446,3 +446,51 @@ def test_wgrad_fused_reduce(prec, R, M, N, splits):
             for k in range(1, S):  # fp64 sum of the same partials in split order
                 sep += ws[k].double()
             assert torch.equal(out, (sep * 0.5).float()), backend
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_readout_aggregate_t_bits_equal_values(prec):
+    """Layer-3 readout backward + agg^T + bias grad: gating on the forward's 1-bit masks
+    gives exactly what gating on the h3 values gives, and both match fp64 numpy."""
+    rng = np.random.default_rng(21)
+    G, W = 9, 64
+    n = rng.integers(3, 40, G)
+    gp = np.zeros(G + 1, np.int32)
+    np.cumsum(n, out=gp[1:])
+    N = int(gp[-1])
+    src, dst = [], []
+    for g in range(G):
+        for v in range(gp[g] + 1, gp[g + 1]):
+            src.append(v - 1)
+            dst.append(v)
+            if v - gp[g] > 2:
+                src.append(int(rng.integers(gp[g], v - 1)))
+                dst.append(v)
+    src, dst = np.array(src), np.array(dst)
+    b = upload_batch(np.zeros((N, 32), np.float32), src, dst, gp, np.zeros((G, 5), np.float32))
+    dt = dev.PRECISIONS[prec]
+    h3, h64, _ = _rand_act(N, W, dt, rng)
+    bits = torch.from_numpy(_bits_of(h64 > 0)).cuda()
+    du = torch.from_numpy(rng.normal(size=(G, W)).astype(np.float32)).cuda()
+    lib = _lib.load()
+    outs = []
+    for use_bits in (False, True):
+        B = ActBuf(N, 2 * W, dt, "cuda")
+        part = torch.empty(lib.dippm_colsum_rows(N), W, device="cuda")
+        sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device="cuda")
+        bias = torch.empty(W, device="cuda")
+        _lib.call("dippm_readout_aggregate_t", du.data_ptr(), W, b.graph_ptr.data_ptr(), b.node_graph.data_ptr(),
+                  h3.view(), B.view(), W, N, b.t_rowptr.data_ptr(), b.t_col.data_ptr(), b.inv_deg.data_ptr(),
+                  part.data_ptr(), bias.data_ptr(), sync.data_ptr(), bits.data_ptr() if use_bits else None,
+                  N, dev._stream())
+        outs.append((B.to_float().clone(), bias.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    # fp64 reference: dz3[v] = du[g(v)] / N_g * (h3 > 0); agg^T dz3; bias = sum dz3
+    gid = np.repeat(np.arange(G), n)
+    dz = du.double().cpu().numpy()[gid] / n[gid][:, None] * (h64 > 0)
+    agg = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist())))
+    got = outs[0][0].double().cpu().numpy()
+    tol = 2e-2 if prec == "bf16" else 1e-5
+    assert np.allclose(got[:, :W], dz, atol=tol * np.abs(dz).max())
+    assert np.allclose(got[:, W:], agg.T @ dz, atol=tol * np.abs(dz).max())
+    assert np.allclose(outs[0][1].double().cpu().numpy(), dz.sum(0), atol=tol * np.abs(dz).sum(0).max())

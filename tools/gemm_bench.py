@@ -61,7 +61,7 @@ for prec in ("bf16", "fp32"):
                              f["cta_pair"], f["tile_sync"], f["out_scale"])
         return lambda: _lib.check(lib.dippm_gemm(args, 0, dev._stream()))
 
-    bits = torch.zeros(M, N // 32, dtype=torch.int32, device="cuda")
+    bits = torch.zeros(N // 32, M, dtype=torch.int32, device="cuda")
     Sf = lib.dippm_wgrad_splits(K, N, M)
     sync = torch.zeros(lib.dippm_wgrad_sync_ints(K, N), dtype=torch.int32, device="cuda")
     wout = torch.empty(K, N, device="cuda")
@@ -76,12 +76,12 @@ for prec in ("bf16", "fp32"):
             f"fwd  A:K B:MN pair{pair}": g(0, A.view(), 0, Wmn.view(), 1, M, N, K, bias=bias.data_ptr(), relu=1,
                                            out=out.view(), cta_pair=pair),
             f"fwd +bits     pair{pair}": g(0, A.view(), 0, Wmn.view(), 1, M, N, K, bias=bias.data_ptr(), relu=1,
-                                           out=out.view(), relu_bits=bits.data_ptr(), bits_ld=N // 32,
+                                           out=out.view(), relu_bits=bits.data_ptr(), bits_ld=M,
                                            cta_pair=pair),
             f"gate values   pair{pair}": g(3, A.view(), 0, Wk.view(), 0, M, N, K, out=out.view(), gate=gate.view(),
                                            cta_pair=pair),
             f"gate bits     pair{pair}": g(3, A.view(), 0, Wk.view(), 0, M, N, K, out=out.view(),
-                                           gate_bits=bits.data_ptr(), bits_ld=N // 32, cta_pair=pair),
+                                           gate_bits=bits.data_ptr(), bits_ld=M, cta_pair=pair),
             f"store(N=1024) pair{pair}": g(1, dz.view(), 0, Wmn.view(), 0, M, K, N, c=c.data_ptr(), ldc=K,
                                            cta_pair=pair),
             f"wgrad MN/MN   pair{pair}": g(2, dz.view(), 1, A.view(), 1, N, K, M, c=ws.data_ptr(), ldc=K, splits=S,
