@@ -199,6 +199,16 @@ typedef struct dippm_gemm_args {
   int32_t* tile_sync;        /* WGRAD fused reduce: device int32[dippm_wgrad_sync_ints(M, N)], zeroed once  */
                              /* by the caller; every launch leaves it zero again (graph-replay safe)      */
   double out_scale;          /* WGRAD fused reduce: out = out_scale * sum_s C_s                            */
+  /* FWD with the K4 readout fused into the epilogue (gnn.py:214, rows = nodes, N = width):
+   * per 32-row block, a segmented (by graph) column sum of the stored activation goes to
+   * pool_graph [G, N] (graphs wholly inside the block) or to pool_partial [2*ceil(M/32), N]
+   * (slot 0: the block's first graph, slot 1: its last, when they cross the block edge);
+   * dippm_pool_combine then forms the means.  out.data may be NULL (the activation itself is
+   * not needed).  Tensor-core backend only. */
+  float* pool_partial;
+  float* pool_graph;
+  const int32_t* node_graph;   /* [M] node -> graph */
+  const int32_t* graph_ptr;    /* [G+1] */
 } dippm_gemm_args_t;
 
 /* Split count the tensor-core WGRAD would like for this problem. */
@@ -210,6 +220,14 @@ int32_t dippm_gemm(const dippm_gemm_args_t* args, int32_t backend, void* stream)
 /* out[j*ldo + i] = scale * sum_s in[s*M*N + i*N + j]  (split-K reduce + transpose; fixed order) */
 int32_t dippm_splitk_reduce_t(const float* in, int32_t splits, int64_t M, int64_t N, double scale, float* out,
                               int64_t ldo, void* stream);
+
+/* K4 second stage of the fused readout: u[g] = [ (sum of g's block sums, fixed block
+ * order) / N_g , (fs[g] - fs_mean) / fs_std , 0 ... ] from the FWD epilogue's pool_partial /
+ * pool_graph (see dippm_gemm_args_t).  dippm_pool_partial_rows(N) = rows of pool_partial. */
+int64_t dippm_pool_partial_rows(int64_t num_nodes);
+int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, const int32_t* graph_ptr,
+                           int64_t num_graphs, int32_t width, const float* fs_raw, const double* norm, dippm_act_t u,
+                           void* stream);
 
 /* ---------------------------------------------------------------------------
  * K4 — readout + static features (gnn.py:214-215, normalize_fs gnn.py:96-97):

@@ -47,6 +47,8 @@ class GemmArgs(C.Structure):
         ("ldm", C.c_int64), ("drop_p", C.c_double), ("seed", C.c_uint64), ("seed_dev", C.c_void_p),
         ("relu_bits", C.c_void_p), ("gate_bits", C.c_void_p), ("bits_ld", C.c_int64), ("cta_pair", C.c_int64),
         ("tile_sync", C.c_void_p), ("out_scale", C.c_double),
+        ("pool_partial", C.c_void_p), ("pool_graph", C.c_void_p), ("node_graph", C.c_void_p),
+        ("graph_ptr", C.c_void_p),
     ]
 
 
@@ -87,6 +89,8 @@ SIGNATURES = {
     "dippm_gemm": (I32, [C.POINTER(GemmArgs), I32, P]),
     "dippm_splitk_reduce_t": (I32, [P, I32, I64, I64, F64, P, I64, P]),
     "dippm_pool_concat": (I32, [Act, P, I64, I32, P, P, Act, P]),
+    "dippm_pool_partial_rows": (I64, [I64]),
+    "dippm_pool_combine": (I32, [P, P, P, I64, I32, P, P, Act, P]),
     "dippm_fc3_forward": (I32, [Act, I64, I32, P, P, P, P, P, P, P, P]),
     "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),

@@ -415,6 +415,34 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const i
   }
 }
 
+// Second stage of the fused readout (see tc_gemm.cu pool_chunk): per graph, the block
+// sums it owns in fixed block order, divided by N_g; then the static features.
+__global__ void __launch_bounds__(256) k_pool_combine(const float* __restrict__ part, const float* __restrict__ whole,
+                                                      const int* __restrict__ graph_ptr, int width,
+                                                      const float* __restrict__ fs_raw, const double* __restrict__ norm,
+                                                      ActView u) {
+  const int g = blockIdx.x;
+  const int gs = graph_ptr[g], ge = graph_ptr[g + 1];
+  const int bf = gs >> 5, bl = (ge - 1) >> 5;
+  const double inv_n = 1.0 / (double)(ge - gs);
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    double t;  // block sums combined in fp64, block order
+    if (bf == bl) {
+      t = whole[(int64_t)g * width + c];
+    } else {
+      t = part[((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c];
+      for (int b = bf + 1; b < bl; ++b) t += part[(int64_t)b * 2 * width + c];
+      t += part[(int64_t)bl * 2 * width + c];
+    }
+    act_store(u, g, c, (float)(t * inv_n));
+  }
+  for (int k = threadIdx.x; k < u.ld - width; k += blockDim.x) {
+    float v = 0.f;
+    if (k < kStaticWidth) v = (float)(((double)fs_raw[g * kStaticWidth + k] - norm[6 + k]) / norm[11 + k]);
+    act_store(u, g, width + k, v);
+  }
+}
+
 // MLP baseline input (gnn.py:253-255 with normalize_fs :96-97): u[g] = [(fs-mu)/sigma | 0].
 __global__ void k_fs_normalize(const float* __restrict__ fs_raw, int64_t G, const double* __restrict__ norm,
                                ActView u, int cols) {
@@ -578,6 +606,17 @@ int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, in
 #undef DIPPM_POOL_C
 #undef DIPPM_POOL
   DIPPM_LAUNCH_CHECK("k_pool_concat");
+  return DIPPM_OK;
+}
+
+int64_t dippm_pool_partial_rows(int64_t num_nodes) { return 2 * ((num_nodes + 31) / 32); }
+
+int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, const int32_t* graph_ptr, int64_t G,
+                           int32_t width, const float* fs_raw, const double* norm, dippm_act_t u, void* stream) {
+  DIPPM_ARG_CHECK(G >= 1 && width >= 1 && u.ld >= width + kStaticWidth, "pool_combine: bad args");
+  k_pool_combine<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(pool_partial, pool_graph, graph_ptr, width, fs_raw,
+                                                               norm, make_view(u));
+  DIPPM_LAUNCH_CHECK("k_pool_combine");
   return DIPPM_OK;
 }
 

@@ -59,6 +59,11 @@ struct Params {
   int64_t ldo;
   double out_scale;
   int* sync;
+  // FWD with the fused readout (pool != nullptr): segmented column sums per 32-row block
+  float* pool_part;
+  float* pool_graph;
+  const int* node_graph;
+  const int* graph_ptr;
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -399,6 +404,65 @@ __device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, i
   }
 }
 
+// Fused readout: a warp holds 32 consecutive rows (one per lane) x 32 columns.  A
+// segmented inclusive scan over the lanes (segments = graphs, node rows of a graph are
+// contiguous) leaves each graph's block sum on its last lane, which stores it: to
+// pool_graph[g] when g lies wholly inside this 32-row block, else to the block's
+// boundary slot (0: segment holding the block's first row, 1: the one holding its last).
+// dippm_pool_combine adds the boundary slots of the blocks a graph spans, in block order.
+__device__ __forceinline__ void pool_chunk(const Params& p, const float (&v)[32], int64_t row, int64_t r0, int n,
+                                           int lane) {
+  const int gid = row < p.M ? __ldg(p.node_graph + row) : -1;
+  const int g0 = __shfl_sync(0xffffffffu, gid, 0);
+  if (g0 >= 0 && __all_sync(0xffffffffu, gid == g0)) {
+    // common case, all 32 rows in one graph: transpose-reduce (31 shuffles), lane L ends
+    // with the block sum of column n + L, and the warp stores 128 contiguous bytes
+    float t[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+      const bool upper = lane & k;
+#pragma unroll
+      for (int i = 0; i < k; ++i) {
+        const float send = upper ? t[i] : t[i + k];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, k);
+        t[i] = (upper ? t[i + k] : t[i]) + recv;
+      }
+    }
+    const int gs = __ldg(p.graph_ptr + g0), ge = __ldg(p.graph_ptr + g0 + 1);
+    float* dst = ((gs >> 5) == ((ge - 1) >> 5)) ? p.pool_graph + (int64_t)g0 * p.N + n
+                                                 : p.pool_part + ((r0 >> 5) * 2 + 0) * p.N + n;  // gs <= r0 here
+    dst[lane] = t[0];
+    return;
+  }
+  float s[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s[i] = gid >= 0 ? v[i] : 0.f;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int gu = __shfl_up_sync(0xffffffffu, gid, off);
+    const bool take = lane >= off && gu == gid;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float t = __shfl_up_sync(0xffffffffu, s[i], off);
+      if (take) s[i] += t;
+    }
+  }
+  const int gn = __shfl_down_sync(0xffffffffu, gid, 1);
+  if (gid < 0 || (lane < 31 && gn == gid)) return;  // not the last row of its segment
+  const int gs = __ldg(p.graph_ptr + gid), ge = __ldg(p.graph_ptr + gid + 1);
+  float* dst;
+  if ((gs >> 5) == ((ge - 1) >> 5)) {
+    dst = p.pool_graph + (int64_t)gid * p.N + n;  // whole graph inside this block
+  } else {
+    const int64_t b = r0 >> 5;
+    dst = p.pool_part + (b * 2 + (gs <= r0 ? 0 : 1)) * p.N + n;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(s[i], s[i + 1], s[i + 2], s[i + 3]);
+}
+
 // One persistent kernel for both tile shapes.  kCta == 2: a cluster of two
 // CTAs on one TPC computes a 256 x kBN tile with cta_group::2 MMAs issued by the
 // even CTA; each CTA stages its own 128 A rows and half of the kBN B rows, so
@@ -690,8 +754,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) bits |= (uint32_t)(v[i] > 0.f) << i;
             p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;  // chunk-major: a warp stores 128 contiguous bytes
           }
-          epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
-                          local * (kBN / 64) + (ch >> 1));
+          if (p.pool_part) pool_chunk(p, v, row, m0 + q * 32, n, lane);  // fused readout (K4, gnn.py:214)
+          if (p.out.base)
+            epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
+                            local * (kBN / 64) + (ch >> 1));
         } else if (row < p.M) {
           if (kEpi == EPI_PARTIAL && p.reduce_mode == 3) {  // single split: final output, scaled
             float* dst = p.wout + row * p.ldo + n;
@@ -858,6 +924,10 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.seed = a->seed;
   p.seed_dev = a->seed_dev;
   p.relu_bits = a->relu_bits;
+  p.pool_part = a->pool_partial;
+  p.pool_graph = a->pool_graph;
+  p.node_graph = a->node_graph;
+  p.graph_ptr = a->graph_ptr;
   p.gate_bits = a->gate_bits;
   p.bits_ld = a->bits_ld;
   const int total = p.m_tiles * p.n_tiles * p.splits;
@@ -874,7 +944,7 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
     p.out_scale = a->out_scale;
     p.sync = a->tile_sync;
   }
-  if (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP || kEpi == EPI_GATE) {
+  if ((kEpi == EPI_FWD || kEpi == EPI_FWD_DROP || kEpi == EPI_GATE) && a->out.data) {
     st = make_map(&mc, a->out, a->M, a->N, 32, 32, false, true);  // epilogue TMA-store target
     if (st) return st;
   } else {
@@ -958,6 +1028,7 @@ extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void*
                   (long long)a->N, (long long)a->K);
   DIPPM_ARG_CHECK(a->a.dtype == a->b.dtype, "gemm: operand dtypes differ");
   cudaStream_t s = (cudaStream_t)stream;
+  DIPPM_ARG_CHECK(!a->pool_partial || backend == 0, "gemm: the fused readout is a tensor-core epilogue");
   if (backend == 1) return dippm_gemm_simt_impl(a, s);
   DIPPM_ARG_CHECK(a->a.dtype == DIPPM_DT_BF16 || a->a.dtype == DIPPM_DT_TF32X3,
                   "gemm: tensor-core path needs bf16 or tf32x3 operands");
@@ -967,6 +1038,10 @@ extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void*
   const bool mn = a->kind == DIPPM_GEMM_WGRAD;
   DIPPM_ARG_CHECK(mn == (a->a_mn_major != 0) && (mn == (a->b_mn_major != 0) || a->kind == DIPPM_GEMM_FWD),
                   "gemm: FWD takes K-major A (B either), STORE/GATE K-major, WGRAD MN-major");
+  DIPPM_ARG_CHECK(!a->pool_partial || (a->kind == DIPPM_GEMM_FWD && a->pool_graph && a->node_graph && a->graph_ptr),
+                  "gemm: the fused readout needs FWD on the tensor-core backend with pool_graph, node_graph, graph_ptr");
+  DIPPM_ARG_CHECK(a->out.data || a->pool_partial || a->kind == DIPPM_GEMM_STORE || a->kind == DIPPM_GEMM_WGRAD,
+                  "gemm: FWD/GATE need an output view");
   DIPPM_ARG_CHECK(a->drop_mode == 0 || ((a->mask || a->drop_mode == 2) && a->kind == DIPPM_GEMM_FWD &&
                                         a->b_mn_major && a->drop_p >= 0 && a->drop_p < 1 && a->ldm % 4 == 0),
                   "gemm: dropout needs FWD with MN-major B, 0 <= p < 1, ldm %% 4 == 0 and (mode 1) a mask buffer");

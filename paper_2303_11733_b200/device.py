@@ -330,7 +330,10 @@ class Workspace:
             (a1[0] if dt == DT_TF32X3 else a1)[:, 2 * FEATURE_WIDTH] = 1.0
             if dt == DT_TF32X3:
                 a1[1][:, 2 * FEATURE_WIDTH:].zero_()
-            self.H3 = ActBuf(N, hp, dt, dev)
+            self.H3 = ActBuf(N, hp, dt, dev) if eng.backend != 0 else None  # SIMT anchor only (unfused readout)
+            # fused readout (layer-3 GEMM epilogue): per-32-row-block boundary sums + whole-graph sums
+            self.pool_part = torch.empty(lib.dippm_pool_partial_rows(N), hp, **f32)
+            self.pool_graph = torch.empty(G, hp, **f32)
         self.u = ActBuf(G, eng.L.u_width, dt, dev)
         self.x2 = ActBuf(G, hp, dt, dev)
         self.x3 = ActBuf(G, hp, dt, dev)
@@ -467,10 +470,11 @@ class Engine:
     # -- kernels --------------------------------------------------------------
     def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1,
               gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None,
-              relu_bits=None, gate_bits=None, bits_ld=0, tile_sync=None, out_scale=1.0):
+              relu_bits=None, gate_bits=None, bits_ld=0, tile_sync=None, out_scale=1.0, pool_partial=None,
+              pool_graph=None, node_graph=None, graph_ptr=None):
         args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits, gate, gate_scale,
                         drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1), seed_dev, relu_bits, gate_bits,
-                        bits_ld, self.cta_pair, tile_sync, out_scale)
+                        bits_ld, self.cta_pair, tile_sync, out_scale, pool_partial, pool_graph, node_graph, graph_ptr)
         if self.gemm_hook is not None:
             self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
@@ -498,17 +502,24 @@ class Engine:
             return
         _lib.call("dippm_sage_aggregate", f32_act(b.x), ws.A[0].view(FEATURE_WIDTH), ws.A[0].view(0), b.N,
                   FEATURE_WIDTH, _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
-        outs = [ws.A[1].view(0), ws.A[2].view(0), ws.H3.view(0)]
+        fused = self.backend == 0  # readout fused into the layer-3 GEMM epilogue (h3 never stored)
+        outs = [ws.A[1].view(0), ws.A[2].view(0), NULL_ACT if fused else ws.H3.view(0)]
         bits = ws.relu_bits if ws.train else None
         for i in range(3):
             if i > 0:
                 _lib.call("dippm_sage_aggregate", ws.A[i].view(0), ws.A[i].view(hp), NULL_ACT, b.N, hp,
                           _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
+            pool = dict(pool_partial=_p(ws.pool_part), pool_graph=_p(ws.pool_graph), node_graph=_p(b.node_graph),
+                        graph_ptr=_p(b.graph_ptr)) if fused and i == 2 else {}
             self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.Wf[i].view(), 1,
                        bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i],
-                       relu_bits=_p(bits[i]) if bits is not None else None, bits_ld=ws.N)
-        _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
-                  ws.u.view(), s)
+                       relu_bits=_p(bits[i]) if bits is not None else None, bits_ld=ws.N, **pool)
+        if fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
+            _lib.call("dippm_pool_combine", _p(ws.pool_part), _p(ws.pool_graph), _p(b.graph_ptr), b.G, hp,
+                      _p(b.fs), _p(self.norm), ws.u.view(), s)
+        else:
+            _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
+                      ws.u.view(), s)
         self.launches += 3 + 1
         self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
 
@@ -560,8 +571,9 @@ class Engine:
                 continue
             if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
-                          ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr), _p(b.t_col), _p(b.inv_deg),
-                          _p(ws.colsum), bias, _p(ws.colsum_sync), _p(ws.relu_bits[2]), ws.N, s)
+                          NULL_ACT if ws.H3 is None else ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr),
+                          _p(b.t_col), _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync),
+                          _p(ws.relu_bits[2]) if self.backend == 0 else None, ws.N, s)  # SIMT: no bit masks
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
                           _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)

@@ -181,3 +181,47 @@ def test_pipelined_host_steps_equal_sequential_and_resident(cfg1):
     for p, l in runs[1:]:
         assert np.array_equal(p, runs[0][0])
         assert l == runs[0][1]
+
+
+def test_fused_readout_matches_unfused_pool_and_simt_engine():
+    """The readout fused into the layer-3 GEMM epilogue (segmented block sums + combine) gives
+    the same pooled vectors as the unfused pool kernel of the SIMT anchor engine, for graph
+    sizes around the 32-row block edges (1, 2, 31, 32, 33, 63, 64, 65, ...) and a 5k-node
+    graph; training gradients of the two engines agree too (fp32)."""
+    from paper_2303_11733_b200.device import Engine, Workspace
+    sizes = [1, 2, 31, 32, 33, 63, 64, 65, 3, 127, 128, 129, 1, 300, 5000, 17, 1, 1, 40]
+    rng = np.random.default_rng(12)
+    gp = np.zeros(len(sizes) + 1, np.int32)
+    np.cumsum(sizes, out=gp[1:])
+    src, dst = [], []
+    for g, n in enumerate(sizes):
+        for v in range(1, n):
+            src.append(gp[g] + v - 1)
+            dst.append(gp[g] + v)
+            if v > 2 and rng.random() < 0.3:
+                src.append(gp[g] + int(rng.integers(0, v - 1)))
+                dst.append(gp[g] + v)
+    N = int(gp[-1])
+    x = np.abs(rng.normal(size=(N, 32))).astype(np.float32)
+    fs = rng.normal(size=(len(sizes), 5)).astype(np.float32)
+    y = np.abs(rng.normal(size=(len(sizes), 3))).astype(np.float32) + 1
+    b = upload_batch(x, np.array(src), np.array(dst), gp, fs, y, device="cuda")
+    norm = gnn.Normalizer(np.zeros(3), np.ones(3), np.zeros(5), np.ones(5))
+    model = _trained_like(make_dataset(64, seed=3), hidden=128, seed=5)
+    model.normalizer = norm
+    res = {}
+    for backend in ("tc", "simt"):
+        eng = Engine(128, "fp32", backend=backend)
+        eng.set_params(model.param_items(), norm)
+        ws = Workspace(eng, b.N, b.G, train=True)
+        eng.forward(b, ws)
+        eng.loss(b, ws)
+        eng.backward(b, ws)
+        res[backend] = (ws.u.to_float()[:, :128].double().cpu().numpy(), ws.out.double().cpu().numpy(),
+                        eng.get_grads())
+    u_tc, u_simt = res["tc"][0], res["simt"][0]
+    assert np.max(np.abs(u_tc - u_simt)) <= 1e-5 * max(1.0, np.abs(u_simt).max())
+    assert np.max(np.abs(res["tc"][1] - res["simt"][1])) <= 1e-4 * max(1.0, np.abs(res["simt"][1]).max())
+    for k, g in res["simt"][2].items():
+        d = np.linalg.norm(res["tc"][2][k] - g)
+        assert d <= 1e-3 * np.linalg.norm(g) + 1e-6 * np.sqrt(g.size), (k, d, np.linalg.norm(g))
