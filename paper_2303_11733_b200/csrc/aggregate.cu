@@ -172,6 +172,43 @@ __device__ __forceinline__ void relu_gate(const ReadoutArgs& ro, int64_t r, int 
   }
 }
 
+// Fused bias-gradient reduction (gnn.py:230) after a block has written its column partial:
+// two fixed-order levels — the last block of each group of kColsumGroup blocks folds the
+// group's partials (block order) into a level-2 row, the last group folds those (group
+// order) into bias_out.  Counters return to zero.  s_scratch: >= 8 KB of shared memory.
+__device__ __forceinline__ void finish_bias(float* colsum_partial, int width, float* bias_out, int* sync,
+                                            float* s_scratch) {
+    // Fused bias-gradient reduction (gnn.py:230), two fixed-order levels: the last
+    // block of each group of kColsumGroup blocks folds the group's partials (in
+    // block order) into a level-2 row; the last group to finish folds those (in
+    // group order) into bias_out.  Counters return to zero for the next launch.
+    __shared__ int s_last;
+    const int nblk = (int)gridDim.x, ngroups = colsum_groups(nblk);
+    const int grp = blockIdx.x / kColsumGroup;
+    float* l2 = colsum_partial + (int64_t)nblk * width;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int gsize = min(kColsumGroup, nblk - grp * kColsumGroup);
+      s_last = atomicAdd(&sync[grp], 1) == gsize - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    const int b0 = grp * kColsumGroup, b1 = min(nblk, b0 + kColsumGroup);
+    double* s_fold = reinterpret_cast<double*>(s_scratch);  // the warp partials are no longer needed
+    fold_rows_block(colsum_partial, b0, b1, width, l2 + (int64_t)grp * width, s_fold);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sync[grp] = 0;
+      __threadfence();
+      s_last = atomicAdd(&sync[ngroups], 1) == ngroups - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    fold_rows_block(l2, 0, ngroups, width, bias_out, s_fold);
+    if (threadIdx.x == 0) sync[ngroups] = 0;
+}
+
 template <int DT, int CPL, bool kReadout>
 __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
                                                                 const int* __restrict__ t_rowptr,
@@ -192,6 +229,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
   const int cbeg = t_rowptr[r0];
   const int ncol = t_rowptr[r0 + nrows] - cbeg;
   const bool staged = ncol <= kAggColCap;
+  __shared__ int s_g[kRowsPerBlock];  // readout: graph of each row of the block
   if (write_agg) {
     for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
     if (staged)
@@ -200,25 +238,31 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
         s_col[i] = v;
         s_cw[i] = inv_deg[v];
       }
+    if constexpr (kReadout)
+      for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_g[i] = ro.node_graph[r0 + i];
     __syncthreads();
   }
   const int c0 = sub * 8, stride = L * 8;
   float part[CPL][8] = {};
+  float dr[CPL][8];  // readout: du[g(row)] / N_g (shared by the row and its neighbours), kept while g repeats
+  int g_cur = -1;
   if (grp < gpw) {
     for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
       const int64_t row = r0 + lr;
       float own[CPL][8];
-      float dr[CPL][8];  // readout: du[g(row)] / N_g (shared by the row and its neighbours)
       if constexpr (kReadout) {
-        const int g = ro.node_graph[row];
-        const float inv_n = 1.0f / (float)(ro.graph_ptr[g + 1] - ro.graph_ptr[g]);
-        const float* dp = ro.du + (int64_t)g * ro.ld_du;
+        const int g = s_g[lr];
+        if (g != g_cur) {  // rows of a graph are contiguous: reload only at graph changes
+          g_cur = g;
+          const float inv_n = 1.0f / (float)(ro.graph_ptr[g + 1] - ro.graph_ptr[g]);
+          const float* dp = ro.du + (int64_t)g * ro.ld_du;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride));
-          const float4 b2 = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride + 4));
-          dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
-          dr[q][4] = b2.x * inv_n; dr[q][5] = b2.y * inv_n; dr[q][6] = b2.z * inv_n; dr[q][7] = b2.w * inv_n;
+          for (int q = 0; q < CPL; ++q) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride));
+            const float4 b2 = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride + 4));
+            dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
+            dr[q][4] = b2.x * inv_n; dr[q][5] = b2.y * inv_n; dr[q][6] = b2.z * inv_n; dr[q][7] = b2.w * inv_n;
+          }
         }
         bool gt[CPL][8];
         relu_gate<DT, CPL>(ro, row, c0, stride, gt);
@@ -274,37 +318,126 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
     for (int q = 0; q < slots; ++q) t += s_part[q * width + c];
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
-  if (bias_out) {
-    // Fused bias-gradient reduction (gnn.py:230), two fixed-order levels: the last
-    // block of each group of kColsumGroup blocks folds the group's partials (in
-    // block order) into a level-2 row; the last group to finish folds those (in
-    // group order) into bias_out.  Counters return to zero for the next launch.
-    __shared__ int s_last;
-    const int nblk = (int)gridDim.x, ngroups = colsum_groups(nblk);
-    const int grp = blockIdx.x / kColsumGroup;
-    float* l2 = colsum_partial + (int64_t)nblk * width;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const int gsize = min(kColsumGroup, nblk - grp * kColsumGroup);
-      s_last = atomicAdd(&sync[grp], 1) == gsize - 1;
+  if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
+}
+
+// Layer-3 readout backward gated by the forward's bit masks (the fast path of
+// dippm_readout_aggregate_t):  dz3[v, c] = dr[g, c] * bit(v, c) with dr = du[g] / N_g, and
+// since every neighbour of u lies in u's graph,
+//   (agg^T dz3)[u, c] = dr[g, c] * sum_{u->v} bit(v, c) / deg(v).
+// One warp per row, CPL chunks of 8 columns per lane; the bit words of the row and of up to
+// kPre neighbours are loaded together before any use (the kernel is load-latency bound).
+constexpr int kPre = 2;
+template <int DT, int CPL>
+__global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, int width, int64_t N,
+                                                                     const int* __restrict__ t_rowptr,
+                                                                     const int* __restrict__ t_col,
+                                                                     const float* __restrict__ inv_deg,
+                                                                     float* __restrict__ colsum_partial, ReadoutArgs ro,
+                                                                     float* __restrict__ bias_out,
+                                                                     int* __restrict__ sync) {
+  extern __shared__ float s_part[];  // [8 warps][width]
+  __shared__ int s_ptr[kRowsPerBlock + 1];
+  __shared__ int s_col[kAggColCap];
+  __shared__ float s_cw[kAggColCap];
+  __shared__ int s_g[kRowsPerBlock];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int cbeg = t_rowptr[r0];
+  const int ncol = t_rowptr[r0 + nrows] - cbeg;
+  const bool staged = ncol <= kAggColCap;
+  for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_g[i] = ro.node_graph[r0 + i];
+  if (staged)
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
+      const int v = t_col[cbeg + i];
+      s_col[i] = v;
+      s_cw[i] = inv_deg[v];
     }
-    __syncthreads();
-    if (!s_last) return;
-    const int b0 = grp * kColsumGroup, b1 = min(nblk, b0 + kColsumGroup);
-    double* s_fold = reinterpret_cast<double*>(s_part);  // the warp partials are no longer needed
-    fold_rows_block(colsum_partial, b0, b1, width, l2 + (int64_t)grp * width, s_fold);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      sync[grp] = 0;
-      __threadfence();
-      s_last = atomicAdd(&sync[ngroups], 1) == ngroups - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    fold_rows_block(l2, 0, ngroups, width, bias_out, s_fold);
-    if (threadIdx.x == 0) sync[ngroups] = 0;
+  __syncthreads();
+  const int stride = 32 * 8;  // a warp covers one row: lane chunks c0 = 8*lane + q*256
+  const int c0 = lane * 8;
+  int wofs[CPL], wsh[CPL];  // word index (column chunk) and bit offset of each of the lane's chunks
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    wofs[q] = (c0 + q * stride) >> 5;
+    wsh[q] = (c0 + q * stride) & 31;
   }
+  const int64_t bld = ro.bits_ld;
+  float part[CPL][8] = {};
+  float dr[CPL][8];
+  int g_cur = -1;
+  for (int lr = warp; lr < nrows; lr += kAggThreads / 32) {
+    const int64_t row = r0 + lr;
+    const int b = s_ptr[lr], e = s_ptr[lr + 1];
+    // issue every independent load of this row first: own bits, up to 4 neighbours' bits
+    uint32_t wown[CPL], wn[kPre][CPL];
+    int nv[kPre];
+    float nw[kPre];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) wown[q] = __ldg(ro.h3_bits + wofs[q] * bld + row);
+#pragma unroll
+    for (int t = 0; t < kPre; ++t) {
+      const int j = b + t;
+      nv[t] = j < e ? (staged ? s_col[j] : t_col[cbeg + j]) : -1;
+      nw[t] = j < e ? (staged ? s_cw[j] : inv_deg[nv[t]]) : 0.f;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) wn[t][q] = nv[t] >= 0 ? __ldg(ro.h3_bits + wofs[q] * bld + nv[t]) : 0u;
+    }
+    const int g = s_g[lr];
+    if (g != g_cur) {  // rows of a graph are contiguous: reload dr only at graph changes
+      g_cur = g;
+      const float inv_n = 1.0f / (float)(ro.graph_ptr[g + 1] - ro.graph_ptr[g]);
+      const float* dp = ro.du + (int64_t)g * ro.ld_du;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride));
+        const float4 a2 = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * stride + 4));
+        dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
+        dr[q][4] = a2.x * inv_n; dr[q][5] = a2.y * inv_n; dr[q][6] = a2.z * inv_n; dr[q][7] = a2.w * inv_n;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      float own[8], acc[8];
+      const uint32_t wo = wown[q] >> wsh[q];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        own[k] = (wo >> k) & 1u ? dr[q][k] : 0.f;
+        part[q][k] += own[k];
+        acc[k] = 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < kPre; ++t) {
+        const uint32_t wv = wn[t][q] >> wsh[q];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += (wv >> k) & 1u ? nw[t] : 0.f;
+      }
+      for (int j = b + kPre; j < e; ++j) {  // beyond the prefetched out-edges
+        const int v0 = staged ? s_col[j] : t_col[cbeg + j];
+        const float w0 = staged ? s_cw[j] : inv_deg[v0];
+        const uint32_t wv = __ldg(ro.h3_bits + wofs[q] * bld + v0) >> wsh[q];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += (wv >> k) & 1u ? w0 : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] *= dr[q][k];
+      act_store8_t<DT>(B, row, c0 + q * stride, own);
+      act_store8_t<DT>(B, row, width + c0 + q * stride, acc);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_part[warp * width + c0 + q * stride + k] = part[q][k];
+  __syncthreads();
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    float t = 0.f;
+    for (int q = 0; q < kAggThreads / 32; ++q) t += s_part[q * width + c];
+    colsum_partial[(int64_t)blockIdx.x * width + c] = t;
+  }
+  if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
 }
 
 // Readout backward (gnn.py:224, 227): dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0).
@@ -544,6 +677,34 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
   return DIPPM_OK;
 }
 
+static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const int32_t* t_rowptr, const int32_t* t_col,
+                               const float* inv_deg, float* colsum_partial, ReadoutArgs ro, float* bias_out,
+                               int32_t* sync, cudaStream_t s) {
+  DIPPM_ARG_CHECK(N >= 1 && width % 256 == 0 && width <= 1024, "readout_aggregate_t: width %d must be 256/512/768/1024",
+                  width);
+  DIPPM_ARG_CHECK(!bias_out || sync, "readout_aggregate_t: bias_grad needs the sync counters");
+  const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double));
+  const int grid = ceil_div_i(N, kRowsPerBlock);
+  ActView bv = make_view(B);
+#define DIPPM_RB(D, C)                                                                                            \
+  do {                                                                                                            \
+    if (smem > 48 * 1024)                                                                                         \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_readout_agg_bits<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            (int)smem));                                                          \
+    k_readout_agg_bits<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, t_rowptr, t_col, inv_deg, colsum_partial, \
+                                                            ro, bias_out, sync);                                  \
+  } while (0)
+#define DIPPM_RB_C(D) \
+  do { if (width == 256) DIPPM_RB(D, 1); else if (width == 512) DIPPM_RB(D, 2); else if (width == 768) DIPPM_RB(D, 3); else DIPPM_RB(D, 4); } while (0)
+  if (B.dtype == DIPPM_DT_BF16) DIPPM_RB_C(DIPPM_DT_BF16);
+  else if (B.dtype == DIPPM_DT_TF32X3) DIPPM_RB_C(DIPPM_DT_TF32X3);
+  else DIPPM_RB_C(DIPPM_DT_F32);
+#undef DIPPM_RB_C
+#undef DIPPM_RB
+  DIPPM_LAUNCH_CHECK("k_readout_agg_bits");
+  return DIPPM_OK;
+}
+
 int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t write_agg, const int32_t* t_rowptr,
                                const int32_t* t_col, const float* inv_deg, float* colsum_partial, float* bias_grad,
                                int32_t* sync, void* stream) {
@@ -560,6 +721,9 @@ int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t*
   DIPPM_ARG_CHECK((h3_bits || h3.dtype == B.dtype) && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
   DIPPM_ARG_CHECK(!h3_bits || bits_ld >= N, "readout_aggregate_t: bits_ld %lld < rows", (long long)bits_ld);
   ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3), h3_bits, bits_ld};
+  if (h3_bits && width % 256 == 0 && width <= 1024)
+    return launch_readout_bits(B, width, N, t_rowptr, t_col, inv_deg, colsum_partial, ro, bias_grad, sync,
+                               (cudaStream_t)stream);
   return launch_aggregate_t(B, width, N, 1, t_rowptr, t_col, inv_deg, colsum_partial, ro, true, bias_grad, sync,
                             (cudaStream_t)stream);
 }

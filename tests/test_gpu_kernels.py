@@ -98,6 +98,34 @@ def test_aggregate_matches_dense(width):
     ref = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist()))) @ h.astype(np.float64)
     assert np.allclose(m.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
     assert torch.equal(s, ht)
+    # with and without the self copy: the same m, bit for bit
+    m2 = torch.empty(N, width, device="cuda")
+    _lib.call("dippm_sage_aggregate", dev.f32_act(ht), dev.f32_act(m2), dev.NULL_ACT, N, width,
+              b.rowptr.data_ptr(), b.col.data_ptr(), b.inv_deg.data_ptr(), dev._stream())
+    assert torch.equal(m, m2)
+
+
+@pytest.mark.parametrize("width", [64, 512])
+def test_aggregate_t_with_fused_bias_reduce(width):
+    """agg^T + the in-kernel bias-gradient reduction agree with fp64 numpy; counters end at zero."""
+    rng = np.random.default_rng(width + 1)
+    N = 1500
+    src = rng.integers(0, N, 4000)
+    dst = rng.integers(0, N, 4000)
+    b = upload_batch(np.zeros((N, 32), np.float32), src, dst, np.array([0, N], np.int32), np.zeros((1, 5), np.float32))
+    dz = rng.normal(size=(N, width)).astype(np.float32)
+    B = torch.zeros(N, 2 * width, device="cuda")
+    B[:, :width] = torch.from_numpy(dz).cuda()
+    lib = _lib.load()
+    part = torch.empty(lib.dippm_colsum_rows(N), width, device="cuda")
+    sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device="cuda")
+    bias = torch.empty(width, device="cuda")
+    _lib.call("dippm_sage_aggregate_t", dev.f32_act(B), width, N, 1, b.t_rowptr.data_ptr(), b.t_col.data_ptr(),
+              b.inv_deg.data_ptr(), part.data_ptr(), bias.data_ptr(), sync.data_ptr(), dev._stream())
+    agg = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist())))
+    assert np.allclose(B[:, width:].cpu().numpy(), agg.T @ dz.astype(np.float64), rtol=1e-5, atol=1e-5)
+    assert np.allclose(bias.cpu().numpy(), dz.astype(np.float64).sum(0), rtol=1e-5, atol=1e-3)
+    assert int(sync.abs().sum()) == 0
 
 
 def _rand_act(rows, cols, dt, rng, scale=1.0):
