@@ -984,7 +984,7 @@ static int run_bn(const dippm_gemm_args_t* a, cudaStream_t s) {
     return DIPPM_ERR_ARG;
   }
   if (pair) return run<kFmt, kAMN, kBMN, 256, kEpi, 2>(a, s);
-  const bool narrow = kEpi != EPI_PARTIAL && m_tiles * (a->N / 256) < num_sms() / 2;
+  const bool narrow = (kEpi != EPI_PARTIAL || splits == 1) && m_tiles * (a->N / 256) < num_sms() / 2;
   if (a->N % 256 == 0 && !narrow) return run<kFmt, kAMN, kBMN, 256, kEpi, 1>(a, s);
   if (a->N % 128 == 0 && !(narrow && m_tiles * (a->N / 128) < num_sms() / 2))
     return run<kFmt, kAMN, kBMN, 128, kEpi, 1>(a, s);
@@ -1014,6 +1014,9 @@ extern "C" int32_t dippm_wgrad_splits(int64_t M, int64_t N, int64_t K) {
   const int bn = N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64);
   const int64_t tiles = (int64_t)ceil_div_i(M, tc::kBM) * (N / bn);
   const int kb_total = ceil_div_i(K, 64);  // bf16 k-block; tf32 uses 32-row blocks (twice as many)
+  // Short reductions (the head's K = #graphs): no split — narrow output tiles supply the
+  // parallelism and the epilogue stores the result directly (no partials, no reduce).
+  if (kb_total <= 8) return 1;
   int want = (int)std::max<int64_t>(1, num_sms() / std::max<int64_t>(1, tiles));
   return std::min(want, kb_total);  // every split owns >= 1 k-block for both k-block sizes
 }
