@@ -120,6 +120,123 @@ __global__ void __launch_bounds__(256) k_adam_pack(double* __restrict__ p, doubl
   }
 }
 
+// Vectorised variant: 4 consecutive parameters per thread (16/32-byte loads and stores),
+// the packing of GEMM operand copies specialised on their dtype.  Valid when every
+// segment's src_off and cols are multiples of 4 (the padded layout guarantees it); the
+// arithmetic per element is exactly k_adam_pack's.
+template <int DT>
+__global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, double* __restrict__ m,
+                                                    double* __restrict__ v, const float* __restrict__ g,
+                                                    double gscale, int64_t n, double lr, double b1, double b2,
+                                                    double eps, double bc1, double bc2, const int64_t* t_dev,
+                                                    int do_adam, float* __restrict__ p32, PackSegs segs) {
+  if (t_dev && do_adam) {
+    __shared__ double s_bc[2];
+    if (threadIdx.x == 0) {
+      const double t = (double)t_dev[0];
+      s_bc[0] = 1.0 - pow(b1, t);
+      s_bc[1] = 1.0 - pow(b2, t);
+    }
+    __syncthreads();
+    bc1 = s_bc[0];
+    bc2 = s_bc[1];
+  }
+  const double inv_bc1 = 1.0 / bc1, inv_bc2 = 1.0 / bc2;
+  const int64_t n4 = n >> 2;
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {  // the < 4 trailing parameters (no packing segments there)
+    const int64_t i = (n4 << 2) + threadIdx.x;
+    double val = p[i];
+    if (do_adam) {
+      const double gi = (double)g[i] * gscale;
+      double mi = m[i] * b1;
+      mi += (1.0 - b1) * gi;
+      double tmp = gi * gi;
+      tmp *= 1.0 - b2;
+      double vi = v[i] * b2;
+      vi += tmp;
+      double denom = vi * inv_bc2;
+      denom = sqrt(denom);
+      denom += eps;
+      double step = mi * inv_bc1;
+      step /= denom;
+      step *= -lr;
+      step += val;
+      m[i] = mi;
+      v[i] = vi;
+      p[i] = step;
+      val = step;
+    }
+    p32[i] = (float)val;
+  }
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q << 2;
+    double val[4];
+    {
+      const double2 a = reinterpret_cast<const double2*>(p + i)[0], b = reinterpret_cast<const double2*>(p + i)[1];
+      val[0] = a.x; val[1] = a.y; val[2] = b.x; val[3] = b.y;
+    }
+    if (do_adam) {
+      const float4 g4 = reinterpret_cast<const float4*>(g + i)[0];
+      const double2 ma = reinterpret_cast<const double2*>(m + i)[0], mb = reinterpret_cast<const double2*>(m + i)[1];
+      const double2 va = reinterpret_cast<const double2*>(v + i)[0], vb = reinterpret_cast<const double2*>(v + i)[1];
+      const double gg[4] = {(double)g4.x * gscale, (double)g4.y * gscale, (double)g4.z * gscale, (double)g4.w * gscale};
+      const double mm[4] = {ma.x, ma.y, mb.x, mb.y}, vv[4] = {va.x, va.y, vb.x, vb.y};
+      double mo[4], vo[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double mi = mm[k] * b1;
+        mi += (1.0 - b1) * gg[k];
+        double tmp = gg[k] * gg[k];
+        tmp *= 1.0 - b2;
+        double vi = vv[k] * b2;
+        vi += tmp;
+        double denom = vi * inv_bc2;
+        denom = sqrt(denom);
+        denom += eps;
+        double step = mi * inv_bc1;
+        step /= denom;
+        step *= -lr;
+        step += val[k];
+        mo[k] = mi;
+        vo[k] = vi;
+        val[k] = step;
+      }
+      reinterpret_cast<double2*>(m + i)[0] = make_double2(mo[0], mo[1]);
+      reinterpret_cast<double2*>(m + i)[1] = make_double2(mo[2], mo[3]);
+      reinterpret_cast<double2*>(v + i)[0] = make_double2(vo[0], vo[1]);
+      reinterpret_cast<double2*>(v + i)[1] = make_double2(vo[2], vo[3]);
+      reinterpret_cast<double2*>(p + i)[0] = make_double2(val[0], val[1]);
+      reinterpret_cast<double2*>(p + i)[1] = make_double2(val[2], val[3]);
+    }
+    const float f[4] = {(float)val[0], (float)val[1], (float)val[2], (float)val[3]};
+    reinterpret_cast<float4*>(p32 + i)[0] = make_float4(f[0], f[1], f[2], f[3]);
+    for (int k = 0; k < segs.n; ++k) {
+      const auto& sg = segs.s[k];
+      const int64_t j = i - sg.src_off;
+      if (j < 0 || j >= sg.rows * sg.cols) continue;
+      const int64_t r = j / sg.cols, c = sg.dst_col_off + j % sg.cols;
+      if constexpr (DT == DIPPM_DT_BF16) {
+        __nv_bfloat162 h[2] = {__floats2bfloat162_rn(f[0], f[1]), __floats2bfloat162_rn(f[2], f[3])};
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sg.dst.base) + r * sg.dst.ld + c) =
+            *reinterpret_cast<uint2*>(h);
+      } else if constexpr (DT == DIPPM_DT_TF32X3) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hi[e] = tf32_hi(f[e]);
+          lo[e] = tf32_rn(f[e] - hi[e]);
+        }
+        float* d = reinterpret_cast<float*>(sg.dst.base) + r * sg.dst.ld + c;
+        *reinterpret_cast<float4*>(d) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(d + sg.dst.plane_stride) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(sg.dst.base) + r * sg.dst.ld + c) =
+            make_float4(f[0], f[1], f[2], f[3]);
+      }
+    }
+  }
+}
+
 __global__ void k_step_counter(int64_t* t) { t[0] += 1; }
 
 __global__ void k_pack(const double* __restrict__ w, int64_t rows, int64_t cols, int transpose, ActView dst) {
@@ -196,6 +313,31 @@ int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads
   double bc1 = do_adam && t >= 1 ? 1.0 - pow(beta1, (double)t) : 1.0;
   double bc2 = do_adam && t >= 1 ? 1.0 - pow(beta2, (double)t) : 1.0;
   int blocks = (int)std::min<int64_t>(ceil_div_i(n, 256), 8 * num_sms());
+  // vectorised path: 4 parameters per thread when every segment is 4-aligned and all
+  // operand copies share one dtype; the <4 tail (and any other layout) runs the scalar kernel
+  bool vec = true;
+  for (int k = 0; k < nsegs; ++k)
+    vec &= segs[k].src_off % 4 == 0 && segs[k].cols % 4 == 0 && segs[k].dst_col_off % 4 == 0 &&
+           segs[k].dst.ld % 4 == 0 && segs[k].dst.plane_stride % 4 == 0 && (uintptr_t)segs[k].dst.data % 16 == 0 &&
+           segs[k].src_off + segs[k].rows * segs[k].cols <= (n & ~int64_t(3)) && segs[k].dst.dtype == segs[0].dst.dtype;
+  vec &= ((uintptr_t)params | (uintptr_t)m | (uintptr_t)v | (uintptr_t)grads | (uintptr_t)p32) % 32 == 0;
+  const int64_t n4 = vec ? (n & ~int64_t(3)) : 0;
+  if (n4) {
+    const int b4 = (int)std::min<int64_t>(ceil_div_i(n4 / 4, 256), 8 * num_sms());
+    const int dt = nsegs ? (int)segs[0].dst.dtype : DIPPM_DT_F32;
+    if (dt == DIPPM_DT_BF16)
+      k_adam_pack4<DIPPM_DT_BF16><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1,
+                                                                      beta2, eps, bc1, bc2, t_dev, do_adam, p32, ps);
+    else if (dt == DIPPM_DT_TF32X3)
+      k_adam_pack4<DIPPM_DT_TF32X3><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr,
+                                                                        beta1, beta2, eps, bc1, bc2, t_dev, do_adam,
+                                                                        p32, ps);
+    else
+      k_adam_pack4<DIPPM_DT_F32><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1,
+                                                                     beta2, eps, bc1, bc2, t_dev, do_adam, p32, ps);
+    DIPPM_LAUNCH_CHECK("k_adam_pack4");
+    return DIPPM_OK;
+  }
   k_adam_pack<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1, beta2, eps,
                                                         bc1, bc2, t_dev, do_adam, p32, ps);
   DIPPM_LAUNCH_CHECK("k_adam_pack");

@@ -293,6 +293,11 @@ namespace dippm {
 constexpr int kGThreads = 512;
 
 __device__ __forceinline__ void bitonic_sort_smem(int* a, int n) {  // n power of 2, ascending
+  // Featurizer output is usually already in (dst, src) order (featurize.py:154-162): one
+  // block-wide check skips the O(log^2 n) barrier-bound network in that case.
+  int ok = 1;
+  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) ok &= a[i] <= a[i + 1];
+  if (__syncthreads_and(ok)) return;
   for (int k = 2; k <= n; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = threadIdx.x; i < n; i += blockDim.x) {

@@ -19,6 +19,8 @@
 // Operand majorness: K-major for FWD/STORE; both MN-major for WGRAD (dz and
 // [h|m] are row-major [nodes, features] and the reduction runs over nodes),
 // which the UMMA descriptors express directly (no transposed copies).
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
