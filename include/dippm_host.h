@@ -70,6 +70,13 @@ void dippm_feat_sizes(const dippm_feat_batch* b, int64_t* num_nodes, int64_t* nu
  *   x32     float  [total_nodes, 32]  optional (may be NULL): x rounded to fp32 for the device
  * Any pointer may be NULL to skip that output. */
 void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int64_t* fs_int, float* x32);
+/* Per-document metadata in one call (any pointer may be NULL):
+ *   status  int32 [count]      (dippm_feat_status codes)
+ *   fs_log  double [count, 5]  StaticFeatures.as_vector = log1p of the five integers (featurize.py:76-87)
+ *   name_off int64 [count + 1] and names (UTF-8, concatenated; names_cap bytes available):
+ *   returns the total name bytes (call with names = NULL first to size the buffer). */
+int64_t dippm_feat_meta(const dippm_feat_batch* b, int32_t* status, double* fs_log, int64_t* name_off, char* names,
+                        int64_t names_cap);
 void dippm_feat_free(dippm_feat_batch* b);
 
 #ifdef __cplusplus

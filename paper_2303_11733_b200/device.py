@@ -250,8 +250,10 @@ def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=Tr
     dev = torch.device(device)
 
     def h2d(a):
-        t = torch.from_numpy(np.ascontiguousarray(a))
-        return t.pin_memory().to(dev, non_blocking=True) if t.numel() else t.to(dev)
+        # already-pinned tensors copy asynchronously; numpy arrays go straight from pageable
+        # memory (a fresh pinned staging buffer per call costs more than it saves)
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(dev, non_blocking=t.is_pinned())
 
     if edge_ptr is None:
         edge_ptr = group_edges(src, dst, graph_ptr)
@@ -412,16 +414,25 @@ class Engine:
 
     # -- parameters -----------------------------------------------------------
     def set_params(self, items, normalizer) -> None:
+        """Upload the host model's current values (padded layout) and refresh the operand copies.
+        Skipped when the values are bit-identical to the last upload (repeated predict calls)."""
         host = np.zeros(self.L.total, dtype=np.float64)
         for name, arr in items:
             off = self.L.offsets[name]
             padded = self.L.pad(name, arr)
             host[off:off + padded.size] = padded.ravel()
+        norm = np.concatenate([np.asarray(normalizer.y_mean, np.float64), np.asarray(normalizer.y_std, np.float64),
+                               np.asarray(normalizer.fs_mean, np.float64), np.asarray(normalizer.fs_std, np.float64)])
+        last = getattr(self, "_uploaded", None)
+        if last is not None and np.array_equal(last[0], host) and np.array_equal(last[1], norm):
+            return
         self.params.copy_(torch.from_numpy(host), non_blocking=False)
         self.set_normalizer(normalizer)
         self.refresh()
+        self._uploaded = (host, norm)
 
     def set_normalizer(self, norm) -> None:
+        self._uploaded = None
         vec = np.concatenate([np.asarray(norm.y_mean, np.float64), np.asarray(norm.y_std, np.float64),
                               np.asarray(norm.fs_mean, np.float64), np.asarray(norm.fs_std, np.float64)])
         self.norm.copy_(torch.from_numpy(vec))
@@ -458,6 +469,7 @@ class Engine:
 
     def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale: float = 1.0) -> None:
         """numerics.adam_step over all 15 tensors + operand refresh (t += 1 on the device first)."""
+        self._uploaded = None  # device values now differ from the last host upload
         _lib.call("dippm_step_counter", _p(self.t_dev), _stream())
         self._adam_pack(1, lr, beta1, beta2, eps, grad_scale)
 
@@ -527,6 +539,8 @@ class Engine:
                       predict: bool) -> None:
         """K5: fc1/fc2 tcgen05 GEMMs (bias, ReLU, dropout epilogue) + fc3/de-normalise/MIG (gnn.py:265-284)."""
         s, hp = _stream(), self.L.hp
+        if predict:
+            ws.nonfinite.zero_()  # workspaces are reused across calls
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
         for j, (x, W, out) in enumerate(((ws.u, self.W1h, ws.x2), (ws.x2, self.W2h, ws.x3))):
             self._gemm(GEMM_FWD, b.G, hp, x.cols, x.view(), 0, W.view(), 1, bias=self._f32(f"fc{j + 1}.b"), relu=1,

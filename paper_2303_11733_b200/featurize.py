@@ -50,6 +50,7 @@ def _host():
             "dippm_feat_sizes": (None, [P, P, P, P, P]),
             "dippm_feat_export": (None, [P, P, P, P, P]),
             "dippm_feat_free": (None, [P]),
+            "dippm_feat_meta": (I64, [P, P, P, P, C.c_char_p, I64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -101,29 +102,31 @@ class FeaturizedBatch:
                                      None if bo is None else bo.ctypes.data, int(threads))
         if not h:
             raise MemoryError("dippm_featurize_docs: allocation failed")
-        try:
-            self.n = np.zeros(G, np.int64)
-            self.ne = np.zeros(G, np.int64)
-            tn, te = C.c_int64(0), C.c_int64(0)
-            lib.dippm_feat_sizes(h, self.n.ctypes.data, self.ne.ctypes.data, C.byref(tn), C.byref(te))
-            self.x = np.empty((tn.value, FEATURE_WIDTH), np.float64)
-            self.x32 = np.empty((tn.value, FEATURE_WIDTH), np.float32) if x32 else None
-            self.edges = np.empty((te.value, 2), np.int64)
-            self.fs_int = np.zeros((G, STATIC_WIDTH), np.int64)
-            lib.dippm_feat_export(h, self.x.ctypes.data, self.edges.ctypes.data, self.fs_int.ctypes.data,
-                                  None if self.x32 is None else self.x32.ctypes.data)
-            msg = C.create_string_buffer(512)
-            self.status = np.zeros(G, np.int32)
-            self.messages, self.names = [], []
-            for i in range(G):
-                self.status[i] = lib.dippm_feat_status(h, i, msg, 512)
-                self.messages.append(msg.value.decode("utf-8", "replace"))
-                ln = lib.dippm_feat_name(h, i, None, 0)
-                nb = C.create_string_buffer(ln + 1)
-                lib.dippm_feat_name(h, i, nb, ln + 1)
-                self.names.append(nb.raw[:ln].decode("utf-8"))
-        finally:
-            lib.dippm_feat_free(h)
+        self._h = h  # kept until the object dies: the float64 rows are exported on first use
+        self.n = np.zeros(G, np.int64)
+        self.ne = np.zeros(G, np.int64)
+        tn, te = C.c_int64(0), C.c_int64(0)
+        lib.dippm_feat_sizes(h, self.n.ctypes.data, self.ne.ctypes.data, C.byref(tn), C.byref(te))
+        self._x = None
+        self.x32 = np.empty((tn.value, FEATURE_WIDTH), np.float32) if x32 else None
+        self.edges = np.empty((te.value, 2), np.int64)
+        self.fs_int = np.zeros((G, STATIC_WIDTH), np.int64)
+        lib.dippm_feat_export(h, None, self.edges.ctypes.data, self.fs_int.ctypes.data,
+                              None if self.x32 is None else self.x32.ctypes.data)
+        self.status = np.zeros(G, np.int32)
+        self._fs_log = np.zeros((G, STATIC_WIDTH), np.float64)
+        name_off = np.zeros(G + 1, np.int64)
+        nbytes = lib.dippm_feat_meta(h, None, None, None, None, 0)
+        buf = C.create_string_buffer(max(int(nbytes), 1))
+        lib.dippm_feat_meta(h, self.status.ctypes.data, self._fs_log.ctypes.data, name_off.ctypes.data, buf,
+                            int(nbytes))
+        raw = buf.raw[:nbytes]
+        self.names = [raw[name_off[i]:name_off[i + 1]].decode("utf-8") for i in range(G)]
+        msg = C.create_string_buffer(512)
+        self.messages = [""] * G
+        for i in np.nonzero(self.status)[0]:  # messages only for the documents that failed
+            lib.dippm_feat_status(h, int(i), msg, 512)
+            self.messages[int(i)] = msg.value.decode("utf-8", "replace")
         self.node_ptr = np.zeros(G + 1, np.int64)
         np.cumsum(self.n, out=self.node_ptr[1:])
         self.edge_ptr = np.zeros(G + 1, np.int64)
@@ -131,6 +134,19 @@ class FeaturizedBatch:
 
     def __len__(self) -> int:
         return len(self.n)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:
+            _lib.dippm_feat_free(h)
+
+    @property
+    def x(self) -> np.ndarray:
+        """[sum n, 32] float64 feature rows (exported from the native batch on first use)."""
+        if self._x is None:
+            self._x = np.empty((int(self.n.sum()), FEATURE_WIDTH), np.float64)
+            _host().dippm_feat_export(self._h, self._x.ctypes.data, None, None, None)
+        return self._x
 
     def error(self, i: int):
         """The exception the reference raises for document i (None if it featurised)."""
@@ -143,8 +159,8 @@ class FeaturizedBatch:
             raise self.error(int(bad[0]))
 
     def fs_vectors(self) -> np.ndarray:
-        """StaticFeatures.as_vector for every document (log1p, float64)."""
-        return np.array([[math.log1p(int(v)) for v in row] for row in self.fs_int], dtype=np.float64)
+        """StaticFeatures.as_vector for every document (libm log1p of the integers, float64)."""
+        return self._fs_log
 
     def encoding(self, i: int) -> GraphEncoding:
         self.raise_if(i)
@@ -166,7 +182,7 @@ class FeaturizedBatch:
         """(x f32, src, dst, graph_ptr, fs f32, edge_ptr) over all documents, node ids
         batch-global — the arrays device.upload_batch takes.  Raises the first error."""
         self.raise_first_error()
-        x = self.x32 if self.x32 is not None else self.x.astype(np.float32)
+        x = self.x32 if self.x32 is not None else self.x.astype(np.float32)  # noqa: E501
         gp = self.node_ptr.astype(np.int32)
         off = np.repeat(self.node_ptr[:-1], self.ne)
         src = self.edges[:, 0] + off
@@ -205,13 +221,13 @@ def predict_featurized(model, fb: FeaturizedBatch, precision: str = "fp32"):
     import torch
 
     from . import gnn
-    from .device import Workspace, upload_batch
+    from .device import upload_batch
     x, src, dst, gp, fs, ep = fb.collate()
     eng = gnn._engine(model, precision)
     b = upload_batch(x, src, dst, gp, fs, None, device=eng.device, build_csr=eng.arch == "sage", edge_ptr=ep)
-    ws = Workspace(eng, b.N, b.G, train=False)
+    ws = gnn.infer_workspace(eng, b.N, b.G)
     eng.forward(b, ws)
     torch.cuda.current_stream().synchronize()
     if int(ws.nonfinite.item()):
         raise E.NonFinite("memory prediction is not finite")
-    return ws.y_pred.cpu().numpy(), ws.mig.cpu().numpy()
+    return ws.y_pred[:b.G].cpu().numpy(), ws.mig[:b.G].cpu().numpy()

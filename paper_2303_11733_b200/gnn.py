@@ -221,10 +221,20 @@ def _records_arrays(encodings, fss, targets=None):
                         None if targets is None else [target_vector(t) for t in targets])
 
 
+def infer_workspace(eng: Engine, N: int, G: int) -> Workspace:
+    """The engine's reusable inference workspace, grown (x1.25) when a batch needs more rows/graphs."""
+    ws = getattr(eng, "_infer_ws", None)
+    if ws is None or ws.N < N or ws.G < G:
+        ws = Workspace(eng, max(N, int(1.25 * (ws.N if ws else 0))), max(G, int(1.25 * (ws.G if ws else 0))),
+                       train=False)
+        eng._infer_ws = ws
+    return ws
+
+
 def _run_forward(eng: Engine, encodings, fss, targets=None, mask_mode=0, masks=None, train_buffers=False):
     x, src, dst, gp, fs, y = _records_arrays(encodings, fss, targets)
     b = upload_batch(x, src, dst, gp, fs, y, device=eng.device, build_csr=eng.arch == "sage")
-    ws = Workspace(eng, b.N, b.G, train=train_buffers)
+    ws = Workspace(eng, b.N, b.G, train=True) if train_buffers else infer_workspace(eng, b.N, b.G)
     if masks is not None:
         ws.masks[:, :, :masks.shape[-1]].copy_(torch.from_numpy(masks.astype(np.float32)))
     eng.forward(b, ws, mask_mode=mask_mode)
@@ -336,7 +346,8 @@ def predict_batch(model, encodings, fss, precision: str = "fp32"):
         raise EmptyDataset("batch is empty")
     eng = _engine(model, precision)
     _, ws = _run_forward(eng, encodings, fss)
-    return ws.y_pred.cpu().numpy(), ws.mig.cpu().numpy()
+    G = len(encodings)
+    return ws.y_pred[:G].cpu().numpy(), ws.mig[:G].cpu().numpy()
 
 
 def predict(model, encoding, fs, precision: str = "fp32") -> TargetVector:

@@ -1026,22 +1026,51 @@ void dippm_feat_sizes(const dippm_feat_batch* b, int64_t* num_nodes, int64_t* nu
 }
 
 void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int64_t* fs_int, float* x32) {
-  int64_t no = 0, eo = 0;
+  const size_t G = b->res.size();
+  std::vector<int64_t> no(G + 1, 0), eo(G + 1, 0);
+  for (size_t i = 0; i < G; ++i) {
+    no[i + 1] = no[i] + b->res[i].n;
+    eo[i + 1] = eo[i] + (int64_t)b->res[i].edges.size();
+  }
+  auto work = [&](size_t i0, size_t i1) {  // documents [i0, i1): disjoint output slices
+    for (size_t i = i0; i < i1; ++i) {
+      const Result& r = b->res[i];
+      if (x && r.n) memcpy(x + no[i] * 32, r.x.data(), sizeof(double) * 32 * (size_t)r.n);
+      if (x32)
+        for (int64_t k = 0; k < r.n * 32; ++k) x32[no[i] * 32 + k] = (float)r.x[(size_t)k];
+      if (edges)
+        for (size_t k = 0; k < r.edges.size(); ++k) {
+          edges[2 * (eo[i] + (int64_t)k)] = r.edges[k].first;
+          edges[2 * (eo[i] + (int64_t)k) + 1] = r.edges[k].second;
+        }
+      if (fs_int)
+        for (int k = 0; k < 5; ++k) fs_int[i * 5 + k] = r.fs[k];
+    }
+  };
+  const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<size_t>(G / 64, 1));
+  if (nt <= 1) {
+    work(0, G);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(work, G * t / nt, G * (t + 1) / nt);
+  for (auto& th : pool) th.join();
+}
+
+int64_t dippm_feat_meta(const dippm_feat_batch* b, int32_t* status, double* fs_log, int64_t* name_off, char* names,
+                        int64_t names_cap) {
+  int64_t off = 0;
   for (size_t i = 0; i < b->res.size(); ++i) {
     const Result& r = b->res[i];
-    if (x && r.n) memcpy(x + no * 32, r.x.data(), sizeof(double) * 32 * (size_t)r.n);
-    if (x32)
-      for (int64_t k = 0; k < r.n * 32; ++k) x32[no * 32 + k] = (float)r.x[(size_t)k];
-    if (edges)
-      for (size_t k = 0; k < r.edges.size(); ++k) {
-        edges[2 * (eo + (int64_t)k)] = r.edges[k].first;
-        edges[2 * (eo + (int64_t)k) + 1] = r.edges[k].second;
-      }
-    if (fs_int)
-      for (int k = 0; k < 5; ++k) fs_int[i * 5 + k] = r.fs[k];
-    no += r.n;
-    eo += (int64_t)r.edges.size();
+    if (status) status[i] = r.status;
+    if (fs_log)
+      for (int k = 0; k < 5; ++k) fs_log[i * 5 + k] = std::log1p((double)r.fs[k]);  // math.log1p(int) semantics
+    if (name_off) name_off[i] = off;
+    if (names && off + (int64_t)r.name.size() <= names_cap) memcpy(names + off, r.name.data(), r.name.size());
+    off += (int64_t)r.name.size();
   }
+  if (name_off) name_off[b->res.size()] = off;
+  return off;
 }
 
 void dippm_feat_free(dippm_feat_batch* b) { delete b; }

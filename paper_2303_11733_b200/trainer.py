@@ -73,6 +73,7 @@ class BatchTrainer:
         per-rank gradients is the global batch mean (gnn.py:402-404)."""
         self._ensure(b)
         self.steps += 1
+        self.engine._uploaded = None  # the step moves the device parameters
         if not self.use_graphs:
             self._step(b, global_graphs)
             return
