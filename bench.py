@@ -48,6 +48,8 @@ def parse_args():
     p.add_argument("--steps", type=int, default=200, help="timed steps (~5 epochs of the 41-batch corpus)")
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                   help="gloo: multi-rank smoke runs (several ranks may share one GPU)")
     p.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
     p.add_argument("--graphs", type=int, default=10508)
     p.add_argument("--batch", type=int, default=256)
@@ -231,7 +233,9 @@ def config_dict(args, world):
             "graphs": args.graphs, "batch_per_rank": args.batch, "global_batch": args.batch * world,
             "hidden": args.hidden, "nodes_per_graph": "U[270,330]", "edges_per_node": 1.33,
             "parallelism": f"dp{world}", "l2": "inputs larger than L2 (no flush)",
-            "launch": "eager" if getattr(args, "no_graphs", False) else "cuda_graph (one per resident batch)"}
+            "launch": "eager" if getattr(args, "no_graphs", False) or world > 1 else "cuda_graph (one per resident batch)",
+            "collective": f"{getattr(args, 'dist_backend', 'nccl')} all-reduce of the fp32 gradient (6.4 MB) per step"
+            if world > 1 else None}
 
 
 # ---------------------------------------------------------------------------
@@ -392,9 +396,13 @@ def main():
 
     import torch
     import torch.distributed as dist
+    local = local % max(torch.cuda.device_count(), 1)  # ranks may share a GPU in gloo smoke runs
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2303_11733_b200 import _lib, gnn
     from paper_2303_11733_b200.device import Engine, Workspace, build_batch_csr, upload_batch
     from paper_2303_11733_b200.synth import make_dataset
@@ -412,7 +420,8 @@ def main():
     from paper_2303_11733_b200.dist import allreduce_sum
     trainer = BatchTrainer(model, precision=args.dtype, lr=gnn.DEFAULT_LEARNING_RATE, seed=11,
                            allreduce=allreduce_sum if world > 1 else None, world_size=world, rank=rank,
-                           use_graphs=not args.no_graphs)
+                           # multi-rank steps launch eagerly: the all-reduce stays outside graph capture
+                           use_graphs=not args.no_graphs and world == 1)
     eng = trainer.engine
     # resident epoch: every batch collated in HBM before timing (CSR is rebuilt each step)
     resident = [upload_batch(*b, device=eng.device, build_csr=False) for b in batches_host]
