@@ -234,7 +234,8 @@ def config_dict(args, world):
             "hidden": args.hidden, "nodes_per_graph": "U[270,330]", "edges_per_node": 1.33,
             "parallelism": f"dp{world}", "l2": "inputs larger than L2 (no flush)",
             "launch": "eager" if getattr(args, "no_graphs", False) or world > 1 else "cuda_graph (one per resident batch)",
-            "collective": f"{getattr(args, 'dist_backend', 'nccl')} all-reduce of the fp32 gradient (6.4 MB) per step"
+            "collective": f"{getattr(args, 'dist_backend', 'nccl')} all-reduce of the fp32 gradient (6.4 MB) per step, "
+                          "2 buckets, head+sage3 overlapped with the layer-2/1 backward"
             if world > 1 else None}
 
 
@@ -417,9 +418,9 @@ def main():
 
     norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
     model = gnn.create_model(hidden=args.hidden, seed=0, normalizer=norm)
-    from paper_2303_11733_b200.dist import allreduce_sum
+    from paper_2303_11733_b200.dist import OverlappedAllReduce
     trainer = BatchTrainer(model, precision=args.dtype, lr=gnn.DEFAULT_LEARNING_RATE, seed=11,
-                           allreduce=allreduce_sum if world > 1 else None, world_size=world, rank=rank,
+                           allreduce=OverlappedAllReduce() if world > 1 else None, world_size=world, rank=rank,
                            # multi-rank steps launch eagerly: the all-reduce stays outside graph capture
                            use_graphs=not args.no_graphs and world == 1)
     eng = trainer.engine

@@ -561,7 +561,7 @@ class Engine:
                   _p(ws.dout) if ws.train else None, _p(ws.loss), _stream())
         self.launches += 1
 
-    def backward(self, b: Batch, ws: Workspace, keep_scale: float = 1.0) -> None:
+    def backward(self, b: Batch, ws: Workspace, keep_scale: float = 1.0, on_partial=None) -> None:
         """Head backward (fc3 fused kernel, fc2/fc1 tcgen05 WGRAD/GATE/STORE), readout
         backward, then per SAGE layer: agg^T + bias, WGRAD, gated dgrad GEMM."""
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
@@ -597,4 +597,6 @@ class Engine:
                            out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
                            gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=ws.N)
                 cur = 1 - cur
+            if i == 2 and on_partial is not None:  # sage3 + head gradients are final here
+                on_partial(L.offsets["sage3.w_self"])
         self.launches += 5 + 3 * 2 - 3 - 1

@@ -59,6 +59,40 @@ def allreduce_sum(tensor, group=None):
     return tensor
 
 
+class OverlappedAllReduce:
+    """The DP gradient exchange split in two buckets so the first overlaps the backward.
+
+    The flat gradient layout is sage1 | sage2 | sage3 | fc1..fc3 (gnn.py:488-491), and the
+    backward finishes fc* and sage3 first: `begin(grads[off:])` is issued right after the
+    layer-3 weight gradient (NCCL orders it after the work already queued on the compute
+    stream and runs it on its own stream while the layer-2/1 backward proceeds), the
+    remaining bucket follows the backward, and `finish()` makes the compute stream wait for
+    both before Adam.  Calling the object on a tensor is a plain blocking all-reduce."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.works = []
+
+    def _active(self):
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def begin(self, tensor) -> None:
+        import torch.distributed as dist
+        if self._active():
+            self.works.append(dist.all_reduce(tensor, group=self.group, async_op=True))
+
+    def finish(self) -> None:
+        for w in self.works:
+            w.wait()
+        self.works.clear()
+
+    def __call__(self, tensor):
+        self.begin(tensor)
+        self.finish()
+        return tensor
+
+
 def gather_predictions(y, mig, group=None):
     """All-gather variable-length per-rank (y [g,3], mig [g]) arrays in rank order."""
     import torch

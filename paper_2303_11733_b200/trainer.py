@@ -115,9 +115,21 @@ class BatchTrainer:
         if self.allreduce is not None:
             den = float(global_graphs if global_graphs else b.G * self.world_size)
         eng.loss(b, ws, self.delta, grad_den=den)
-        eng.backward(b, ws, keep_scale=1.0 / (1.0 - self.dropout_p) if mode else 1.0)
-        if self.allreduce is not None:
-            self.allreduce(eng.grads)          # the one exchange: sum of per-rank gradient shares
+        keep = 1.0 / (1.0 - self.dropout_p) if mode else 1.0
+        if self.allreduce is not None and hasattr(self.allreduce, "begin"):
+            # two buckets: head + sage3 overlaps the layer-2/1 backward, the rest follows it
+            split = {}
+
+            def first_bucket(off):
+                split["off"] = off
+                self.allreduce.begin(eng.grads[off:])
+            eng.backward(b, ws, keep_scale=keep, on_partial=first_bucket)
+            self.allreduce.begin(eng.grads[:split.get("off", eng.grads.numel())])
+            self.allreduce.finish()
+        else:
+            eng.backward(b, ws, keep_scale=keep)
+            if self.allreduce is not None:
+                self.allreduce(eng.grads)      # the one exchange: sum of per-rank gradient shares
         eng.adam_step(self.lr)
 
     def step_host(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None) -> float:

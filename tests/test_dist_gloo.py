@@ -3,8 +3,8 @@ sharded-inference logic in paper_2303_11733_b200/dist.py.
 
 The GPU kernels are exercised by the -m gpu suite; here the per-rank compute is
 the CPU oracle, so what is tested is exactly the host-side N>1 logic:
-sharding by node count, the global-batch gradient denominator + one SUM
-all-reduce reproducing the single-process gnn.backward mean (gnn.py:402-404),
+sharding by node count, the global-batch gradient denominator + the two-bucket
+SUM all-reduce reproducing the single-process gnn.backward mean (gnn.py:402-404),
 and the ordered all-gather of per-rank predictions."""
 
 import os
@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 
 from conftest import unpack_records
 from oracle import dippm_oracle as O
-from paper_2303_11733_b200.dist import allreduce_sum, gather_predictions, global_batch_size, shard_by_nodes
+from paper_2303_11733_b200.dist import OverlappedAllReduce, gather_predictions, global_batch_size, shard_by_nodes
 
 WORLD = 2
 
@@ -55,7 +55,12 @@ def _worker(rank, port, golden, out):
         loss, grads = O.backward(params, norm, mine)
         share = len(mine) / g_total
         flat = torch.from_numpy(np.concatenate([grads[k].ravel() * share for k in O.SAGE_PARAM_NAMES]))
-        allreduce_sum(flat)
+        # the trainer's two buckets: head + sage3 first (overlapping the backward), then the rest
+        off = sum(grads[k].size for k in O.SAGE_PARAM_NAMES[:O.SAGE_PARAM_NAMES.index("sage3.w_self")])
+        ar = OverlappedAllReduce()
+        ar.begin(flat[off:])
+        ar.begin(flat[:off])
+        ar.finish()
         # sharded inference + ordered gather
         y = torch.from_numpy(np.stack([O.predict(params, norm, *r[:4]) for r in mine]))
         mig = torch.tensor([O.mig_code(float(v)) for v in y[:, 1]], dtype=torch.int8)
