@@ -385,6 +385,18 @@ class GemmTimer:
         flops = [f for _, _, f in self.recs]
         return sum(flops), sum(ms), len(ms)
 
+    def classes(self, steps, big=2e10):
+        """Per-step split: the layer-2/3 SAGE GEMMs (M = nodes, K >= 512: >= 20 GFLOP each) vs the
+        rest (layer-1 K = 64 and weight-gradient GEMMs, the 256-row head)."""
+        self.torch.cuda.synchronize()
+        out = {}
+        for name, sel in (("sage_layers_2_3", lambda f: f >= big), ("layer1_and_head", lambda f: f < big)):
+            rs = [(a.elapsed_time(b), f) for a, b, f in self.recs if sel(f)]
+            t, f = sum(r[0] for r in rs), sum(r[1] for r in rs)
+            out[name] = {"launches_per_step": len(rs) / steps, "us_per_step": 1e3 * t / steps,
+                         "tflop_per_step": f / steps / 1e12, "tflops": f / (t / 1e3) / 1e12 if t else None}
+        return out
+
 
 def main():
     args = parse_args()
@@ -542,7 +554,9 @@ def main():
                                  "" if args.dtype == "bf16" else "; fp32 mode = 3-pass tf32: bf16 sustained / 2 / 3"),
                              "gemm_share_of_step": (g_ms / args.steps) / (ms / args.steps),
                              "gemm_launches_per_step": g_n / args.steps,
-                             "algorithmic_tflop_per_step": g_flops / args.steps / 1e12},
+                             "algorithmic_tflop_per_step": g_flops / args.steps / 1e12,
+                             "by_class": {k: dict(v, frac=(v["tflops"] or 0.0) / peak_tf)
+                                          for k, v in timer.classes(args.steps).items()}},
                 "cpu_baseline": cpu, "clocks": clocks, "wall_s_timed_region": wall, "inference": infer}
         print(json.dumps(line), flush=True)
     if world > 1:
