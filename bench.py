@@ -160,53 +160,76 @@ def _cpu_worker_init(shm_name, shapes, hidden):
 
 def _cpu_worker_grads(args):
     from oracle import dippm_oracle as O
-    recs, norm = args
+    ids, norm = args  # graph ids into the dataset the worker inherited at fork time
+    recs = [(r.encoding.num_nodes, r.encoding.edges, r.encoding.features, r.fs.as_vector, r.target.as_array)
+            for r in _SHM["ds"].records(ids)]
     loss, grads = O.backward(_SHM["params"], norm, recs, hidden=_SHM["hidden"])
     n = len(recs)
     return loss * n, {k: g * n for k, g in grads.items()}, n
 
 
-def cpu_baseline(ds, hidden, batch, steps, procs, seed=0):
-    """Batch-protocol CPU training step (gnn.backward over `batch` records + 15
-    Adam updates) on `procs` worker processes, 1 BLAS thread each."""
-    import multiprocessing as mp
-    from multiprocessing import shared_memory
-    from oracle import dippm_oracle as O
+class CpuOracleTrainer:
+    """Batch-protocol CPU training step (gnn.backward over a batch of records + 15 Adam
+    updates, the oracle's fp64 numpy restatement) on `procs` worker processes with 1 BLAS
+    thread each; parameters live in shared memory, the pool is created once."""
 
-    rng = np.random.default_rng(seed)
-    params = O.init_params(hidden, rng)
-    shapes = [(k, params[k].shape) for k in O.SAGE_PARAM_NAMES]
-    total = sum(int(np.prod(s)) for _, s in shapes)
-    shm = shared_memory.SharedMemory(create=True, size=total * 8)
-    flat = np.ndarray((total,), dtype=np.float64, buffer=shm.buf)
-    off = 0
-    views = {}
-    for k, s in shapes:
-        n = int(np.prod(s))
-        flat[off:off + n] = params[k].ravel()
-        views[k] = flat[off:off + n].reshape(s)
-        off += n
-    norm = O.normalizer_fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
-    state = {k: (np.zeros(s), np.zeros(s)) for k, s in shapes}
-    ids = rng.permutation(ds.num_graphs)[:steps * batch]
-    recs = [(r.encoding.num_nodes, r.encoding.edges, r.encoding.features, r.fs.as_vector, r.target.as_array)
-            for r in ds.records(ids)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs, initializer=_cpu_worker_init, initargs=(shm.name, shapes, hidden)) as pool:
-        pool.map(_cpu_worker_grads, [(recs[:1], norm)] * procs)  # warm the workers
+    def __init__(self, ds, hidden, procs, seed=0):
+        import multiprocessing as mp
+        from multiprocessing import shared_memory
+        from oracle import dippm_oracle as O
+        self.O, self.ds, self.procs = O, ds, procs
+        rng = np.random.default_rng(seed)
+        self.rng = rng
+        params = O.init_params(hidden, rng)
+        self.shapes = [(k, params[k].shape) for k in O.SAGE_PARAM_NAMES]
+        total = sum(int(np.prod(s)) for _, s in self.shapes)
+        self.shm = shared_memory.SharedMemory(create=True, size=total * 8)
+        flat = np.ndarray((total,), dtype=np.float64, buffer=self.shm.buf)
+        self.views, off = {}, 0
+        for k, s in self.shapes:
+            n = int(np.prod(s))
+            flat[off:off + n] = params[k].ravel()
+            self.views[k] = flat[off:off + n].reshape(s)
+            off += n
+        self.norm = O.normalizer_fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+        self.state = {k: (np.zeros(s), np.zeros(s)) for k, s in self.shapes}
+        self.t = 0
+        _SHM["ds"] = ds  # inherited by the forked workers: steps ship graph ids, not arrays
+        self.pool = mp.get_context("fork").Pool(procs, initializer=_cpu_worker_init,
+                                                initargs=(self.shm.name, self.shapes, hidden))
+
+    def records(self, n):
+        return self.rng.choice(self.ds.num_graphs, n, replace=False)
+
+    def step(self, recs):
+        parts = [(recs[i::self.procs], self.norm) for i in range(self.procs) if len(recs[i::self.procs])]
+        out = self.pool.map(_cpu_worker_grads, parts)
+        n = sum(o[2] for o in out)
+        grads = {k: sum(o[1][k] for o in out) / n for k, _ in self.shapes}
+        self.t += 1
+        for k, _ in self.shapes:
+            m, v = self.state[k]
+            self.views[k][...] = self.O.adam_step(self.views[k], grads[k], m, v, self.t)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+        self.shm.close()
+        self.shm.unlink()
+
+
+def cpu_baseline(ds, hidden, batch, steps, procs, seed=0):
+    """`steps` CPU steps of `batch` graphs; returns (graphs/s, seconds)."""
+    tr = CpuOracleTrainer(ds, hidden, procs, seed)
+    try:
+        batches = [tr.records(batch) for _ in range(steps)]
+        tr.step(batches[0][:procs])  # warm the workers
         t0 = time.perf_counter()
-        for s in range(steps):
-            chunk = recs[s * batch:(s + 1) * batch]
-            parts = [(chunk[i::procs], norm) for i in range(procs) if chunk[i::procs]]
-            out = pool.map(_cpu_worker_grads, parts)
-            n = sum(o[2] for o in out)
-            grads = {k: sum(o[1][k] for o in out) / n for k, _ in shapes}
-            for k, _ in shapes:
-                m, v = state[k]
-                views[k][...] = O.adam_step(views[k], grads[k], m, v, s + 1)
+        for recs in batches:
+            tr.step(recs)
         dt = time.perf_counter() - t0
-    shm.close()
-    shm.unlink()
+    finally:
+        tr.close()
     return steps * batch / dt, dt
 
 
@@ -241,26 +264,38 @@ def config_dict(args, world):
 
 # ---------------------------------------------------------------------------
 
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, budget_s=150.0):
+    """Reference arm: the CPU port of the reference's path (the oracle: fp64 numpy
+    gnn.backward + Adam, batch protocol) on all host cores, same config and metric.
+    Warm-up steps are untimed; timed steps run until --steps are done or the time budget
+    is spent (full 256-graph steps; the sample actually timed is stated)."""
     if rank != 0:
         return
     from paper_2303_11733_b200.synth import make_dataset
     ds = make_dataset(args.graphs, seed=2)
     procs = host_cores()
-    per_step = []
-    for i in range(args.warmup + args.steps):
-        v, dt = cpu_baseline(ds, args.hidden, args.batch, 1, procs, seed=100 + i)
-        if i >= args.warmup:
-            per_step.append(dt)
-    total = sum(per_step)
-    value = args.steps * args.batch / total
+    tr = CpuOracleTrainer(ds, args.hidden, procs, seed=100)
+    try:
+        for _ in range(args.warmup):
+            tr.step(tr.records(args.batch))
+        done, total = 0, 0.0
+        while done < args.steps and total < budget_s:
+            recs = tr.records(args.batch)
+            t0 = time.perf_counter()
+            tr.step(recs)
+            total += time.perf_counter() - t0
+            done += 1
+    finally:
+        tr.close()
+    value = done * args.batch / total
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / done,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": DATA, "config": config_dict(args, 1),
             "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": procs, "kind": "port",
-                             "sample": f"{args.steps} timed steps x {args.batch} graphs, oracle gnn.backward + "
-                                       f"Adam (fp64 numpy), {procs} procs x 1 BLAS thread, {cpu_model()}"},
+                             "sample": f"{done} of {args.steps} timed steps x {args.batch} graphs (time budget "
+                                       f"{budget_s:.0f} s), oracle gnn.backward + Adam (fp64 numpy), {procs} procs "
+                                       f"x 1 BLAS thread, {cpu_model()}"},
             "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
