@@ -41,7 +41,7 @@ __device__ __forceinline__ void load_chunks(const ActView& a, int64_t r, int c0,
 // DTI: dtype of h (fp32 X for layer 1, the compute dtype after), DTO: of m.
 template <int DTI, int DTO, int CPL>
 __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView m, ActView self_out, int64_t N,
-                                                              int width, const int* __restrict__ rowptr,
+                                                              int rpb, int width, const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
                                                               const float* __restrict__ inv_deg) {
   __shared__ int s_ptr[kRowsPerBlock + 1];
@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
   const int gpw = 32 / L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / L, sub = lane % L;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
-  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
   const int cbeg = rowptr[r0];
   for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = rowptr[r0 + i] - cbeg;
   for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_w[i] = inv_deg[r0 + i];
@@ -210,7 +210,8 @@ __device__ __forceinline__ void finish_bias(float* colsum_partial, int width, fl
 }
 
 template <int DT, int CPL, bool kReadout>
-__global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(ActView B, int width, int64_t N, int write_agg,
+__global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(ActView B, int width, int64_t N,
+                                                                               int rpb, int write_agg,
                                                                 const int* __restrict__ t_rowptr,
                                                                 const int* __restrict__ t_col,
                                                                 const float* __restrict__ inv_deg,
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
   const int gpw = 32 / L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / L, sub = lane % L;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
-  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
   const int cbeg = t_rowptr[r0];
   const int ncol = t_rowptr[r0 + nrows] - cbeg;
   const bool staged = ncol <= kAggColCap;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
 // kPre neighbours are loaded together before any use (the kernel is load-latency bound).
 constexpr int kPre = 2;
 template <int DT, int CPL>
-__global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, int width, int64_t N,
+__global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, int width, int64_t N, int rpb,
                                                                      const int* __restrict__ t_rowptr,
                                                                      const int* __restrict__ t_col,
                                                                      const float* __restrict__ inv_deg,
@@ -342,8 +343,8 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
   __shared__ float s_cw[kAggColCap];
   __shared__ int s_g[kRowsPerBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
-  const int nrows = (int)((N - r0 < kRowsPerBlock) ? N - r0 : kRowsPerBlock);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
   const int cbeg = t_rowptr[r0];
   const int ncol = t_rowptr[r0 + nrows] - cbeg;
   const bool staged = ncol <= kAggColCap;
@@ -600,12 +601,31 @@ using namespace dippm;
 
 extern "C" {
 
+// Rows per block chosen so the grid is a whole number of waves (the kernels are latency bound
+// and a short last wave left ~30 % of the SMs idle): waves = ceil(N / (64 * P)) with P the
+// resident blocks on the GPU, rows = ceil(N / (waves * P)) <= 64.
+static int wave_rows(int64_t N, int blocks_per_sm) {
+  const int64_t P = (int64_t)num_sms() * std::max(1, blocks_per_sm);
+  const int64_t waves = std::max<int64_t>(1, (N + kRowsPerBlock * P - 1) / (kRowsPerBlock * P));
+  return (int)std::max<int64_t>(1, (N + waves * P - 1) / (waves * P));
+}
+constexpr int kColsumBlocksPerSm = 4;  // upper bound of the agg^T kernels' residency (sizing only)
+
+// Upper bound of the grid of a fused-bias agg^T launch with <= num_nodes rows (one partial
+// row per block).  Without the fused reduction the kernels use 64-row blocks
+// (dippm_colsum_blocks), so callers reducing the partials themselves see a fixed count.
+static int64_t colsum_bound(int64_t num_nodes) {
+  const int64_t P = (int64_t)num_sms() * kColsumBlocksPerSm;
+  const int64_t waves = std::max<int64_t>(1, (num_nodes + kRowsPerBlock * P - 1) / (kRowsPerBlock * P));
+  return std::max<int64_t>(ceil_div_i(num_nodes, kRowsPerBlock), waves * P);
+}
+
 int32_t dippm_colsum_blocks(int64_t num_nodes) { return ceil_div_i(num_nodes, kRowsPerBlock); }
 int32_t dippm_colsum_rows(int64_t num_nodes) {
-  const int nblk = dippm_colsum_blocks(num_nodes);
+  const int nblk = (int)colsum_bound(num_nodes);
   return nblk + colsum_groups(nblk);
 }
-int32_t dippm_colsum_sync_ints(int64_t num_nodes) { return colsum_groups(dippm_colsum_blocks(num_nodes)) + 1; }
+int32_t dippm_colsum_sync_ints(int64_t num_nodes) { return colsum_groups((int)colsum_bound(num_nodes)) + 1; }
 
 static int cpl_for(int width) {
   const int chunks = width / 8;
@@ -620,9 +640,11 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
                   "sage_aggregate: unsupported width %d", width);
   DIPPM_ARG_CHECK(!self_out.data || self_out.dtype == m_out.dtype, "sage_aggregate: self_out dtype");
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = ceil_div_i(N, kRowsPerBlock);
+  const int rpb = wave_rows(N, 4);
+  const int grid = ceil_div_i(N, rpb);
   ActView hv = make_view(h), mv = make_view(m_out), sv = make_view(self_out);
-#define DIPPM_AGG(DI, DO, C) k_aggregate<DI, DO, C><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, width, rowptr, col, inv_deg)
+#define DIPPM_AGG(DI, DO, C) \
+  k_aggregate<DI, DO, C><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, rpb, width, rowptr, col, inv_deg)
 #define DIPPM_AGG_C(DI, DO) \
   do { if (cpl == 4) DIPPM_AGG(DI, DO, 4); else if (cpl == 2) DIPPM_AGG(DI, DO, 2); else DIPPM_AGG(DI, DO, 1); } while (0)
 #define DIPPM_AGG_O(DI)                                                   \
@@ -654,14 +676,16 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
   DIPPM_ARG_CHECK(!bias_out || width / 4 <= kAggThreads, "sage_aggregate_t: fused bias reduce needs width <= %d",
                   4 * kAggThreads);
   if (bias_out) smem = std::max(smem, (size_t)kAggThreads * 4 * sizeof(double));  // fold scratch
-  const int grid = ceil_div_i(N, kRowsPerBlock);
+  int rpb = bias_out ? wave_rows(N, readout ? 2 : 3) : kRowsPerBlock;  // caller-reduced partials: fixed blocks
+  if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;           // partial rows are sized for this bound
+  const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
 #define DIPPM_AGGT(D, C, R)                                                                                      \
   do {                                                                                                           \
     if (smem > 48 * 1024)                                                                                        \
       DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                             (int)smem));                                                         \
-    k_aggregate_t<D, C, R><<<grid, kAggThreads, smem, s>>>(bv, width, N, write_agg, t_rowptr, t_col, inv_deg,    \
+    k_aggregate_t<D, C, R><<<grid, kAggThreads, smem, s>>>(bv, width, N, rpb, write_agg, t_rowptr, t_col, inv_deg, \
                                                           colsum_partial, ro, bias_out, sync);                   \
   } while (0)
 #define DIPPM_AGGT_C(D, R) \
@@ -684,14 +708,16 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
                   width);
   DIPPM_ARG_CHECK(!bias_out || sync, "readout_aggregate_t: bias_grad needs the sync counters");
   const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double));
-  const int grid = ceil_div_i(N, kRowsPerBlock);
+  int rpb = bias_out ? wave_rows(N, 3) : kRowsPerBlock;
+  if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
+  const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
 #define DIPPM_RB(D, C)                                                                                            \
   do {                                                                                                            \
     if (smem > 48 * 1024)                                                                                         \
       DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_readout_agg_bits<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                             (int)smem));                                                          \
-    k_readout_agg_bits<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, t_rowptr, t_col, inv_deg, colsum_partial, \
+    k_readout_agg_bits<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, rpb, t_rowptr, t_col, inv_deg, colsum_partial, \
                                                             ro, bias_out, sync);                                  \
   } while (0)
 #define DIPPM_RB_C(D) \

@@ -296,10 +296,9 @@ def test_aggregate_t_and_reduce_rows():
     nblk = lib.dippm_colsum_blocks(N)
     part = torch.empty(lib.dippm_colsum_rows(N), W, device="cuda")
     sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device="cuda")
-    fused = torch.empty(W, device="cuda")
+    # caller-reduced partials (bias_grad NULL): exactly dippm_colsum_blocks(N) rows
     _lib.call("dippm_sage_aggregate_t", dev.f32_act(B), W, N, 1, b.t_rowptr.data_ptr(), b.t_col.data_ptr(),
-              b.inv_deg.data_ptr(), part.data_ptr(), fused.data_ptr(), sync.data_ptr(), dev._stream())
-    assert int(sync.abs().sum()) == 0
+              b.inv_deg.data_ptr(), part.data_ptr(), None, None, dev._stream())
     agg = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist())))
     assert np.allclose(B[:, W:].cpu().numpy(), agg.T @ dz.astype(np.float64), rtol=1e-5, atol=1e-5)
     out = torch.empty(W, device="cuda")
@@ -308,6 +307,10 @@ def test_aggregate_t_and_reduce_rows():
     out2 = torch.empty(W, device="cuda")
     _lib.call("dippm_reduce_rows", part.data_ptr(), nblk, W, W, 1.0, out2.data_ptr(), dev._stream())
     assert torch.equal(out, out2)
+    fused = torch.empty(W, device="cuda")  # in-kernel reduction (its own block partition)
+    _lib.call("dippm_sage_aggregate_t", dev.f32_act(B), W, N, 1, b.t_rowptr.data_ptr(), b.t_col.data_ptr(),
+              b.inv_deg.data_ptr(), part.data_ptr(), fused.data_ptr(), sync.data_ptr(), dev._stream())
+    assert int(sync.abs().sum()) == 0
     assert np.allclose(fused.cpu().numpy(), dz.astype(np.float64).sum(0), rtol=1e-5, atol=1e-4)
     fused2 = torch.empty(W, device="cuda")  # replay: same bits, counters back at zero
     _lib.call("dippm_sage_aggregate_t", dev.f32_act(B), W, N, 0, b.t_rowptr.data_ptr(), b.t_col.data_ptr(),
