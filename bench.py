@@ -359,6 +359,56 @@ def inference_sweep(args, rank, world, lib):
     return out
 
 
+def train_large_graph_skew(args, rank, world, per_rank=32, batches=8, steps=40):
+    """configs[3] per GPU: data-parallel training batches of 32 graphs per rank whose node counts
+    are log-uniform on [12, 5000] (transformer-sized graphs mixed with tiny ones, SURVEY §8d
+    cfg4); resident batches, CUDA-graph steps at N=1 (eager + the bucketed all-reduce at N>1),
+    max-over-ranks device time, graphs/s over all ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_11733_b200 import gnn
+    from paper_2303_11733_b200.device import upload_batch
+    from paper_2303_11733_b200.dist import OverlappedAllReduce
+    from paper_2303_11733_b200.synth import make_dataset
+    rng = np.random.default_rng(40 + rank)
+    n = np.exp(rng.uniform(np.log(12), np.log(5000), per_rank * batches)).astype(np.int64)
+    ds = make_dataset(len(n), seed=40 + rank, nodes=n)
+    norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    model = gnn.create_model(hidden=args.hidden, seed=0, normalizer=norm)
+    from paper_2303_11733_b200.trainer import BatchTrainer
+    tr = BatchTrainer(model, precision=args.dtype, lr=gnn.DEFAULT_LEARNING_RATE, seed=3,
+                      allreduce=OverlappedAllReduce() if world > 1 else None, world_size=world, rank=rank,
+                      use_graphs=world == 1)
+    order = np.argsort(rng.random(len(n)))
+    res = [upload_batch(*ds.collate(order[i * per_rank:(i + 1) * per_rank]), device="cuda", build_csr=False)
+           for i in range(batches)]
+    tr.reserve(max(b.N for b in res), per_rank)
+    for i in range(3):
+        tr.step_resident(res[i % batches])
+    if tr.use_graphs:
+        for b in res:
+            tr.capture(b)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        tr.step_resident(res[i % batches])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nodes = [b.N for b in res]
+    return {"workload": f"configs[3]: DP training, {per_rank} graphs/rank/step, node counts log-uniform on "
+                        f"[12, 5000] (up to {int(max(ds.n))} nodes), hidden {args.hidden}, Adam",
+            "graphs_per_s": steps * per_rank * world / (ms / 1000.0), "ms_per_step": ms / steps,
+            "nodes_per_step_mean": float(np.mean(nodes)), "scaling": "weak"}
+
+
 def predict_from_json(args, rank, world, docs_per_batch=2048, batches=3):
     """configs[4]: end-to-end predict + MIG pick from graph JSON documents with
     power-law operator counts (N in [12, 5000], alpha 1.5): native multi-threaded
@@ -569,6 +619,7 @@ def main():
     if not args.no_infer:
         infer = inference_sweep(args, rank, world, lib)
         infer["predict_from_json"] = predict_from_json(args, rank, world)
+        infer["train_large_graph_skew"] = train_large_graph_skew(args, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -80,9 +80,12 @@ def node_counts(num_graphs: int, rng, n_lo=270, n_hi=330, power_law: float | Non
 
 
 def make_dataset(num_graphs: int, seed: int = 0, n_lo: int = 270, n_hi: int = 330, edge_ratio: float = 1.33,
-                 power_law: float | None = None, n_max: int = 5000, memory_scale: float = 1.0) -> SynthDataset:
+                 power_law: float | None = None, n_max: int = 5000, memory_scale: float = 1.0,
+                 nodes=None) -> SynthDataset:
+    """`nodes` (optional int array [num_graphs]) fixes the node counts explicitly."""
     rng = np.random.default_rng(seed)
-    n = node_counts(num_graphs, rng, n_lo, n_hi, power_law, n_max)
+    n = node_counts(num_graphs, rng, n_lo, n_hi, power_law, n_max) if nodes is None else \
+        np.asarray(nodes, dtype=np.int64).reshape(num_graphs)
     node_ptr = np.zeros(num_graphs + 1, np.int64)
     np.cumsum(n, out=node_ptr[1:])
     total = int(node_ptr[-1])
