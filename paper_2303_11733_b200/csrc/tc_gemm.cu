@@ -787,7 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tid = threadIdx.x - 64;
           int* arrive = p.sync + r * kCta + rank;
           int* depart = arrive + tiles_mn * kCta;
-          uint32_t* s_flag = tslot + 1;
+          __shared__ uint32_t s_go;  // "this CTA reduces" flag, away from the TMEM address slot
+          uint32_t* s_flag = &s_go;
           epi_sync();  // this CTA's partial rows are all written
           if (tid == 0) {
             __threadfence();
