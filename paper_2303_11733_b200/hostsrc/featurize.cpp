@@ -265,7 +265,8 @@ struct Cursor {
     }
     --depth;
   }
-  // Iterate an object's members: f(key) must consume the value.
+  // Iterate an object's members: f(key) must consume the value and must not
+  // use `key` after parsing any string of that value.
   template <class F>
   void object(F&& f) {
     ++p;
@@ -277,7 +278,7 @@ struct Cursor {
     while (true) {
       ws();
       if (p >= e || *p != '"') bad("expected key");
-      const std::string key(string());
+      const std::string_view key = string();  // valid until f parses another string
       ws();
       if (p >= e || *p != ':') bad("expected ':'");
       ++p;
@@ -340,6 +341,22 @@ const char* const kAttrs[12] = {"kernel_h",   "kernel_w",   "stride_h", "stride_
 enum Attr { KH = 0, KW, SH, SW, PH, PW, DH, DW, GROUPS, OUTF, HAS_BIAS, EPS };
 const char* const kNonOperator[10] = {"const", "constant", "var", "variable", "param", "parameter", "input", "tuple",
                                       "tuple_get_item", "tuplegetitem"};  // graph_ir.py:101-114
+
+// classify an operator tail (lower-cased): one-hot kind and is_operator
+void classify(std::string_view tail, int& kind, bool& is_op) {
+  static const std::string_view kinds[16] = {kKinds[0], kKinds[1], kKinds[2],  kKinds[3],  kKinds[4],  kKinds[5],
+                                             kKinds[6], kKinds[7], kKinds[8],  kKinds[9],  kKinds[10], kKinds[11],
+                                             kKinds[12], kKinds[13], kKinds[14], kKinds[15]};
+  static const std::string_view non_op[10] = {kNonOperator[0], kNonOperator[1], kNonOperator[2], kNonOperator[3],
+                                              kNonOperator[4], kNonOperator[5], kNonOperator[6], kNonOperator[7],
+                                              kNonOperator[8], kNonOperator[9]};
+  kind = OTHER;
+  for (int q = 0; q < 16; ++q)
+    if (tail == kinds[q]) kind = q;
+  is_op = true;
+  for (const std::string_view& w : non_op)
+    if (tail == w) is_op = false;
+}
 
 std::string op_tail(const std::string& raw) {  // name.strip().lower().rsplit(".", 1)[-1]
   size_t a = 0, b = raw.size();
@@ -420,7 +437,9 @@ struct RawNode {
   std::vector<int64_t> inputs;
   bool has_attrs = false;
   uint8_t attrs_t = V_NUL;
-  std::vector<std::pair<std::string, Scalar>> attrs;  // final (deduplicated) entries
+  bool has_known[12] = {};                            // KNOWN_ATTRIBUTES, last duplicate wins
+  Scalar known[12];
+  std::vector<std::pair<std::string, Scalar>> attrs;  // other names (only their types matter)
   bool has_shape = false;
   uint8_t shape_t = V_NUL;
   std::vector<Scalar> shape;
@@ -428,7 +447,7 @@ struct RawNode {
 
 void read_node(Cursor& c, RawNode& r) {
   r.is_obj = true;
-  c.object([&](const std::string& key) {
+  c.object([&](std::string_view key) {
     if (key == "id") {
       r.has_id = true;
       r.id = c.value();
@@ -458,16 +477,26 @@ void read_node(Cursor& c, RawNode& r) {
     } else if (key == "attrs") {
       r.has_attrs = true;
       r.attrs.clear();
+      for (bool& h : r.has_known) h = false;
       if (c.peek('{')) {
         r.attrs_t = V_OBJ;
-        c.object([&](const std::string& k) {
+        c.object([&](std::string_view k) {
+          int slot = -1;
+          for (int a = 0; a < 12 && slot < 0; ++a)
+            if (k == kAttrs[a]) slot = a;
+          if (slot >= 0) {
+            r.known[slot] = c.value();
+            r.has_known[slot] = true;
+            return;
+          }
+          std::string key(k);  // copy before the value may overwrite the view
           const Scalar v = c.value();
           for (auto& kv : r.attrs)
-            if (kv.first == k) {
+            if (kv.first == key) {
               kv.second = v;
               return;
             }
-          r.attrs.emplace_back(k, v);
+          r.attrs.emplace_back(std::move(key), v);
         });
       } else {
         r.attrs_t = c.value().t;
@@ -487,6 +516,32 @@ void read_node(Cursor& c, RawNode& r) {
   });
 }
 
+// node id -> entry index: a direct table when the ids are dense (the usual 0..n-1 numbering),
+// else a hash map.
+struct IdIndex {
+  std::vector<int32_t> table;
+  std::unordered_map<int64_t, size_t> map;
+  bool dense = true;
+  explicit IdIndex(const std::vector<RawNode>& raw) {
+    int64_t hi = -1;
+    for (const RawNode& r : raw)
+      if (r.is_obj && r.has_id && r.id.t == V_INT) hi = std::max(hi, r.id.i);
+    dense = hi < (int64_t)raw.size() * 4 + 64;
+    if (dense) table.assign((size_t)(hi + 1), -1);
+    else map.reserve(raw.size() * 2);
+  }
+  int64_t find(int64_t id) const {
+    if (dense) return (id >= 0 && id < (int64_t)table.size()) ? table[(size_t)id] : -1;
+    auto it = map.find(id);
+    return it == map.end() ? -1 : (int64_t)it->second;
+  }
+  size_t at(int64_t id) const { return (size_t)find(id); }  // id known to exist
+  void set(int64_t id, size_t k) {
+    if (dense) table[(size_t)id] = (int32_t)k;
+    else map[id] = k;
+  }
+};
+
 // parse_graph_json graph_ir.py:212-297
 Graph parse_graph(const char* text, int64_t len) {
   Cursor c{text, text + len};
@@ -503,7 +558,7 @@ Graph parse_graph(const char* text, int64_t len) {
     if (c.p != c.e) c.bad("extra data");
     fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "top-level value must be an object");
   }
-  c.object([&](const std::string& key) {
+  c.object([&](std::string_view key) {
     if (key == "nodes") {
       has_nodes = true;
       raw.clear();
@@ -552,8 +607,7 @@ Graph parse_graph(const char* text, int64_t len) {
     fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"batch\" must be a positive integer");
   if (has_name && name_v.t != V_STR) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "\"name\" must be a string");
 
-  std::unordered_map<int64_t, size_t> by_id;
-  by_id.reserve(raw.size() * 2);
+  IdIndex by_id(raw);
   std::vector<int64_t> order_doc;
   order_doc.reserve(raw.size());
   std::vector<Node> entries;
@@ -563,7 +617,7 @@ Graph parse_graph(const char* text, int64_t len) {
     if (!r.has_id || r.id.t != V_INT || r.id.i < 0)
       fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node id must be a non-negative integer");
     const int64_t nid = r.id.i;
-    if (by_id.count(nid)) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "duplicate node id " + I(nid));
+    if (by_id.find(nid) >= 0) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "duplicate node id " + I(nid));
     if (!r.has_op || r.op_t != V_STR || r.op.empty())
       fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": missing operator name");
     Node n;
@@ -578,15 +632,17 @@ Graph parse_graph(const char* text, int64_t len) {
       if (good)
         for (const auto& kv : r.attrs)
           if (kv.second.t != V_INT && kv.second.t != V_FLT) good = false;
+      for (int a = 0; a < 12; ++a)
+        if (r.has_known[a] && r.known[a].t != V_INT && r.known[a].t != V_FLT) good = false;
       if (!good) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": attrs must map names to numbers");
-      for (const auto& kv : r.attrs)
-        for (int a = 0; a < 12; ++a)
-          if (kv.first == kAttrs[a]) {
-            n.has_attr[a] = true;
-            n.attr_int[a] = kv.second.t == V_INT;
-            n.attr_i[a] = kv.second.i;
-            n.attr[a] = kv.second.t == V_INT ? (double)kv.second.i : kv.second.f;
-          }
+      for (int a = 0; a < 12; ++a)
+        if (r.has_known[a]) {
+          const Scalar& v = r.known[a];
+          n.has_attr[a] = true;
+          n.attr_int[a] = v.t == V_INT;
+          n.attr_i[a] = v.i;
+          n.attr[a] = v.t == V_INT ? (double)v.i : v.f;
+        }
     }
     if (r.has_shape && r.shape_t != V_NUL) {
       if (r.shape_t != V_ARR) fail(DIPPM_FEAT_BAD_SHAPE, "node " + I(nid) + ": out_shape must be a list");
@@ -599,17 +655,17 @@ Graph parse_graph(const char* text, int64_t len) {
       }
       n.has_shape = true;
     }
-    by_id[nid] = entries.size();
+    by_id.set(nid, entries.size());
     order_doc.push_back(nid);
     entries.push_back(std::move(n));
   }
   for (size_t k = 0; k < entries.size(); ++k)
     for (int64_t src : entries[k].inputs)
-      if (!by_id.count(src))
+      if (by_id.find(src) < 0)
         fail(DIPPM_FEAT_DANGLING_REFERENCE, "node " + I(order_doc[k]) + " references missing input " + I(src));
   for (const Scalar& o : outputs) {
     const int64_t oid = o.t == V_BOOL ? (int64_t)o.b : o.i;
-    if (!by_id.count(oid)) fail(DIPPM_FEAT_DANGLING_REFERENCE, "output id " + I(oid) + " does not exist");
+    if (by_id.find(oid) < 0) fail(DIPPM_FEAT_DANGLING_REFERENCE, "output id " + I(oid) + " does not exist");
   }
   // _topological_order: Kahn over a min-heap of original ids, inputs counted with multiplicity.
   // Ids are renamed to entry indices for the bookkeeping; the heap orders by original id.
@@ -618,14 +674,14 @@ Graph parse_graph(const char* text, int64_t len) {
   std::vector<size_t> cons;
   for (size_t k = 0; k < M; ++k) {
     pending[k] = (int64_t)entries[k].inputs.size();
-    for (int64_t src : entries[k].inputs) ++cptr[by_id[src] + 1];
+    for (int64_t src : entries[k].inputs) ++cptr[by_id.at(src) + 1];
   }
   for (size_t k = 0; k < M; ++k) cptr[k + 1] += cptr[k];
   cons.resize((size_t)cptr[M]);
   {
     std::vector<int64_t> fillp(cptr.begin(), cptr.end() - 1);
     for (size_t k = 0; k < M; ++k)  // consumers in document order, like the reference's dict
-      for (int64_t src : entries[k].inputs) cons[(size_t)fillp[by_id[src]]++] = k;
+      for (int64_t src : entries[k].inputs) cons[(size_t)fillp[by_id.at(src)]++] = k;
   }
   std::priority_queue<std::pair<int64_t, size_t>, std::vector<std::pair<int64_t, size_t>>, std::greater<>> heap;
   for (size_t k = 0; k < M; ++k)
@@ -658,17 +714,11 @@ Graph parse_graph(const char* text, int64_t len) {
   g.nodes.reserve(M);
   for (size_t k : order) {
     Node n = std::move(entries[k]);
-    for (auto& i : n.inputs) i = remap[by_id[i]];
-    const std::string tail = op_tail(n.raw);
-    n.kind = OTHER;
-    for (int q = 0; q < 16; ++q)
-      if (tail == kKinds[q]) n.kind = q;
-    n.is_op = true;
-    for (const char* w : kNonOperator)
-      if (tail == w) n.is_op = false;
+    for (auto& i : n.inputs) i = remap[by_id.at(i)];
+    classify(op_tail(n.raw), n.kind, n.is_op);
     g.nodes.push_back(std::move(n));
   }
-  for (const Scalar& o : outputs) g.outputs.push_back(remap[by_id[o.t == V_BOOL ? (int64_t)o.b : o.i]]);
+  for (const Scalar& o : outputs) g.outputs.push_back(remap[by_id.at(o.t == V_BOOL ? (int64_t)o.b : o.i)]);
   return g;
 }
 
@@ -684,19 +734,20 @@ int64_t conv_spatial(int64_t size, int64_t k, int64_t s, int64_t pad, int64_t di
 }
 
 // _infer_node_shape graph_ir.py:384-493
-std::vector<int64_t> infer_node(const Node& n, int64_t id, const std::vector<std::vector<int64_t>>& in) {
-  const std::string nid = I(id);
+using Shapes = std::vector<const std::vector<int64_t>*>;
+std::vector<int64_t> infer_node(const Node& n, int64_t id, const Shapes& in) {
+  const auto nid = [id] { return I(id); };  // built only on failure
   if (n.inputs.empty()) {
-    if (!n.has_shape) fail(DIPPM_FEAT_UNDERSPECIFIED, "source node " + nid + " (" + n.raw + ") declares no out_shape");
+    if (!n.has_shape) fail(DIPPM_FEAT_UNDERSPECIFIED, "source node " + nid() + " (" + n.raw + ") declares no out_shape");
     return n.shape;
   }
   const int k = n.kind;
-  const auto& first = in[0];
+  const auto& first = *in[0];
   if (k == CONV2D || k == CONV2D_T) {
     if (first.size() != 4)
-      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": " + kKinds[k] + " input must be rank 4, got " + shape_str(first));
+      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": " + kKinds[k] + " input must be rank 4, got " + shape_str(first));
     const int64_t kh = attr_int(n, KH), kw = attr_int(n, KW);
-    if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": " + kKinds[k] + " kernel size missing");
+    if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": " + kKinds[k] + " kernel size missing");
     int64_t sh = attr_int(n, SH), sw = attr_int(n, SW);
     if (!sh) sh = 1;
     if (!sw) sw = 1;
@@ -707,7 +758,7 @@ std::vector<int64_t> infer_node(const Node& n, int64_t id, const std::vector<std
     int64_t out_c = attr_int(n, OUTF);
     if (out_c < 1) {
       if (n.has_shape && n.shape.size() == 4) out_c = n.shape[1];
-      else fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": " + kKinds[k] + " output channels missing");
+      else fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": " + kKinds[k] + " output channels missing");
     }
     const int64_t nn = first[0], h = first[2], w = first[3];
     if (k == CONV2D) return {nn, out_c, conv_spatial(h, kh, sh, ph, dh), conv_spatial(w, kw, sw, pw, dw)};
@@ -715,9 +766,9 @@ std::vector<int64_t> infer_node(const Node& n, int64_t id, const std::vector<std
   }
   if (k == MAXPOOL || k == AVGPOOL) {
     if (first.size() != 4)
-      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": " + kKinds[k] + " input must be rank 4, got " + shape_str(first));
+      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": " + kKinds[k] + " input must be rank 4, got " + shape_str(first));
     const int64_t kh = attr_int(n, KH), kw = attr_int(n, KW);
-    if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": pool kernel size missing");
+    if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": pool kernel size missing");
     int64_t sh = attr_int(n, SH), sw = attr_int(n, SW);
     if (!sh) sh = kh;
     if (!sw) sw = kw;
@@ -729,36 +780,37 @@ std::vector<int64_t> infer_node(const Node& n, int64_t id, const std::vector<std
   }
   if (k == GAVGPOOL) {
     if (first.size() != 4)
-      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": global pool input must be rank 4, got " + shape_str(first));
+      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": global pool input must be rank 4, got " + shape_str(first));
     return {first[0], first[1], 1, 1};
   }
   if (k == DENSE) {
     const int64_t of = attr_int(n, OUTF);
-    if (of < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": dense out_features missing");
+    if (of < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": dense out_features missing");
     std::vector<int64_t> r(first.begin(), first.end() - 1);
     r.push_back(of);
     return r;
   }
   if (k == BMM) {
-    if (in.size() != 2) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": batch_matmul needs exactly 2 inputs");
-    const auto &a = in[0], &b = in[1];
+    if (in.size() != 2) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": batch_matmul needs exactly 2 inputs");
+    const auto &a = *in[0], &b = *in[1];
     if (a.size() != 3 || b.size() != 3)
-      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": batch_matmul inputs must be rank 3");
-    if (a[0] != b[0] || a[2] != b[1]) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": batch_matmul shapes do not compose");
+      fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": batch_matmul inputs must be rank 3");
+    if (a[0] != b[0] || a[2] != b[1]) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": batch_matmul shapes do not compose");
     return {a[0], a[1], b[2]};
   }
   if (k == ADD || k == MUL) {
     for (size_t j = 1; j < in.size(); ++j)
-      if (in[j] != first) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": elementwise inputs differ");
+      if (*in[j] != first) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": elementwise inputs differ");
     return first;
   }
   if (k == CONCAT) {
-    if (first.size() < 2) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": concat inputs must have rank >= 2");
+    if (first.size() < 2) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": concat inputs must have rank >= 2");
     int64_t ch = 0;
-    for (const auto& s : in) {
+    for (const auto* sp : in) {
+      const auto& s = *sp;
       bool same = s.size() == first.size() && s[0] == first[0];
       for (size_t d = 2; same && d < s.size(); ++d) same = s[d] == first[d];
-      if (!same) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid + ": concat inputs differ outside channel dim");
+      if (!same) fail(DIPPM_FEAT_SHAPE_MISMATCH, "node " + nid() + ": concat inputs differ outside channel dim");
       ch += s[1];
     }
     std::vector<int64_t> r = {first[0], ch};
@@ -777,19 +829,19 @@ std::vector<int64_t> infer_node(const Node& n, int64_t id, const std::vector<std
 }
 
 void infer_shapes(Graph& g) {  // graph_ir.py:357-381 (validation already holds after parsing)
-  std::vector<std::vector<int64_t>> shapes;
-  shapes.reserve(g.nodes.size());
+  // Nodes are in topological order and inputs precede their consumers, so a node's inferred
+  // shape can replace its declared one as soon as it is known: later nodes only read the
+  // inferred shapes of their inputs (the reference's `shapes` dict) and their own declared
+  // shape.  A failure discards the whole graph.
+  Shapes in;
   for (size_t k = 0; k < g.nodes.size(); ++k) {
     Node& n = g.nodes[k];
-    std::vector<std::vector<int64_t>> in;
-    for (int64_t i : n.inputs) in.push_back(shapes[i]);
+    in.clear();
+    for (int64_t i : n.inputs) in.push_back(&g.nodes[i].shape);
     std::vector<int64_t> s = infer_node(n, (int64_t)k, in);
     check_shape(s, (int64_t)k);
-    shapes.push_back(s);
-  }
-  for (size_t k = 0; k < g.nodes.size(); ++k) {
-    g.nodes[k].shape = shapes[k];
-    g.nodes[k].has_shape = true;
+    n.shape = std::move(s);
+    n.has_shape = true;
   }
 }
 
@@ -823,21 +875,34 @@ void operator_graph(const Graph& g, std::vector<int64_t>& order, std::vector<std
   bool any = false;
   for (const Node& n : g.nodes) any |= n.is_op;
   if (!any) fail(DIPPM_FEAT_EMPTY_GRAPH, "graph '" + g.name + "' has no operator nodes");
-  std::vector<std::vector<int64_t>> producers(N);
+  // producers of node v = prod[pptr[v] .. pptr[v+1]) (deduplicated, input order kept)
+  std::vector<int64_t> prod, pptr(N + 1, 0);
+  prod.reserve(N * 2);
   for (size_t v = 0; v < N; ++v) {
-    std::vector<int64_t>& seen = producers[v];
+    const size_t s0 = prod.size();
+    auto add = [&](int64_t c) {
+      for (size_t j = s0; j < prod.size(); ++j)
+        if (prod[j] == c) return;
+      prod.push_back(c);
+    };
     for (int64_t src : g.nodes[v].inputs) {
-      auto add = [&](int64_t c) {
-        if (std::find(seen.begin(), seen.end(), c) == seen.end()) seen.push_back(c);
-      };
       if (g.nodes[src].is_op) add(src);
       else
-        for (int64_t c : producers[src]) add(c);
+        for (int64_t j = pptr[src]; j < pptr[src + 1]; ++j) add(prod[(size_t)j]);
     }
+    pptr[v + 1] = (int64_t)prod.size();
   }
+  struct Span {
+    const int64_t* b;
+    const int64_t* e;
+    const int64_t* begin() const { return b; }
+    const int64_t* end() const { return e; }
+  };
+  auto producers = [&](int64_t v) { return Span{prod.data() + pptr[v], prod.data() + pptr[v + 1]}; };
   std::vector<char> visited(N, 0);
+  std::vector<std::pair<int64_t, bool>> stack;
   auto visit = [&](int64_t root) {
-    std::vector<std::pair<int64_t, bool>> stack{{root, false}};
+    stack.assign(1, {root, false});
     while (!stack.empty()) {
       auto [nid, expanded] = stack.back();
       stack.pop_back();
@@ -848,16 +913,18 @@ void operator_graph(const Graph& g, std::vector<int64_t>& order, std::vector<std
       if (visited[nid]) continue;
       visited[nid] = 1;
       stack.push_back({nid, true});
-      const auto& pr = producers[nid];
-      for (auto it = pr.rbegin(); it != pr.rend(); ++it)
+      const Span pr = producers(nid);
+      for (const int64_t* it = pr.e; it != pr.b;) {
+        --it;
         if (!visited[*it]) stack.push_back({*it, false});
+      }
     }
   };
   for (int64_t out : g.outputs) {
     if (g.nodes[out].is_op) {
       if (!visited[out]) visit(out);
     } else {
-      for (int64_t r : producers[out])
+      for (int64_t r : producers(out))
         if (!visited[r]) visit(r);
     }
   }
@@ -865,12 +932,11 @@ void operator_graph(const Graph& g, std::vector<int64_t>& order, std::vector<std
     if (g.nodes[v].is_op && !visited[v]) visit((int64_t)v);
   std::vector<int64_t> position(N, -1);
   for (size_t i = 0; i < order.size(); ++i) position[order[i]] = (int64_t)i;
-  std::unordered_set<uint64_t> emitted;
+  // The reference filters through an `emitted` set; it never fires: every node occurs once in
+  // `order` and its producer list is already deduplicated, so (src, nid) pairs are unique.
+  edges.reserve(prod.size());
   for (int64_t nid : order)
-    for (int64_t src : producers[nid]) {
-      const uint64_t key = ((uint64_t)position[src] << 32) | (uint64_t)position[nid];
-      if (emitted.insert(key).second) edges.push_back({position[src], position[nid]});
-    }
+    for (int64_t src : producers(nid)) edges.push_back({position[src], position[nid]});
 }
 
 // encode_node featurize.py:166-183
@@ -897,8 +963,8 @@ int64_t compute_macs(const Graph& g) {
   for (size_t k = 0; k < g.nodes.size(); ++k) {
     const Node& n = g.nodes[k];
     if (n.kind != CONV2D && n.kind != CONV2D_T && n.kind != DENSE && n.kind != BMM) continue;
-    const std::string nid = I((int64_t)k);
-    if (n.inputs.empty()) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": input shape unavailable");
+    const auto nid = [k] { return I((int64_t)k); };
+    if (n.inputs.empty()) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": input shape unavailable");
     const auto& in = g.nodes[n.inputs[0]].shape;
     const auto& out = n.shape;
     if (n.kind == DENSE) {
@@ -906,14 +972,14 @@ int64_t compute_macs(const Graph& g) {
       for (size_t d = 0; d + 1 < out.size(); ++d) lead *= out[d];
       total += lead * in.back() * out.back();
     } else if (n.kind == BMM) {
-      if (out.size() < 3 || in.size() < 3) fail(DIPPM_FEAT_VALUE_ERROR, "node " + nid + ": list index out of range");
+      if (out.size() < 3 || in.size() < 3) fail(DIPPM_FEAT_VALUE_ERROR, "node " + nid() + ": list index out of range");
       total += (__int128)out[0] * out[1] * out[2] * in[2];
     } else {
       const int64_t kh = attr_int(n, KH), kw = attr_int(n, KW);
-      if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": kernel size missing");
+      if (kh < 1 || kw < 1) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": kernel size missing");
       int64_t groups = attr_int(n, GROUPS);
       if (!groups) groups = 1;
-      if (in.size() != 4 || out.size() != 4) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid + ": conv shapes must be rank 4");
+      if (in.size() != 4 || out.size() != 4) fail(DIPPM_FEAT_UNDERSPECIFIED, "node " + nid() + ": conv shapes must be rank 4");
       if (n.kind == CONV2D)
         total += (__int128)out[0] * out[1] * out[2] * out[3] * floordiv(in[1], groups) * kh * kw;
       else
