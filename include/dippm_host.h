@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_HOST_ABI_VERSION 1
+#define DIPPM_HOST_ABI_VERSION 2
 
 /* Per-document status: the reference exception class (errors.py:8-83). */
 enum dippm_feat_status {
@@ -70,6 +70,16 @@ void dippm_feat_sizes(const dippm_feat_batch* b, int64_t* num_nodes, int64_t* nu
  *   x32     float  [total_nodes, 32]  optional (may be NULL): x rounded to fp32 for the device
  * Any pointer may be NULL to skip that output. */
 void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int64_t* fs_int, float* x32);
+/* The whole batch in the device layout device.upload_batch / dippm_build_csr_grouped take
+ * (what FeaturizedBatch.collate builds in Python), written straight into the caller's
+ * (typically pinned) buffers; any pointer may be NULL:
+ *   x32       float  [total_nodes, 32]  feature rows rounded to fp32
+ *   src, dst  int64  [total_edges]      edge endpoints as batch-global node ids
+ *   graph_ptr int32  [count + 1]        node offsets; edge_ptr int64 [count + 1] edge offsets
+ *   fs32      float  [count, 5]         log1p static features (fs_log) rounded to fp32
+ * Failed documents contribute no nodes or edges (callers normally reject the batch first). */
+void dippm_feat_collate(const dippm_feat_batch* b, float* x32, int64_t* src, int64_t* dst, int32_t* graph_ptr,
+                        int64_t* edge_ptr, float* fs32);
 /* Per-document metadata in one call (any pointer may be NULL):
  *   status  int32 [count]      (dippm_feat_status codes)
  *   fs_log  double [count, 5]  StaticFeatures.as_vector = log1p of the five integers (featurize.py:76-87)

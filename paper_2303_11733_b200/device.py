@@ -262,7 +262,7 @@ def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=Tr
               dst=h2d(dst), graph_ptr=h2d(graph_ptr), fs=h2d(fs), y=None if y is None else h2d(y),
               h2d_bytes=int(sum(np.asarray(a).nbytes for a in arrays)))
     if edge_ptr is not None:
-        b.edge_ptr = h2d(np.asarray(edge_ptr, np.int64))
+        b.edge_ptr = h2d(edge_ptr if isinstance(edge_ptr, torch.Tensor) else np.asarray(edge_ptr, np.int64))
         b.max_nodes = int(np.diff(np.asarray(graph_ptr)).max())
         b.max_edges = int(np.diff(edge_ptr).max()) if len(edge_ptr) > 1 else 0
         b.h2d_bytes += int(np.asarray(edge_ptr).nbytes)
@@ -416,20 +416,23 @@ class Engine:
     def set_params(self, items, normalizer) -> None:
         """Upload the host model's current values (padded layout) and refresh the operand copies.
         Skipped when the values are bit-identical to the last upload (repeated predict calls)."""
+        items = [(name, np.asarray(arr, np.float64)) for name, arr in items]
+        norm = np.concatenate([np.asarray(normalizer.y_mean, np.float64), np.asarray(normalizer.y_std, np.float64),
+                               np.asarray(normalizer.fs_mean, np.float64), np.asarray(normalizer.fs_std, np.float64)])
+        last = getattr(self, "_uploaded", None)
+        if (last is not None and np.array_equal(last[1], norm) and len(last[0]) == len(items)
+                and all(n0 == n1 and a0.shape == a1.shape and np.array_equal(a0, a1)
+                        for (n0, a0), (n1, a1) in zip(last[0], items))):
+            return
         host = np.zeros(self.L.total, dtype=np.float64)
         for name, arr in items:
             off = self.L.offsets[name]
             padded = self.L.pad(name, arr)
             host[off:off + padded.size] = padded.ravel()
-        norm = np.concatenate([np.asarray(normalizer.y_mean, np.float64), np.asarray(normalizer.y_std, np.float64),
-                               np.asarray(normalizer.fs_mean, np.float64), np.asarray(normalizer.fs_std, np.float64)])
-        last = getattr(self, "_uploaded", None)
-        if last is not None and np.array_equal(last[0], host) and np.array_equal(last[1], norm):
-            return
         self.params.copy_(torch.from_numpy(host), non_blocking=False)
         self.set_normalizer(normalizer)
         self.refresh()
-        self._uploaded = (host, norm)
+        self._uploaded = ([(name, arr.copy()) for name, arr in items], norm)
 
     def set_normalizer(self, norm) -> None:
         self._uploaded = None

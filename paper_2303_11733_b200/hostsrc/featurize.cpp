@@ -13,6 +13,7 @@
 //   multiplicity), infer_shapes :357-499 (Python floor division), the
 //   featurizer featurize.py:106-183 and compute_macs :204-253.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -1041,15 +1042,21 @@ dippm_feat_batch* dippm_featurize_docs(const char* const* docs, const int64_t* l
   b->res.resize(count > 0 ? (size_t)count : 0);
   int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
   nt = (int)std::min<int64_t>(nt, std::max<int64_t>(count, 1));
-  auto work = [&](int t) {
-    for (int64_t i = t; i < count; i += nt)
-      featurize_one(docs[i], lens[i], batch_override ? batch_override[i] : 0, b->res[i]);
+  // dynamic scheduling in small grains: document sizes are heavy-tailed (power-law node
+  // counts) and the host may be shared with other work, so static slices straggle
+  std::atomic<int64_t> next{0};
+  const int64_t grain = 4;
+  auto work = [&] {
+    for (int64_t i0; (i0 = next.fetch_add(grain, std::memory_order_relaxed)) < count;)
+      for (int64_t i = i0; i < std::min(count, i0 + grain); ++i)
+        featurize_one(docs[i], lens[i], batch_override ? batch_override[i] : 0, b->res[i]);
   };
   if (nt <= 1) {
-    work(0);
+    work();
   } else {
     std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t) pool.emplace_back(work, t);
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();  // the calling thread is one of the workers
     for (auto& th : pool) th.join();
   }
   return b;
@@ -1091,14 +1098,45 @@ void dippm_feat_sizes(const dippm_feat_batch* b, int64_t* num_nodes, int64_t* nu
   if (total_edges) *total_edges = te;
 }
 
-void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int64_t* fs_int, float* x32) {
+}  // extern "C"
+
+namespace {
+// node / edge offsets of every document, and a parallel loop over document ranges whose
+// output slices are disjoint
+void doc_offsets(const dippm_feat_batch* b, std::vector<int64_t>& no, std::vector<int64_t>& eo) {
   const size_t G = b->res.size();
-  std::vector<int64_t> no(G + 1, 0), eo(G + 1, 0);
+  no.assign(G + 1, 0);
+  eo.assign(G + 1, 0);
   for (size_t i = 0; i < G; ++i) {
     no[i + 1] = no[i] + b->res[i].n;
     eo[i + 1] = eo[i] + (int64_t)b->res[i].edges.size();
   }
-  auto work = [&](size_t i0, size_t i1) {  // documents [i0, i1): disjoint output slices
+}
+template <class F>
+void parallel_docs(size_t G, F&& work) {  // work(i0, i1) over dynamically claimed document ranges
+  const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<size_t>(G / 64, 1));
+  if (nt <= 1) {
+    work((size_t)0, G);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  const size_t grain = 16;
+  auto loop = [&] {
+    for (size_t i0; (i0 = next.fetch_add(grain, std::memory_order_relaxed)) < G;) work(i0, std::min(G, i0 + grain));
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(loop);
+  loop();
+  for (auto& th : pool) th.join();
+}
+}  // namespace
+
+extern "C" {
+
+void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int64_t* fs_int, float* x32) {
+  std::vector<int64_t> no, eo;
+  doc_offsets(b, no, eo);
+  parallel_docs(b->res.size(), [&](size_t i0, size_t i1) {
     for (size_t i = i0; i < i1; ++i) {
       const Result& r = b->res[i];
       if (x && r.n) memcpy(x + no[i] * 32, r.x.data(), sizeof(double) * 32 * (size_t)r.n);
@@ -1112,15 +1150,31 @@ void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int
       if (fs_int)
         for (int k = 0; k < 5; ++k) fs_int[i * 5 + k] = r.fs[k];
     }
-  };
-  const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<size_t>(G / 64, 1));
-  if (nt <= 1) {
-    work(0, G);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (int t = 0; t < nt; ++t) pool.emplace_back(work, G * t / nt, G * (t + 1) / nt);
-  for (auto& th : pool) th.join();
+  });
+}
+
+void dippm_feat_collate(const dippm_feat_batch* b, float* x32, int64_t* src, int64_t* dst, int32_t* graph_ptr,
+                        int64_t* edge_ptr, float* fs32) {
+  std::vector<int64_t> no, eo;
+  doc_offsets(b, no, eo);
+  const size_t G = b->res.size();
+  if (graph_ptr)
+    for (size_t i = 0; i <= G; ++i) graph_ptr[i] = (int32_t)no[i];
+  if (edge_ptr)
+    for (size_t i = 0; i <= G; ++i) edge_ptr[i] = eo[i];
+  parallel_docs(G, [&](size_t i0, size_t i1) {
+    for (size_t i = i0; i < i1; ++i) {
+      const Result& r = b->res[i];
+      if (x32)
+        for (int64_t k = 0; k < r.n * 32; ++k) x32[no[i] * 32 + k] = (float)r.x[(size_t)k];
+      for (size_t k = 0; k < r.edges.size(); ++k) {
+        if (src) src[eo[i] + (int64_t)k] = no[i] + r.edges[k].first;
+        if (dst) dst[eo[i] + (int64_t)k] = no[i] + r.edges[k].second;
+      }
+      if (fs32)
+        for (int k = 0; k < 5; ++k) fs32[i * 5 + k] = (float)std::log1p((double)r.fs[k]);
+    }
+  });
 }
 
 int64_t dippm_feat_meta(const dippm_feat_batch* b, int32_t* status, double* fs_log, int64_t* name_off, char* names,

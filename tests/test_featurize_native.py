@@ -63,6 +63,14 @@ def test_collate_layout_matches_upload_contract(gf):
         s, d = src[ep[g]:ep[g + 1]], dst[ep[g]:ep[g + 1]]
         assert np.all((s >= gp[g]) & (s < gp[g + 1]) & (d >= gp[g]) & (d < gp[g + 1]))
     assert np.array_equal(x, fb.x.astype(np.float32))
+    # the native collated export (dippm_feat_collate) writes exactly these arrays
+    G, N, E = len(docs), len(x), len(src)
+    nx, ns, nd = np.empty((N, 32), np.float32), np.empty(E, np.int64), np.empty(E, np.int64)
+    ngp, nep, nfs = np.empty(G + 1, np.int32), np.empty(G + 1, np.int64), np.empty((G, 5), np.float32)
+    F._host().dippm_feat_collate(fb._h, nx.ctypes.data, ns.ctypes.data, nd.ctypes.data, ngp.ctypes.data,
+                                 nep.ctypes.data, nfs.ctypes.data)
+    for a, b in ((x, nx), (src, ns), (dst, nd), (gp, ngp), (ep, nep), (fs, nfs)):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
 
 
 class _Node:
@@ -114,3 +122,24 @@ def test_predict_documents_end_to_end_vs_oracle(gf):
         ref = O.predict(params, nd, enc.num_nodes, enc.edges, enc.features, fb.fs_vectors()[i])
         assert np.all(np.abs(y[i] - ref) <= 1e-4 * np.abs(ref) + 1e-3), (i, y[i], ref)
         assert int(mig[i]) == O.mig_code(float(y[i, 1]))
+
+
+@pytest.mark.gpu
+def test_predict_documents_chunked_pipeline_identical():
+    """predict_documents(chunk=k) overlaps featurisation with the device pass; every
+    graph's prediction depends only on its own rows, so chunked and one-pass results agree
+    to fp32 rounding (the readout's 32-row partial sums follow the global row alignment,
+    which moves with the chunk: ulp-level differences), MIG codes equal, names in order."""
+    from paper_2303_11733_b200 import gnn
+    from paper_2303_11733_b200.synth import make_graph_documents
+    docs = make_graph_documents(300, seed=77)
+    fb = F.featurize_documents(docs)
+    norm = gnn.Normalizer.fit(np.abs(np.random.default_rng(1).normal(size=(64, 3))) * [3, 9000, 2] + 1,
+                              fb.fs_vectors())
+    model = gnn.create_model(hidden=128, seed=2, normalizer=norm)
+    for prec in ("bf16", "fp32"):
+        y1, m1, n1 = F.predict_documents(model, docs, precision=prec)
+        y2, m2, n2 = F.predict_documents(model, docs, precision=prec, chunk=64)
+        assert n1 == n2 == fb.names
+        np.testing.assert_allclose(y1, y2, rtol=2e-6, atol=0)
+        np.testing.assert_array_equal(m1, m2)
