@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 2
+#define DIPPM_ABI_VERSION 3
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -273,6 +273,63 @@ int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t num_graph
                     double delta, double grad_den, float* dout, double* loss_out, void* stream);
 /*   grad_den: denominator of dout (<= 0: num_graphs).  Data-parallel training passes the
  *   GLOBAL batch size so the all-reduced sum of per-rank gradients is the global mean. */
+
+/* ---------------------------------------------------------------------------
+ * K5/K6 fused — the whole FC head of one step in ONE cooperative launch (bf16, small
+ * batches: 1 <= G <= dippm_head_fused_max_graphs(), hp % 64 == 0, hp <= 512, u_width a
+ * multiple of 64 <= 576).  Replaces, for those shapes, the fc1/fc2 dippm_gemm calls,
+ * dippm_fc3_forward, dippm_huber, dippm_fc3_backward, dippm_colsum_act and the fc2/fc1
+ * WGRAD / GATE / STORE GEMMs (gnn.py:265-299, numerics.py:58-73):
+ *   always    x2 = drop1(relu(u W1 + b1)), x3 = drop2(relu(x2 W2 + b2)) (bf16 [G, hp]),
+ *             out = x3 W3 + b3 (normalised fp32 [G, 3]); bits (if non-NULL) = x2 > 0,
+ *             word [(c/32)*bits_ld + g]; y_pred / mig / nonfinite as dippm_fc3_forward.
+ *   y_raw     Huber per graph, loss_out = {mean loss, APE sums} as dippm_huber, dout.
+ *   train     d2 = (dout W3^T)[x3 > 0] keep, d1 = (d2 W2^T)[x2 > 0] keep (bf16 + fp32
+ *             copies), gw3/gb3/gw2/gb2/gw1/gb1 (fp32, padded layouts [hp,3], [hp,hp],
+ *             [u_width,hp]) and, if du != NULL, du = d1 W1[:hp]^T (fp32 [G, hp]).
+ * Dropout: mode 0 none, 1 multiply mask1/mask2 ([G, hp] fp32), 2 the counter hash of
+ * dippm_gemm (seed1/seed2, seed_dev mixed in identically), so the draws match that path.
+ * sync: int32[2] zeroed once by the caller; left ready for the next launch.
+ * Every reduction has a fixed order (deterministic). */
+typedef struct dippm_head_args {
+  int64_t G;
+  int32_t hp, u_width;
+  const void* u;                 /* bf16 [G, u_width] */
+  const void* w1;                /* bf16 [u_width, hp] */
+  const void* w2;                /* bf16 [hp, hp] */
+  const float *b1, *b2, *w3, *b3;/* fp32 [hp], [hp], [hp, 3], [3] */
+  void *x2, *x3;                 /* bf16 [G, hp] (written) */
+  uint32_t* bits;                /* word [(c/32)*bits_ld + g], or NULL */
+  int64_t bits_ld;               /* >= G */
+  int32_t drop_mode;
+  double drop_p;
+  float keep_scale;              /* backward gate scale: 1/(1-p) with dropout, else 1 */
+  uint64_t seed1, seed2;
+  const int64_t* seed_dev;
+  const float *mask1, *mask2;
+  float* out;                    /* fp32 [G, 3] */
+  const double* norm;            /* double[16] as dippm_pool_concat */
+  double* y_pred;                /* [G, 3] or NULL */
+  int8_t* mig;
+  int32_t* nonfinite;
+  const float* y_raw;            /* [G, 3] targets or NULL (no loss) */
+  double delta, grad_den;
+  double* loss_out;              /* double[4] */
+  double* row_loss;              /* scratch double [G, 4] */
+  float* dout;                   /* [G, 3] (train) */
+  void *d2, *d1;                 /* bf16 [G, hp] */
+  float *d2f, *d1f;              /* fp32 [G, hp] */
+  float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3;
+  float* du;                     /* fp32 [G, hp] or NULL (MLP: no readout below) */
+  int32_t* sync;
+  int32_t train;
+} dippm_head_args_t;
+int32_t dippm_head_fused_max_graphs(void);
+int32_t dippm_head_fused(const dippm_head_args_t* args, void* stream);
+/* Diagnostics (synchronous): SM clock cycles, relative to kernel start, of CTA 0 of the last
+ * launch: per phase (A, B: slots 1-4 / 5-8; C ends at 9, barrier 10; D 11-14; E 15-18) its
+ * first unit's operands landed, that unit done, its last unit done, the grid barrier opened. */
+int32_t dippm_head_fused_trace(int64_t* out24);
 
 /* ---------------------------------------------------------------------------
  * K8 — bias-corrected Adam (numerics.py:93-114, same op order) on fp64 master

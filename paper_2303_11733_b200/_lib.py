@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 2  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 3  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -53,6 +53,23 @@ class GemmArgs(C.Structure):
 
 
 P, I32, I64, U64, F32, F64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_size_t
+
+
+class HeadArgs(C.Structure):
+    """dippm_head_args_t (the fused FC head, dippm_head_fused)."""
+    _fields_ = [
+        ("G", C.c_int64), ("hp", C.c_int32), ("u_width", C.c_int32),
+        ("u", P), ("w1", P), ("w2", P), ("b1", P), ("b2", P), ("w3", P), ("b3", P),
+        ("x2", P), ("x3", P), ("bits", P), ("bits_ld", C.c_int64),
+        ("drop_mode", C.c_int32), ("drop_p", C.c_double), ("keep_scale", C.c_float),
+        ("seed1", C.c_uint64), ("seed2", C.c_uint64), ("seed_dev", P), ("mask1", P), ("mask2", P),
+        ("out", P), ("norm", P), ("y_pred", P), ("mig", P), ("nonfinite", P),
+        ("y_raw", P), ("delta", C.c_double), ("grad_den", C.c_double), ("loss_out", P), ("row_loss", P),
+        ("dout", P), ("d2", P), ("d1", P), ("d2f", P), ("d1f", P),
+        ("gw1", P), ("gb1", P), ("gw2", P), ("gb2", P), ("gw3", P), ("gb3", P), ("du", P),
+        ("sync", P), ("train", C.c_int32),
+    ]
+
 
 class PackSeg(C.Structure):
     """dippm_pack_seg_t: one fp64-master -> compute-copy segment refreshed by dippm_adam_pack."""
@@ -93,6 +110,9 @@ SIGNATURES = {
     "dippm_pool_combine": (I32, [P, P, P, I64, I32, P, P, Act, P]),
     "dippm_fc3_forward": (I32, [Act, I64, I32, P, P, P, P, P, P, P, P]),
     "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
+    "dippm_head_fused_max_graphs": (I32, []),
+    "dippm_head_fused": (I32, [C.POINTER(HeadArgs), P]),
+    "dippm_head_fused_trace": (I32, [P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),
     "dippm_huber": (I32, [P, P, I64, P, F64, F64, P, P, P]),
     "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, P, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),

@@ -25,6 +25,8 @@ Node rows of a graph are contiguous (graph_ptr), edges carry global ids.
 
 from __future__ import annotations
 
+import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -37,6 +39,9 @@ from .errors import EmptyGraph, ShapeMismatch
 FEATURE_WIDTH = 32   # featurize.py:38
 STATIC_WIDTH = 5     # featurize.py:39
 PRECISIONS = {"fp32": DT_TF32X3, "bf16": DT_BF16}
+# the whole FC head in one cooperative launch (head_fused.cu) for bf16 batches of up to
+# dippm_head_fused_max_graphs() graphs; DIPPM_FUSED_HEAD=0 keeps the per-op launches
+FUSED_HEAD = os.environ.get("DIPPM_FUSED_HEAD", "1") != "0"
 BACKENDS = {"tc": 0, "simt": 1}
 
 
@@ -345,12 +350,16 @@ class Workspace:
         self.mig = torch.empty(G, dtype=torch.int8, device=dev)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.loss = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.row_loss = torch.empty(G, 4, dtype=torch.float64, device=dev)   # fused head: per-graph loss terms
+        self.head_sync = torch.zeros(2, dtype=torch.int32, device=dev)        # fused head: grid barrier
+        self.head_pending = None  # forward(defer_head=True) -> loss() -> backward() runs the fused head once
         self.train = train
         if train:
             self.dout = torch.empty(G, 3, **f32)
             self.d2 = ActBuf(G, hp, dt, dev)
             self.d1 = ActBuf(G, hp, dt, dev)
             self.head_bits = torch.empty(hp // 32, G, dtype=torch.int32, device=dev)
+            self.dhead_f32 = torch.empty(2, G, hp, **f32)  # fused head: fp32 d2, d1 (bias-gradient sums)
             if sage:
                 self.du = torch.empty(G, hp, **f32)
                 self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
@@ -411,6 +420,8 @@ class Engine:
         self.launches = 0
         self.cta_pair = 0       # GEMM tile policy passed to the library: 0 auto, 1 single-CTA, 2 CTA pair
         self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
+        self.fused_head = True  # FUSED_HEAD and this flag gate the fused head kernel
+        self.head_fused_max = int(_lib.load().dippm_head_fused_max_graphs())
 
     # -- parameters -----------------------------------------------------------
     def set_params(self, items, normalizer) -> None:
@@ -505,15 +516,24 @@ class Engine:
         self._gemm(GEMM_WGRAD, width, hp, rows, x, 1, dz, 1, out=Act(self._g32(out_name), hp, 0, DT_F32),
                    c=_p(ws.splitk), ldc=hp, splits=splits, tile_sync=_p(ws.tile_sync), out_scale=1.0)
 
+    def fused_head_ok(self, G: int) -> bool:
+        """The fused head kernel covers this batch (bf16 tensor-core path, small batch)."""
+        return (FUSED_HEAD and self.fused_head and self.backend == 0 and self.dtype == DT_BF16
+                and self.L.hp <= 512 and self.L.u_width <= 576 and G <= self.head_fused_max)
+
     def forward(self, b: Batch, ws: Workspace, mask_mode: int = 0, dropout_p: float = 0.0, seed: int = 0,
-                predict: bool = True) -> None:
+                predict: bool = True, defer_head: bool = False) -> None:
         """Eval (mask_mode 0) or train-mode forward (1: masks in ws.masks, 2: generated):
-        K2 aggregation -> K3 GEMM x3, K4 pooling, K5 head (2 GEMMs + fc3)."""
+        K2 aggregation -> K3 GEMM x3, K4 pooling, K5 head (2 GEMMs + fc3).
+
+        defer_head (training steps: forward -> loss -> backward): when the fused head kernel
+        covers the batch, the head is not run here; loss() records its arguments and backward()
+        runs forward, loss and backward of the head in one launch."""
         s, L, hp = _stream(), self.L, self.L.hp
         if self.arch == "mlp":  # MlpModel.forward_norm (gnn.py:253-255): the head on [fs_norm | 0]
             _lib.call("dippm_fs_normalize", _p(b.fs), b.G, _p(self.norm), ws.u.view(), L.u_width, s)
             self.launches += 1
-            self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
+            self._head_or_defer(b, ws, mask_mode, dropout_p, seed, predict, defer_head)
             return
         _lib.call("dippm_sage_aggregate", f32_act(b.x), ws.A[0].view(FEATURE_WIDTH), ws.A[0].view(0), b.N,
                   FEATURE_WIDTH, _p(b.rowptr), _p(b.col), _p(b.inv_deg), s)
@@ -536,12 +556,60 @@ class Engine:
             _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
                       ws.u.view(), s)
         self.launches += 3 + 1
+        self._head_or_defer(b, ws, mask_mode, dropout_p, seed, predict, defer_head)
+
+    def _head_or_defer(self, b, ws, mask_mode, dropout_p, seed, predict, defer_head) -> None:
+        if defer_head and ws.train and not predict and self.fused_head_ok(b.G):
+            ws.head_pending = dict(mask_mode=mask_mode, dropout_p=dropout_p, seed=seed)
+            return
+        ws.head_pending = None
         self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
+
+    def _head_fused(self, b: Batch, ws: Workspace, mask_mode: int, dropout_p: float, seed: int, predict: bool,
+                    loss=None, keep_scale: float = 1.0) -> None:
+        """K5/K6 in one cooperative launch (head_fused.cu): forward, and with loss = (delta,
+        grad_den) the Huber loss and, on a training workspace, the whole head backward."""
+        L, hp = self.L, self.L.hp
+        drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
+        train = loss is not None and ws.train
+        if predict:
+            ws.nonfinite.zero_()
+        a = _lib.HeadArgs()
+        a.G, a.hp, a.u_width = b.G, hp, L.u_width
+        a.u, a.w1, a.w2 = _p(ws.u.t), _p(self.W1h.t), _p(self.W2h.t)
+        a.b1, a.b2, a.w3, a.b3 = self._f32("fc1.b"), self._f32("fc2.b"), self._f32("fc3.w"), self._f32("fc3.b")
+        a.x2, a.x3 = _p(ws.x2.t), _p(ws.x3.t)
+        if ws.train:
+            a.bits, a.bits_ld = _p(ws.head_bits), ws.G
+        a.drop_mode, a.drop_p, a.keep_scale = drop, float(dropout_p), float(keep_scale)
+        a.seed1, a.seed2 = (int(seed) * 2) & (2**64 - 1), (int(seed) * 2 + 1) & (2**64 - 1)  # dippm_gemm's seeds
+        a.seed_dev = _p(self.t_dev) if drop == 2 else None
+        if drop == 1:
+            a.mask1, a.mask2 = _p(ws.masks[0]), _p(ws.masks[1])
+        a.out, a.norm = _p(ws.out), _p(self.norm)
+        if predict:
+            a.y_pred, a.mig, a.nonfinite = _p(ws.y_pred), _p(ws.mig), _p(ws.nonfinite)
+        if loss is not None:
+            a.y_raw, a.delta, a.grad_den = _p(b.y), float(loss[0]), float(loss[1])
+            a.loss_out, a.row_loss = _p(ws.loss), _p(ws.row_loss)
+        if train:
+            a.dout, a.d2, a.d1 = _p(ws.dout), _p(ws.d2.t), _p(ws.d1.t)
+            a.d2f, a.d1f = _p(ws.dhead_f32[0]), _p(ws.dhead_f32[1])
+            a.gw1, a.gb1, a.gw2, a.gb2 = self._g32("fc1.w"), self._g32("fc1.b"), self._g32("fc2.w"), self._g32("fc2.b")
+            a.gw3, a.gb3 = self._g32("fc3.w"), self._g32("fc3.b")
+            a.du = _p(ws.du) if self.arch == "sage" else None
+            a.train = 1
+        a.sync = _p(ws.head_sync)
+        _lib.call("dippm_head_fused", C.byref(a), _stream())
+        self.launches += 1
 
     def _head_forward(self, b: Batch, ws: Workspace, mask_mode: int, dropout_p: float, seed: int,
                       predict: bool) -> None:
         """K5: fc1/fc2 tcgen05 GEMMs (bias, ReLU, dropout epilogue) + fc3/de-normalise/MIG (gnn.py:265-284)."""
         s, hp = _stream(), self.L.hp
+        if self.fused_head_ok(b.G):
+            self._head_fused(b, ws, mask_mode, dropout_p, seed, predict)
+            return
         if predict:
             ws.nonfinite.zero_()  # workspaces are reused across calls
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
@@ -560,6 +628,9 @@ class Engine:
 
     def loss(self, b: Batch, ws: Workspace, delta: float = 1.0, grad_den: float = 0.0) -> None:
         """Huber loss + dout (numerics.py:58-73); grad_den = global batch size under DP (0: this batch)."""
+        if ws.head_pending is not None:  # deferred fused head: runs in backward()
+            ws.head_pending.update(delta=float(delta), grad_den=float(grad_den))
+            return
         _lib.call("dippm_huber", _p(ws.out), _p(b.y), b.G, _p(self.norm), float(delta), float(grad_den),
                   _p(ws.dout) if ws.train else None, _p(ws.loss), _stream())
         self.launches += 1
@@ -568,17 +639,26 @@ class Engine:
         """Head backward (fc3 fused kernel, fc2/fc1 tcgen05 WGRAD/GATE/STORE), readout
         backward, then per SAGE layer: agg^T + bias, WGRAD, gated dgrad GEMM."""
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
-        _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout), float(keep_scale),
-                  self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
-        self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
-        self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
-                   gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=ws.G)
-        _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
-        self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
-        if self.arch == "mlp":  # no graph network below the head
-            self.launches += 2
-            return
-        self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
+        pend, ws.head_pending = ws.head_pending, None
+        if pend is not None:  # the deferred head: forward + loss + backward in one launch
+            if "delta" not in pend:
+                raise RuntimeError("forward(defer_head=True) needs loss() before backward()")
+            self._head_fused(b, ws, pend["mask_mode"], pend["dropout_p"], pend["seed"], False,
+                             loss=(pend["delta"], pend["grad_den"]), keep_scale=keep_scale)
+            if self.arch == "mlp":
+                return
+        else:
+            _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout),
+                      float(keep_scale), self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
+            self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
+            self._gemm(GEMM_GATE, b.G, hp, hp, ws.d2.view(), 0, self.W2h.view(), 0, out=ws.d1.view(),
+                       gate=ws.x2.view(), gate_scale=keep_scale, gate_bits=_p(ws.head_bits), bits_ld=ws.G)
+            _lib.call("dippm_colsum_act", ws.d1.view(), b.G, hp, self._g32("fc1.b"), s)
+            self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
+            if self.arch == "mlp":  # no graph network below the head
+                self.launches += 2
+                return
+            self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
         cur = 0
         for i in (2, 1, 0):
             B = ws.B[cur]

@@ -110,7 +110,7 @@ class BatchTrainer:
         build_batch_csr(b)
         mode = 2 if self.dropout_p > 0 else 0
         eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 131 + self.rank,
-                    predict=False)
+                    predict=False, defer_head=True)
         den = 0.0
         if self.allreduce is not None:
             den = float(global_graphs if global_graphs else b.G * self.world_size)
