@@ -46,7 +46,9 @@ BACKENDS = {"tc": 0, "simt": 1}
 
 
 def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    # the raw cudaStream_t of the current stream: a direct C call (torch.cuda.current_stream()
+    # re-validates the device through Python on every call, ~15 us, and a step makes ~20 calls)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def require_device(device=None) -> torch.device:
