@@ -130,6 +130,17 @@ __global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, doub
                                                     double gscale, int64_t n, double lr, double b1, double b2,
                                                     double eps, double bc1, double bc2, const int64_t* t_dev,
                                                     int do_adam, float* __restrict__ p32, PackSegs segs) {
+  const int64_t n4 = n >> 2;
+  // warm this thread's first group in L1 while thread 0 evaluates the bias corrections
+  const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q0 < n4) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p + (q0 << 2)));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(g + (q0 << 2)));
+    if (do_adam) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(m + (q0 << 2)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(v + (q0 << 2)));
+    }
+  }
   if (t_dev && do_adam) {
     __shared__ double s_bc[2];
     if (threadIdx.x == 0) {
@@ -142,7 +153,6 @@ __global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, doub
     bc2 = s_bc[1];
   }
   const double inv_bc1 = 1.0 / bc1, inv_bc2 = 1.0 / bc2;
-  const int64_t n4 = n >> 2;
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {  // the < 4 trailing parameters (no packing segments there)
     const int64_t i = (n4 << 2) + threadIdx.x;
     double val = p[i];
@@ -213,8 +223,10 @@ __global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, doub
     for (int k = 0; k < segs.n; ++k) {
       const auto& sg = segs.s[k];
       const int64_t j = i - sg.src_off;
-      if (j < 0 || j >= sg.rows * sg.cols) continue;
-      const int64_t r = j / sg.cols, c = sg.dst_col_off + j % sg.cols;
+      if ((uint64_t)j >= (uint64_t)(sg.rows * sg.cols)) continue;
+      // segments hold one weight matrix (< 2^31 elements): 32-bit index arithmetic
+      const uint32_t j32 = (uint32_t)j, cols = (uint32_t)sg.cols;
+      const int64_t r = j32 / cols, c = sg.dst_col_off + j32 % cols;
       if constexpr (DT == DIPPM_DT_BF16) {
         __nv_bfloat162 h[2] = {__floats2bfloat162_rn(f[0], f[1]), __floats2bfloat162_rn(f[2], f[3])};
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sg.dst.base) + r * sg.dst.ld + c) =
