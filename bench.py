@@ -572,9 +572,11 @@ def main():
     timer = GemmTimer()
     eng.gemm_hook = timer
     trainer.use_graphs = False  # per-GEMM events need eager launches
+    overlap, eng.overlap_wgrad = eng.overlap_wgrad, False  # each GEMM timed alone on one stream
     for i in range(args.steps):
         step(args.warmup + args.steps + i)
     eng.gemm_hook = None
+    eng.overlap_wgrad = overlap
     g_flops, g_ms, g_n = timer.summary()
     pk, pk_src = peaks()
     peak_tf = pk["bf16_tflops_sustained"] if args.dtype == "bf16" else pk["bf16_tflops_sustained"] / 6.0

@@ -364,7 +364,9 @@ class Workspace:
             self.dhead_f32 = torch.empty(2, G, hp, **f32)  # fused head: fp32 d2, d1 (bias-gradient sums)
             if sage:
                 self.du = torch.empty(G, hp, **f32)
-                self.B = [ActBuf(N, 2 * hp, dt, dev), ActBuf(N, 2 * hp, dt, dev)]
+                # one [dz_l | agg^T dz_l] buffer per layer: the weight-gradient GEMM of layer l may
+                # still read B_l on the side stream while the dgrad chain fills B_{l-1}
+                self.B = [ActBuf(N, 2 * hp, dt, dev) for _ in range(3)]
                 # 1-bit ReLU' masks of h1, h2 (and of the head's x2, dropout included) written by the
                 # forward GEMM epilogues and read by the GATE epilogues (replaces re-reading activations)
                 # chunk-major [3, Hp/32, N]: word (c/32, r); a warp's 32 rows store/load 128 contiguous bytes
@@ -423,6 +425,11 @@ class Engine:
         self.cta_pair = 0       # GEMM tile policy passed to the library: 0 auto, 1 single-CTA, 2 CTA pair
         self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
         self.fused_head = True  # FUSED_HEAD and this flag gate the fused head kernel
+        # backward: the weight-gradient GEMMs run on a side stream, off the dgrad critical path
+        # (readout -> GATE_3 -> agg^T_2 -> GATE_2 -> WGRAD_1), so they fill the tail waves and
+        # memory-bound gaps of that chain; the step joins the side stream before Adam
+        self.overlap_wgrad = os.environ.get("DIPPM_OVERLAP_WGRAD", "1") != "0"
+        self._side = None
         self.head_fused_max = int(_lib.load().dippm_head_fused_max_graphs())
 
     # -- parameters -----------------------------------------------------------
@@ -661,12 +668,29 @@ class Engine:
                 self.launches += 2
                 return
             self._gemm(GEMM_STORE, b.G, hp, hp, ws.d1.view(), 0, self.W1h.view(), 0, c=_p(ws.du), ldc=hp)
-        cur = 0
+        side = None
+        if self.overlap_wgrad and on_partial is None and self.backend == 0:
+            if self._side is None:
+                self._side = torch.cuda.Stream(self.device)
+            side = self._side
+        main = torch.cuda.current_stream()
+
+        def wgrad(B, i):
+            width = 2 * L.d_in[i] + (1 if i == 0 else 0)  # layer 1: + the ones row (bias gradient)
+            if side is None:
+                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self")
+                return
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self")
+
         for i in (2, 1, 0):
-            B = ws.B[cur]
+            B = ws.B[i]
             bias = self._g32(f"sage{i + 1}.bias")  # gnn.py:230, reduced inside the kernel
             if i == 0:  # layer 1: the bias gradient comes out of the WGRAD GEMM (ones column of A1)
-                self._wgrad(B.view(0), ws.A[0].view(0), N, 2 * L.d_in[0] + 1, ws, "sage1.w_self")
+                wgrad(B, 0)
                 continue
             if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
@@ -676,12 +700,14 @@ class Engine:
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
                           _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)
-            self._wgrad(B.view(0), ws.A[i].view(0), N, 2 * L.d_in[i], ws, f"sage{i + 1}.w_self")
-            if i > 0:
-                self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
-                           out=ws.B[1 - cur].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
-                           gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=ws.N)
-                cur = 1 - cur
+            wgrad(B, i)
+            self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
+                       out=ws.B[i - 1].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
+                       gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=ws.N)
             if i == 2 and on_partial is not None:  # sage3 + head gradients are final here
                 on_partial(L.offsets["sage3.w_self"])
+        if side is not None:  # join: Adam reads every gradient
+            ev = torch.cuda.Event()
+            ev.record(side)
+            main.wait_event(ev)
         self.launches += 5 + 3 * 2 - 3 - 1
