@@ -67,13 +67,42 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
     const int64_t row = r0 + lr;
     const int b = s_ptr[lr], e = s_ptr[lr + 1];
     float acc[CPL][8] = {};
-    for (int j = b; j < e; ++j) {
-      float x[CPL][8];
-      load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
+    float xs[CPL][8];
+    if constexpr (DTI == DIPPM_DT_F32) {
+      // layer 1: the row's own features (copied next to the mean) and its first two neighbours
+      // are loaded before any of them is used, one memory latency per row for the common
+      // in-degrees; pairs are summed in CSR order
+      if (self_out.base) load_chunks<DTI, CPL>(h, row, c0, stride, xs);
+      int j = b;
+      for (; j + 1 < e; j += 2) {
+        float x0[CPL][8], x1[CPL][8];
+        load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x0);
+        load_chunks<DTI, CPL>(h, staged ? s_col[j + 1] : col[cbeg + j + 1], c0, stride, x1);
 #pragma unroll
-      for (int q = 0; q < CPL; ++q)
+        for (int q = 0; q < CPL; ++q)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
+          for (int k = 0; k < 8; ++k) {
+            acc[q][k] += x0[q][k];
+            acc[q][k] += x1[q][k];
+          }
+      }
+      if (j < e) {
+        float x[CPL][8];
+        load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
+      }
+    } else {  // the 512-wide layers measured fastest one neighbour at a time
+      for (int j = b; j < e; ++j) {
+        float x[CPL][8];
+        load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
+      }
     }
     const float w = s_w[lr];
 #pragma unroll
@@ -83,10 +112,9 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
       act_store8_t<DTO>(m, row, c0 + q * stride, acc[q]);
     }
     if (self_out.base) {
-      float x[CPL][8];
-      load_chunks<DTI, CPL>(h, row, c0, stride, x);
+      if constexpr (DTI != DIPPM_DT_F32) load_chunks<DTI, CPL>(h, row, c0, stride, xs);
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) act_store8_t<DTO>(self_out, row, c0 + q * stride, x[q]);
+      for (int q = 0; q < CPL; ++q) act_store8_t<DTO>(self_out, row, c0 + q * stride, xs[q]);
     }
   }
 }
