@@ -30,6 +30,10 @@ __host__ __device__ inline int colsum_groups(int nblk) { return (nblk + kColsumG
 // flight.  A warp covers one row when width/8 >= 32 (hidden 512: 2 chunks per
 // lane), or 32/L rows for narrow layers (layer 1, width 32).
 constexpr int kRowsPerBlock = 64;
+// agg^T / readout kernels with the fused bias reduction: up to this many rows per block, so
+// the grid is one wave of resident blocks (their per-block barrier / fold tail is amortised
+// over more rows per warp)
+constexpr int kRowsPerBlockT = 256;
 
 template <int DT, int CPL>
 __device__ __forceinline__ void load_chunks(const ActView& a, int64_t r, int c0, int stride, float (&x)[CPL][8]) {
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
                                                                 float* __restrict__ colsum_partial, ReadoutArgs ro,
                                                                 float* __restrict__ bias_out, int* __restrict__ sync) {
   extern __shared__ float s_part[];  // [8 warps * gpw][width]
-  __shared__ int s_ptr[kRowsPerBlock + 1];
+  __shared__ int s_ptr[kRowsPerBlockT + 1];
   __shared__ int s_col[kAggColCap];
   __shared__ float s_cw[kAggColCap];
   const int L = (width >> 3) / CPL;
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
   const int cbeg = t_rowptr[r0];
   const int ncol = t_rowptr[r0 + nrows] - cbeg;
   const bool staged = ncol <= kAggColCap;
-  __shared__ int s_g[kRowsPerBlock];  // readout: graph of each row of the block
+  __shared__ int s_g[kRowsPerBlockT];  // readout: graph of each row of the block
   if (write_agg) {
     for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
     if (staged)
@@ -366,10 +370,10 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
                                                                      float* __restrict__ bias_out,
                                                                      int* __restrict__ sync) {
   extern __shared__ float s_part[];  // [8 warps][width]
-  __shared__ int s_ptr[kRowsPerBlock + 1];
+  __shared__ int s_ptr[kRowsPerBlockT + 1];
   __shared__ int s_col[kAggColCap];
   __shared__ float s_cw[kAggColCap];
-  __shared__ int s_g[kRowsPerBlock];
+  __shared__ int s_g[kRowsPerBlockT];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * rpb;
   const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
@@ -632,6 +636,12 @@ extern "C" {
 // Rows per block chosen so the grid is a whole number of waves (the kernels are latency bound
 // and a short last wave left ~30 % of the SMs idle): waves = ceil(N / (64 * P)) with P the
 // resident blocks on the GPU, rows = ceil(N / (waves * P)) <= 64.
+// one wave of resident blocks when the rows fit (<= kRowsPerBlockT per block), else whole waves
+static int wave_rows_t(int64_t N, int blocks_per_sm) {
+  const int64_t P = (int64_t)num_sms() * std::max(1, blocks_per_sm);
+  const int64_t waves = std::max<int64_t>(1, (N + kRowsPerBlockT * P - 1) / (kRowsPerBlockT * P));
+  return (int)std::max<int64_t>(1, (N + waves * P - 1) / (waves * P));
+}
 static int wave_rows(int64_t N, int blocks_per_sm) {
   const int64_t P = (int64_t)num_sms() * std::max(1, blocks_per_sm);
   const int64_t waves = std::max<int64_t>(1, (N + kRowsPerBlock * P - 1) / (kRowsPerBlock * P));
@@ -704,7 +714,7 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
   DIPPM_ARG_CHECK(!bias_out || width / 4 <= kAggThreads, "sage_aggregate_t: fused bias reduce needs width <= %d",
                   4 * kAggThreads);
   if (bias_out) smem = std::max(smem, (size_t)kAggThreads * 4 * sizeof(double));  // fold scratch
-  int rpb = bias_out ? wave_rows(N, readout ? 2 : 3) : kRowsPerBlock;  // caller-reduced partials: fixed blocks
+  int rpb = bias_out ? wave_rows_t(N, readout ? 2 : 3) : kRowsPerBlock;  // caller-reduced partials: fixed blocks
   if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;           // partial rows are sized for this bound
   const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
@@ -736,7 +746,7 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
                   width);
   DIPPM_ARG_CHECK(!bias_out || sync, "readout_aggregate_t: bias_grad needs the sync counters");
   const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double));
-  int rpb = bias_out ? wave_rows(N, 3) : kRowsPerBlock;
+  int rpb = bias_out ? wave_rows_t(N, 3) : kRowsPerBlock;
   if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
   const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
