@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
                                                               int rpb, int width, const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
                                                               const float* __restrict__ inv_deg) {
-  __shared__ int s_ptr[kRowsPerBlock + 1];
-  __shared__ float s_w[kRowsPerBlock];
+  __shared__ int s_ptr[kRowsPerBlockT + 1];
+  __shared__ float s_w[kRowsPerBlockT];
   __shared__ int s_col[kAggColCap];
   const int L = (width >> 3) / CPL;  // lanes per row
   const int gpw = 32 / L;
@@ -678,7 +678,7 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
                   "sage_aggregate: unsupported width %d", width);
   DIPPM_ARG_CHECK(!self_out.data || self_out.dtype == m_out.dtype, "sage_aggregate: self_out dtype");
   cudaStream_t s = (cudaStream_t)stream;
-  const int rpb = wave_rows(N, 4);
+  const int rpb = wave_rows_t(N, 4);
   const int grid = ceil_div_i(N, rpb);
   ActView hv = make_view(h), mv = make_view(m_out), sv = make_view(self_out);
 #define DIPPM_AGG(DI, DO, C) \
