@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict_
       if (s < 0 || s >= ng || d < 0 || d >= ng) {
         atomicExch(bad, 1);
       } else {
-        key = (int)d * ng + (int)s;
+        key = ((int)d << 16) | (int)s;  // (dst, src), ng < 2^15 (checked by the launcher)
         atomicAdd(&cnt[d], 1);
       }
     }
@@ -441,36 +441,49 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict_
   const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
   const int64_t e0 = edge_ptr[g];
   const int U = uniq[g], off = coff[g];
-  int upad = 1;
-  while (upad < U) upad <<= 1;
-  int* keys = sm;             // [upad]
-  int* cnt = sm + epad_max;   // [ng + 1]
+  const int* keys = scratch + e0;  // sorted distinct (dst, src) keys
+  int* cnt = sm;                   // [ng + 1]
   for (int v = threadIdx.x; v <= ng; v += blockDim.x) cnt[v] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < U; i += blockDim.x) {
-    const int k = scratch[e0 + i];
-    col[off + i] = n0 + k % ng;       // src, ascending within the dst row
-    atomicAdd(&cnt[k / ng], 1);
-    keys[i] = (k % ng) * ng + k / ng;  // transposed key (src, dst)
+    const int k = keys[i];
+    col[off + i] = n0 + (k & 0xFFFF);  // src, ascending within the dst row
+    atomicAdd(&cnt[k >> 16], 1);
   }
-  for (int i = U + threadIdx.x; i < upad; i += blockDim.x) keys[i] = INT_MAX;
   __syncthreads();
   block_scan_smem(cnt, ng, s_tmp);
   for (int v = threadIdx.x; v < ng; v += blockDim.x) rowptr[n0 + v] = off + cnt[v];
   if (g == G - 1 && threadIdx.x == 0) rowptr[N] = off + U;
   __syncthreads();
-  bitonic_sort_smem(keys, upad);
+  // transposed pattern by a stable counting sort on src (no re-sort): counts, scan, then one
+  // warp walks the keys in (dst, src) order and places each at its src row's running offset,
+  // lanes with the same src ranked by lane order (__match_any_sync), so every src row lists
+  // its dsts in ascending order -- the order a (src, dst) sort gives
   for (int v = threadIdx.x; v <= ng; v += blockDim.x) cnt[v] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < U; i += blockDim.x) {
-    const int k = keys[i];
-    t_col[off + i] = n0 + k % ng;     // dst, ascending within the src row
-    atomicAdd(&cnt[k / ng], 1);
-  }
+  for (int i = threadIdx.x; i < U; i += blockDim.x) atomicAdd(&cnt[keys[i] & 0xFFFF], 1);
   __syncthreads();
   block_scan_smem(cnt, ng, s_tmp);
   for (int v = threadIdx.x; v < ng; v += blockDim.x) t_rowptr[n0 + v] = off + cnt[v];
   if (g == G - 1 && threadIdx.x == 0) t_rowptr[N] = off + U;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int base = 0; base < U; base += 32) {
+      const int i = base + lane;
+      const int k = i < U ? keys[i] : 0;
+      const int sv = i < U ? (k & 0xFFFF) : -1 - lane;  // inactive lanes match nobody
+      const unsigned grp = __match_any_sync(0xffffffffu, sv);
+      const int rank = __popc(grp & ((1u << lane) - 1u));
+      const int start = i < U ? cnt[sv] : 0;
+      __syncwarp();
+      if (i < U) {
+        t_col[off + start + rank] = n0 + (k >> 16);  // dst, ascending within the src row
+        if (lane == 31 - __clz(grp)) cnt[sv] = start + __popc(grp);  // the group's last lane advances it
+      }
+      __syncwarp();
+    }
+  }
 }
 
 }  // namespace dippm
@@ -493,7 +506,7 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
   while (epad < max_edges_per_graph) epad <<= 1;
   const int64_t nmax = std::max<int64_t>(max_nodes_per_graph + 1, epad);
   const size_t smem = (size_t)(epad + nmax) * sizeof(int);
-  DIPPM_ARG_CHECK(smem <= 200 * 1024 && epad / kGThreads <= 32,
+  DIPPM_ARG_CHECK(smem <= 200 * 1024 && epad / kGThreads <= 32 && max_nodes_per_graph < 32768,
                   "build_csr_grouped: graph too large for the per-graph path (%d nodes, %d edges)",
                   max_nodes_per_graph, max_edges_per_graph);
   cudaStream_t s = (cudaStream_t)stream;
