@@ -597,7 +597,16 @@ __global__ void __launch_bounds__(256) k_pool_combine(const float* __restrict__ 
       t = whole[(int64_t)g * width + c];
     } else {
       t = part[((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c];
-      for (int b = bf + 1; b < bl; ++b) t += part[(int64_t)b * 2 * width + c];
+      int b = bf + 1;
+      for (; b + 4 <= bl; b += 4) {  // 4 loads in flight, added in block order
+        const float v0 = part[(int64_t)b * 2 * width + c], v1 = part[(int64_t)(b + 1) * 2 * width + c];
+        const float v2 = part[(int64_t)(b + 2) * 2 * width + c], v3 = part[(int64_t)(b + 3) * 2 * width + c];
+        t += v0;
+        t += v1;
+        t += v2;
+        t += v3;
+      }
+      for (; b < bl; ++b) t += part[(int64_t)b * 2 * width + c];
       t += part[(int64_t)bl * 2 * width + c];
     }
     act_store(u, g, c, (float)(t * inv_n));
