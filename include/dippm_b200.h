@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 3
+#define DIPPM_ABI_VERSION 4
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -89,13 +89,14 @@ size_t dippm_csr_workspace_bytes(int64_t num_nodes, int64_t num_edges);
  * graphs — graph_ptr [G+1] over nodes, edge_ptr [G+1] over edges (int64), every
  * edge inside its own graph (else *bad_edge = 1).  One CTA per graph builds its
  * CSR in shared memory (3 launches per batch).  Limits: G <= 8192, per-graph
- * padded edge count <= 16384; callers fall back to dippm_build_csr beyond. */
+ * padded edge count <= 16384; callers fall back to dippm_build_csr beyond.
+ * node_graph (nullable): also writes the node -> graph map (dippm_node_graph) in the same pass. */
 size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t num_edges);
 int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
                                 const int64_t* edge_ptr, int64_t num_graphs, int64_t num_nodes, int64_t num_edges,
                                 int32_t max_nodes_per_graph, int32_t max_edges_per_graph,
                                 int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,
-                                int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge,
+                                int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge, int32_t* node_graph,
                                 void* workspace, size_t workspace_bytes, void* stream);
 int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64_t num_edges, int64_t num_nodes,
                         int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict_
                                                       const int32_t* __restrict__ graph_ptr,
                                                       const int64_t* __restrict__ edge_ptr, int epad_max,
                                                       int32_t* deg, float* inv_deg, int32_t* scratch, int32_t* uniq,
-                                                      int32_t* bad) {
+                                                      int32_t* bad, int32_t* node_graph) {
   extern __shared__ int sm[];
   __shared__ int s_tmp[33];
   const int g = blockIdx.x;
@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict_
   __syncthreads();
   for (int v = threadIdx.x; v < ng; v += blockDim.x) {
     const int d = cnt[v];
+    if (node_graph) node_graph[n0 + v] = g;
     deg[n0 + v] = d;
     inv_deg[n0 + v] = d > 0 ? 1.0f / (float)d : 0.0f;  // gnn.py:136 (zero row when isolated)
   }
@@ -496,8 +497,8 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
                                            const int64_t* edge_ptr, int64_t G, int64_t N, int64_t E,
                                            int32_t max_nodes_per_graph, int32_t max_edges_per_graph,
                                            int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,
-                                           int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge, void* workspace,
-                                           size_t workspace_bytes, void* stream) {
+                                           int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge, int32_t* node_graph,
+                                           void* workspace, size_t workspace_bytes, void* stream) {
   using namespace dippm;
   DIPPM_ARG_CHECK(G >= 1 && N >= 1 && E >= 0, "build_csr_grouped: bad sizes");
   DIPPM_ARG_CHECK(G <= 8192, "build_csr_grouped: %lld graphs per batch (max 8192)", (long long)G);
@@ -521,7 +522,7 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
   }
   DIPPM_CUDA_CHECK(cudaMemsetAsync(bad_edge, 0, sizeof(int), s));
   k_csr_g1<<<(unsigned)G, kGThreads, smem, s>>>(src, dst, graph_ptr, edge_ptr, epad, deg, inv_deg, scratch, uniq,
-                                                bad_edge);
+                                                bad_edge, node_graph);
   k_scan_small<<<1, 1024, (size_t)G * sizeof(int), s>>>(uniq, (int)G, coff);
   k_csr_g3<<<(unsigned)G, kGThreads, smem, s>>>(graph_ptr, edge_ptr, scratch, uniq, coff, epad, N, (int)G, rowptr,
                                                 col, t_rowptr, t_col);

@@ -298,18 +298,18 @@ def build_batch_csr(b: Batch, grouped: bool | None = None) -> Batch:
     b.t_col = torch.empty(max(E, 1), **i32)
     b.bad = torch.empty(1, **i32)
     b.node_graph = torch.empty(max(N, 1), **i32)
-    _lib.call("dippm_node_graph", _p(b.graph_ptr), b.G, _p(b.node_graph), _stream())
     lib = _lib.load()
     if grouped is None:
         grouped = (b.edge_ptr is not None and b.G <= GROUPED_MAX_GRAPHS and b.max_edges <= GROUPED_MAX_EDGES
                    and b.max_nodes <= GROUPED_MAX_EDGES)
-    if grouped:
+    if grouped:  # the per-graph kernels also write node -> graph
         ws_bytes = lib.dippm_csr_grouped_workspace_bytes(b.G, E)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         _lib.call("dippm_build_csr_grouped", _p(b.src), _p(b.dst), _p(b.graph_ptr), _p(b.edge_ptr), b.G, N, E,
                   b.max_nodes, b.max_edges, _p(b.rowptr), _p(b.col), _p(b.deg), _p(b.inv_deg), _p(b.t_rowptr),
-                  _p(b.t_col), _p(b.bad), _p(ws), ws_bytes, _stream())
+                  _p(b.t_col), _p(b.bad), _p(b.node_graph), _p(ws), ws_bytes, _stream())
         return b
+    _lib.call("dippm_node_graph", _p(b.graph_ptr), b.G, _p(b.node_graph), _stream())
     ws_bytes = lib.dippm_csr_workspace_bytes(N, E)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.call("dippm_build_csr", _p(b.src), _p(b.dst), E, N, _p(b.rowptr), _p(b.col), _p(b.deg), _p(b.inv_deg),
