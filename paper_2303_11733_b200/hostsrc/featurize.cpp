@@ -382,6 +382,35 @@ struct Node {
   bool has_shape = false;
   std::vector<int64_t> shape;
   std::vector<int64_t> inputs;
+  // this <- src for the fields the graph uses; the buffers are exchanged, not copied (src is
+  // reset before its next use)
+  void take(Node& src) {
+    raw.swap(src.raw);
+    shape.swap(src.shape);
+    inputs.swap(src.inputs);
+    kind = src.kind;
+    is_op = src.is_op;
+    has_shape = src.has_shape;
+    for (int a = 0; a < 12; ++a) {
+      has_attr[a] = src.has_attr[a];
+      attr[a] = src.attr[a];
+      attr_int[a] = src.attr_int[a];
+      attr_i[a] = src.attr_i[a];
+    }
+  }
+  void reset() {  // a fresh node, keeping the vectors' capacity
+    raw.clear();
+    kind = OTHER;
+    is_op = true;
+    for (int a = 0; a < 12; ++a) {
+      has_attr[a] = attr_int[a] = false;
+      attr[a] = 0.0;
+      attr_i[a] = 0;
+    }
+    has_shape = false;
+    shape.clear();
+    inputs.clear();
+  }
 };
 
 struct Graph {
@@ -444,6 +473,34 @@ struct RawNode {
   bool has_shape = false;
   uint8_t shape_t = V_NUL;
   std::vector<Scalar> shape;
+  void reset() {  // back to the parsed-nothing state, keeping the vectors' capacity
+    is_obj = has_id = has_op = has_inputs = has_attrs = has_shape = false;
+    id = Scalar();
+    op_t = inputs_t = attrs_t = shape_t = V_NUL;
+    op.clear();
+    inputs_ok = true;
+    inputs.clear();
+    for (bool& h : has_known) h = false;
+    attrs.clear();
+    shape.clear();
+  }
+};
+
+// Per-thread pool of node entries: documents are parsed back to back on a worker thread, so
+// the entries (and their small vectors) are reused instead of reallocated per node.
+struct RawPool {
+  std::vector<RawNode> v;
+  size_t n = 0;
+  RawNode& next() {
+    if (n == v.size()) v.emplace_back();
+    RawNode& r = v[n++];
+    r.reset();
+    return r;
+  }
+  RawNode* begin() { return v.data(); }
+  RawNode* end() { return v.data() + n; }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
 };
 
 void read_node(Cursor& c, RawNode& r) {
@@ -482,9 +539,12 @@ void read_node(Cursor& c, RawNode& r) {
       if (c.peek('{')) {
         r.attrs_t = V_OBJ;
         c.object([&](std::string_view k) {
+          static const std::string_view names[12] = {kAttrs[0], kAttrs[1], kAttrs[2], kAttrs[3],
+                                                     kAttrs[4], kAttrs[5], kAttrs[6], kAttrs[7],
+                                                     kAttrs[8], kAttrs[9], kAttrs[10], kAttrs[11]};
           int slot = -1;
           for (int a = 0; a < 12 && slot < 0; ++a)
-            if (k == kAttrs[a]) slot = a;
+            if (k == names[a]) slot = a;
           if (slot >= 0) {
             r.known[slot] = c.value();
             r.has_known[slot] = true;
@@ -523,7 +583,7 @@ struct IdIndex {
   std::vector<int32_t> table;
   std::unordered_map<int64_t, size_t> map;
   bool dense = true;
-  explicit IdIndex(const std::vector<RawNode>& raw) {
+  explicit IdIndex(RawPool& raw) {
     int64_t hi = -1;
     for (const RawNode& r : raw)
       if (r.is_obj && r.has_id && r.id.t == V_INT) hi = std::max(hi, r.id.i);
@@ -543,12 +603,13 @@ struct IdIndex {
   }
 };
 
-// parse_graph_json graph_ir.py:212-297
-Graph parse_graph(const char* text, int64_t len) {
+// parse_graph_json graph_ir.py:212-297.  g is the caller's (per-thread, reused) graph.
+void parse_graph(const char* text, int64_t len, Graph& g) {
   Cursor c{text, text + len};
   bool has_nodes = false, nodes_arr = false, has_outputs = false, outputs_arr = false, has_batch = false,
        has_name = false;
-  std::vector<RawNode> raw;
+  static thread_local RawPool raw;
+  raw.n = 0;
   std::vector<Scalar> outputs;
   Scalar batch, name_v;
   std::string name;
@@ -562,12 +623,12 @@ Graph parse_graph(const char* text, int64_t len) {
   c.object([&](std::string_view key) {
     if (key == "nodes") {
       has_nodes = true;
-      raw.clear();
+      raw.n = 0;
       nodes_arr = c.peek('[');
       if (nodes_arr) {
         c.array([&] {
-          raw.emplace_back();
-          if (c.peek('{')) read_node(c, raw.back());
+          RawNode& r = raw.next();
+          if (c.peek('{')) read_node(c, r);
           else c.value();
         });
       } else {
@@ -611,8 +672,10 @@ Graph parse_graph(const char* text, int64_t len) {
   IdIndex by_id(raw);
   std::vector<int64_t> order_doc;
   order_doc.reserve(raw.size());
-  std::vector<Node> entries;
-  entries.reserve(raw.size());
+  // document-order entries, a per-thread pool swapped with g.nodes below (capacity reused)
+  static thread_local std::vector<Node> entries;
+  if (entries.size() < raw.size()) entries.resize(raw.size());
+  size_t ne = 0;
   for (RawNode& r : raw) {
     if (!r.is_obj) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "every node must be an object");
     if (!r.has_id || r.id.t != V_INT || r.id.i < 0)
@@ -621,12 +684,13 @@ Graph parse_graph(const char* text, int64_t len) {
     if (by_id.find(nid) >= 0) fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "duplicate node id " + I(nid));
     if (!r.has_op || r.op_t != V_STR || r.op.empty())
       fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": missing operator name");
-    Node n;
-    n.raw = std::move(r.op);
+    Node& n = entries[ne];
+    n.reset();
+    n.raw = r.op;
     if (r.has_inputs) {
       if (r.inputs_t != V_ARR || !r.inputs_ok)
         fail(DIPPM_FEAT_MALFORMED_DOCUMENT, "node " + I(nid) + ": inputs must be a list of node ids");
-      n.inputs = std::move(r.inputs);
+      n.inputs = r.inputs;
     }
     if (r.has_attrs) {
       bool good = r.attrs_t == V_OBJ;
@@ -656,11 +720,11 @@ Graph parse_graph(const char* text, int64_t len) {
       }
       n.has_shape = true;
     }
-    by_id.set(nid, entries.size());
+    by_id.set(nid, ne);
     order_doc.push_back(nid);
-    entries.push_back(std::move(n));
+    ++ne;
   }
-  for (size_t k = 0; k < entries.size(); ++k)
+  for (size_t k = 0; k < ne; ++k)
     for (int64_t src : entries[k].inputs)
       if (by_id.find(src) < 0)
         fail(DIPPM_FEAT_DANGLING_REFERENCE, "node " + I(order_doc[k]) + " references missing input " + I(src));
@@ -670,7 +734,7 @@ Graph parse_graph(const char* text, int64_t len) {
   }
   // _topological_order: Kahn over a min-heap of original ids, inputs counted with multiplicity.
   // Ids are renamed to entry indices for the bookkeeping; the heap orders by original id.
-  const size_t M = entries.size();
+  const size_t M = ne;
   std::vector<int64_t> pending(M), cptr(M + 1, 0);
   std::vector<size_t> cons;
   for (size_t k = 0; k < M; ++k) {
@@ -709,18 +773,17 @@ Graph parse_graph(const char* text, int64_t len) {
   }
   std::vector<int64_t> remap(M);
   for (size_t k = 0; k < M; ++k) remap[order[k]] = (int64_t)k;
-  Graph g;
   g.batch = batch.i;
   g.name = std::move(name);
-  g.nodes.reserve(M);
-  for (size_t k : order) {
-    Node n = std::move(entries[k]);
-    for (auto& i : n.inputs) i = remap[by_id.at(i)];
+  g.nodes.resize(M);
+  for (size_t i = 0; i < M; ++i) {
+    g.nodes[i].take(entries[order[i]]);  // entries keeps the previous graph's buffers
+    Node& n = g.nodes[i];
+    for (auto& x : n.inputs) x = remap[by_id.at(x)];
     classify(op_tail(n.raw), n.kind, n.is_op);
-    g.nodes.push_back(std::move(n));
   }
+  g.outputs.clear();
   for (const Scalar& o : outputs) g.outputs.push_back(remap[by_id.at(o.t == V_BOOL ? (int64_t)o.b : o.i)]);
-  return g;
 }
 
 int64_t numel(const std::vector<int64_t>& s) {
@@ -993,7 +1056,8 @@ int64_t compute_macs(const Graph& g) {
 
 void featurize_one(const char* doc, int64_t len, int64_t batch_override, Result& r) {
   try {
-    Graph g = parse_graph(doc, len);
+    static thread_local Graph g;
+    parse_graph(doc, len, g);
     bool missing = false;
     for (const Node& n : g.nodes) missing |= !n.has_shape;
     if (missing) infer_shapes(g);
