@@ -88,7 +88,7 @@ size_t dippm_csr_workspace_bytes(int64_t num_nodes, int64_t num_edges);
 /* Grouped fast path (same outputs, bit for bit): the batch is a concatenation of
  * graphs — graph_ptr [G+1] over nodes, edge_ptr [G+1] over edges (int64), every
  * edge inside its own graph (else *bad_edge = 1).  One CTA per graph builds its
- * CSR in shared memory (3 launches per batch).  Limits: G <= 8192, per-graph
+ * CSR in shared memory (2 launches per batch).  Limits: G <= 8192, per-graph
  * padded edge count <= 16384; callers fall back to dippm_build_csr beyond.
  * node_graph (nullable): also writes the node -> graph map (dippm_node_graph) in the same pass. */
 size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t num_edges);

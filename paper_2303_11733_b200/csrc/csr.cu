@@ -285,7 +285,7 @@ extern "C" int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64
 // (graph_ptr over nodes, edge_ptr over edges, every edge inside its graph) —
 // exactly what the collation produces.  One CTA per graph does the whole
 // per-graph CSR in shared memory (count, bitonic sort of (dst, src) keys,
-// de-duplication, transposed sort), so the batch CSR costs 3 launches instead
+// de-duplication, transposed counting sort), so the batch CSR costs 2 launches instead
 // of ~17.  Output is identical to the global path (same sort order, same
 // duplicate semantics), which the GPU tests check bit for bit.
 namespace dippm {
@@ -417,23 +417,12 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict_
   if (threadIdx.x == 0) uniq[g] = U;
 }
 
-// Single-block exclusive scan of uniq[0..G) -> coff[0..G], coff[G] = total.
-__global__ void __launch_bounds__(1024) k_scan_small(const int32_t* __restrict__ in, int n, int32_t* out) {
-  extern __shared__ int sm[];
-  __shared__ int s_tmp[33];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = in[i];
-  __syncthreads();
-  const int total = block_scan_smem(sm, n, s_tmp);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = sm[i];
-  if (threadIdx.x == 0) out[n] = total;
-}
-
 // Phase 3 (CTA per graph): CSR rows from the sorted distinct keys, then the
 // transposed pattern from a (src, dst) re-sort.
 __global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict__ graph_ptr,
                                                       const int64_t* __restrict__ edge_ptr,
                                                       const int32_t* __restrict__ scratch,
-                                                      const int32_t* __restrict__ uniq, const int32_t* __restrict__ coff,
+                                                      const int32_t* __restrict__ uniq,
                                                       int epad_max, int64_t N, int G, int32_t* rowptr, int32_t* col,
                                                       int32_t* t_rowptr, int32_t* t_col) {
   extern __shared__ int sm[];
@@ -441,7 +430,18 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict_
   const int g = blockIdx.x;
   const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
   const int64_t e0 = edge_ptr[g];
-  const int U = uniq[g], off = coff[g];
+  const int U = uniq[g];
+  // this graph's offset in the packed CSR = sum of the earlier graphs' unique counts (each
+  // block sums its prefix itself: no separate scan launch; integer sums, order-free)
+  int part = 0;
+  for (int i = threadIdx.x; i < g; i += blockDim.x) part += uniq[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) s_tmp[threadIdx.x >> 5] = part;
+  __syncthreads();
+  int off = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) off += s_tmp[w];
+  __syncthreads();
   const int* keys = scratch + e0;  // sorted distinct (dst, src) keys
   int* cnt = sm;                   // [ng + 1]
   for (int v = threadIdx.x; v <= ng; v += blockDim.x) cnt[v] = 0;
@@ -513,7 +513,6 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* scratch = reinterpret_cast<int32_t*>(workspace);
   int32_t* uniq = scratch + (E > 0 ? E : 1);
-  int32_t* coff = uniq + G;
   static int smem_set = 0;
   if ((int)smem > smem_set) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_csr_g1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -523,9 +522,8 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
   DIPPM_CUDA_CHECK(cudaMemsetAsync(bad_edge, 0, sizeof(int), s));
   k_csr_g1<<<(unsigned)G, kGThreads, smem, s>>>(src, dst, graph_ptr, edge_ptr, epad, deg, inv_deg, scratch, uniq,
                                                 bad_edge, node_graph);
-  k_scan_small<<<1, 1024, (size_t)G * sizeof(int), s>>>(uniq, (int)G, coff);
-  k_csr_g3<<<(unsigned)G, kGThreads, smem, s>>>(graph_ptr, edge_ptr, scratch, uniq, coff, epad, N, (int)G, rowptr,
+  k_csr_g3<<<(unsigned)G, kGThreads, smem, s>>>(graph_ptr, edge_ptr, scratch, uniq, epad, N, (int)G, rowptr,
                                                 col, t_rowptr, t_col);
-  DIPPM_LAUNCH_CHECK_N(3, "build_csr_grouped");
+  DIPPM_LAUNCH_CHECK_N(2, "build_csr_grouped");
   return DIPPM_OK;
 }

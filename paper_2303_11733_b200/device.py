@@ -286,7 +286,7 @@ def build_batch_csr(b: Batch, grouped: bool | None = None) -> Batch:
     """K1: deterministic CSR + transposed CSR of the batch (gnn.py:130-137).
 
     Uses the per-graph shared-memory kernel when the batch is grouped by graph
-    (3 launches), else the global path; both give bit-identical output."""
+    (2 launches), else the global path; both give bit-identical output."""
     dev = b.x.device
     N, E = b.N, b.E
     i32 = dict(dtype=torch.int32, device=dev)
