@@ -412,11 +412,31 @@ __device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, i
 // pool_graph[g] when g lies wholly inside this 32-row block, else to the block's
 // boundary slot (0: segment holding the block's first row, 1: the one holding its last).
 // dippm_pool_combine adds the boundary slots of the blocks a graph spans, in block order.
-__device__ __forceinline__ void pool_chunk(const Params& p, const float (&v)[32], int64_t row, int64_t r0, int n,
-                                           int lane) {
-  const int gid = row < p.M ? __ldg(p.node_graph + row) : -1;
-  const int g0 = __shfl_sync(0xffffffffu, gid, 0);
-  if (g0 >= 0 && __all_sync(0xffffffffu, gid == g0)) {
+// The warp's graph layout is the same for every column chunk of a tile: looked up once.
+struct PoolRows {
+  int gid;        // graph of this lane's row (-1 past M)
+  bool uniform;   // all 32 rows in one graph
+  float* whole;   // uniform case: pool_graph row of that graph if it lies inside the block, else
+                  // the block's slot-0 partial row (column offset added per chunk)
+};
+__device__ __forceinline__ PoolRows pool_rows(const Params& p, int64_t row, int64_t r0) {
+  PoolRows pr;
+  pr.gid = row < p.M ? __ldg(p.node_graph + row) : -1;
+  const int g0 = __shfl_sync(0xffffffffu, pr.gid, 0);
+  pr.uniform = g0 >= 0 && __all_sync(0xffffffffu, pr.gid == g0);
+  pr.whole = nullptr;
+  if (pr.uniform) {
+    const int gs = __ldg(p.graph_ptr + g0), ge = __ldg(p.graph_ptr + g0 + 1);
+    pr.whole = ((gs >> 5) == ((ge - 1) >> 5)) ? p.pool_graph + (int64_t)g0 * p.N
+                                               : p.pool_part + ((r0 >> 5) * 2 + 0) * p.N;  // gs <= r0 here
+  }
+  return pr;
+}
+
+__device__ __forceinline__ void pool_chunk(const Params& p, const PoolRows& pr, const float (&v)[32], int64_t r0,
+                                           int n, int lane) {
+  const int gid = pr.gid;
+  if (pr.uniform) {
     // common case, all 32 rows in one graph: transpose-reduce (31 shuffles), lane L ends
     // with the block sum of column n + L, and the warp stores 128 contiguous bytes
     float t[32];
@@ -432,10 +452,7 @@ __device__ __forceinline__ void pool_chunk(const Params& p, const float (&v)[32]
         t[i] = (upper ? t[i + k] : t[i]) + recv;
       }
     }
-    const int gs = __ldg(p.graph_ptr + g0), ge = __ldg(p.graph_ptr + g0 + 1);
-    float* dst = ((gs >> 5) == ((ge - 1) >> 5)) ? p.pool_graph + (int64_t)g0 * p.N + n
-                                                 : p.pool_part + ((r0 >> 5) * 2 + 0) * p.N + n;  // gs <= r0 here
-    dst[lane] = t[0];
+    pr.whole[n + lane] = t[0];
     return;
   }
   float s[32];
@@ -689,6 +706,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         release(acc);
         continue;
       }
+      // fused readout: this warp's graph layout, looked up before the accumulator is ready
+      PoolRows pr{};
+      if constexpr (kEpi == EPI_FWD)
+        if (p.pool_part) pr = pool_rows(p, row, m0 + q * 32);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       // TMEM reads run one chunk ahead: chunk i+1 is in flight while chunk i is processed.
@@ -756,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) bits |= (uint32_t)(v[i] > 0.f) << i;
             p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;  // chunk-major: a warp stores 128 contiguous bytes
           }
-          if (p.pool_part) pool_chunk(p, v, row, m0 + q * 32, n, lane);  // fused readout (K4, gnn.py:214)
+          if (p.pool_part) pool_chunk(p, pr, v, m0 + q * 32, n, lane);  // fused readout (K4, gnn.py:214)
           if (p.out.base)
             epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
                             local * (kBN / 64) + (ch >> 1));
