@@ -710,6 +710,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       PoolRows pr{};
       if constexpr (kEpi == EPI_FWD)
         if (p.pool_part) pr = pool_rows(p, row, m0 + q * 32);
+      // 1-CTA tiles (short-K layer 1: the epilogue is the bottleneck): lane l holds bias column l
+      // of each of this warp's chunks, fetched before the accumulator wait and broadcast with
+      // shuffles, so no load latency sits inside the chunk loop.  Pair tiles (long K, epilogue
+      // hidden under the MMAs) load the bias per chunk: fewer instructions.
+      float bl[kBN / 64];
+      if constexpr ((kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) && kCta == 1) {
+#pragma unroll
+        for (int i = 0; i < kBN / 64; ++i) bl[i] = p.bias ? __ldg(p.bias + n0 + (half + 2 * i) * 32 + lane) : 0.f;
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       // TMEM reads run one chunk ahead: chunk i+1 is in flight while chunk i is processed.
@@ -725,7 +734,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = n0 + ch * 32;
         if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
           float v[32];
-          if (p.bias) {
+          if constexpr (kCta == 1) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = __shfl_sync(0xffffffffu, bl[i], k);
+          } else if (p.bias) {
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + g);
@@ -733,12 +745,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int k = 0; k < 32; ++k) v[k] = 0.f;
           }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(raw[i]) + v[i];
-            v[i] = p.relu ? fmaxf(x, 0.f) : x;
+          for (int k = 0; k < 32; ++k) {
+            const float x = __uint_as_float(raw[k]) + v[k];
+            v[k] = p.relu ? fmaxf(x, 0.f) : x;
           }
           if constexpr (kEpi == EPI_FWD_DROP) {  // inverted dropout after ReLU (gnn.py:277-281)
             const uint64_t seed = p.seed ^ (p.seed_dev ? (uint64_t)p.seed_dev[0] * 0x9E3779B97F4A7C15ull : 0ull);
