@@ -141,7 +141,8 @@ int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t*
                                   const float* inv_deg, float* colsum_partial, float* bias_grad, int32_t* sync,
                                   const uint32_t* h3_bits, int64_t bits_ld, void* stream);
 /*   h3_bits (optional): the layer-3 forward GEMM's 1-bit (h3 > 0) masks (dippm_gemm relu_bits
- *   layout, bits_ld >= N); used instead of reading h3 for the ReLU gate. */
+ *   layout: chunk-major with bits_ld >= N, or row-major with bits_ld == 0 -- the layout this
+ *   kernel reads best, one row's words being contiguous); used instead of reading h3. */
 /* node_graph[v] = g for v in [graph_ptr[g], graph_ptr[g+1]). */
 int32_t dippm_node_graph(const int32_t* graph_ptr, int64_t num_graphs, int32_t* node_graph, void* stream);
 
@@ -192,7 +193,8 @@ typedef struct dippm_gemm_args {
   double drop_p;
   uint64_t seed;
   const int64_t* seed_dev; /* nullable device step counter mixed into the dropout seed (graph replays) */
-  uint32_t* relu_bits;       /* FWD (optional): bit c%32 of word [(c/32)*bits_ld + r] = (stored out[r,c] > 0) */
+  uint32_t* relu_bits;       /* FWD (optional): bit c%32 of word [(c/32)*bits_ld + r] = (stored out[r,c] > 0); */
+                             /* bits_ld == 0: row-major instead, word [r*(N/32) + c/32] (FWD relu_bits only)  */
   const uint32_t* gate_bits; /* GATE (optional): use these bits instead of reading `gate` values          */
                              /* (relu_bits / gate_bits: tensor-core backend; the SIMT anchor gates on values) */
   int64_t bits_ld;           /* words per 32-column chunk of relu_bits / gate_bits (chunk-major, >= M)   */

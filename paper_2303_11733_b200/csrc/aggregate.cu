@@ -179,7 +179,9 @@ struct ReadoutArgs {
   const int* node_graph;    // [N]
   ActView h3;               // ReLU gate (values), used when h3_bits is NULL
   const uint32_t* h3_bits;  // 1-bit (h3 > 0) masks from the layer-3 forward epilogue, word [(c/32)*bits_ld + r]
+                            // (bits_ld 0: row-major, word [r*(width/32) + c/32])
   int64_t bits_ld;
+  int64_t width_words;      // width / 32 (row-major bit masks)
 };
 
 // ReLU'(z3) for 8 consecutive columns per chunk: from the forward's bit mask (4 bytes per 32
@@ -190,7 +192,8 @@ __device__ __forceinline__ void relu_gate(const ReadoutArgs& ro, int64_t r, int 
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int c = c0 + q * stride;
-      const uint32_t w = __ldg(ro.h3_bits + (int64_t)(c >> 5) * ro.bits_ld + r) >> (c & 31);
+      const uint32_t w = __ldg(ro.bits_ld ? ro.h3_bits + (int64_t)(c >> 5) * ro.bits_ld + r
+                                          : ro.h3_bits + r * (int64_t)(ro.width_words) + (c >> 5)) >> (c & 31);
 #pragma unroll
       for (int k = 0; k < 8; ++k) gt[q][k] = (w >> k) & 1u;
     }
@@ -397,7 +400,8 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
     wofs[q] = (c0 + q * stride) >> 5;
     wsh[q] = (c0 + q * stride) & 31;
   }
-  const int64_t bld = ro.bits_ld;
+  // word of (row, chunk): chunk-major (stride bits_ld per chunk) or row-major (stride 1)
+  const int64_t cstride = ro.bits_ld ? ro.bits_ld : 1, rstride = ro.bits_ld ? 1 : width >> 5;
   float part[CPL][8] = {};
   float dr[CPL][8];
   int g_cur = -1;
@@ -409,14 +413,15 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
     int nv[kPre];
     float nw[kPre];
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) wown[q] = __ldg(ro.h3_bits + wofs[q] * bld + row);
+    for (int q = 0; q < CPL; ++q) wown[q] = __ldg(ro.h3_bits + wofs[q] * cstride + row * rstride);
 #pragma unroll
     for (int t = 0; t < kPre; ++t) {
       const int j = b + t;
       nv[t] = j < e ? (staged ? s_col[j] : t_col[cbeg + j]) : -1;
       nw[t] = j < e ? (staged ? s_cw[j] : inv_deg[nv[t]]) : 0.f;
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) wn[t][q] = nv[t] >= 0 ? __ldg(ro.h3_bits + wofs[q] * bld + nv[t]) : 0u;
+      for (int q = 0; q < CPL; ++q)
+        wn[t][q] = nv[t] >= 0 ? __ldg(ro.h3_bits + wofs[q] * cstride + (int64_t)nv[t] * rstride) : 0u;
     }
     const int g = s_g[lr];
     if (g != g_cur) {  // rows of a graph are contiguous: reload dr only at graph changes
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
       for (int j = b + kPre; j < e; ++j) {  // beyond the prefetched out-edges
         const int v0 = staged ? s_col[j] : t_col[cbeg + j];
         const float w0 = staged ? s_cw[j] : inv_deg[v0];
-        const uint32_t wv = __ldg(ro.h3_bits + wofs[q] * bld + v0) >> wsh[q];
+        const uint32_t wv = __ldg(ro.h3_bits + wofs[q] * cstride + (int64_t)v0 * rstride) >> wsh[q];
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[k] += (wv >> k) & 1u ? w0 : 0.f;
       }
@@ -792,8 +797,9 @@ int32_t dippm_readout_aggregate_t(const float* du, int64_t ld_du, const int32_t*
                                   float* bias_grad, int32_t* sync, const uint32_t* h3_bits, int64_t bits_ld,
                                   void* stream) {
   DIPPM_ARG_CHECK((h3_bits || h3.dtype == B.dtype) && ld_du % 4 == 0, "readout_aggregate_t: dtype / alignment");
-  DIPPM_ARG_CHECK(!h3_bits || bits_ld >= N, "readout_aggregate_t: bits_ld %lld < rows", (long long)bits_ld);
-  ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3), h3_bits, bits_ld};
+  DIPPM_ARG_CHECK(!h3_bits || bits_ld >= N || bits_ld == 0, "readout_aggregate_t: bits_ld %lld < rows",
+                  (long long)bits_ld);
+  ReadoutArgs ro{du, ld_du, graph_ptr, node_graph, make_view(h3), h3_bits, bits_ld, (int64_t)(width >> 5)};
   if (h3_bits && width % 256 == 0 && width <= 1024)
     return launch_readout_bits(B, width, N, t_rowptr, t_col, inv_deg, colsum_partial, ro, bias_grad, sync,
                                (cudaStream_t)stream);

@@ -787,7 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t bits = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) bits |= (uint32_t)(v[i] > 0.f) << i;
-            p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;  // chunk-major: a warp stores 128 contiguous bytes
+            if (p.bits_ld > 0) p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;  // chunk-major: 128 B per warp
+            else p.relu_bits[row * (p.N >> 5) + (n >> 5)] = bits;  // row-major (bits_ld 0): read per row
           }
           if (p.pool_part) pool_chunk(p, pr, v, m0 + q * 32, n, lane);  // fused readout (K4, gnn.py:214)
           if (p.out.base)

@@ -557,7 +557,9 @@ class Engine:
                         graph_ptr=_p(b.graph_ptr)) if fused and i == 2 else {}
             self._gemm(GEMM_FWD, b.N, hp, 2 * L.d_in[i], ws.A[i].view(0), 0, self.Wf[i].view(), 1,
                        bias=self._f32(f"sage{i + 1}.bias"), relu=1, out=outs[i],
-                       relu_bits=_p(bits[i]) if bits is not None else None, bits_ld=ws.N, **pool)
+                       relu_bits=_p(bits[i]) if bits is not None else None,
+                       # h3's mask is read per row by the readout backward: row-major (bits_ld 0)
+                       bits_ld=0 if i == 2 else ws.N, **pool)
         if fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
             _lib.call("dippm_pool_combine", _p(ws.pool_part), _p(ws.pool_graph), _p(b.graph_ptr), b.G, hp,
                       _p(b.fs), _p(self.norm), ws.u.view(), s)
@@ -696,7 +698,7 @@ class Engine:
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
                           NULL_ACT if ws.H3 is None else ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr),
                           _p(b.t_col), _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync),
-                          _p(ws.relu_bits[2]) if self.backend == 0 else None, ws.N, s)  # SIMT: no bit masks
+                          _p(ws.relu_bits[2]) if self.backend == 0 else None, 0, s)  # row-major; SIMT: no bits
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
                           _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)

@@ -480,11 +480,13 @@ def test_wgrad_fused_reduce(prec, R, M, N, splits):
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
-def test_readout_aggregate_t_bits_equal_values(prec):
+@pytest.mark.parametrize("W", [64, 512])
+def test_readout_aggregate_t_bits_equal_values(prec, W):
     """Layer-3 readout backward + agg^T + bias grad: gating on the forward's 1-bit masks
-    gives exactly what gating on the h3 values gives, and both match fp64 numpy."""
+    (chunk-major, and row-major with bits_ld 0) gives exactly what gating on the h3 values
+    gives, and all match fp64 numpy.  W = 512 takes the bits kernel's fast path."""
     rng = np.random.default_rng(21)
-    G, W = 9, 64
+    G = 9
     n = rng.integers(3, 40, G)
     gp = np.zeros(G + 1, np.int32)
     np.cumsum(n, out=gp[1:])
@@ -501,27 +503,35 @@ def test_readout_aggregate_t_bits_equal_values(prec):
     b = upload_batch(np.zeros((N, 32), np.float32), src, dst, gp, np.zeros((G, 5), np.float32))
     dt = dev.PRECISIONS[prec]
     h3, h64, _ = _rand_act(N, W, dt, rng)
-    bits = torch.from_numpy(_bits_of(h64 > 0)).cuda()
+    bits_np = _bits_of(h64 > 0)
+    bits = torch.from_numpy(bits_np).cuda()
+    bits_rm = torch.from_numpy(np.ascontiguousarray(bits_np.T)).cuda()  # [N, W/32] row-major
     du = torch.from_numpy(rng.normal(size=(G, W)).astype(np.float32)).cuda()
     lib = _lib.load()
     outs = []
-    for use_bits in (False, True):
+    for use_bits in (0, 1, 2):  # values, chunk-major bits, row-major bits
         B = ActBuf(N, 2 * W, dt, "cuda")
         part = torch.empty(lib.dippm_colsum_rows(N), W, device="cuda")
         sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device="cuda")
         bias = torch.empty(W, device="cuda")
         _lib.call("dippm_readout_aggregate_t", du.data_ptr(), W, b.graph_ptr.data_ptr(), b.node_graph.data_ptr(),
                   h3.view(), B.view(), W, N, b.t_rowptr.data_ptr(), b.t_col.data_ptr(), b.inv_deg.data_ptr(),
-                  part.data_ptr(), bias.data_ptr(), sync.data_ptr(), bits.data_ptr() if use_bits else None,
-                  N, dev._stream())
+                  part.data_ptr(), bias.data_ptr(), sync.data_ptr(),
+                  None if use_bits == 0 else (bits if use_bits == 1 else bits_rm).data_ptr(),
+                  N if use_bits == 1 else 0, dev._stream())
         outs.append((B.to_float().clone(), bias.clone()))
-    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    # the two bit layouts run the same arithmetic: identical
+    assert torch.equal(outs[1][0], outs[2][0]) and torch.equal(outs[1][1], outs[2][1])
+    if W < 256:  # generic kernel: bits and values gate the same terms in the same order
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    # (W = 512: the bits kernel factorises agg^T dz3 = dr * sum bit/deg -- checked against fp64 below)
     # fp64 reference: dz3[v] = du[g(v)] / N_g * (h3 > 0); agg^T dz3; bias = sum dz3
     gid = np.repeat(np.arange(G), n)
     dz = du.double().cpu().numpy()[gid] / n[gid][:, None] * (h64 > 0)
     agg = O.aggregation_matrix(N, list(zip(src.tolist(), dst.tolist())))
-    got = outs[0][0].double().cpu().numpy()
     tol = 2e-2 if prec == "bf16" else 1e-5
-    assert np.allclose(got[:, :W], dz, atol=tol * np.abs(dz).max())
-    assert np.allclose(got[:, W:], agg.T @ dz, atol=tol * np.abs(dz).max())
-    assert np.allclose(outs[0][1].double().cpu().numpy(), dz.sum(0), atol=tol * np.abs(dz).sum(0).max())
+    for k in (0, 1):
+        got = outs[k][0].double().cpu().numpy()
+        assert np.allclose(got[:, :W], dz, atol=tol * np.abs(dz).max())
+        assert np.allclose(got[:, W:], agg.T @ dz, atol=tol * np.abs(dz).max())
+        assert np.allclose(outs[k][1].double().cpu().numpy(), dz.sum(0), atol=tol * np.abs(dz).sum(0).max())
