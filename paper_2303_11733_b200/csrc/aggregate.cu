@@ -67,7 +67,22 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
   __syncthreads();
   if (grp >= gpw) return;
   const int c0 = sub * 8, stride = L * 8;
-  for (int lr = warp * gpw + grp; lr < nrows; lr += (kAggThreads / 32) * gpw) {
+  const int rstep = (kAggThreads / 32) * gpw;
+  // bf16 rows: the next row's first neighbour is fetched (raw) while this row is summed, so
+  // each warp keeps two rows' loads in flight
+  uint4 nxt[CPL];
+  auto fetch_first = [&](int lr2) {
+    if constexpr (DTI == DIPPM_DT_BF16) {
+      if (lr2 < nrows && s_ptr[lr2] < s_ptr[lr2 + 1]) {
+        const int v = staged ? s_col[s_ptr[lr2]] : col[cbeg + s_ptr[lr2]];
+        const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(h.base) + (int64_t)v * h.ld + c0;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) nxt[q] = __ldg(reinterpret_cast<const uint4*>(src + q * stride));
+      }
+    }
+  };
+  fetch_first(warp * gpw + grp);
+  for (int lr = warp * gpw + grp; lr < nrows; lr += rstep) {
     const int64_t row = r0 + lr;
     const int b = s_ptr[lr], e = s_ptr[lr + 1];
     float acc[CPL][8] = {};
@@ -98,7 +113,32 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
       }
-    } else {  // the 512-wide layers measured fastest one neighbour at a time
+    } else if constexpr (DTI == DIPPM_DT_BF16) {
+      uint4 cur[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) cur[q] = nxt[q];
+      fetch_first(lr + rstep);
+      if (b < e) {  // first neighbour (prefetched), then the rest in CSR order
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&cur[q]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(hh[i]);
+            acc[q][2 * i] += f.x;
+            acc[q][2 * i + 1] += f.y;
+          }
+        }
+      }
+      for (int j = b + 1; j < e; ++j) {
+        float x[CPL][8];
+        load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[q][k] += x[q][k];
+      }
+    } else {
       for (int j = b; j < e; ++j) {
         float x[CPL][8];
         load_chunks<DTI, CPL>(h, staged ? s_col[j] : col[cbeg + j], c0, stride, x);
