@@ -334,12 +334,17 @@ def inference_sweep(args, rank, world, lib):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)), args.clock_ms)
+        if not args.no_clocks:
+            sampler.start()
+        sampler.mark()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(args.infer_steps):
             step(i)
         e1.record()
         torch.cuda.synchronize()
+        clocks = sampler.stop()
         ms = e0.elapsed_time(e1)
         if world > 1:
             t = torch.tensor([ms], device="cuda")
@@ -353,7 +358,7 @@ def inference_sweep(args, rank, world, lib):
         graphs = args.infer_steps * args.infer_batch * world
         out[prec] = {"graphs_per_s": graphs / (ms / 1000.0), "ms_per_batch": ms / args.infer_steps,
                      "gemm_tflops": g_flops / (g_ms / 1000.0) / 1e12,
-                     "gemm_share": g_ms / ms}
+                     "gemm_share": g_ms / ms, "clocks": clocks}
         del ws, eng
         torch.cuda.empty_cache()
     return out
