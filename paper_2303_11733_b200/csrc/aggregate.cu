@@ -687,18 +687,13 @@ using namespace dippm;
 
 extern "C" {
 
-// Rows per block chosen so the grid is a whole number of waves (the kernels are latency bound
-// and a short last wave left ~30 % of the SMs idle): waves = ceil(N / (64 * P)) with P the
-// resident blocks on the GPU, rows = ceil(N / (waves * P)) <= 64.
-// one wave of resident blocks when the rows fit (<= kRowsPerBlockT per block), else whole waves
+// Rows per block chosen so the grid is a whole number of waves of resident blocks (the
+// kernels are latency bound; a short last wave left ~30 % of the SMs idle, and the per-block
+// CSR staging / barrier / fold tail is paid once per block): waves = ceil(N / (256 * P)) with
+// P the resident blocks on the GPU, rows = ceil(N / (waves * P)) <= kRowsPerBlockT.
 static int wave_rows_t(int64_t N, int blocks_per_sm) {
   const int64_t P = (int64_t)num_sms() * std::max(1, blocks_per_sm);
   const int64_t waves = std::max<int64_t>(1, (N + kRowsPerBlockT * P - 1) / (kRowsPerBlockT * P));
-  return (int)std::max<int64_t>(1, (N + waves * P - 1) / (waves * P));
-}
-static int wave_rows(int64_t N, int blocks_per_sm) {
-  const int64_t P = (int64_t)num_sms() * std::max(1, blocks_per_sm);
-  const int64_t waves = std::max<int64_t>(1, (N + kRowsPerBlock * P - 1) / (kRowsPerBlock * P));
   return (int)std::max<int64_t>(1, (N + waves * P - 1) / (waves * P));
 }
 constexpr int kColsumBlocksPerSm = 4;  // upper bound of the agg^T kernels' residency (sizing only)
