@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 4
+#define DIPPM_ABI_VERSION 5
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -326,6 +326,13 @@ typedef struct dippm_head_args {
   float* du;                     /* fp32 [G, hp] or NULL (MLP: no readout below) */
   int32_t* sync;
   int32_t train;
+  /* optional (all four or none): u's readout columns are formed in-kernel from the layer-3
+   * FWD epilogue's block sums, exactly as dippm_pool_combine does (then u is written, not read
+   * from a separate launch); fs_raw [G, 5] fp32. */
+  const float* pool_partial;
+  const float* pool_graph;
+  const int32_t* graph_ptr;
+  const float* fs_raw;
 } dippm_head_args_t;
 int32_t dippm_head_fused_max_graphs(void);
 int32_t dippm_head_fused(const dippm_head_args_t* args, void* stream);

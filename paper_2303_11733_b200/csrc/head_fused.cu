@@ -57,6 +57,8 @@ struct Args {
   float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3, *du;
   int* sync;
   int train;
+  const float *pool_part, *pool_graph, *fs_raw;  // phase 0 (optional): u from the readout's block sums
+  const int* graph_ptr;
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -599,6 +601,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   GridBar bar;
   bar.init(a.sync);
   const int mt = (a.G + kT - 1) / kT, nh = a.hp / kT, nu = a.uw / kT;
+  if (a.pool_part) {
+    // 0: u = [mean of the layer-3 rows | (fs - mu) / sigma | 0], dippm_pool_combine's
+    // arithmetic (fp64 block sums in block order, bf16), one graph per CTA at a time
+    __nv_bfloat16* u = const_cast<__nv_bfloat16*>(a.u);
+    for (int g = blockIdx.x; g < a.G; g += gridDim.x) {
+      const int gs = a.graph_ptr[g], ge = a.graph_ptr[g + 1];
+      const int bf = gs >> 5, bl = (ge - 1) >> 5;
+      const double inv_n = 1.0 / (double)(ge - gs);
+      for (int c = threadIdx.x; c < a.hp; c += kThreads) {
+        double t;
+        if (bf == bl) {
+          t = a.pool_graph[(int64_t)g * a.hp + c];
+        } else {
+          t = a.pool_part[((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * a.hp + c];
+          int b = bf + 1;
+          for (; b + 4 <= bl; b += 4) {
+            const float v0 = a.pool_part[(int64_t)b * 2 * a.hp + c], v1 = a.pool_part[(int64_t)(b + 1) * 2 * a.hp + c];
+            const float v2 = a.pool_part[(int64_t)(b + 2) * 2 * a.hp + c];
+            const float v3 = a.pool_part[(int64_t)(b + 3) * 2 * a.hp + c];
+            t += v0;
+            t += v1;
+            t += v2;
+            t += v3;
+          }
+          for (; b < bl; ++b) t += a.pool_part[(int64_t)b * 2 * a.hp + c];
+          t += a.pool_part[(int64_t)bl * 2 * a.hp + c];
+        }
+        u[(int64_t)g * a.uw + c] = __float2bfloat16_rn((float)(t * inv_n));
+      }
+      for (int k = threadIdx.x; k < a.uw - a.hp; k += kThreads) {
+        float v = 0.f;
+        if (k < kStaticWidth) v = (float)(((double)a.fs_raw[g * kStaticWidth + k] - a.norm[6 + k]) / a.norm[11 + k]);
+        u[(int64_t)g * a.uw + a.hp + k] = __float2bfloat16_rn(v);
+      }
+    }
+    bar.sync();
+  }
   // A, B: the two hidden layers
   run_phase(a, smem, mt * nh, [&](int t) { return Unit{U_FWD1, (t / nh) * kT, (t % nh) * kT}; }, 1);
   bar.sync();
@@ -665,6 +704,9 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   DIPPM_ARG_CHECK(h->u && h->w1 && h->w2 && h->b1 && h->b2 && h->w3 && h->b3 && h->x2 && h->x3 && h->out && h->sync,
                   "head_fused: missing operand");
   DIPPM_ARG_CHECK(!h->bits || h->bits_ld >= h->G, "head_fused: bits_ld < G");
+  DIPPM_ARG_CHECK(!h->pool_partial || (h->pool_graph && h->graph_ptr && h->fs_raw && h->norm &&
+                                       h->u_width >= h->hp + kStaticWidth),
+                  "head_fused: in-kernel readout needs pool_graph, graph_ptr, fs_raw, norm, u_width >= hp + 5");
   DIPPM_ARG_CHECK(h->drop_mode >= 0 && h->drop_mode <= 2 && h->drop_p >= 0 && h->drop_p < 1,
                   "head_fused: bad dropout arguments");
   DIPPM_ARG_CHECK(h->drop_mode != 1 || (h->mask1 && h->mask2), "head_fused: dropout mode 1 needs both masks");
@@ -721,6 +763,10 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   a.du = h->du;
   a.sync = h->sync;
   a.train = h->train ? 1 : 0;
+  a.pool_part = h->pool_partial;
+  a.pool_graph = h->pool_graph;
+  a.graph_ptr = h->graph_ptr;
+  a.fs_raw = h->fs_raw;
   static bool attr = false;
   if (!attr) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(hf::k_head_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,

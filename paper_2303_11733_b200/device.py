@@ -355,6 +355,7 @@ class Workspace:
         self.row_loss = torch.empty(G, 4, dtype=torch.float64, device=dev)   # fused head: per-graph loss terms
         self.head_sync = torch.zeros(2, dtype=torch.int32, device=dev)        # fused head: grid barrier
         self.head_pending = None  # forward(defer_head=True) -> loss() -> backward() runs the fused head once
+        self.u_pending = None     # batch whose u the fused head still has to form (its phase 0)
         self.train = train
         if train:
             self.dout = torch.empty(G, 3, **f32)
@@ -560,7 +561,10 @@ class Engine:
                        relu_bits=_p(bits[i]) if bits is not None else None,
                        # h3's mask is read per row by the readout backward: row-major (bits_ld 0)
                        bits_ld=0 if i == 2 else ws.N, **pool)
-        if fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
+        ws.u_pending = None
+        if fused and self.fused_head_ok(b.G):  # K4 second stage inside the fused head (its phase 0)
+            ws.u_pending = b
+        elif fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
             _lib.call("dippm_pool_combine", _p(ws.pool_part), _p(ws.pool_graph), _p(b.graph_ptr), b.G, hp,
                       _p(b.fs), _p(self.norm), ws.u.view(), s)
         else:
@@ -611,6 +615,10 @@ class Engine:
             a.du = _p(ws.du) if self.arch == "sage" else None
             a.train = 1
         a.sync = _p(ws.head_sync)
+        pb, ws.u_pending = getattr(ws, "u_pending", None), None
+        if pb is not None:  # u's readout columns from the layer-3 block sums (dippm_pool_combine's work)
+            a.pool_partial, a.pool_graph, a.graph_ptr, a.fs_raw = (_p(ws.pool_part), _p(ws.pool_graph),
+                                                                   _p(pb.graph_ptr), _p(pb.fs))
         _lib.call("dippm_head_fused", C.byref(a), _stream())
         self.launches += 1
 
