@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 5
+#define DIPPM_ABI_VERSION 6
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -333,6 +333,9 @@ typedef struct dippm_head_args {
   const float* pool_graph;
   const int32_t* graph_ptr;
   const float* fs_raw;
+  /* optional (training): step_counter[0] += 1 once every CTA is past the forward's dropout
+   * draws (which read it through seed_dev) -- dippm_step_counter folded into this launch. */
+  int64_t* step_counter;
 } dippm_head_args_t;
 int32_t dippm_head_fused_max_graphs(void);
 int32_t dippm_head_fused(const dippm_head_args_t* args, void* stream);

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 5  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 6  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -68,7 +68,7 @@ class HeadArgs(C.Structure):
         ("dout", P), ("d2", P), ("d1", P), ("d2f", P), ("d1f", P),
         ("gw1", P), ("gb1", P), ("gw2", P), ("gb2", P), ("gw3", P), ("gb3", P), ("du", P),
         ("sync", P), ("train", C.c_int32),
-        ("pool_partial", P), ("pool_graph", P), ("graph_ptr", P), ("fs_raw", P),
+        ("pool_partial", P), ("pool_graph", P), ("graph_ptr", P), ("fs_raw", P), ("step_counter", P),
     ]
 
 

@@ -59,6 +59,7 @@ struct Args {
   int train;
   const float *pool_part, *pool_graph, *fs_raw;  // phase 0 (optional): u from the readout's block sums
   const int* graph_ptr;
+  long long* step_counter;  // incremented in phase E (after every CTA's dropout draws)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -666,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   if (!a.train) return;
   bar.sync();
   stamp(14);
+  if (a.step_counter && blockIdx.x == 0 && threadIdx.x == 0) a.step_counter[0] += 1;  // phases A/B are done
   // E: dW1, du, db1
   {
     const int n_w = nu * nh, n_s = a.du ? mt * nh : 0, n_c = nh;
@@ -767,6 +769,7 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   a.pool_graph = h->pool_graph;
   a.graph_ptr = h->graph_ptr;
   a.fs_raw = h->fs_raw;
+  a.step_counter = reinterpret_cast<long long*>(h->step_counter);
   static bool attr = false;
   if (!attr) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(hf::k_head_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -426,6 +426,7 @@ class Engine:
         self.cta_pair = 0       # GEMM tile policy passed to the library: 0 auto, 1 single-CTA, 2 CTA pair
         self.gemm_hook = None  # bench instrumentation: called ("pre"|"post", flops) around each GEMM
         self.fused_head = True  # FUSED_HEAD and this flag gate the fused head kernel
+        self._t_advanced = False  # the fused head advanced the step counter for the coming adam_step
         # backward: the weight-gradient GEMMs run on a side stream, off the dgrad critical path
         # (readout -> GATE_3 -> agg^T_2 -> GATE_2 -> WGRAD_1), so they fill the tail waves and
         # memory-bound gaps of that chain; the step joins the side stream before Adam
@@ -494,7 +495,9 @@ class Engine:
     def adam_step(self, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale: float = 1.0) -> None:
         """numerics.adam_step over all 15 tensors + operand refresh (t += 1 on the device first)."""
         self._uploaded = None  # device values now differ from the last host upload
-        _lib.call("dippm_step_counter", _p(self.t_dev), _stream())
+        if not self._t_advanced:  # (the fused head of this step already advanced it)
+            _lib.call("dippm_step_counter", _p(self.t_dev), _stream())
+        self._t_advanced = False
         self._adam_pack(1, lr, beta1, beta2, eps, grad_scale)
 
     def _f32(self, name: str) -> int:
@@ -581,7 +584,7 @@ class Engine:
         self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
 
     def _head_fused(self, b: Batch, ws: Workspace, mask_mode: int, dropout_p: float, seed: int, predict: bool,
-                    loss=None, keep_scale: float = 1.0) -> None:
+                    loss=None, keep_scale: float = 1.0, advance_step: bool = False) -> None:
         """K5/K6 in one cooperative launch (head_fused.cu): forward, and with loss = (delta,
         grad_den) the Huber loss and, on a training workspace, the whole head backward."""
         L, hp = self.L, self.L.hp
@@ -614,6 +617,9 @@ class Engine:
             a.gw3, a.gb3 = self._g32("fc3.w"), self._g32("fc3.b")
             a.du = _p(ws.du) if self.arch == "sage" else None
             a.train = 1
+            if advance_step:  # this step's t += 1 here (the adam_step that follows skips its launch)
+                a.step_counter = _p(self.t_dev)
+                self._t_advanced = True
         a.sync = _p(ws.head_sync)
         pb, ws.u_pending = getattr(ws, "u_pending", None), None
         if pb is not None:  # u's readout columns from the layer-3 block sums (dippm_pool_combine's work)
@@ -654,7 +660,8 @@ class Engine:
                   _p(ws.dout) if ws.train else None, _p(ws.loss), _stream())
         self.launches += 1
 
-    def backward(self, b: Batch, ws: Workspace, keep_scale: float = 1.0, on_partial=None) -> None:
+    def backward(self, b: Batch, ws: Workspace, keep_scale: float = 1.0, on_partial=None,
+                 advance_step: bool = False) -> None:
         """Head backward (fc3 fused kernel, fc2/fc1 tcgen05 WGRAD/GATE/STORE), readout
         backward, then per SAGE layer: agg^T + bias, WGRAD, gated dgrad GEMM."""
         s, L, hp, N = _stream(), self.L, self.L.hp, b.N
@@ -662,8 +669,11 @@ class Engine:
         if pend is not None:  # the deferred head: forward + loss + backward in one launch
             if "delta" not in pend:
                 raise RuntimeError("forward(defer_head=True) needs loss() before backward()")
+            # advance_step: an adam_step follows this backward, so the fused head may advance the
+            # device step counter itself (one launch fewer)
             self._head_fused(b, ws, pend["mask_mode"], pend["dropout_p"], pend["seed"], False,
-                             loss=(pend["delta"], pend["grad_den"]), keep_scale=keep_scale)
+                             loss=(pend["delta"], pend["grad_den"]), keep_scale=keep_scale,
+                             advance_step=advance_step)
             if self.arch == "mlp":
                 return
         else:

@@ -444,7 +444,7 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
                     ws1.masks[:, :, :model.hidden].copy_(torch.from_numpy(m.astype(np.float32)), non_blocking=True)
                 eng.forward(b, ws1, mask_mode=1 if dropout else 0, predict=False, defer_head=True)
                 eng.loss(b, ws1, config.huber_delta)
-                eng.backward(b, ws1, keep_scale=keep)
+                eng.backward(b, ws1, keep_scale=keep, advance_step=True)
                 acc.add_(ws1.loss)  # after backward: a deferred fused head computes the loss there
                 eng.adam_step(config.lr)
         else:
@@ -458,7 +458,7 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
                 eng.forward(b, ws, mask_mode=2 if dropout else 0, dropout_p=model.dropout_p,
                             seed=config.seed * 1000003 + step, predict=False, defer_head=True)
                 eng.loss(b, ws, config.huber_delta)
-                eng.backward(b, ws, keep_scale=keep)
+                eng.backward(b, ws, keep_scale=keep, advance_step=True)
                 acc.add_(ws.loss * torch.tensor([b.G, 1, 1, 1], dtype=torch.float64, device=eng.device))
                 eng.adam_step(config.lr)
         a = acc.cpu().numpy()

@@ -123,11 +123,11 @@ class BatchTrainer:
             def first_bucket(off):
                 split["off"] = off
                 self.allreduce.begin(eng.grads[off:])
-            eng.backward(b, ws, keep_scale=keep, on_partial=first_bucket)
+            eng.backward(b, ws, keep_scale=keep, on_partial=first_bucket, advance_step=True)
             self.allreduce.begin(eng.grads[:split.get("off", eng.grads.numel())])
             self.allreduce.finish()
         else:
-            eng.backward(b, ws, keep_scale=keep)
+            eng.backward(b, ws, keep_scale=keep, advance_step=True)
             if self.allreduce is not None:
                 self.allreduce(eng.grads)      # the one exchange: sum of per-rank gradient shares
         eng.adam_step(self.lr)
