@@ -42,6 +42,9 @@ PRECISIONS = {"fp32": DT_TF32X3, "bf16": DT_BF16}
 # the whole FC head in one cooperative launch (head_fused.cu) for bf16 batches of up to
 # dippm_head_fused_max_graphs() graphs; DIPPM_FUSED_HEAD=0 keeps the per-op launches
 FUSED_HEAD = os.environ.get("DIPPM_FUSED_HEAD", "1") != "0"
+# the readout's second stage as the fused head's phase 0 instead of its own launch: measured ~8 us
+# slower per step (one graph per CTA, latency-bound, plus a grid barrier), so off unless asked for
+HEAD_POOL = os.environ.get("DIPPM_HEAD_POOL", "0") == "1"
 BACKENDS = {"tc": 0, "simt": 1}
 
 
@@ -565,7 +568,7 @@ class Engine:
                        # h3's mask is read per row by the readout backward: row-major (bits_ld 0)
                        bits_ld=0 if i == 2 else ws.N, **pool)
         ws.u_pending = None
-        if fused and self.fused_head_ok(b.G):  # K4 second stage inside the fused head (its phase 0)
+        if fused and self.fused_head_ok(b.G) and HEAD_POOL:  # K4 second stage inside the fused head (phase 0)
             ws.u_pending = b
         elif fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
             _lib.call("dippm_pool_combine", _p(ws.pool_part), _p(ws.pool_graph), _p(b.graph_ptr), b.G, hp,
