@@ -179,3 +179,20 @@ def test_side_stream_weight_gradients_bit_identical():
             grads.append(eng.grads.clone())
     assert torch.equal(grads[0], grads[1])
     assert torch.equal(grads[0], grads[2])
+
+
+def test_head_phase0_readout_combine_bit_identical(monkeypatch):
+    """The optional phase 0 (u formed inside the fused head from the layer-3 block sums)
+    reproduces dippm_pool_combine exactly: same u, same loss and gradients."""
+    from paper_2303_11733_b200 import device as dev_mod
+    G = 200
+    ds = make_dataset(G, seed=19)
+    model = _model(ds, 512, seed=12)
+    b = upload_batch(*ds.collate(range(G)), device="cuda")
+    res = []
+    for flag in (False, True):
+        monkeypatch.setattr(dev_mod, "HEAD_POOL", flag)
+        eng, ws = _step(model, b, True, 0.05)
+        res.append((ws.u.t[:G].clone(), ws.loss.clone(), eng.grads.clone()))
+    for x, y in zip(res[0], res[1]):
+        assert torch.equal(x, y)
