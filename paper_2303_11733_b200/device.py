@@ -4,7 +4,8 @@ batched GraphSAGE forward / backward / Adam step over the C ABI.
 PyTorch is used for device memory (caching allocator), streams and pinned
 host buffers only; every FLOP runs in libdippm_b200.so.
 
-HBM layout (hidden H padded to Hp = ceil64(H); padded weights are zero and
+HBM layout (hidden H padded to Hp = ceil64(H), rounded up to a power of two for the SAGE
+layers (the aggregation kernels tile 8-column chunks over a warp); padded weights are zero and
 stay exactly zero under Adam, so results equal the unpadded network):
   params  fp64 [P]   master weights, reference order gnn.py:488-491, with
                      sage{l}.w_self/w_neigh adjacent -> W_cat_l [2 d_l, Hp];
@@ -112,7 +113,13 @@ class Layout:
         if arch not in ARCHS:
             raise ValueError(f"arch must be one of {ARCHS}, got {arch!r}")
         self.hidden, self.arch = hidden, arch
-        self.hp = hp = -(-hidden // 64) * 64
+        # padded width: a multiple of 64 (tensor-core K blocks); for the SAGE layers a power of two,
+        # the widths whose 8-column chunks tile a warp exactly in the aggregation kernels (64, 128,
+        # 256, 512, 1024).  Padded weights are zero and stay zero, so results equal the unpadded net.
+        hp = -(-hidden // 64) * 64
+        if arch == "sage":
+            hp = 1 << (hp - 1).bit_length()
+        self.hp = hp
         self.d_in = [FEATURE_WIDTH, hp, hp] if arch == "sage" else []
         shapes = []
         for i, d in enumerate(self.d_in, start=1):

@@ -196,3 +196,19 @@ def test_head_phase0_readout_combine_bit_identical(monkeypatch):
         res.append((ws.u.t[:G].clone(), ws.loss.clone(), eng.grads.clone()))
     for x, y in zip(res[0], res[1]):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("hidden,G", [(64, 5), (128, 33), (192, 70)])
+def test_fused_head_small_shapes_match_per_op_path(hidden, G):
+    """Narrow hidden widths (one or a few 32-column tiles, hp < 256 in the fc3 row pass) and
+    tiny / ragged batches through the fused head."""
+    ds = make_dataset(G, seed=29)
+    model = _model(ds, hidden, seed=3)
+    b = upload_batch(*ds.collate(range(G)), device="cuda")
+    e1, w1 = _step(model, b, True, 0.05)
+    e0, w0 = _step(model, b, False, 0.05)
+    assert e1.fused_head_ok(G)
+    np.testing.assert_allclose(w1.loss.cpu().numpy()[0], w0.loss.cpu().numpy()[0], rtol=2e-3)
+    g1, g0 = e1.get_grads(), e0.get_grads()
+    for name in g0:
+        assert _rel(g1[name], g0[name]) < REL, (name, _rel(g1[name], g0[name]))
