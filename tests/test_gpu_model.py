@@ -179,3 +179,20 @@ def test_reference_protocol_training_matches_golden(golden):
     assert hist == hist2  # deterministic
     for (_, a), (_, b) in zip(model.param_items(), model2.param_items()):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("hidden", [40, 200, 1000])
+def test_odd_hidden_widths_match_oracle(hidden):
+    """Hidden widths that are not powers of two are padded (64 / 256 / 1024 wide on the
+    device) with zero weights: predictions equal the fp64 oracle's at fp32 tolerance."""
+    from paper_2303_11733_b200.synth import make_dataset
+    ds = make_dataset(6, seed=31, n_lo=20, n_hi=60)
+    norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    model = gnn.create_model(hidden=hidden, seed=2, normalizer=norm)
+    recs = ds.records(range(6))
+    y, _ = gnn.predict_batch(model, [r.encoding for r in recs], [r.fs for r in recs], precision="fp32")
+    params = {k: np.array(v) for k, v in model.param_items()}
+    nd = {"y_mean": norm.y_mean, "y_std": norm.y_std, "fs_mean": norm.fs_mean, "fs_std": norm.fs_std}
+    for i, r in enumerate(recs):
+        ref = O.predict(params, nd, r.encoding.num_nodes, r.encoding.edges, r.encoding.features, r.fs.as_vector)
+        assert np.allclose(y[i], ref, rtol=1e-4, atol=1e-3 * np.abs(ref).max()), (hidden, i, y[i], ref)
