@@ -596,8 +596,10 @@ def main():
     if not args.no_e2e:
         from paper_2303_11733_b200.device import group_edges
         # the collated host batch (+ its per-graph edge offsets, as a collator emits them)
+        # (static features and targets in float64, the host layout collate_host produces)
         pinned = [[torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-                   for a in (*b, group_edges(b[1], b[2], b[3]))] for b in batches_host]
+                   for a in (*b[:4], b[4].astype(np.float64), b[5].astype(np.float64), group_edges(b[1], b[2], b[3]))]
+                  for b in batches_host]
         h2d = sum(sum(t.numel() * t.element_size() for t in b) for b in pinned) / len(pinned)
         for i in range(2):
             trainer.step_host(*pinned[i % nb])

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 6
+#define DIPPM_ABI_VERSION 7
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -229,7 +229,7 @@ int32_t dippm_splitk_reduce_t(const float* in, int32_t splits, int64_t M, int64_
  * pool_graph (see dippm_gemm_args_t).  dippm_pool_partial_rows(N) = rows of pool_partial. */
 int64_t dippm_pool_partial_rows(int64_t num_nodes);
 int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, const int32_t* graph_ptr,
-                           int64_t num_graphs, int32_t width, const float* fs_raw, const double* norm, dippm_act_t u,
+                           int64_t num_graphs, int32_t width, const double* fs_raw, const double* norm, dippm_act_t u,
                            void* stream);
 
 /* ---------------------------------------------------------------------------
@@ -239,11 +239,11 @@ int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, c
  * (zero padded so fc1 runs as a K-aligned tensor-core GEMM).
  * norm: device double[16] = y_mean[3], y_std[3], fs_mean[5], fs_std[5]. */
 int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t num_graphs, int32_t width,
-                          const float* fs_raw, const double* norm, dippm_act_t u, void* stream);
+                          const double* fs_raw, const double* norm, dippm_act_t u, void* stream);
 
 /* MLP baseline input (MlpModel.forward_norm gnn.py:253-255, normalize_fs gnn.py:96-97):
  * u[g, c] = (fs_raw[g, c] - fs_mean[c]) / fs_std[c] for c < 5, 0 for 5 <= c < cols. */
-int32_t dippm_fs_normalize(const float* fs_raw, int64_t num_graphs, const double* norm, dippm_act_t u,
+int32_t dippm_fs_normalize(const double* fs_raw, int64_t num_graphs, const double* norm, dippm_act_t u,
                            int32_t cols, void* stream);
 
 /* ---------------------------------------------------------------------------
@@ -268,11 +268,11 @@ int32_t dippm_fc3_backward(dippm_act_t x3, int64_t num_graphs, int32_t width, co
 int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, void* stream);
 
 /* Huber loss + gradient, numerics.py:58-73, averaged over the batch
- * (gnn.py:398-404): dout[g] = grad_g / G (dout may be NULL).  y_raw [G,3] fp32
+ * (gnn.py:398-404): dout[g] = grad_g / G (dout may be NULL).  y_raw [G,3] fp64
  * targets are normalised on device (gnn.py:90-91).  loss_out: device double[4]
  * = {mean loss, sum APE latency, memory, energy} (APE on de-normalised
  * outputs, gnn.py:458-459). */
-int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t num_graphs, const double* norm,
+int32_t dippm_huber(const float* out_norm, const double* y_raw, int64_t num_graphs, const double* norm,
                     double delta, double grad_den, float* dout, double* loss_out, void* stream);
 /*   grad_den: denominator of dout (<= 0: num_graphs).  Data-parallel training passes the
  *   GLOBAL batch size so the all-reduced sum of per-rank gradients is the global mean. */
@@ -315,7 +315,7 @@ typedef struct dippm_head_args {
   double* y_pred;                /* [G, 3] or NULL */
   int8_t* mig;
   int32_t* nonfinite;
-  const float* y_raw;            /* [G, 3] targets or NULL (no loss) */
+  const double* y_raw;           /* [G, 3] fp64 targets or NULL (no loss) */
   double delta, grad_den;
   double* loss_out;              /* double[4] */
   double* row_loss;              /* scratch double [G, 4] */
@@ -328,11 +328,11 @@ typedef struct dippm_head_args {
   int32_t train;
   /* optional (all four or none): u's readout columns are formed in-kernel from the layer-3
    * FWD epilogue's block sums, exactly as dippm_pool_combine does (then u is written, not read
-   * from a separate launch); fs_raw [G, 5] fp32. */
+   * from a separate launch); fs_raw [G, 5] fp64. */
   const float* pool_partial;
   const float* pool_graph;
   const int32_t* graph_ptr;
-  const float* fs_raw;
+  const double* fs_raw;
   /* optional (training): step_counter[0] += 1 once every CTA is past the forward's dropout
    * draws (which read it through seed_dev) -- dippm_step_counter folded into this launch. */
   int64_t* step_counter;
@@ -369,6 +369,48 @@ int32_t dippm_step_counter(int64_t* t_dev, void* stream);
 /* Pack a fp64 matrix into a compute copy (tests / single-layer API):
  *  w [rows, cols] fp64 row-major -> dst view; transpose != 0 writes dst[c, r]. */
 int32_t dippm_pack(const double* w, int64_t rows, int64_t cols, int32_t transpose, dippm_act_t dst, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * fp64 numerics of the drop-in `numerics` module (numerics.py:23-114), bit-exact
+ * with numpy for the element-wise operations (no FMA contraction, same operation
+ * order) and for the Huber mean (numpy's pairwise summation order).
+ *
+ * numerics.py:58-73 huber_loss over n >= 1 elements: grad[i] = dL/dpred[i], elems[i]
+ * the per-element loss (scratch, n doubles), loss[0] = mean.  Two launches. */
+int32_t dippm_huber_f64(const double* pred, const double* target, int64_t n, double delta, double* grad,
+                        double* elems, double* loss, void* stream);
+/* numerics.py:93-114 adam_step on n elements: m, v updated in place, param_out = new value
+ * (may alias param).  The scalars one_minus_beta{1,2} = 1 - beta and bias_corr{1,2} =
+ * 1 - beta**t are passed from the host exactly as the reference computes them. */
+int32_t dippm_adam(const double* param, const double* grad, double* m, double* v, double* param_out, int64_t n,
+                   double lr, double beta1, double beta2, double eps, double one_minus_beta1,
+                   double one_minus_beta2, double bias_corr1, double bias_corr2, void* stream);
+/* numerics.py:31-42: op 0 out = a + b, op 1 out = a * s, op 2 out = max(a, 0) (NaN kept). */
+int32_t dippm_elementwise_f64(int32_t op, const double* a, const double* b, double s, double* out, int64_t n,
+                              void* stream);
+/* numerics.py:23-28: c[M,N] = a[M,K] @ b[K,N], fp64 row-major. */
+int32_t dippm_dgemm(const double* a, const double* b, double* c, int64_t M, int64_t K, int64_t N, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * MIG-pick parity of the bf16 predict path (mig.py:32-45): graphs whose
+ * bf16-predicted memory (y_pred [G,3] fp64, column 1) lies within band_mb of a profile
+ * ceiling are re-scored in fp32.  Edges must be grouped by graph (edge_ptr [G+1]).
+ *
+ * Select (one launch): sel_idx [G] gets the band graphs in order, sel_node_ptr [G+1] int32 /
+ * sel_edge_ptr [G+1] int64 the exclusive prefix sums of their node / edge counts (the
+ * sub-batch's graph_ptr / edge_ptr), totals[3] = {count, nodes, edges} (device). */
+int32_t dippm_mig_band_select(const double* y_pred, int64_t num_graphs, double band_mb, const int32_t* graph_ptr,
+                              const int64_t* edge_ptr, int32_t* sel_idx, int32_t* sel_node_ptr, int64_t* sel_edge_ptr,
+                              int64_t* totals, void* stream);
+/* Gather the count selected graphs into a compact sub-batch: x_out [nodes, 32] f32, edges
+ * re-based onto the sub-batch's node ids, fs_out [count, 5] fp64.  One CTA per graph. */
+int32_t dippm_gather_graphs(const int32_t* sel_idx, int64_t count, const int32_t* sel_node_ptr,
+                            const int64_t* sel_edge_ptr, const int32_t* graph_ptr, const int64_t* edge_ptr,
+                            const float* x, const int64_t* src, const int64_t* dst, const double* fs, float* x_out,
+                            int64_t* src_out, int64_t* dst_out, double* fs_out, void* stream);
+/* y_pred[sel_idx[k]] = y_sub[k], mig[sel_idx[k]] = mig_sub[k] for k < count. */
+int32_t dippm_scatter_rescore(const int32_t* sel_idx, int64_t count, const double* y_sub, const int8_t* mig_sub,
+                              double* y_pred, int8_t* mig, void* stream);
 
 #ifdef __cplusplus
 }

@@ -76,10 +76,10 @@ void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int
  *   x32       float  [total_nodes, 32]  feature rows rounded to fp32
  *   src, dst  int64  [total_edges]      edge endpoints as batch-global node ids
  *   graph_ptr int32  [count + 1]        node offsets; edge_ptr int64 [count + 1] edge offsets
- *   fs32      float  [count, 5]         log1p static features (fs_log) rounded to fp32
+ *   fs64      double [count, 5]         log1p static features (fs_log, StaticFeatures.as_vector)
  * Failed documents contribute no nodes or edges (callers normally reject the batch first). */
 void dippm_feat_collate(const dippm_feat_batch* b, float* x32, int64_t* src, int64_t* dst, int32_t* graph_ptr,
-                        int64_t* edge_ptr, float* fs32);
+                        int64_t* edge_ptr, double* fs64);
 /* Per-document metadata in one call (any pointer may be NULL):
  *   status  int32 [count]      (dippm_feat_status codes)
  *   fs_log  double [count, 5]  StaticFeatures.as_vector = log1p of the five integers (featurize.py:76-87)

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 6  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 7  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -119,6 +119,13 @@ SIGNATURES = {
     "dippm_adam_pack": (I32, [P, P, P, P, F64, I64, I64, P, F64, F64, F64, F64, I32, P, C.POINTER(PackSeg), I32, P]),
     "dippm_step_counter": (I32, [P, P]),
     "dippm_pack": (I32, [P, I64, I64, I32, Act, P]),
+    "dippm_huber_f64": (I32, [P, P, I64, F64, P, P, P, P]),
+    "dippm_adam": (I32, [P, P, P, P, P, I64, F64, F64, F64, F64, F64, F64, F64, F64, P]),
+    "dippm_elementwise_f64": (I32, [I32, P, P, F64, P, I64, P]),
+    "dippm_dgemm": (I32, [P, P, P, I64, I64, I64, P]),
+    "dippm_mig_band_select": (I32, [P, I64, F64, P, P, P, P, P, P, P]),
+    "dippm_gather_graphs": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "dippm_scatter_rescore": (I32, [P, I64, P, P, P, P, P]),
 }
 
 _lib = None

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdippm_b200.so"
-SOURCES = ["capi.cu", "csr.cu", "aggregate.cu", "head.cu", "head_fused.cu", "tc_gemm.cu"]
+SOURCES = ["capi.cu", "csr.cu", "aggregate.cu", "head.cu", "head_fused.cu", "tc_gemm.cu", "numerics.cu", "rescore.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -52,16 +52,21 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "dippm_b200.h"]
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         s = CSRC / src
         o = objdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
-            if verbose:
-                print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
+            cmds.append([NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)])
+    # the translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    for cmd in cmds:
+        if verbose:
+            print(" ".join(cmd))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for f in [pool.submit(subprocess.run, cmd, check=True) for cmd in cmds]:
+            f.result()
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(LIB), *map(str, objs), "-lcuda"]
         if verbose:

@@ -231,7 +231,7 @@ class Corpus:
             if len(ids) else np.zeros(0, np.int64)
         x = self.x[node_rows]
         e = self.edges[edge_rows].astype(np.int64) + np.repeat(gp[:-1].astype(np.int64), ne)[:, None]
-        return (x, e[:, 0].copy(), e[:, 1].copy(), gp, self.fs[ids].astype(np.float32), self.y[ids].astype(np.float32),
+        return (x, e[:, 0].copy(), e[:, 1].copy(), gp, self.fs[ids].astype(np.float64), self.y[ids].astype(np.float64),
                 ep)
 
     def records(self, ids=None) -> list:

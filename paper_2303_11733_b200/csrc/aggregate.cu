@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(1024) k_reduce_rows(const float* __restrict__ 
 constexpr int kPoolThreads = 512;
 template <int DT, int CPL>
 __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const int* __restrict__ graph_ptr,
-                                                              int width, const float* __restrict__ fs_raw,
+                                                              int width, const double* __restrict__ fs_raw,
                                                               const double* __restrict__ norm, ActView u) {
   extern __shared__ float s_part[];  // [slots][width]
   const int g = blockIdx.x;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const i
     if (k < kStaticWidth) {
       const double* fs_mean = norm + 6;
       const double* fs_std = norm + 11;
-      v = (float)(((double)fs_raw[g * kStaticWidth + k] - fs_mean[k]) / fs_std[k]);
+      v = (float)((fs_raw[g * kStaticWidth + k] - fs_mean[k]) / fs_std[k]);
     }
     act_store(u, g, width + k, v);
   }
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const i
 // sums it owns in fixed block order, divided by N_g; then the static features.
 __global__ void __launch_bounds__(256) k_pool_combine(const float* __restrict__ part, const float* __restrict__ whole,
                                                       const int* __restrict__ graph_ptr, int width,
-                                                      const float* __restrict__ fs_raw, const double* __restrict__ norm,
+                                                      const double* __restrict__ fs_raw, const double* __restrict__ norm,
                                                       ActView u) {
   const int g = blockIdx.x;
   const int gs = graph_ptr[g], ge = graph_ptr[g + 1];
@@ -658,20 +658,20 @@ __global__ void __launch_bounds__(256) k_pool_combine(const float* __restrict__ 
   }
   for (int k = threadIdx.x; k < u.ld - width; k += blockDim.x) {
     float v = 0.f;
-    if (k < kStaticWidth) v = (float)(((double)fs_raw[g * kStaticWidth + k] - norm[6 + k]) / norm[11 + k]);
+    if (k < kStaticWidth) v = (float)((fs_raw[g * kStaticWidth + k] - norm[6 + k]) / norm[11 + k]);
     act_store(u, g, width + k, v);
   }
 }
 
 // MLP baseline input (gnn.py:253-255 with normalize_fs :96-97): u[g] = [(fs-mu)/sigma | 0].
-__global__ void k_fs_normalize(const float* __restrict__ fs_raw, int64_t G, const double* __restrict__ norm,
+__global__ void k_fs_normalize(const double* __restrict__ fs_raw, int64_t G, const double* __restrict__ norm,
                                ActView u, int cols) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G * cols) return;
   const int64_t g = i / cols;
   const int c = (int)(i % cols);
   float v = 0.f;
-  if (c < kStaticWidth) v = (float)(((double)fs_raw[g * kStaticWidth + c] - norm[6 + c]) / norm[11 + c]);
+  if (c < kStaticWidth) v = (float)((fs_raw[g * kStaticWidth + c] - norm[6 + c]) / norm[11 + c]);
   act_store(u, g, c, v);
 }
 
@@ -859,7 +859,7 @@ int32_t dippm_reduce_rows(const float* in, int64_t rows, int64_t ld, int32_t col
   return DIPPM_OK;
 }
 
-int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, int32_t width, const float* fs_raw,
+int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, int32_t width, const double* fs_raw,
                           const double* norm, dippm_act_t u, void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && width >= 8 && width % 8 == 0 && u.ld >= width + 5, "pool_concat: bad args");
   const int cpl = cpl_for(width);
@@ -890,7 +890,7 @@ int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, in
 int64_t dippm_pool_partial_rows(int64_t num_nodes) { return 2 * ((num_nodes + 31) / 32); }
 
 int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, const int32_t* graph_ptr, int64_t G,
-                           int32_t width, const float* fs_raw, const double* norm, dippm_act_t u, void* stream) {
+                           int32_t width, const double* fs_raw, const double* norm, dippm_act_t u, void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && width >= 1 && u.ld >= width + kStaticWidth, "pool_combine: bad args");
   k_pool_combine<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(pool_partial, pool_graph, graph_ptr, width, fs_raw,
                                                                norm, make_view(u));
@@ -898,7 +898,7 @@ int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, c
   return DIPPM_OK;
 }
 
-int32_t dippm_fs_normalize(const float* fs_raw, int64_t G, const double* norm, dippm_act_t u, int32_t cols,
+int32_t dippm_fs_normalize(const double* fs_raw, int64_t G, const double* norm, dippm_act_t u, int32_t cols,
                            void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && cols >= kStaticWidth && cols <= u.ld, "fs_normalize: bad shape");
   k_fs_normalize<<<ceil_div_i(G * cols, 256), 256, 0, (cudaStream_t)stream>>>(fs_raw, G, norm, make_view(u), cols);

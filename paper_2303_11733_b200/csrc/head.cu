@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) k_colsum_act(ActView a, int64_t rows, int
 }
 
 // numerics.py:58-73 per graph, mean over the batch (gnn.py:402-404).
-__global__ void k_huber(const float* __restrict__ out, const float* __restrict__ y_raw, int64_t G,
+__global__ void k_huber(const float* __restrict__ out, const double* __restrict__ y_raw, int64_t G,
                         const double* __restrict__ norm, double delta, double grad_den, float* __restrict__ dout,
                         double* __restrict__ loss_out) {
   __shared__ double s_loss[256], s_ape[3][256];
@@ -293,7 +293,7 @@ __global__ void k_huber(const float* __restrict__ out, const float* __restrict__
     double le = 0.0;
     for (int k = 0; k < 3; ++k) {
       double pred = (double)out[g * 3 + k];
-      double y = (double)y_raw[g * 3 + k];
+      double y = y_raw[g * 3 + k];
       double t = (y - norm[k]) / norm[3 + k];
       double r = pred - t, a = fabs(r);
       bool quad = a <= delta;
@@ -353,7 +353,7 @@ int32_t dippm_colsum_act(dippm_act_t a, int64_t rows, int32_t cols, float* out, 
   return DIPPM_OK;
 }
 
-int32_t dippm_huber(const float* out_norm, const float* y_raw, int64_t G, const double* norm, double delta,
+int32_t dippm_huber(const float* out_norm, const double* y_raw, int64_t G, const double* norm, double delta,
                     double grad_den, float* dout, double* loss_out, void* stream) {
   DIPPM_ARG_CHECK(G >= 1 && delta > 0, "huber: bad args");
   k_huber<<<1, 256, 0, (cudaStream_t)stream>>>(out_norm, y_raw, G, norm, delta, grad_den > 0 ? grad_den : (double)G,

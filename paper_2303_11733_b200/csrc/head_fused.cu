@@ -47,7 +47,7 @@ struct Args {
   double* y_pred;
   int8_t* mig;
   int* nonfinite;
-  const float* y_raw;
+  const double* y_raw;
   double delta, grad_den;
   double* loss_out;
   float* dout;
@@ -57,7 +57,8 @@ struct Args {
   float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3, *du;
   int* sync;
   int train;
-  const float *pool_part, *pool_graph, *fs_raw;  // phase 0 (optional): u from the readout's block sums
+  const float *pool_part, *pool_graph;
+  const double* fs_raw;  // phase 0 (optional): u from the readout's block sums
   const int* graph_ptr;
   long long* step_counter;  // incremented in phase E (after every CTA's dropout draws)
 };
@@ -558,7 +559,7 @@ __device__ void head_rows(const Args& a) {
       if (a.y_raw) {  // k_huber's per-graph terms (head.cu)
         double le = 0.0;
         for (int k = 0; k < 3; ++k) {
-          const double pred = (double)o3[k], y = (double)a.y_raw[g * 3 + k];
+          const double pred = (double)o3[k], y = a.y_raw[g * 3 + k];
           const double t = (y - a.norm[k]) / a.norm[3 + k];
           const double r = pred - t, ab = fabs(r);
           const bool quad = ab <= a.delta;
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
       }
       for (int k = threadIdx.x; k < a.uw - a.hp; k += kThreads) {
         float v = 0.f;
-        if (k < kStaticWidth) v = (float)(((double)a.fs_raw[g * kStaticWidth + k] - a.norm[6 + k]) / a.norm[11 + k]);
+        if (k < kStaticWidth) v = (float)((a.fs_raw[g * kStaticWidth + k] - a.norm[6 + k]) / a.norm[11 + k]);
         u[(int64_t)g * a.uw + a.hp + k] = __float2bfloat16_rn(v);
       }
     }

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -60,6 +61,16 @@ def require_device(device=None) -> torch.device:
     if not torch.cuda.is_available():
         raise _lib.DeviceUnavailable("no CUDA device visible; the DIPPM B200 path has no CPU fallback")
     return torch.device(device if device is not None else "cuda")
+
+
+_libc = C.CDLL(None)
+_libc.memcmp.restype = C.c_int
+_libc.memcmp.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+
+
+def _same_bytes(a: np.ndarray, b: np.ndarray) -> bool:
+    """Byte equality of two C-contiguous arrays (memcmp)."""
+    return a.nbytes == b.nbytes and (a.nbytes == 0 or _libc.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0)
 
 
 def _p(t) -> int | None:
@@ -196,8 +207,8 @@ class Batch:
     src: torch.Tensor        # i64 [E]
     dst: torch.Tensor        # i64 [E]
     graph_ptr: torch.Tensor  # i32 [G+1]
-    fs: torch.Tensor         # f32 [G, 5] log1p static features
-    y: torch.Tensor | None   # f32 [G, 3] raw targets
+    fs: torch.Tensor         # f64 [G, 5] log1p static features
+    y: torch.Tensor | None   # f64 [G, 3] raw targets
     rowptr: torch.Tensor | None = None
     col: torch.Tensor | None = None
     deg: torch.Tensor | None = None
@@ -214,13 +225,22 @@ class Batch:
 
 def group_edges(src, dst, graph_ptr):
     """edge_ptr [G+1] if the edge list is a concatenation of per-graph edge lists
-    (what collation produces), else None.  Host-side, O(E)."""
+    (what collation produces), else None.  Host-side, O(E).
+
+    Also the host validation of a collated batch (the reference builds each graph's
+    aggregation matrix from its own edges, gnn.py:130-137): an endpoint outside
+    [0, N) or an edge joining two graphs raises ShapeMismatch."""
     src, dst, gp = np.asarray(src), np.asarray(dst), np.asarray(graph_ptr, dtype=np.int64)
     G = len(gp) - 1
     if len(dst) == 0:
         return np.zeros(G + 1, np.int64)
+    n = int(gp[-1])
+    if min(int(src.min()), int(dst.min())) < 0 or max(int(src.max()), int(dst.max())) >= n:
+        raise ShapeMismatch(f"edge endpoint outside [0, {n})")
     gd = np.searchsorted(gp, dst, side="right") - 1
-    if np.any(np.diff(gd) < 0) or np.any(np.searchsorted(gp, src, side="right") - 1 != gd):
+    if np.any(np.searchsorted(gp, src, side="right") - 1 != gd):
+        raise ShapeMismatch("edge joins two different graphs of the batch")
+    if np.any(np.diff(gd) < 0):
         return None
     ep = np.zeros(G + 1, np.int64)
     np.cumsum(np.bincount(gd, minlength=G), out=ep[1:])
@@ -257,26 +277,38 @@ def collate_host(encodings, fs_vectors, targets=None):
     x = np.concatenate(xs).astype(np.float32) if G else np.zeros((0, FEATURE_WIDTH), np.float32)
     src = np.concatenate(srcs) if G else np.zeros(0, np.int64)
     dst = np.concatenate(dsts) if G else np.zeros(0, np.int64)
-    fs = np.asarray(fs_vectors, dtype=np.float32).reshape(G, STATIC_WIDTH)
-    y = None if targets is None else np.asarray(targets, dtype=np.float32).reshape(G, 3)
+    # static features and targets stay float64 (StaticFeatures.as_vector, TargetVector.as_array):
+    # the device z-scores them in fp64, so a small fs / y std cannot amplify an fp32 rounding
+    fs = np.asarray(fs_vectors, dtype=np.float64).reshape(G, STATIC_WIDTH)
+    y = None if targets is None else np.asarray(targets, dtype=np.float64).reshape(G, 3)
     return x, src, dst, graph_ptr, fs, y
 
 
-def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=True, edge_ptr=None) -> Batch:
-    """Pinned host -> device copies of a collated batch, then K1 CSR on device."""
+def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=True, edge_ptr=None,
+                 validate=True) -> Batch:
+    """Pinned host -> device copies of a collated batch, then K1 CSR on device.
+
+    validate: host check of the edge endpoints (group_edges); False leaves bad edges to
+    the device flag `Batch.bad` (kernel tests)."""
     dev = torch.device(device)
 
-    def h2d(a):
+    def h2d(a, dtype=None):
         # already-pinned tensors copy asynchronously; numpy arrays go straight from pageable
         # memory (a fresh pinned staging buffer per call costs more than it saves)
         t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
-        return t.to(dev, non_blocking=t.is_pinned())
+        return t.to(dev, dtype=dtype, non_blocking=t.is_pinned())
 
     if edge_ptr is None:
-        edge_ptr = group_edges(src, dst, graph_ptr)
+        try:
+            edge_ptr = group_edges(src, dst, graph_ptr)
+        except ShapeMismatch:
+            if validate:
+                raise
+            edge_ptr = None
     arrays = [x, src, dst, graph_ptr, fs] + ([y] if y is not None else [])
     b = Batch(G=int(len(graph_ptr) - 1), N=int(graph_ptr[-1]), E=int(len(src)), x=h2d(x), src=h2d(src),
-              dst=h2d(dst), graph_ptr=h2d(graph_ptr), fs=h2d(fs), y=None if y is None else h2d(y),
+              dst=h2d(dst), graph_ptr=h2d(graph_ptr), fs=h2d(fs, torch.float64),
+              y=None if y is None else h2d(y, torch.float64),
               h2d_bytes=int(sum(np.asarray(a).nbytes for a in arrays)))
     if edge_ptr is not None:
         b.edge_ptr = h2d(edge_ptr if isinstance(edge_ptr, torch.Tensor) else np.asarray(edge_ptr, np.int64))
@@ -401,6 +433,8 @@ class Engine:
     """Device-resident DIPPM GraphSAGE network (weights, Adam state, GEMM operand copies)."""
 
     def __init__(self, hidden: int, precision: str = "fp32", device=None, backend: str = "tc", arch: str = "sage"):
+        """backend is test-only: "simt" selects the library's SIMT GEMM anchor, which the kernel
+        tests compare the tcgen05 path against.  The package itself always runs "tc"."""
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
         if backend not in BACKENDS:
@@ -417,6 +451,8 @@ class Engine:
         self.grads = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.p32 = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.norm = torch.zeros(16, **f64)
+        # [y_mean | y_std | 0 | 1]: for callers that hand over fs already normalised (forward_norm)
+        self.norm_fs_id = torch.zeros(16, **f64)
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)  # Adam step count (graph-safe)
         hp, dt, d = L.hp, self.dtype, self.device
         self.Wf = [ActBuf(2 * di, hp, dt, d) for di in L.d_in]
@@ -443,34 +479,46 @@ class Engine:
         self.overlap_wgrad = os.environ.get("DIPPM_OVERLAP_WGRAD", "1") != "0"
         self._side = None
         self.head_fused_max = int(_lib.load().dippm_head_fused_max_graphs())
+        self._lock = threading.Lock()  # parameter uploads vs concurrent read-only predict calls
 
     # -- parameters -----------------------------------------------------------
     def set_params(self, items, normalizer) -> None:
         """Upload the host model's current values (padded layout) and refresh the operand copies.
-        Skipped when the values are bit-identical to the last upload (repeated predict calls)."""
-        items = [(name, np.asarray(arr, np.float64)) for name, arr in items]
+        Skipped when the values are byte-identical to the last upload (repeated predict calls):
+        one memcmp per tensor, ~13 MB at hidden 512, instead of an elementwise compare."""
+        items = [(name, np.ascontiguousarray(arr, np.float64)) for name, arr in items]
         norm = np.concatenate([np.asarray(normalizer.y_mean, np.float64), np.asarray(normalizer.y_std, np.float64),
                                np.asarray(normalizer.fs_mean, np.float64), np.asarray(normalizer.fs_std, np.float64)])
-        last = getattr(self, "_uploaded", None)
-        if (last is not None and np.array_equal(last[1], norm) and len(last[0]) == len(items)
-                and all(n0 == n1 and a0.shape == a1.shape and np.array_equal(a0, a1)
-                        for (n0, a0), (n1, a1) in zip(last[0], items))):
-            return
-        host = np.zeros(self.L.total, dtype=np.float64)
-        for name, arr in items:
-            off = self.L.offsets[name]
-            padded = self.L.pad(name, arr)
-            host[off:off + padded.size] = padded.ravel()
-        self.params.copy_(torch.from_numpy(host), non_blocking=False)
-        self.set_normalizer(normalizer)
-        self.refresh()
-        self._uploaded = ([(name, arr.copy()) for name, arr in items], norm)
+        with self._lock:
+            last = getattr(self, "_uploaded", None)
+            if (last is not None and _same_bytes(last[1], norm) and len(last[0]) == len(items)
+                    and all(n0 == n1 and a0.shape == a1.shape and _same_bytes(a0, a1)
+                            for (n0, a0), (n1, a1) in zip(last[0], items))):
+                return
+            host = np.zeros(self.L.total, dtype=np.float64)
+            for name, arr in items:
+                off = self.L.offsets[name]
+                padded = self.L.pad(name, arr)
+                host[off:off + padded.size] = padded.ravel()
+            self.params.copy_(torch.from_numpy(host), non_blocking=False)
+            self.set_normalizer(normalizer)
+            self.refresh()
+            self._uploaded = ([(name, arr.copy()) for name, arr in items], norm)
+
+    def check_batch(self, b: "Batch") -> None:
+        """Raise ShapeMismatch if K1 flagged an edge endpoint outside its graph (synchronises;
+        the per-call drop-in paths read results back right after anyway)."""
+        if b.bad is not None and int(b.bad[0].item()):
+            raise ShapeMismatch("edge endpoint outside its graph's node range")
 
     def set_normalizer(self, norm) -> None:
         self._uploaded = None
         vec = np.concatenate([np.asarray(norm.y_mean, np.float64), np.asarray(norm.y_std, np.float64),
                               np.asarray(norm.fs_mean, np.float64), np.asarray(norm.fs_std, np.float64)])
         self.norm.copy_(torch.from_numpy(vec))
+        vec = vec.copy()
+        vec[6:11], vec[11:16] = 0.0, 1.0
+        self.norm_fs_id.copy_(torch.from_numpy(vec))
 
     def reset_adam(self) -> None:
         self.m.zero_()
@@ -545,16 +593,20 @@ class Engine:
                 and self.L.hp <= 512 and self.L.u_width <= 576 and G <= self.head_fused_max)
 
     def forward(self, b: Batch, ws: Workspace, mask_mode: int = 0, dropout_p: float = 0.0, seed: int = 0,
-                predict: bool = True, defer_head: bool = False) -> None:
+                predict: bool = True, defer_head: bool = False, fs_normalized: bool = False) -> None:
         """Eval (mask_mode 0) or train-mode forward (1: masks in ws.masks, 2: generated):
         K2 aggregation -> K3 GEMM x3, K4 pooling, K5 head (2 GEMMs + fc3).
 
         defer_head (training steps: forward -> loss -> backward): when the fused head kernel
         covers the batch, the head is not run here; loss() records its arguments and backward()
-        runs forward, loss and backward of the head in one launch."""
+        runs forward, loss and backward of the head in one launch.
+
+        fs_normalized: b.fs already holds normalised static features (the model protocol's
+        forward_norm receives fs_norm, gnn.py:212), so the device z-score is the identity."""
         s, L, hp = _stream(), self.L, self.L.hp
+        fs_norm = self.norm_fs_id if fs_normalized else self.norm
         if self.arch == "mlp":  # MlpModel.forward_norm (gnn.py:253-255): the head on [fs_norm | 0]
-            _lib.call("dippm_fs_normalize", _p(b.fs), b.G, _p(self.norm), ws.u.view(), L.u_width, s)
+            _lib.call("dippm_fs_normalize", _p(b.fs), b.G, _p(fs_norm), ws.u.view(), L.u_width, s)
             self.launches += 1
             self._head_or_defer(b, ws, mask_mode, dropout_p, seed, predict, defer_head)
             return
@@ -575,13 +627,13 @@ class Engine:
                        # h3's mask is read per row by the readout backward: row-major (bits_ld 0)
                        bits_ld=0 if i == 2 else ws.N, **pool)
         ws.u_pending = None
-        if fused and self.fused_head_ok(b.G) and HEAD_POOL:  # K4 second stage inside the fused head (phase 0)
+        if fused and self.fused_head_ok(b.G) and HEAD_POOL and not fs_normalized:  # K4 second stage inside the fused head (phase 0)
             ws.u_pending = b
         elif fused:  # K4 second stage: means from the block sums + static features (gnn.py:214-215)
             _lib.call("dippm_pool_combine", _p(ws.pool_part), _p(ws.pool_graph), _p(b.graph_ptr), b.G, hp,
-                      _p(b.fs), _p(self.norm), ws.u.view(), s)
+                      _p(b.fs), _p(fs_norm), ws.u.view(), s)
         else:
-            _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(self.norm),
+            _lib.call("dippm_pool_concat", ws.H3.view(0), _p(b.graph_ptr), b.G, hp, _p(b.fs), _p(fs_norm),
                       ws.u.view(), s)
         self.launches += 3 + 1
         self._head_or_defer(b, ws, mask_mode, dropout_p, seed, predict, defer_head)
@@ -741,3 +793,49 @@ class Engine:
             ev.record(side)
             main.wait_event(ev)
         self.launches += 5 + 3 * 2 - 3 - 1
+
+
+# ---------------------------------------------------------------------------
+# MIG-pick parity of the bf16 predict path
+
+# the re-score band in normalised units: the stated bf16 tolerance of the normalised
+# outputs; times y_std[memory] it is the band in MB around each ceiling
+BF16_MIG_BAND = 2e-2
+
+
+def mig_band_rescore(eng32: "Engine", b: Batch, ws: Workspace, band_mb: float, holder) -> int:
+    """Re-score in fp32 the graphs of batch `b` whose bf16-predicted memory (ws.y_pred) lies
+    within band_mb of a MIG ceiling, and write their fp32 predictions and picks back into
+    ws.y_pred / ws.mig.  Outside the band the bf16 pick equals the reference's (the bf16
+    error is below the band); inside it the fp32 pick does, except within the fp32
+    tolerance of a ceiling.  Device-side select / gather / scatter (rescore.cu); one small
+    read-back of the band size.  Returns the number of graphs re-scored."""
+    if b.edge_ptr is None:
+        raise ShapeMismatch("MIG re-score needs edges grouped by graph (edge_ptr)")
+    dv, G = b.x.device, b.G
+    i32, i64 = dict(dtype=torch.int32, device=dv), dict(dtype=torch.int64, device=dv)
+    sel_idx, node_ptr = torch.empty(G, **i32), torch.empty(G + 1, **i32)
+    edge_ptr, totals = torch.empty(G + 1, **i64), torch.empty(3, **i64)
+    s = _stream()
+    _lib.call("dippm_mig_band_select", _p(ws.y_pred), G, float(band_mb), _p(b.graph_ptr), _p(b.edge_ptr),
+              _p(sel_idx), _p(node_ptr), _p(edge_ptr), _p(totals), s)
+    count, nodes, edges = (int(v) for v in totals.cpu().tolist())
+    if count == 0:
+        return 0
+    f32 = dict(dtype=torch.float32, device=dv)
+    x, fs = torch.empty(nodes, FEATURE_WIDTH, **f32), torch.empty(count, STATIC_WIDTH, dtype=torch.float64, device=dv)
+    src, dst = torch.empty(max(edges, 1), **i64), torch.empty(max(edges, 1), **i64)
+    _lib.call("dippm_gather_graphs", _p(sel_idx), count, _p(node_ptr), _p(edge_ptr), _p(b.graph_ptr), _p(b.edge_ptr),
+              _p(b.x), _p(b.src), _p(b.dst), _p(b.fs), _p(x), _p(src), _p(dst), _p(fs), s)
+    sub = Batch(G=count, N=nodes, E=edges, x=x, src=src[:edges], dst=dst[:edges], graph_ptr=node_ptr[:count + 1],
+                fs=fs, y=None, edge_ptr=edge_ptr[:count + 1], max_nodes=b.max_nodes, max_edges=b.max_edges)
+    if eng32.arch == "sage":
+        build_batch_csr(sub)
+    ws32 = getattr(holder, "rescore_ws", None)
+    if ws32 is None or ws32.N < nodes or ws32.G < count:
+        holder.rescore_ws = ws32 = None
+        ws32 = Workspace(eng32, max(nodes, b.N // 8), max(count, G // 8), train=False)
+        holder.rescore_ws = ws32
+    eng32.forward(sub, ws32, predict=True)
+    _lib.call("dippm_scatter_rescore", _p(sel_idx), count, _p(ws32.y_pred), _p(ws32.mig), _p(ws.y_pred), _p(ws.mig), s)
+    return count

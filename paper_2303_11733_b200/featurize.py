@@ -180,7 +180,7 @@ class FeaturizedBatch:
             raise err
 
     def collate(self):
-        """(x f32, src, dst, graph_ptr, fs f32, edge_ptr) over all documents, node ids
+        """(x f32, src, dst, graph_ptr, fs f64, edge_ptr) over all documents, node ids
         batch-global — the arrays device.upload_batch takes.  Raises the first error."""
         self.raise_first_error()
         x = self.x32 if self.x32 is not None else self.x.astype(np.float32)  # noqa: E501
@@ -188,7 +188,7 @@ class FeaturizedBatch:
         off = np.repeat(self.node_ptr[:-1], self.ne)
         src = self.edges[:, 0] + off
         dst = self.edges[:, 1] + off
-        return x, src, dst, gp, self.fs_vectors().astype(np.float32), self.edge_ptr
+        return x, src, dst, gp, self.fs_vectors().astype(np.float64), self.edge_ptr
 
     def collate_pinned(self):
         """collate() written by the native library straight into pinned host tensors
@@ -204,7 +204,7 @@ class FeaturizedBatch:
         x = pinned((N, FEATURE_WIDTH), torch.float32)
         src, dst = pinned((E,), torch.int64), pinned((E,), torch.int64)
         gp, ep = pinned((G + 1,), torch.int32), pinned((G + 1,), torch.int64)
-        fs = pinned((G, STATIC_WIDTH), torch.float32)
+        fs = pinned((G, STATIC_WIDTH), torch.float64)
         _host().dippm_feat_collate(self._h, x.data_ptr(), src.data_ptr(), dst.data_ptr(), gp.data_ptr(),
                                    ep.data_ptr(), fs.data_ptr())
         return x, src, dst, gp, fs, ep
@@ -228,7 +228,7 @@ def static_features(graph, batch_size: int | None = None) -> StaticFeatures:
 
 
 def predict_documents(model, docs, batch_sizes=None, precision: str = "fp32", threads: int = 0,
-                      chunk: int = 0):
+                      chunk: int = 0, info: dict | None = None):
     """The `dippm predict` path (cli.py:148-172) for many documents at once:
     native featurisation, one device pass (gnn.predict_batch semantics).
     Returns (y float64 [G, 3] latency_ms / memory_mb / energy_j, MIG codes int8 [G], names).
@@ -240,7 +240,7 @@ def predict_documents(model, docs, batch_sizes=None, precision: str = "fp32", th
     document raises the same exception."""
     if chunk <= 0 or len(docs) <= chunk:
         fb = featurize_documents(docs, batch_sizes, threads)
-        y, mig = predict_featurized(model, fb, precision)
+        y, mig = predict_featurized(model, fb, precision, info=info)
         return y, mig, fb.names
     from concurrent.futures import ThreadPoolExecutor
     spans = [(a, min(a + chunk, len(docs))) for a in range(0, len(docs), chunk)]
@@ -262,14 +262,15 @@ def predict_documents(model, docs, batch_sizes=None, precision: str = "fp32", th
             fb, arrays = ahead.result()
             if k + 1 < len(spans):
                 ahead = ex.submit(feat_collate, spans[k + 1])
-            y, mig = predict_featurized(model, fb, precision, arrays, eng)
+            y, mig = predict_featurized(model, fb, precision, arrays, eng, info=info)
             ys.append(y)
             migs.append(mig)
             names += fb.names
     return np.concatenate(ys), np.concatenate(migs), names
 
 
-def predict_featurized(model, fb: FeaturizedBatch, precision: str = "fp32", arrays=None, eng=None):
+def predict_featurized(model, fb: FeaturizedBatch, precision: str = "fp32", arrays=None, eng=None,
+                       info: dict | None = None):
     """Device half of predict_documents: one forward over an already featurised batch
     (`arrays` = its collate_pinned() output when already made; `eng` = the model's engine
     when the caller already refreshed it for this call)."""
@@ -283,7 +284,10 @@ def predict_featurized(model, fb: FeaturizedBatch, precision: str = "fp32", arra
     b = upload_batch(x, src, dst, gp, fs, None, device=eng.device, build_csr=eng.arch == "sage", edge_ptr=ep)
     ws = gnn.infer_workspace(eng, b.N, b.G)
     eng.forward(b, ws)
-    torch.cuda.current_stream().synchronize()
-    if int(ws.nonfinite.item()):
+    n_band = gnn.mig_rescore(model, eng, b, ws, precision)  # bf16: fp32 picks near the ceilings
+    if info is not None:
+        info["mig_rescored"] = info.get("mig_rescored", 0) + n_band
+    y, mig, nf = gnn._readback(ws.y_pred[:b.G], ws.mig[:b.G], ws.nonfinite)
+    if int(nf[0]):
         raise E.NonFinite("memory prediction is not finite")
-    return ws.y_pred[:b.G].cpu().numpy(), ws.mig[:b.G].cpu().numpy()
+    return y, mig

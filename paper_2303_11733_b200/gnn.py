@@ -7,7 +7,7 @@ host model object keeps the fp64 "truth" exactly like the reference
 uploads the current values, so in-place edits between calls are honoured.
 
 Additions (batched surface): `predict_batch`, `predict_records`,
-`TrainConfig.batch_size / precision / device / backend`.
+`TrainConfig.batch_size / precision / device`.
 
 Numerics: `precision="fp32"` (default) runs the SAGE GEMMs as 3-pass TF32 on
 the tensor cores (fp32-grade), everything else in fp32 with fp64 Adam
@@ -19,14 +19,17 @@ from __future__ import annotations
 
 import json
 import math
+import threading
 from dataclasses import dataclass
 from pathlib import Path
+from types import SimpleNamespace
 from typing import ClassVar
 
 import numpy as np
 import torch
 
 from . import _lib, device as dev
+from ._lib import Act
 from .device import ActBuf, Batch, Engine, Workspace, collate_host, f32_act, upload_batch
 from .errors import EmptyDataset, EmptyGraph, IoFailure, NonFinite, ShapeMismatch, VersionMismatch
 from .mig import profile_from_code
@@ -102,7 +105,6 @@ class TrainConfig:
     batch_size: int = 1
     precision: str = "fp32"
     device: str | None = None
-    backend: str = "tc"
 
     def __post_init__(self):
         if self.epochs < 1:
@@ -151,6 +153,15 @@ class DippmModel:
             items.append((f"fc{i}.b", layer.b))
         return items
 
+    def forward_norm(self, prep, fs_norm, train: bool = False, rng=None, precision: str = "fp32"):
+        """gnn.py:212-217 on the device: embed -> mean readout -> [r | fs_norm] -> FC head.
+        Returns (out (3,) normalised, cache); the cache keeps the activations in HBM."""
+        return _device_forward_norm(self, prep, fs_norm, train, rng, precision)
+
+    def backward_from(self, cache, dout) -> dict:
+        """gnn.py:219-233 on the device: every parameter's gradient of <out, dout>."""
+        return _device_backward_from(self, cache, dout)
+
 
 @dataclass
 class MlpModel:
@@ -173,6 +184,14 @@ class MlpModel:
             items.append((f"fc{i}.w", layer.w))
             items.append((f"fc{i}.b", layer.b))
         return items
+
+    def forward_norm(self, prep, fs_norm, train: bool = False, rng=None, precision: str = "fp32"):
+        """gnn.py:255-257 on the device: the FC head on fs_norm alone."""
+        return _device_forward_norm(self, prep, fs_norm, train, rng, precision)
+
+    def backward_from(self, cache, dout) -> dict:
+        """gnn.py:259-262 on the device."""
+        return _device_backward_from(self, cache, dout)
 
 
 def create_model(hidden: int = DEFAULT_HIDDEN, seed: int = 0, dropout_p: float = DEFAULT_DROPOUT,
@@ -201,17 +220,101 @@ def _new_sage_model(hidden, rng, dropout_p, normalizer) -> DippmModel:
 
 
 # ---------------------------------------------------------------------------
+# per-record preparation and the duck-typed model protocol (gnn.py:120-154, 212-262)
+
+@dataclass
+class _Prepared:
+    """Per-record arrays (gnn.py:120-127).  The reference's dense aggregation matrix is
+    replaced by the edge list: the device builds the CSR (K1) from it at forward time."""
+
+    num_nodes: int
+    features: np.ndarray      # (N, 32) float64
+    edges: np.ndarray         # (E, 2) int64, (src, dst) producer -> consumer
+    fs_raw: np.ndarray        # (5,) log1p static features
+    y_raw: np.ndarray | None  # (3,) original-unit targets, None at predict time
+
+
+def _prepare_encoding(encoding, fs, target=None) -> _Prepared:
+    """gnn.py:140-150: validation (EmptyGraph, ShapeMismatch) + the arrays the forward needs."""
+    n = int(encoding.num_nodes)
+    if n < 1:
+        raise EmptyGraph("encoding has no nodes")
+    feats = np.asarray(encoding.features)
+    if feats.shape != (n, FEATURE_WIDTH):
+        raise ShapeMismatch(f"feature matrix {feats.shape} does not match {n} nodes")
+    e = np.asarray(encoding.edges, dtype=np.int64).reshape(-1, 2)
+    if e.size and (e.min() < 0 or e.max() >= n):
+        raise ShapeMismatch(f"edge endpoint outside [0, {n})")
+    return _Prepared(num_nodes=n, features=np.asarray(feats, dtype=np.float64), edges=e, fs_raw=fs_vector(fs),
+                     y_raw=None if target is None else target_vector(target))
+
+
+def _prepare_record(record) -> _Prepared:
+    """gnn.py:153-154."""
+    return _prepare_encoding(record.encoding, record.fs, record.target)
+
+
+class _DeviceCache:
+    """What forward_norm hands to backward_from: the device batch and the training workspace
+    holding the layer activations and ReLU masks (the reference caches (h, m, z) per layer
+    and the head inputs on the host, gnn.py:217)."""
+
+    __slots__ = ("precision", "batch", "ws", "keep")
+
+    def __init__(self, precision, batch, ws, keep):
+        self.precision, self.batch, self.ws, self.keep = precision, batch, ws, keep
+
+
+def _device_forward_norm(model, prep, fs_norm, train, rng, precision):
+    masks = _draw_masks(model, rng) if train else None  # gnn.py:277-281 draw order (fc1, fc2)
+    eng = _engine(model, precision)
+    n = prep.num_nodes
+    fsn = np.asarray(fs_norm, dtype=np.float64).reshape(1, STATIC_WIDTH)
+    e = prep.edges
+    b = upload_batch(prep.features.astype(np.float32), e[:, 0].copy(), e[:, 1].copy(), np.array([0, n], np.int32),
+                     fsn, device=eng.device, build_csr=model.arch == "sage")
+    ws = Workspace(eng, b.N, 1, train=True)
+    if masks is not None:
+        ws.masks[:, :, :masks.shape[-1]].copy_(torch.from_numpy(masks.astype(np.float32)))
+    # fs_norm comes from the caller already normalised (gnn.py:353): the device skips its z-score
+    eng.forward(b, ws, mask_mode=1 if masks is not None else 0, predict=False, fs_normalized=True)
+    eng.check_batch(b)
+    keep = 1.0 / (1.0 - model.dropout_p) if masks is not None else 1.0
+    return ws.out[0].double().cpu().numpy(), _DeviceCache(precision, b, ws, keep)
+
+
+def _device_backward_from(model, cache, dout) -> dict:
+    if not isinstance(cache, _DeviceCache):
+        raise TypeError("backward_from needs the cache returned by this package's forward_norm")
+    dout = np.asarray(dout, dtype=np.float64)
+    if dout.shape != (3,):
+        raise ShapeMismatch(f"dout must have shape (3,), got {dout.shape}")
+    # the reference's backward reads the model's CURRENT weights with the cached activations
+    eng = _engine(model, cache.precision)
+    ws = cache.ws
+    ws.dout[0].copy_(torch.from_numpy(dout.astype(np.float32)))
+    eng.backward(cache.batch, ws, keep_scale=cache.keep)
+    return eng.get_grads()
+
+
+# ---------------------------------------------------------------------------
 # engine binding
 
-def _engine(model, precision: str = "fp32", device=None, backend: str = "tc") -> Engine:
+_ENGINE_LOCK = threading.Lock()
+
+
+def _engine(model, precision: str = "fp32", device=None) -> Engine:
     """Device engine for `model`, refreshed from the model's current host values."""
     arch = getattr(model, "arch", "sage")
-    key = (precision, str(device), backend, int(model.hidden), arch)
-    cache = model.__dict__.setdefault("_b200_engines", {})
-    eng = cache.get(key)
-    if eng is None:
-        eng = Engine(model.hidden, precision, device, backend, arch=arch)
-        cache[key] = eng
+    if device is not None and torch.device(device) == torch.device("cuda", torch.cuda.current_device()):
+        device = None
+    key = (precision, str(device), int(model.hidden), arch)
+    with _ENGINE_LOCK:
+        cache = model.__dict__.setdefault("_b200_engines", {})
+        eng = cache.get(key)
+        if eng is None:
+            eng = Engine(model.hidden, precision, device, arch=arch)
+            cache[key] = eng
     eng.set_params(model.param_items(), model.normalizer)
     return eng
 
@@ -221,24 +324,66 @@ def _records_arrays(encodings, fss, targets=None):
                         None if targets is None else [target_vector(t) for t in targets])
 
 
-def infer_workspace(eng: Engine, N: int, G: int) -> Workspace:
-    """The engine's reusable inference workspace, grown (x1.25) when a batch needs more rows/graphs."""
-    ws = getattr(eng, "_infer_ws", None)
+def _grow(holder, key, eng: Engine, N: int, G: int, train: bool) -> Workspace:
+    """A grow-only workspace kept in `holder` under `key`: reused for every batch that fits
+    (workspaces accept batches smaller than their capacity), regrown x1.25 otherwise, so
+    batches of ever-different node counts cost one allocation, not one each."""
+    ws = getattr(holder, key, None)
     if ws is None or ws.N < N or ws.G < G:
-        ws = Workspace(eng, max(N, int(1.25 * (ws.N if ws else 0))), max(G, int(1.25 * (ws.G if ws else 0))),
-                       train=False)
-        eng._infer_ws = ws
+        if ws is not None:  # drop the old buffers before allocating the larger set
+            setattr(holder, key, None)
+            del ws
+        old = getattr(holder, key + "_cap", (0, 0))
+        ws = Workspace(eng, max(N, int(1.25 * old[0])), max(G, int(1.25 * old[1])), train=train)
+        setattr(holder, key, ws)
+        setattr(holder, key + "_cap", (ws.N, ws.G))
     return ws
+
+
+def _thread_slots(eng: Engine):
+    """Per-thread workspace slots of an engine: concurrent read-only predict calls on one
+    shared model never share activation buffers (the reference guarantees concurrent
+    inference on a trained model)."""
+    tls = eng.__dict__.get("_tls")
+    if tls is None:
+        tls = eng.__dict__.setdefault("_tls", threading.local())
+    return tls
+
+
+def infer_workspace(eng: Engine, N: int, G: int) -> Workspace:
+    """This thread's reusable inference workspace for the engine (grow-only)."""
+    return _grow(_thread_slots(eng), "infer", eng, N, G, train=False)
+
+
+def train_workspace(eng: Engine, N: int, G: int) -> Workspace:
+    """This thread's reusable training workspace for the engine (grow-only)."""
+    return _grow(_thread_slots(eng), "train", eng, N, G, train=True)
 
 
 def _run_forward(eng: Engine, encodings, fss, targets=None, mask_mode=0, masks=None, train_buffers=False):
     x, src, dst, gp, fs, y = _records_arrays(encodings, fss, targets)
     b = upload_batch(x, src, dst, gp, fs, y, device=eng.device, build_csr=eng.arch == "sage")
-    ws = Workspace(eng, b.N, b.G, train=True) if train_buffers else infer_workspace(eng, b.N, b.G)
+    ws = train_workspace(eng, b.N, b.G) if train_buffers else infer_workspace(eng, b.N, b.G)
     if masks is not None:
         ws.masks[:, :, :masks.shape[-1]].copy_(torch.from_numpy(masks.astype(np.float32)))
     eng.forward(b, ws, mask_mode=mask_mode)
     return b, ws
+
+
+def _readback(*tensors):
+    """Device -> pinned host copies of several results, then ONE wait for all of them."""
+    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in tensors]
+    for o, t in zip(outs, tensors):
+        o.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return [o.numpy() for o in outs]
+
+
+def _check_flags(b, ws, bad_flag, nonfinite_flag):
+    if b is not None and b.bad is not None and int(bad_flag[0]):
+        raise ShapeMismatch("edge endpoint outside its graph's node range")
+    if nonfinite_flag is not None and int(nonfinite_flag[0]):
+        raise NonFinite("predicted memory is NaN or infinite")
 
 
 def _check_mode(mode):
@@ -275,14 +420,14 @@ def sage_forward(encoding, layer: SageLayerParams, h_in: np.ndarray, precision: 
     n, d_in, d_out = h_in.shape[0], h_in.shape[1], w_self.shape[1]
     if n < 1:
         raise EmptyGraph("encoding has no nodes")
-    dip, dop = -(-d_in // 32) * 32, -(-d_out // 64) * 64
+    dip, dop = _agg_width(d_in, 32), -(-d_out // 64) * 64
     e = np.asarray(encoding.edges, dtype=np.int64).reshape(-1, 2)
     if e.size and (e.min() < 0 or e.max() >= n):
         raise ShapeMismatch(f"edge endpoint outside [0, {n})")
     xp = np.zeros((n, dip), np.float32)
     xp[:, :d_in] = h_in
     b = upload_batch(np.zeros((n, FEATURE_WIDTH), np.float32), e[:, 0].copy(), e[:, 1].copy(),
-                     np.array([0, n], np.int32), np.zeros((1, STATIC_WIDTH), np.float32), device=device)
+                     np.array([0, n], np.int32), np.zeros((1, STATIC_WIDTH)), device=device)
     dt = dev.PRECISIONS[precision]
     w_cat = np.zeros((2 * dip, dop))
     w_cat[:d_in, :d_out] = w_self
@@ -296,8 +441,10 @@ def sage_forward(encoding, layer: SageLayerParams, h_in: np.ndarray, precision: 
     Wt = ActBuf(dop, 2 * dip, dt, device)
     out = ActBuf(n, dop, dev.DT_F32, device)
     s = dev._stream()
-    _lib.call("dippm_sage_aggregate", f32_act(xt), A.view(dip), A.view(0), n, dip, b.rowptr.data_ptr(),
-              b.col.data_ptr(), b.inv_deg.data_ptr(), s)
+    for c0 in range(0, dip, 1024):  # the aggregation kernel takes power-of-two widths up to 1024
+        w = min(dip - c0, 1024)
+        _lib.call("dippm_sage_aggregate", Act(xt.data_ptr() + 4 * c0, dip, 0, dev.DT_F32), A.view(dip + c0),
+                  A.view(c0), n, w, b.rowptr.data_ptr(), b.col.data_ptr(), b.inv_deg.data_ptr(), s)
     _lib.call("dippm_pack", wt64.data_ptr(), 2 * dip, dop, 1, Wt.view(), s)
     args = _lib.GemmArgs(_lib.GEMM_FWD, n, dop, 2 * dip, A.view(0), 0, Wt.view(), 0, bt.data_ptr(), 1, out.view(),
                          None, 0, 1)
@@ -305,23 +452,35 @@ def sage_forward(encoding, layer: SageLayerParams, h_in: np.ndarray, precision: 
     return out.t[:, :d_out].double().cpu().numpy()
 
 
+def _agg_width(d: int, lo: int) -> int:
+    """Padded width for the aggregation / pooling kernels: a power of two >= lo up to 1024
+    (their 8-column chunks tile a warp), beyond that a multiple of 1024 (column chunks)."""
+    if d <= 1024:
+        return max(lo, 1 << (max(d, 1) - 1).bit_length())
+    return -(-d // 1024) * 1024
+
+
 def readout_mean(z: np.ndarray) -> np.ndarray:
-    """Arithmetic mean over node embeddings (gnn.py:341-345), on device (K4)."""
+    """Arithmetic mean over node embeddings (gnn.py:341-345), on device (K4), any width."""
     z = np.asarray(z)
     if z.ndim != 2 or z.shape[0] < 1:
         raise EmptyGraph("readout needs at least one node embedding")
     device = dev.require_device()
     n, d = z.shape
-    dp = -(-d // 8) * 8
+    dp = _agg_width(d, 8)
     zp = torch.zeros(n, dp, dtype=torch.float32)
     zp[:, :d] = torch.from_numpy(np.asarray(z, dtype=np.float32))
     zt = zp.to(device)
     gp = torch.tensor([0, n], dtype=torch.int32, device=device)
-    fs = torch.zeros(1, STATIC_WIDTH, dtype=torch.float32, device=device)
+    fs = torch.zeros(1, STATIC_WIDTH, dtype=torch.float64, device=device)
     norm = torch.tensor([0.0] * 6 + [0.0] * 5 + [1.0] * 5, dtype=torch.float64, device=device)
-    u = torch.empty(1, dp + 8, dtype=torch.float32, device=device)
-    _lib.call("dippm_pool_concat", f32_act(zt), gp.data_ptr(), 1, dp, fs.data_ptr(), norm.data_ptr(), f32_act(u),
-              dev._stream())
+    # two rows: a column chunk also writes its [fs | 0] tail past its own columns; chunks run in
+    # ascending order, so the tail lands on the next chunk's columns (rewritten next) or row 1
+    u = torch.empty(2, dp + 8, dtype=torch.float32, device=device)
+    for c0 in range(0, dp, 1024):
+        w = min(dp - c0, 1024)
+        _lib.call("dippm_pool_concat", Act(zt.data_ptr() + 4 * c0, dp, 0, dev.DT_F32), gp.data_ptr(), 1, w,
+                  fs.data_ptr(), norm.data_ptr(), Act(u.data_ptr() + 4 * c0, dp + 8, 0, dev.DT_F32), dev._stream())
     return u[0, :d].double().cpu().numpy()
 
 
@@ -330,29 +489,52 @@ def forward(encoding, fs, model, mode: str = "eval", rng=None, precision: str = 
     _check_mode(mode)
     masks = _draw_masks(model, rng) if mode == "train" else None
     eng = _engine(model, precision)
-    _, ws = _run_forward(eng, [encoding], [fs], mask_mode=1 if masks is not None else 0, masks=masks)
-    return ws.out[0].double().cpu().numpy()
+    b, ws = _run_forward(eng, [encoding], [fs], mask_mode=1 if masks is not None else 0, masks=masks)
+    out, bad = _readback(ws.out[0], b.bad if b.bad is not None else ws.nonfinite)
+    _check_flags(b, ws, bad, None)
+    return out.astype(np.float64)
 
 
-def predict_batch(model, encodings, fss, precision: str = "fp32"):
+def mig_rescore(model, eng: Engine, b, ws, precision: str) -> int:
+    """bf16 predictions: re-score the graphs near a MIG ceiling in fp32 so the picks are the
+    reference's (see device.mig_band_rescore).  Returns the number re-scored (0 in fp32)."""
+    if precision != "bf16":
+        return 0
+    band = dev.BF16_MIG_BAND * float(np.asarray(model.normalizer.y_std)[1])
+    return dev.mig_band_rescore(_engine(model, "fp32", eng.device), b, ws, band, _thread_slots(eng))
+
+
+def predict_batch(model, encodings, fss, precision: str = "fp32", check_nonfinite: bool = True,
+                  info: dict | None = None):
     """Batched eval prediction: (y float64 [G, 3] in original units, MIG codes int8 [G]).
 
     MIG codes: 0=1g.5gb, 1=2g.10gb, 2=3g.20gb, 3=7g.40gb, -1=None; computed on
-    the device from y[:, 1] with the same rule as mig.mig_profile.
+    the device from y[:, 1] with the same rule as mig.mig_profile.  A NaN/Inf predicted
+    memory raises NonFinite like mig_profile (mig.py:38-39) unless check_nonfinite=False
+    (then its code is -1 and y carries the NaN, as the reference's predict returns it).
+    precision="bf16": graphs whose bf16 memory prediction is within the stated bf16
+    tolerance of a profile ceiling are re-scored in fp32 (their y and pick are the fp32
+    ones), so picks match the reference's wherever fp32 does; info["mig_rescored"] counts them.
     """
     if len(encodings) != len(fss):
         raise ShapeMismatch(f"{len(encodings)} encodings vs {len(fss)} static-feature vectors")
     if not encodings:
         raise EmptyDataset("batch is empty")
     eng = _engine(model, precision)
-    _, ws = _run_forward(eng, encodings, fss)
+    b, ws = _run_forward(eng, encodings, fss)
     G = len(encodings)
-    return ws.y_pred[:G].cpu().numpy(), ws.mig[:G].cpu().numpy()
+    n_band = mig_rescore(model, eng, b, ws, precision)
+    if info is not None:
+        info["mig_rescored"] = n_band
+    y, mig, bad, nf = _readback(ws.y_pred[:G], ws.mig[:G], b.bad if b.bad is not None else ws.nonfinite,
+                                ws.nonfinite)
+    _check_flags(b, ws, bad, nf if check_nonfinite else None)
+    return y, mig
 
 
 def predict(model, encoding, fs, precision: str = "fp32") -> TargetVector:
     """Original-unit eval-mode prediction (gnn.py:358-361)."""
-    y, _ = predict_batch(model, [encoding], [fs], precision)
+    y, _ = predict_batch(model, [encoding], [fs], precision, check_nonfinite=False)
     return TargetVector(latency_ms=float(y[0, 0]), memory_mb=float(y[0, 1]), energy_j=float(y[0, 2]))
 
 
@@ -362,7 +544,8 @@ def predict_record(model, record, precision: str = "fp32") -> TargetVector:
 
 def predict_records(model, records, precision: str = "fp32", with_mig: bool = False):
     """Batched `predict_record` over many records (one device pass)."""
-    y, mig = predict_batch(model, [r.encoding for r in records], [r.fs for r in records], precision)
+    y, mig = predict_batch(model, [r.encoding for r in records], [r.fs for r in records], precision,
+                           check_nonfinite=with_mig)
     preds = [TargetVector(latency_ms=float(a), memory_mb=float(b), energy_j=float(c)) for a, b, c in y]
     if with_mig:
         return preds, [profile_from_code(int(c)) for c in mig]
@@ -377,7 +560,9 @@ def batch_loss(model, records, huber_delta: float = 1.0, precision: str = "fp32"
     b, ws = _run_forward(eng, [r.encoding for r in records], [r.fs for r in records],
                          [r.target for r in records], train_buffers=True)
     eng.loss(b, ws, huber_delta)
-    return float(ws.loss[0].item())
+    loss, bad = _readback(ws.loss[:1], b.bad if b.bad is not None else ws.nonfinite)
+    _check_flags(b, ws, bad, None)
+    return float(loss[0])
 
 
 def backward(model, records, huber_delta: float = 1.0, precision: str = "fp32"):
@@ -392,7 +577,9 @@ def backward(model, records, huber_delta: float = 1.0, precision: str = "fp32"):
                          [r.target for r in records], train_buffers=True)
     eng.loss(b, ws, huber_delta)
     eng.backward(b, ws)
-    return float(ws.loss[0].item()), eng.get_grads()
+    loss, bad = _readback(ws.loss[:1], b.bad if b.bad is not None else ws.nonfinite)
+    _check_flags(b, ws, bad, None)
+    return float(loss[0]), eng.get_grads()
 
 
 # ---------------------------------------------------------------------------
@@ -416,7 +603,7 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
     statics = np.stack([fs_vector(r.fs) for r in train_records])
     normalizer = Normalizer.fit(targets, statics)
     model = make_model(config.hidden, rng, DEFAULT_DROPOUT, normalizer)
-    eng = Engine(config.hidden, config.precision, config.device, config.backend, arch=model.arch)
+    eng = Engine(config.hidden, config.precision, config.device, arch=model.arch)
     eng.set_params(model.param_items(), normalizer)
     sage = model.arch == "sage"
     n = len(train_records)
@@ -429,7 +616,7 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
                                 build_csr=sage) for r in train_records]
     n_max = max(b.N for b in batches) if B == 1 else None
     ws1 = Workspace(eng, n_max, 1, train=True) if B == 1 else None
-    ws_cache = {}
+    slots = SimpleNamespace()  # grow-only training / evaluation workspaces
     acc = torch.zeros(4, dtype=torch.float64, device=eng.device)
     history = []
     step = 0
@@ -453,13 +640,14 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
                 recs = [train_records[i] for i in idx]
                 b = upload_batch(*_records_arrays([r.encoding for r in recs], [r.fs for r in recs],
                                                   [r.target for r in recs]), device=eng.device, build_csr=sage)
-                ws = _workspace(ws_cache, eng, b, train=True)
+                ws = _grow(slots, "train", eng, b.N, b.G, train=True)
                 step += 1
                 eng.forward(b, ws, mask_mode=2 if dropout else 0, dropout_p=model.dropout_p,
                             seed=config.seed * 1000003 + step, predict=False, defer_head=True)
                 eng.loss(b, ws, config.huber_delta)
                 eng.backward(b, ws, keep_scale=keep, advance_step=True)
-                acc.add_(ws.loss * torch.tensor([b.G, 1, 1, 1], dtype=torch.float64, device=eng.device))
+                acc[:1].add_(ws.loss[:1], alpha=float(b.G))  # loss is the batch mean; APE terms are sums
+                acc[1:].add_(ws.loss[1:])
                 eng.adam_step(config.lr)
         a = acc.cpu().numpy()
         if not np.all(np.isfinite(a)):
@@ -467,7 +655,7 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
         entry = {"epoch": epoch, "train_loss": float(a[0] / n), "train_mape": float((a[1:] / n).mean()),
                  "val_loss": None, "val_mape": None}
         if val_records:
-            v_loss, v_ape = _evaluate(eng, val_records, config.huber_delta, ws_cache)
+            v_loss, v_ape = _evaluate(eng, val_records, config.huber_delta, slots)
             entry["val_loss"] = v_loss
             entry["val_mape"] = v_ape
         history.append(entry)
@@ -477,22 +665,14 @@ def _fit(make_model, train_records, val_records, config: TrainConfig):
     return model, history
 
 
-def _workspace(cache, eng, b, train):
-    key = (b.N, b.G, train)
-    ws = cache.get(key)
-    if ws is None:
-        ws = Workspace(eng, b.N, b.G, train=train)
-        cache[key] = ws
-    return ws
-
-
-def _evaluate(eng, records, delta, ws_cache, chunk=256):
+def _evaluate(eng, records, delta, slots, chunk=256):
+    """Eval-mode loss and MAPE over `records` (gnn.py:466-475), one read-back per chunk."""
     loss_sum, ape = 0.0, np.zeros(3)
     for s0 in range(0, len(records), chunk):
         recs = records[s0:s0 + chunk]
         b = upload_batch(*_records_arrays([r.encoding for r in recs], [r.fs for r in recs],
                                           [r.target for r in recs]), device=eng.device, build_csr=eng.arch == "sage")
-        ws = _workspace(ws_cache, eng, b, train=True)
+        ws = _grow(slots, "eval", eng, b.N, b.G, train=False)
         eng.forward(b, ws, predict=False)
         eng.loss(b, ws, delta)
         out = ws.loss.cpu().numpy()

@@ -1218,7 +1218,7 @@ void dippm_feat_export(const dippm_feat_batch* b, double* x, int64_t* edges, int
 }
 
 void dippm_feat_collate(const dippm_feat_batch* b, float* x32, int64_t* src, int64_t* dst, int32_t* graph_ptr,
-                        int64_t* edge_ptr, float* fs32) {
+                        int64_t* edge_ptr, double* fs64) {
   std::vector<int64_t> no, eo;
   doc_offsets(b, no, eo);
   const size_t G = b->res.size();
@@ -1235,8 +1235,8 @@ void dippm_feat_collate(const dippm_feat_batch* b, float* x32, int64_t* src, int
         if (src) src[eo[i] + (int64_t)k] = no[i] + r.edges[k].first;
         if (dst) dst[eo[i] + (int64_t)k] = no[i] + r.edges[k].second;
       }
-      if (fs32)
-        for (int k = 0; k < 5; ++k) fs32[i * 5 + k] = (float)std::log1p((double)r.fs[k]);
+      if (fs64)
+        for (int k = 0; k < 5; ++k) fs64[i * 5 + k] = std::log1p((double)r.fs[k]);
     }
   });
 }

@@ -66,15 +66,16 @@ def evaluate(model, records, precision: str = "fp32", batch_size: int = 4096, wi
         raise ZeroActual("actual target contains a zero component")
     eng = gnn._engine(model, precision)
     acc = torch.zeros(4, dtype=torch.float64, device=eng.device)
-    ws_cache = {}
+    slots = gnn.SimpleNamespace()
     for s0 in range(0, len(records), batch_size):
         recs = records[s0:s0 + batch_size]
         arrays = gnn._records_arrays([r.encoding for r in recs], [r.fs for r in recs], [r.target for r in recs])
         b = upload_batch(*arrays, device=eng.device, build_csr=eng.arch == "sage")
-        ws = gnn._workspace(ws_cache, eng, b, train=True)
+        ws = gnn._grow(slots, "eval", eng, b.N, b.G, train=False)
         eng.forward(b, ws, predict=False)
         eng.loss(b, ws, 1.0)
-        acc.add_(ws.loss * torch.tensor([b.G, 1.0, 1.0, 1.0], dtype=torch.float64, device=eng.device))
+        acc[:1].add_(ws.loss[:1], alpha=float(b.G))
+        acc[1:].add_(ws.loss[1:])
     a = acc.cpu().numpy() / len(records)
     res = MapeResult(latency=float(a[1]), memory=float(a[2]), energy=float(a[3]), overall=float(a[1:].mean()))
     return (res, float(a[0])) if with_loss else res

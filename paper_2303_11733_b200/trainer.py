@@ -23,9 +23,9 @@ from .device import Batch, Engine, Workspace, build_batch_csr
 class BatchTrainer:
     def __init__(self, model, precision: str = "bf16", lr: float = 2.754e-5, seed: int = 0, dropout: bool = True,
                  huber_delta: float = 1.0, allreduce=None, world_size: int = 1, rank: int = 0, device=None,
-                 backend: str = "tc", use_graphs: bool = False):
+                 use_graphs: bool = False):
         self.model = model
-        self.engine = Engine(model.hidden, precision, device, backend)
+        self.engine = Engine(model.hidden, precision, device, arch=getattr(model, "arch", "sage"))
         self.engine.set_params(model.param_items(), model.normalizer)
         self.lr, self.seed, self.delta = lr, seed, huber_delta
         self.dropout_p = model.dropout_p if dropout else 0.0
@@ -54,8 +54,8 @@ class BatchTrainer:
             "x": torch.empty(max_nodes, dev.FEATURE_WIDTH, dtype=torch.float32, device=d),
             "src": torch.empty(e, dtype=torch.int64, device=d), "dst": torch.empty(e, dtype=torch.int64, device=d),
             "gp": torch.empty(max_graphs + 1, dtype=torch.int32, device=d),
-            "fs": torch.empty(max_graphs, dev.STATIC_WIDTH, dtype=torch.float32, device=d),
-            "y": torch.empty(max_graphs, 3, dtype=torch.float32, device=d),
+            "fs": torch.empty(max_graphs, dev.STATIC_WIDTH, dtype=torch.float64, device=d),
+            "y": torch.empty(max_graphs, 3, dtype=torch.float64, device=d),
             "ep": torch.empty(max_graphs + 1, dtype=torch.int64, device=d),
             "free": torch.cuda.Event(), "ready": torch.cuda.Event(),
         } for _ in range(2)]

@@ -66,7 +66,7 @@ def test_collate_layout_matches_upload_contract(gf):
     # the native collated export (dippm_feat_collate) writes exactly these arrays
     G, N, E = len(docs), len(x), len(src)
     nx, ns, nd = np.empty((N, 32), np.float32), np.empty(E, np.int64), np.empty(E, np.int64)
-    ngp, nep, nfs = np.empty(G + 1, np.int32), np.empty(G + 1, np.int64), np.empty((G, 5), np.float32)
+    ngp, nep, nfs = np.empty(G + 1, np.int32), np.empty(G + 1, np.int64), np.empty((G, 5), np.float64)
     F._host().dippm_feat_collate(fb._h, nx.ctypes.data, ns.ctypes.data, nd.ctypes.data, ngp.ctypes.data,
                                  nep.ctypes.data, nfs.ctypes.data)
     for a, b in ((x, nx), (src, ns), (dst, nd), (gp, ngp), (ep, nep), (fs, nfs)):

@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_2303_11733_b200 import _lib, device as dev  # noqa: E402
 from paper_2303_11733_b200.device import ActBuf, upload_batch  # noqa: E402
+from paper_2303_11733_b200.errors import ShapeMismatch  # noqa: E402
 
 
 def _batch_from(recs):
@@ -78,8 +79,10 @@ def test_csr_deterministic_and_bad_edges():
     assert np.array_equal(a.rowptr.cpu().numpy(), rowptr)
     assert np.array_equal(a.col.cpu().numpy()[:len(col)], col)
     assert np.array_equal(a.deg.cpu().numpy(), deg)
-    bad = upload_batch(x, np.array([0, N + 3]), np.array([1, 2]), gp, fs)
+    bad = upload_batch(x, np.array([0, N + 3]), np.array([1, 2]), gp, fs, validate=False)
     assert int(bad.bad.item()) == 1
+    with pytest.raises(ShapeMismatch):  # the host validation rejects it before upload
+        upload_batch(x, np.array([0, N + 3]), np.array([1, 2]), gp, fs)
 
 
 @pytest.mark.parametrize("width", [32, 64, 512])
@@ -200,7 +203,7 @@ def test_pool_concat_and_mig_codes(golden):
     gp = np.zeros(G + 1, np.int32)
     np.cumsum(n, out=gp[1:])
     h = rng.normal(size=(gp[-1], 64)).astype(np.float32)
-    fs = rng.normal(size=(G, 5)).astype(np.float32)
+    fs = rng.normal(size=(G, 5))
     norm = np.concatenate([np.zeros(6), rng.normal(size=5), rng.uniform(0.5, 2, 5)])
     u = torch.full((G, 128), float("nan"), device="cuda")
     keep = [torch.from_numpy(a).cuda() for a in (h, gp, fs, norm)]  # hold the buffers across the launch
@@ -384,8 +387,14 @@ def test_grouped_csr_equals_global_path(golden, case):
     slow = _csr_arrays(b)
     for f, s in zip(fast, slow):
         assert np.array_equal(f, s)
-    # an edge crossing graphs is rejected by the grouped kernel
-    assert group_edges(np.array([0, 5]), np.array([1, 1]), np.array([0, 3, 6])) is None
+    # an edge crossing graphs is rejected by the host validation ...
+    with pytest.raises(ShapeMismatch):
+        group_edges(np.array([0, 5]), np.array([1, 1]), np.array([0, 3, 6]))
+    # ... and flagged by the grouped kernel when it reaches the device
+    x = upload_batch(np.zeros((6, 32), np.float32), np.array([0, 4]), np.array([1, 1]), np.array([0, 3, 6], np.int32),
+                     np.zeros((2, 5), np.float32), build_csr=False, edge_ptr=np.array([0, 2, 2]))
+    build_batch_csr(x, grouped=True)
+    assert int(x.bad.item()) == 1
 
 
 def _bits_of(x):
