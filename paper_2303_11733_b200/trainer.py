@@ -13,11 +13,14 @@ Adam follows numerics.py:93-114 on fp64 masters.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 
 from . import device as dev
 from .device import Batch, Engine, Workspace, build_batch_csr
+from .errors import NonFinite, ShapeMismatch
 
 
 class BatchTrainer:
@@ -41,6 +44,7 @@ class BatchTrainer:
         self._slot_next = 0
         self._copy_stream = torch.cuda.Stream() if torch.cuda.is_available() else None
         self._loss_ring = [torch.zeros(1, dtype=torch.float64).pin_memory() for _ in range(64)]
+        self._flag_ring = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(64)]
         self._loss_next = 0
 
     def reserve(self, max_nodes: int, max_graphs: int, max_edges: int | None = None) -> None:
@@ -132,14 +136,16 @@ class BatchTrainer:
                 self.allreduce(eng.grads)      # the one exchange: sum of per-rank gradient shares
         eng.adam_step(self.lr)
 
-    def step_host(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None) -> float:
+    def step_host(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None, global_graphs: int | None = None) -> float:
         """End-to-end step from host (ideally pinned) buffers; returns the batch loss.
 
         edge_ptr [G+1] (edges grouped by graph, as collation produces) enables the
-        per-graph CSR kernel; if omitted it is derived on the host when possible."""
-        return self.submit(x, src, dst, graph_ptr, fs, y, edge_ptr).loss()
+        per-graph CSR kernel; if omitted it is derived on the host when possible.
+        global_graphs: the data-parallel batch size over all ranks (the gradient
+        denominator); default: summed over the ranks with one small all-reduce."""
+        return self.submit(x, src, dst, graph_ptr, fs, y, edge_ptr, global_graphs).loss()
 
-    def submit(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None) -> "StepHandle":
+    def submit(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None, global_graphs: int | None = None) -> "StepHandle":
         """Asynchronous end-to-end step from host buffers (pipelined `step_host`).
 
         The batch is copied host->device on a side copy stream into one of two
@@ -147,7 +153,11 @@ class BatchTrainer:
         runs on the current stream and its loss is read back device->host into
         pinned memory.  Returns a StepHandle whose .loss() waits for that read.
         Steps stay in submission order (one compute stream), so the result is
-        the same as calling step_host repeatedly."""
+        the same as calling step_host repeatedly.
+
+        The batch is validated on the host first (edge endpoints inside their graph,
+        ShapeMismatch otherwise); the handle's .loss() raises NonFinite for a non-finite
+        loss (gnn.py:455-456) and ShapeMismatch if the device CSR build flagged an edge."""
         if edge_ptr is None:
             edge_ptr = dev.group_edges(np.asarray(src), np.asarray(dst), np.asarray(graph_ptr))
         arrays = [x, src, dst, graph_ptr, fs, y] + ([edge_ptr] if edge_ptr is not None else [])
@@ -176,17 +186,21 @@ class BatchTrainer:
             gp, ep = t[3].numpy(), np.asarray(edge_ptr)
             b.edge_ptr, b.max_nodes = views[6], int(np.diff(gp).max())
             b.max_edges = int(np.diff(ep).max()) if len(ep) > 1 else 0
+        if global_graphs is None and self.allreduce is not None:
+            from .dist import global_batch_size
+            global_graphs = global_batch_size(G)  # ragged per-rank batches: the true global mean
         self._ensure(b)
         self.steps += 1
-        self._step(b, None)  # ragged shapes: host batches run eagerly
+        self._step(b, global_graphs)  # ragged shapes: host batches run eagerly
         sl["free"].record(compute)
         j = self._loss_next
         self._loss_next = (j + 1) % len(self._loss_ring)
-        host = self._loss_ring[j]
+        host, flag = self._loss_ring[j], self._flag_ring[j]
         host.copy_(self.ws.loss[:1], non_blocking=True)
+        flag.copy_(b.bad[:1], non_blocking=True)
         done = torch.cuda.Event()
         done.record(compute)
-        return StepHandle(done, host)
+        return StepHandle(done, host, flag)
 
     def sync_model(self):
         """Copy the device fp64 masters back into the host model's live arrays."""
@@ -199,12 +213,17 @@ class BatchTrainer:
 class StepHandle:
     """Result of BatchTrainer.submit: .loss() waits for the step's loss read-back."""
 
-    def __init__(self, event, host):
-        self._event, self._host = event, host
+    def __init__(self, event, host, flag=None):
+        self._event, self._host, self._flag = event, host, flag
 
     def done(self) -> bool:
         return self._event.query()
 
     def loss(self) -> float:
         self._event.synchronize()
-        return float(self._host[0])
+        if self._flag is not None and int(self._flag[0]):
+            raise ShapeMismatch("edge endpoint outside its graph's node range")
+        v = float(self._host[0])
+        if not math.isfinite(v):
+            raise NonFinite("training loss is not finite")
+        return v

@@ -298,3 +298,68 @@ def test_reference_fit_loop_over_the_protocol_reproduces_golden_training(golden)
     for name, arr in model.param_items():
         r = golden[f"train_param_{name}"]
         assert np.max(np.abs(arr - r)) <= 1e-5 * max(1.0, np.abs(r).max()), name
+
+
+# -- safety: concurrent read-only inference, error paths ---------------------
+
+
+def test_concurrent_predict_on_shared_model(golden):
+    """Several threads predicting with ONE model at once get exactly the serial results
+    (each thread owns its workspaces; the parameters are read-only)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2303_11733_b200.synth import make_dataset
+    ds = make_dataset(96, seed=21, n_lo=20, n_hi=400)
+    model = gnn.create_model(hidden=128, seed=2, normalizer=Normalizer.fit(ds.y.astype(float), ds.fs.astype(float)))
+    recs = ds.records(range(96))
+    chunks = [recs[i::6] for i in range(6)]
+    serial = [gnn.predict_batch(model, [r.encoding for r in c], [r.fs for r in c], precision=p)
+              for c in chunks for p in ("fp32", "bf16")]
+
+    def work(k):
+        c, p = chunks[k // 2], ("fp32", "bf16")[k % 2]
+        outs = []
+        for _ in range(5):
+            outs.append(gnn.predict_batch(model, [r.encoding for r in c], [r.fs for r in c], precision=p))
+        return outs
+
+    with ThreadPoolExecutor(6) as ex:
+        results = list(ex.map(work, range(12)))
+    for k, outs in enumerate(results):
+        for y, mig in outs:
+            assert np.array_equal(y, serial[k][0]) and np.array_equal(mig, serial[k][1]), k
+
+
+def test_nonfinite_prediction_raises_in_batch_api_not_in_predict(golden):
+    from paper_2303_11733_b200.errors import NonFinite
+    recs = _records(golden)[:3]
+    model = _fitted_model(recs, hidden=16)
+    model.fc[2].b[1] = np.nan  # memory output NaN
+    with pytest.raises(NonFinite):
+        gnn.predict_batch(model, [r.encoding for r in recs], [r.fs for r in recs])
+    tv = gnn.predict(model, recs[0].encoding, recs[0].fs)  # the reference's predict returns the NaN
+    assert math.isnan(tv.memory_mb)
+
+
+def test_trainer_rejects_corrupt_host_batch():
+    import torch
+    from paper_2303_11733_b200.synth import make_dataset
+    from paper_2303_11733_b200.trainer import BatchTrainer
+    ds = make_dataset(8, seed=3)
+    model = gnn.create_model(hidden=64, seed=1, normalizer=Normalizer.fit(ds.y.astype(float), ds.fs.astype(float)))
+    tr = BatchTrainer(model, precision="bf16")
+    x, src, dst, gp, fs, y = ds.collate(np.arange(8))
+    assert np.isfinite(tr.step_host(x, src, dst, gp, fs, y))
+    bad = dst.copy()
+    bad[5] = gp[-1] + 7  # endpoint outside the batch
+    with pytest.raises(ShapeMismatch):
+        tr.step_host(x, src, bad, gp, fs, y)
+    cross = src.copy()
+    cross[-1] = 0  # last graph's edge from graph 0's node
+    with pytest.raises(ShapeMismatch):
+        tr.step_host(x, cross, dst, gp, fs, y)
+    ynan = y.copy()
+    ynan[0, 0] = np.nan
+    from paper_2303_11733_b200.errors import NonFinite
+    with pytest.raises(NonFinite):
+        tr.step_host(x, src, dst, gp, fs, ynan)
+    del torch
