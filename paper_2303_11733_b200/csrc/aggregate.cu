@@ -401,18 +401,21 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
 // dippm_readout_aggregate_t):  dz3[v, c] = dr[g, c] * bit(v, c) with dr = du[g] / N_g, and
 // since every neighbour of u lies in u's graph,
 //   (agg^T dz3)[u, c] = dr[g, c] * sum_{u->v} bit(v, c) / deg(v).
-// One warp per row, CPL chunks of 8 columns per lane; the bit words of the row and of up to
-// kPre neighbours are loaded together before any use (the kernel is load-latency bound).
-constexpr int kPre = 2;
+// The block first stages the bit words of its own rows plus a halo of kBitsHalo rows past
+// them (operator graphs are topologically ordered, so out-neighbours are mostly a few rows
+// ahead) in shared memory with one burst of coalesced loads; the per-row work is then
+// shared-memory reads and 128-bit stores, with a global load only for a neighbour outside
+// the staged window.  One warp per row, CPL chunks of 8 columns per lane.
+constexpr int kBitsHalo = 64;
 template <int DT, int CPL>
-__global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, int width, int64_t N, int rpb,
+__global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 3) k_readout_agg_bits(ActView B, int width, int64_t N, int rpb,
                                                                      const int* __restrict__ t_rowptr,
                                                                      const int* __restrict__ t_col,
                                                                      const float* __restrict__ inv_deg,
                                                                      float* __restrict__ colsum_partial, ReadoutArgs ro,
                                                                      float* __restrict__ bias_out,
                                                                      int* __restrict__ sync) {
-  extern __shared__ float s_part[];  // [8 warps][width]
+  extern __shared__ float s_part[];  // [8 warps][width] floats, then the staged bit words
   __shared__ int s_ptr[kRowsPerBlockT + 1];
   __shared__ int s_col[kAggColCap];
   __shared__ float s_cw[kAggColCap];
@@ -423,6 +426,15 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
   const int cbeg = t_rowptr[r0];
   const int ncol = t_rowptr[r0 + nrows] - cbeg;
   const bool staged = ncol <= kAggColCap;
+  // word of (row, chunk): chunk-major (stride bits_ld per chunk) or row-major (stride 1)
+  const int64_t cstride = ro.bits_ld ? ro.bits_ld : 1, rstride = ro.bits_ld ? 1 : width >> 5;
+  const int W = width >> 5;
+  const int R = (int)((N - r0 < rpb + kBitsHalo) ? N - r0 : rpb + kBitsHalo);  // staged rows [r0, r0 + R)
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_part + (kAggThreads / 32) * width);  // [W][R]
+  for (int i = threadIdx.x; i < W * R; i += blockDim.x) {
+    const int w = i / R, r = i - w * R;
+    s_bits[i] = __ldg(ro.h3_bits + w * cstride + (r0 + r) * rstride);
+  }
   for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
   for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_g[i] = ro.node_graph[r0 + i];
   if (staged)
@@ -440,29 +452,12 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
     wofs[q] = (c0 + q * stride) >> 5;
     wsh[q] = (c0 + q * stride) & 31;
   }
-  // word of (row, chunk): chunk-major (stride bits_ld per chunk) or row-major (stride 1)
-  const int64_t cstride = ro.bits_ld ? ro.bits_ld : 1, rstride = ro.bits_ld ? 1 : width >> 5;
   float part[CPL][8] = {};
   float dr[CPL][8];
   int g_cur = -1;
   for (int lr = warp; lr < nrows; lr += kAggThreads / 32) {
     const int64_t row = r0 + lr;
     const int b = s_ptr[lr], e = s_ptr[lr + 1];
-    // issue every independent load of this row first: own bits, up to 4 neighbours' bits
-    uint32_t wown[CPL], wn[kPre][CPL];
-    int nv[kPre];
-    float nw[kPre];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) wown[q] = __ldg(ro.h3_bits + wofs[q] * cstride + row * rstride);
-#pragma unroll
-    for (int t = 0; t < kPre; ++t) {
-      const int j = b + t;
-      nv[t] = j < e ? (staged ? s_col[j] : t_col[cbeg + j]) : -1;
-      nw[t] = j < e ? (staged ? s_cw[j] : inv_deg[nv[t]]) : 0.f;
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        wn[t][q] = nv[t] >= 0 ? __ldg(ro.h3_bits + wofs[q] * cstride + (int64_t)nv[t] * rstride) : 0u;
-    }
     const int g = s_g[lr];
     if (g != g_cur) {  // rows of a graph are contiguous: reload dr only at graph changes
       g_cur = g;
@@ -476,33 +471,32 @@ __global__ void __launch_bounds__(kAggThreads, 3) k_readout_agg_bits(ActView B, 
         dr[q][4] = a2.x * inv_n; dr[q][5] = a2.y * inv_n; dr[q][6] = a2.z * inv_n; dr[q][7] = a2.w * inv_n;
       }
     }
+    float acc[CPL][8] = {};
+    for (int j = b; j < e; ++j) {  // out-edges in CSR order
+      const int v0 = staged ? s_col[j] : t_col[cbeg + j];
+      const float w0 = staged ? s_cw[j] : inv_deg[v0];
+      const unsigned rel = (unsigned)(v0 - r0);
+      uint32_t wv[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        wv[q] = (rel < (unsigned)R ? s_bits[wofs[q] * R + rel] : __ldg(ro.h3_bits + wofs[q] * cstride + (int64_t)v0 * rstride)) >> wsh[q];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[q][k] += (wv[q] >> k) & 1u ? w0 : 0.f;
+    }
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      float own[8], acc[8];
-      const uint32_t wo = wown[q] >> wsh[q];
+      float own[8];
+      const uint32_t wo = s_bits[wofs[q] * R + lr] >> wsh[q];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         own[k] = (wo >> k) & 1u ? dr[q][k] : 0.f;
         part[q][k] += own[k];
-        acc[k] = 0.f;
+        acc[q][k] *= dr[q][k];
       }
-#pragma unroll
-      for (int t = 0; t < kPre; ++t) {
-        const uint32_t wv = wn[t][q] >> wsh[q];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += (wv >> k) & 1u ? nw[t] : 0.f;
-      }
-      for (int j = b + kPre; j < e; ++j) {  // beyond the prefetched out-edges
-        const int v0 = staged ? s_col[j] : t_col[cbeg + j];
-        const float w0 = staged ? s_cw[j] : inv_deg[v0];
-        const uint32_t wv = __ldg(ro.h3_bits + wofs[q] * cstride + (int64_t)v0 * rstride) >> wsh[q];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += (wv >> k) & 1u ? w0 : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] *= dr[q][k];
       act_store8_t<DT>(B, row, c0 + q * stride, own);
-      act_store8_t<DT>(B, row, width + c0 + q * stride, acc);
+      act_store8_t<DT>(B, row, width + c0 + q * stride, acc[q]);
     }
   }
 #pragma unroll
@@ -794,16 +788,21 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
   DIPPM_ARG_CHECK(N >= 1 && width % 256 == 0 && width <= 1024, "readout_aggregate_t: width %d must be 256/512/768/1024",
                   width);
   DIPPM_ARG_CHECK(!bias_out || sync, "readout_aggregate_t: bias_grad needs the sync counters");
-  const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double));
-  int rpb = bias_out ? wave_rows_t(N, 3) : kRowsPerBlock;
+  int rpb = bias_out ? wave_rows_t(N, width >= 768 ? 2 : 3) : kRowsPerBlock;  // the kernel's residency
   if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
+  // [warp partials | fold scratch] then the staged bit words of rpb + halo rows
+  const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double)) +
+                      (size_t)(width / 32) * (rpb + kBitsHalo) * sizeof(uint32_t);
   const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
 #define DIPPM_RB(D, C)                                                                                            \
   do {                                                                                                            \
-    if (smem > 48 * 1024)                                                                                         \
+    static bool attr_set = false; /* dynamic + static shared memory can pass 48 KB at any size */               \
+    if (!attr_set) {                                                                                              \
       DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_readout_agg_bits<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                            (int)smem));                                                          \
+                                            160 * 1024));                                                         \
+      attr_set = true;                                                                                            \
+    }                                                                                                             \
     k_readout_agg_bits<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, rpb, t_rowptr, t_col, inv_deg, colsum_partial, \
                                                             ro, bias_out, sync);                                  \
   } while (0)
