@@ -66,6 +66,9 @@ struct Params {
   float* pool_graph;
   const int* node_graph;
   const int* graph_ptr;
+  unsigned long long* ts;  // diagnostics only (DIPPM_GEMM_TS=<device address>): per-CTA globaltimer stamps
+  int dbg;  // diagnostics only (DIPPM_GEMM_DEBUG): bit 0 skip epilogue stores, bit 1 skip the
+            // bit masks, bit 2 skip the whole chunk loop (release the accumulator at once)
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -300,6 +303,69 @@ __device__ __forceinline__ void epi_store_chunk(uint8_t* stg_base, const CUtenso
   }
 }
 
+// Packed epilogue helpers (FWD, bf16 output): bias add on the fp32 pair pipe (FADD2), round to
+// bf16x2, ReLU on the packed pair (max(round(x), 0) == round(max(x, 0)): rounding is monotone),
+// and the 1-bit (stored value > 0) mask from the packed pair (HSETP2) -- about 2.7 instructions per
+// element against 5 for the per-float sequence (the layer-1 epilogue is instruction-bound).
+__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t relu_bf16x2(uint32_t w) {
+  uint32_t r;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(0u));
+  return r;
+}
+// bits 2i / 2i+1 of `bits` |= (low / high half of w) > 0
+template <int I>
+__device__ __forceinline__ void pos_bits_bf16x2(uint32_t& bits, uint32_t w) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.gt.bf16x2 p|q, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t@q or.b32 %0, %0, %4;\n\t}"
+      : "+r"(bits)
+      : "r"(w), "r"(0u), "n"(1u << (2 * I)), "n"(1u << (2 * I + 1)));
+}
+// four independent predicated-OR chains (words i, i+4, i+8, i+12), then a 3-level OR: the
+// dependent chain per chunk is 8 ORs instead of 32 (the epilogue runs 2 warps per scheduler)
+template <int I>
+struct PosBits {
+  static __device__ __forceinline__ void run(uint32_t (&b)[4], const uint32_t (&w)[16]) {
+    PosBits<I - 1>::run(b, w);
+    pos_bits_bf16x2<I - 1>(b[(I - 1) & 3], w[I - 1]);
+  }
+};
+template <>
+struct PosBits<0> {
+  static __device__ __forceinline__ void run(uint32_t (&)[4], const uint32_t (&)[16]) {}
+};
+__device__ __forceinline__ uint32_t pos_bits32(const uint32_t (&w)[16]) {
+  uint32_t b[4] = {0u, 0u, 0u, 0u};
+  PosBits<16>::run(b, w);
+  return (b[0] | b[1]) | (b[2] | b[3]);
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// 32 packed bf16 of one row (this lane) -> the warp's 64B-swizzled staging slot -> TMA store
+__device__ __forceinline__ void epi_store_packed(uint8_t* stg_base, const CUtensorMap* map, int lane,
+                                                 const uint32_t (&w)[16], int x, int y, int chunk) {
+  uint8_t* stg = stg_base + (chunk & 1) * 2048;
+  stage_wait(lane, 1);
+  const uint32_t d = smem_u32(stg + lane * 64);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) sts128(d + ((k ^ ((lane >> 1) & 3)) << 4), w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+  stage_issue(map, stg, lane, x, y, 0);
+}
+
 template <int kFmt, int kBN, int kCta>
 struct Cfg {
   static constexpr int kElem = kFmt == 1 ? 2 : 4;
@@ -311,10 +377,15 @@ struct Cfg {
   static constexpr int kATile = kBM * 128;      // bytes per plane
   static constexpr int kBTile = kBNl * 128;
   static constexpr int kStageBytes = kPlanes * (kATile + kBTile);
-  static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
+  // bias staging for the packed FWD epilogue (bf16): up to 1024 columns, paid for by one ring stage
+  // fewer on the 1-CTA 256-wide tile (the only shape whose ring fills the shared memory)
+  static constexpr int kBiasCols = (kFmt == 1 && kCta == 1 && kBN == 256) ? 1024 : 0;
+  static constexpr int kBiasBytes = kBiasCols * 4;
+  static constexpr int kRing = 196608 - ((kFmt == 1 && kCta == 1 && kBN == 256) ? kStageBytes : 0);
+  static constexpr int kStages = (kRing / kStageBytes) < 8 ? (kRing / kStageBytes) : 8;
   static constexpr int kTmemCols = 2 * kBN;     // double-buffered accumulator
   static constexpr int kEpiStage = kEpiWarps * kStageWarpBytes;  // TMA-store staging of the epilogue warps
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiStage + 1024 + 256;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiStage + kBiasBytes + 1024 + 256;
 };
 
 // ---- CTA-pair (cta_group::2) plumbing -------------------------------------
@@ -375,35 +446,78 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 
 // Fixed-order split-K reduction of one CTA's 128-row tile slice: out = scale * sum_s C_s
-// (fp64 sums, split order 0..S-1, independent of which CTA reduces, so results are
-// deterministic).  Partials are read through L2 (ld.global.cg).
+// (fp64 sums, independent of which CTA reduces, so results are deterministic).  Partials are
+// read through L2 (ld.global.cg).  When the slice is small (the layer-1 weight gradient: ~1 row
+// x 64 float4 per CTA against 74 splits) the splits are cut into G contiguous groups summed by
+// different threads (16 loads in flight each) and the group sums are added in group order in
+// shared memory: the reduction is no longer a 74-deep chain of L2 round trips.
 template <int kBN>
-__device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, int n0, int r0, int r1, int tid) {
-  constexpr int kC4 = kBN / 4;
+__device__ __forceinline__ void sum_splits(const Params& p, const float* src, int s0, int s1, double (&a)[4]) {
   const int64_t plane = p.M * p.ldc;
-  for (int idx = tid; idx < (r1 - r0) * kC4; idx += kEpiWarps * 32) {
-    const int64_t r = m0 + r0 + idx / kC4;
-    const int c = n0 + (idx % kC4) * 4;
-    const float* src = p.c + r * p.ldc + c;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int s = 0;
-    for (; s + 8 <= p.splits; s += 8) {  // 8 loads in flight, summed in split order
-      float4 v[8];
+  int s = s0;
+  for (; s + 16 <= s1; s += 16) {  // 16 loads in flight, summed in split order
+    float4 v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src + (s + j) * plane));
+    for (int j = 0; j < 16; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src + (s + j) * plane));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        a0 += v[j].x; a1 += v[j].y; a2 += v[j].z; a3 += v[j].w;
-      }
+    for (int j = 0; j < 16; ++j) {
+      a[0] += v[j].x; a[1] += v[j].y; a[2] += v[j].z; a[3] += v[j].w;
     }
-    for (; s < p.splits; ++s) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * plane));
-      a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
-    }
-    const double sc = p.out_scale;
-    *reinterpret_cast<float4*>(p.wout + r * p.ldo + c) =
-        make_float4((float)(a0 * sc), (float)(a1 * sc), (float)(a2 * sc), (float)(a3 * sc));
   }
+  for (; s + 4 <= s1; s += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src + (s + j) * plane));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[0] += v[j].x; a[1] += v[j].y; a[2] += v[j].z; a[3] += v[j].w;
+    }
+  }
+  for (; s < s1; ++s) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * plane));
+    a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
+  }
+}
+
+template <int kBN>
+__device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, int n0, int r0, int r1, int tid,
+                                                  double4* s_red /* kEpiWarps * 32 entries */) {
+  constexpr int kC4 = kBN / 4;
+  constexpr int kT = kEpiWarps * 32;
+  const int items = (r1 - r0) * kC4;
+  int G = 1;  // split groups: a power of two with G * items <= kT / 2, at least 4 splits per group
+  while (G < 8 && 2 * G * items <= kT && 4 * G <= p.splits) G <<= 1;
+  const double sc = p.out_scale;
+  if (G == 1) {
+    for (int idx = tid; idx < items; idx += kT) {
+      const int64_t r = m0 + r0 + idx / kC4;
+      const int c = n0 + (idx % kC4) * 4;
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      sum_splits<kBN>(p, p.c + r * p.ldc + c, 0, p.splits, a);
+      *reinterpret_cast<float4*>(p.wout + r * p.ldo + c) =
+          make_float4((float)(a[0] * sc), (float)(a[1] * sc), (float)(a[2] * sc), (float)(a[3] * sc));
+    }
+    return;
+  }
+  // one pass: thread (group gi, item idx); every epilogue thread reaches both barriers
+  const int per = kT / G, gi = tid / per, idx = tid % per;
+  const bool valid = idx < items;
+  const int64_t r = m0 + r0 + idx / kC4;
+  const int c = n0 + (idx % kC4) * 4;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  if (valid)
+    sum_splits<kBN>(p, p.c + r * p.ldc + c, (int)((int64_t)gi * p.splits / G), (int)((int64_t)(gi + 1) * p.splits / G), a);
+  s_red[tid] = make_double4(a[0], a[1], a[2], a[3]);
+  epi_sync();
+  if (gi == 0 && valid) {
+    for (int g = 1; g < G; ++g) {  // group order
+      const double4 t = s_red[g * per + idx];
+      a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+    }
+    *reinterpret_cast<float4*>(p.wout + r * p.ldo + c) =
+        make_float4((float)(a[0] * sc), (float)(a[1] * sc), (float)(a[2] * sc), (float)(a[3] * sc));
+  }
+  epi_sync();
 }
 
 // Fused readout: a warp holds 32 consecutive rows (one per lane) x 32 columns.  A
@@ -495,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + C::kStages * C::kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + C::kEpiStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + C::kEpiStage + C::kBiasBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -504,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = kCta == 2 ? cluster_rank() : 0u;
   const int cid = blockIdx.x / kCta, ncl = gridDim.x / kCta;
+  if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 0] = globaltimer();
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -533,6 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 1] = globaltimer();
 
   const int tiles_mn = p.m_tiles * p.n_tiles;
   const int total = tiles_mn * p.splits;
@@ -649,6 +765,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mbar_arrive(&tempty[acc]);
       }
     };
+    // the whole bias vector in shared memory once (packed FWD epilogue: 8 broadcast LDS.128 per chunk)
+    const uint32_t s_bias = smem_u32(epi_stage + C::kEpiStage);
+    if constexpr (C::kBiasCols > 0 && kEpi == EPI_FWD) {
+      if (p.bias && p.N <= C::kBiasCols) {
+        for (int c = threadIdx.x - 64; c < p.N; c += kEpiWarps * 32)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(s_bias + 4 * c), "f"(__ldg(p.bias + c)) : "memory");
+        epi_sync();
+      }
+    }
     uint32_t local = 0;
     for (int t = cid; t < total; t += ncl, ++local) {
       const int split = t / tiles_mn, r = t % tiles_mn;
@@ -714,13 +839,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // of each of this warp's chunks, fetched before the accumulator wait and broadcast with
       // shuffles, so no load latency sits inside the chunk loop.  Pair tiles (long K, epilogue
       // hidden under the MMAs) load the bias per chunk: fewer instructions.
+      // packed FWD epilogue: bf16 output with bias and ReLU and no fused readout (layers 1-2)
+      const bool fast_fwd = kFmt == 1 && kEpi == EPI_FWD && kCta == 1 && p.out.base && p.out.dtype == DIPPM_DT_BF16 && p.relu &&
+                            p.bias && !p.pool_part && (C::kBiasCols == 0 || p.N <= C::kBiasCols) && !(p.dbg & 8);
       float bl[kBN / 64];
       if constexpr ((kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) && kCta == 1) {
+        if (!fast_fwd) {
 #pragma unroll
-        for (int i = 0; i < kBN / 64; ++i) bl[i] = p.bias ? __ldg(p.bias + n0 + (half + 2 * i) * 32 + lane) : 0.f;
+          for (int i = 0; i < kBN / 64; ++i) bl[i] = p.bias ? __ldg(p.bias + n0 + (half + 2 * i) * 32 + lane) : 0.f;
+        }
       }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
+      if (p.ts && threadIdx.x == 64 && local == 0) p.ts[blockIdx.x * 8 + 4] = globaltimer();
+      if (p.dbg & 4) {
+        release(acc);
+        continue;
+      }
       // TMEM reads run one chunk ahead: chunk i+1 is in flight while chunk i is processed.
       const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBN;
       uint32_t rawb[2][32];
@@ -732,7 +867,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i + 1 < kBN / 64) tmem_ld32_issue(tq + (ch + 2) * 32, rawb[(i + 1) & 1]);
         uint32_t(&raw)[32] = rawb[i & 1];
         const int n = n0 + ch * 32;
-        if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
+        if (kEpi == EPI_FWD && fast_fwd) {
+          // bf16 output + bias + ReLU, no readout: the packed sequence (see pos_bits_bf16x2)
+          uint32_t w[16];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 b = C::kBiasCols ? lds128f(s_bias + (uint32_t)(n * 4 + g * 16))  // broadcast
+                                          : __ldg(reinterpret_cast<const float4*>(p.bias + n) + g);
+            const float2 x0 = add_f32x2(make_float2(__uint_as_float(raw[4 * g]), __uint_as_float(raw[4 * g + 1])),
+                                        make_float2(b.x, b.y));
+            const float2 x1 = add_f32x2(make_float2(__uint_as_float(raw[4 * g + 2]), __uint_as_float(raw[4 * g + 3])),
+                                        make_float2(b.z, b.w));
+            w[2 * g] = relu_bf16x2(pack_bf16x2(x0.x, x0.y));
+            w[2 * g + 1] = relu_bf16x2(pack_bf16x2(x1.x, x1.y));
+          }
+          if (p.relu_bits && row < p.M && !(p.dbg & 2)) {
+            const uint32_t bits = pos_bits32(w);
+            if (p.bits_ld > 0) p.relu_bits[(n >> 5) * p.bits_ld + row] = bits;
+            else p.relu_bits[row * (p.N >> 5) + (n >> 5)] = bits;
+          }
+          if (!(p.dbg & 1))
+            epi_store_packed(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, lane, w, n, m0 + q * 32,
+                             local * (kBN / 64) + (ch >> 1));
+          else if (w[0] == 0x12345678u && w[15] == 0x9abcdef0u)  // keep the values live
+            p.relu_bits[0] = w[3];
+        } else if constexpr (kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) {
           float v[32];
           if constexpr (kCta == 1) {
 #pragma unroll
@@ -824,6 +983,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __shared__ uint32_t s_go;  // "this CTA reduces" flag, away from the TMEM address slot
           uint32_t* s_flag = &s_go;
           epi_sync();  // this CTA's partial rows are all written
+          if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 5] = globaltimer();
           if (tid == 0) {
             __threadfence();
             const int old = atomicAdd(arrive, 1);
@@ -842,11 +1002,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             *s_flag = go;
           }
           epi_sync();
+          if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 6] = globaltimer();
           const int rows_valid = (int)(p.M - m0 < kBM ? p.M - m0 : kBM);
           if (*s_flag && rows_valid > 0) {
             const int r0 = p.reduce_mode == 1 ? (int)((int64_t)split * rows_valid / p.splits) : 0;
             const int r1 = p.reduce_mode == 1 ? (int)((int64_t)(split + 1) * rows_valid / p.splits) : rows_valid;
-            reduce_rows_slice<kBN>(p, m0, n0, r0, r1, tid);
+            reduce_rows_slice<kBN>(p, m0, n0, r0, r1, tid, reinterpret_cast<double4*>(epi_stage));
           }
           if (p.reduce_mode == 1) {
             epi_sync();
@@ -862,9 +1023,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores drained
   }
+  if (p.ts && threadIdx.x == 64) p.ts[blockIdx.x * 8 + 2] = globaltimer();  // first epilogue thread done
   tc_fence_before();
   if constexpr (kCta == 2) cluster_sync_all();  // both CTAs done with TMEM and with remote barriers
   else __syncthreads();
+  if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 3] = globaltimer();
   if (warp == 1) {
     tc_fence_after();
     if constexpr (kCta == 2)
@@ -967,6 +1130,10 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.graph_ptr = a->graph_ptr;
   p.gate_bits = a->gate_bits;
   p.bits_ld = a->bits_ld;
+  static const int dbg = getenv("DIPPM_GEMM_DEBUG") ? atoi(getenv("DIPPM_GEMM_DEBUG")) : 0;
+  p.dbg = dbg;
+  static unsigned long long* ts = getenv("DIPPM_GEMM_TS") ? (unsigned long long*)strtoull(getenv("DIPPM_GEMM_TS"), nullptr, 0) : nullptr;
+  p.ts = ts;
   const int total = p.m_tiles * p.n_tiles * p.splits;
   const int clusters = std::min(total, num_sms() / kCta);
   p.reduce_mode = 0;
@@ -1001,6 +1168,193 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   cfg.numAttrs = kCta == 2 ? 1 : 0;
   DIPPM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p));
   DIPPM_LAUNCH_CHECK("k_tc_gemm");
+  return DIPPM_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Short-K forward (layer 1: z = [X | agg X] @ W1 + b, K = 64): the MMAs are trivial and the
+// kernel is bound by its epilogue (bias + ReLU + bf16 rounding + 1-bit masks + 78 MB of stores),
+// which the general kernel runs with only 8 epilogue warps (2 per scheduler: latency-bound at
+// ~0.4 IPC).  Here one warp does TMA + MMA and 16 warps drain the accumulators (4 per TMEM lane
+// quarter, 2 of a tile's 8 column chunks each); the whole B (W1, N x 64) stays resident in
+// shared memory, A streams through a 6-deep ring of 128 x 64 k-blocks, and the two 256-column
+// TMEM accumulators alternate between tiles.
+namespace sk {
+constexpr int kEpi = 16;                 // epilogue warps
+constexpr int kThreads = 32 * (1 + kEpi);
+constexpr int kBN = 256;                 // tile columns (one accumulator)
+constexpr int kStages = 5;
+constexpr int kATile = kBM * 128;        // 128 rows x 64 bf16
+constexpr int kMaxN = 512;
+constexpr int kBBytes = kMaxN * 128;     // N rows x 64 bf16 (MN-major boxes of 64 x 64)
+constexpr int kStage = kEpi * 4096;
+constexpr int kSmem = kBBytes + kStages * kATile + kStage + kMaxN * 4 + 1024 + 256;
+}  // namespace sk
+
+__global__ void __launch_bounds__(sk::kThreads, 1)
+    k_fwd_shortk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, Params p) {
+  using namespace sk;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nb = (int)p.N / 64;                 // 64-column boxes of B
+  uint8_t* sB = smem;                           // [nb][64 k-rows x 128 B]
+  uint8_t* sA = sB + nb * 8192;
+  uint8_t* stage = sA + kStages * kATile;
+  float* s_bias = reinterpret_cast<float*>(stage + kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_bias + p.N);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpi);
+    }
+    mbar_init(bfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else {
+    for (int c = threadIdx.x - 32; c < p.N; c += kEpi * 32) s_bias[c] = __ldg(p.bias + c);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const int n_tiles = (int)p.N / kBN;
+  const int total = p.m_tiles * n_tiles;
+  if (warp == 0) {
+    if (lane == 0) {
+      // B once: nb boxes of (64 N-columns x 64 K-rows), MN-major, 128B swizzle
+      mbar_expect_tx(bfull, nb * 8192);
+      for (int c = 0; c < nb; ++c) tma_load_3d(sB + c * 8192, &tmB, bfull, c * 64, 0, 0);
+      constexpr uint32_t idesc = make_idesc(1, false, true, kBM, kBN);
+      uint32_t it_load = 0, it_mma = 0, local = 0;
+      // A k-blocks are fetched up to kStages tiles ahead of the MMAs (one k-block per tile)
+      auto issue_load = [&](int t) {
+        const int s = it_load % kStages;
+        mbar_wait(&empty[s], ((it_load / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], kATile);
+        tma_load_3d(sA + s * kATile, &tmA, &full[s], 0, (t / n_tiles) * kBM, 0);
+        ++it_load;
+      };
+      int t_load = blockIdx.x;
+      for (int k = 0; k < kStages && t_load < total; ++k, t_load += gridDim.x) issue_load(t_load);
+      mbar_wait(bfull, 0);
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const uint32_t acc = local & 1, use = local >> 1;
+        const int n0 = (t % n_tiles) * kBN;
+        const int s = it_mma % kStages;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        mbar_wait(&full[s], (it_mma / kStages) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + s * kATile), b0 = smem_u32(sB + (n0 / 64) * 8192);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          umma<1>(tbase + acc * kBN, sdesc(a0 + j * 32, 16, 1024), sdesc(b0 + j * 2048, 8192, 1024), idesc, j > 0);
+        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
+        // refill the slot the PREVIOUS tile used (its MMAs have had a tile's time to retire), so
+        // this thread never waits on the MMAs it has just issued
+        if (it_mma > 0 && t_load < total) {
+          issue_load(t_load);
+          t_load += gridDim.x;
+        }
+        ++it_mma;
+      }
+      for (int i = 0; i < kStages; ++i, ++it_load) mbar_wait(&empty[it_load % kStages], ((it_load / kStages) & 1) ^ 1);
+    }
+  } else {
+    const int e = warp - 1;
+    const int q = warp & 3;          // TMEM lane quarter this warp may read
+    const int sub = (warp - 1) >> 2;  // 0..3: chunks sub and sub + 4 of each tile
+    uint8_t* stg = stage + e * 4096;
+    const uint32_t sb = smem_u32(s_bias);
+    uint32_t local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const uint32_t acc = local & 1, use = local >> 1;
+      const int m0 = (t / n_tiles) * kBM, n0 = (t % n_tiles) * kBN;
+      const int64_t row = (int64_t)m0 + q * 32 + lane;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBN;
+      uint32_t raw[2][32];
+      tmem_ld32_issue(tq + sub * 32, raw[0]);
+      tmem_ld32_issue(tq + (sub + 4) * 32, raw[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // the accumulator is in registers: the MMAs may go on
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int n = n0 + (sub + 4 * i) * 32;
+        uint32_t w[16];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float4 b = lds128f(sb + (uint32_t)(n * 4 + g * 16));
+          const float2 x0 = add_f32x2(make_float2(__uint_as_float(raw[i][4 * g]), __uint_as_float(raw[i][4 * g + 1])),
+                                      make_float2(b.x, b.y));
+          const float2 x1 = add_f32x2(make_float2(__uint_as_float(raw[i][4 * g + 2]), __uint_as_float(raw[i][4 * g + 3])),
+                                      make_float2(b.z, b.w));
+          w[2 * g] = relu_bf16x2(pack_bf16x2(x0.x, x0.y));
+          w[2 * g + 1] = relu_bf16x2(pack_bf16x2(x1.x, x1.y));
+        }
+        if (p.relu_bits && row < p.M) p.relu_bits[(n >> 5) * p.bits_ld + row] = pos_bits32(w);
+        epi_store_packed(stg, &tmC, lane, w, n, m0 + q * 32, i);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+static bool shortk_ok(const dippm_gemm_args_t* a) {
+  return a->kind == DIPPM_GEMM_FWD && a->a.dtype == DIPPM_DT_BF16 && a->K == 64 && a->b_mn_major && !a->drop_mode &&
+         a->relu && a->bias && a->out.data && a->out.dtype == DIPPM_DT_BF16 && !a->pool_partial && a->N % sk::kBN == 0 &&
+         a->N <= sk::kMaxN && (!a->relu_bits || a->bits_ld >= a->M) && a->cta_pair == 0 && !getenv("DIPPM_NO_SHORTK");
+}
+
+static int run_shortk(const dippm_gemm_args_t* a, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_fwd_shortk, cudaFuncAttributeMaxDynamicSharedMemorySize, sk::kSmem));
+    attr_set = true;
+  }
+  CUtensorMap ma, mb, mc;
+  int st = make_map(&ma, a->a, a->M, a->K, 64, kBM);
+  if (!st) st = make_map(&mb, a->b, a->K, a->N, 64, 64);
+  if (!st) st = make_map(&mc, a->out, a->M, a->N, 32, 32, false, true);
+  if (st) return st;
+  Params p{};
+  p.M = a->M;
+  p.N = a->N;
+  p.K = a->K;
+  p.m_tiles = ceil_div_i(a->M, kBM);
+  p.n_tiles = (int)(a->N / sk::kBN);
+  p.bias = a->bias;
+  p.relu = 1;
+  p.out = make_view(a->out);
+  p.relu_bits = a->relu_bits;
+  p.bits_ld = a->bits_ld;
+  const int total = p.m_tiles * p.n_tiles;
+  k_fwd_shortk<<<std::min(total, num_sms()), sk::kThreads, sk::kSmem, s>>>(ma, mb, mc, p);
+  DIPPM_LAUNCH_CHECK("k_fwd_shortk");
   return DIPPM_OK;
 }
 
@@ -1087,6 +1441,7 @@ extern "C" int32_t dippm_gemm(const dippm_gemm_args_t* a, int32_t backend, void*
                   "gemm: dropout needs FWD with MN-major B, 0 <= p < 1, ldm %% 4 == 0 and (mode 1) a mask buffer");
   const int bk = a->a.dtype == DIPPM_DT_BF16 ? 64 : 32;
   DIPPM_ARG_CHECK(mn || a->K % bk == 0, "gemm: K=%lld must be a multiple of %d", (long long)a->K, bk);
+  if (tc::shortk_ok(a)) return tc::run_shortk(a, s);
   if (a->a.dtype == DIPPM_DT_BF16) return tc::dispatch<1>(a, s);
   return tc::dispatch<2>(a, s);
 }

@@ -544,3 +544,31 @@ def test_readout_aggregate_t_bits_equal_values(prec, W):
         assert np.allclose(got[:, :W], dz, atol=tol * np.abs(dz).max())
         assert np.allclose(got[:, W:], agg.T @ dz, atol=tol * np.abs(dz).max())
         assert np.allclose(outs[k][1].double().cpu().numpy(), dz.sum(0), atol=tol * np.abs(dz).sum(0).max())
+
+
+@pytest.mark.parametrize("M,N", [(76800, 512), (3001, 256), (5, 512), (129, 512)])
+def test_shortk_forward_equals_general_kernel(M, N):
+    """The dedicated K = 64 forward (layer 1: 16 epilogue warps, resident W1) gives bit-identical
+    activations and 1-bit masks to the general tcgen05 kernel (forced with cta_pair=1), and both
+    match fp64 within the bf16 tolerance; rows past M are never written."""
+    rng = np.random.default_rng(M + N)
+    K = 64
+    A, a64, _ = _rand_act(M, K, dev.DT_BF16, rng)
+    W, w64, _ = _rand_act(K, N, dev.DT_BF16, rng, 0.1)
+    bias = torch.from_numpy(rng.normal(scale=0.2, size=N).astype(np.float32)).cuda()
+    ref = np.maximum(a64 @ w64 + bias.double().cpu().numpy(), 0)
+    res = {}
+    for pair in (0, 1):
+        out = ActBuf(M + 3, 2 * N, dev.DT_BF16, "cuda")  # write the left half of a wider buffer, like A2
+        out.t.fill_(7.0)
+        bits = torch.full((N // 32, M + 3), -1, dtype=torch.int32, device="cuda")
+        _gemm(_lib.GEMM_FWD, M, N, K, A.view(), 0, W.view(), 1, bias=bias.data_ptr(), relu=1,
+              out=_lib.Act(out.t.data_ptr(), 2 * N, 0, dev.DT_BF16), relu_bits=bits.data_ptr(), bits_ld=M + 3,
+              cta_pair=pair)
+        h = out.t[:M, :N].double().cpu().numpy()
+        assert np.max(np.abs(h - ref)) <= 2e-2 * np.abs(ref).max()
+        assert np.array_equal(bits[:, :M].cpu().numpy(), _bits_of(h > 0))
+        assert bool((out.t[M:, :] == 7.0).all()) and bool((out.t[:, N:] == 7.0).all())
+        assert bool((bits[:, M:] == -1).all())
+        res[pair] = (out.t.clone(), bits.clone())
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
