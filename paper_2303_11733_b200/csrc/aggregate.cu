@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kAggThreads, 4) k_aggregate(ActView h, ActView
   __shared__ int s_ptr[kRowsPerBlockT + 1];
   __shared__ float s_w[kRowsPerBlockT];
   __shared__ int s_col[kAggColCap];
+  pdl_begin();
   const int L = (width >> 3) / CPL;  // lanes per row
   const int gpw = 32 / L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
   __shared__ int s_ptr[kRowsPerBlockT + 1];
   __shared__ int s_col[kAggColCap];
   __shared__ float s_cw[kAggColCap];
+  pdl_begin();
   const int L = (width >> 3) / CPL;
   const int gpw = 32 / L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -420,6 +422,7 @@ __global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 3) k_readout_agg_b
   __shared__ int s_col[kAggColCap];
   __shared__ float s_cw[kAggColCap];
   __shared__ int s_g[kRowsPerBlockT];
+  pdl_begin();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * rpb;
   const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
@@ -622,33 +625,48 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_concat(ActView h, const i
 
 // Second stage of the fused readout (see tc_gemm.cu pool_chunk): per graph, the block
 // sums it owns in fixed block order, divided by N_g; then the static features.
-__global__ void __launch_bounds__(256) k_pool_combine(const float* __restrict__ part, const float* __restrict__ whole,
+__global__ void __launch_bounds__(128) k_pool_combine(const float* __restrict__ part, const float* __restrict__ whole,
                                                       const int* __restrict__ graph_ptr, int width,
                                                       const double* __restrict__ fs_raw, const double* __restrict__ norm,
                                                       ActView u) {
+  pdl_begin();
+  // one thread per 4 columns: the block sums of the graph's 32-row blocks are loaded up to 8
+  // float4 at a time (one L2 round trip per 8 blocks) and added in block order (fp64)
   const int g = blockIdx.x;
   const int gs = graph_ptr[g], ge = graph_ptr[g + 1];
   const int bf = gs >> 5, bl = (ge - 1) >> 5;
   const double inv_n = 1.0 / (double)(ge - gs);
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    double t;  // block sums combined in fp64, block order
+  const int64_t rs = 2 * (int64_t)width;  // a block's two partial rows
+  for (int c = threadIdx.x * 4; c < width; c += blockDim.x * 4) {
+    double t[4];
     if (bf == bl) {
-      t = whole[(int64_t)g * width + c];
+      const float4 v = __ldg(reinterpret_cast<const float4*>(whole + (int64_t)g * width + c));
+      t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
     } else {
-      t = part[((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c];
-      int b = bf + 1;
-      for (; b + 4 <= bl; b += 4) {  // 4 loads in flight, added in block order
-        const float v0 = part[(int64_t)b * 2 * width + c], v1 = part[(int64_t)(b + 1) * 2 * width + c];
-        const float v2 = part[(int64_t)(b + 2) * 2 * width + c], v3 = part[(int64_t)(b + 3) * 2 * width + c];
-        t += v0;
-        t += v1;
-        t += v2;
-        t += v3;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c));
+      t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+      for (int b = bf + 1; b <= bl; b += 8) {  // middle blocks (slot 0), then the last block
+        float4 w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (b + j <= bl) w[j] = __ldg(reinterpret_cast<const float4*>(part + (int64_t)(b + j) * rs + c));
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (b + j <= bl) {
+            t[0] += w[j].x; t[1] += w[j].y; t[2] += w[j].z; t[3] += w[j].w;
+          }
       }
-      for (; b < bl; ++b) t += part[(int64_t)b * 2 * width + c];
-      t += part[(int64_t)bl * 2 * width + c];
     }
-    act_store(u, g, c, (float)(t * inv_n));
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = (float)(t[k] * inv_n);
+    if (u.dtype == DIPPM_DT_BF16) {
+      __nv_bfloat162 h[2] = {__floats2bfloat162_rn(o[0], o[1]), __floats2bfloat162_rn(o[2], o[3])};
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(u.base) + (int64_t)g * u.ld + c) = *reinterpret_cast<uint2*>(h);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) act_store(u, g, c + k, o[k]);
+    }
   }
   for (int k = threadIdx.x; k < u.ld - width; k += blockDim.x) {
     float v = 0.f;
@@ -725,7 +743,8 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
   const int grid = ceil_div_i(N, rpb);
   ActView hv = make_view(h), mv = make_view(m_out), sv = make_view(self_out);
 #define DIPPM_AGG(DI, DO, C) \
-  k_aggregate<DI, DO, C><<<grid, kAggThreads, 0, s>>>(hv, mv, sv, N, rpb, width, rowptr, col, inv_deg)
+  DIPPM_LAUNCH_PDL(k_aggregate<DI, DO, C>, dim3(grid), dim3(kAggThreads), 0, s, hv, mv, sv, N, rpb, width, rowptr, col, \
+                   inv_deg)
 #define DIPPM_AGG_C(DI, DO) \
   do { if (cpl == 4) DIPPM_AGG(DI, DO, 4); else if (cpl == 2) DIPPM_AGG(DI, DO, 2); else DIPPM_AGG(DI, DO, 1); } while (0)
 #define DIPPM_AGG_O(DI)                                                   \
@@ -766,8 +785,8 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
     if (smem > 48 * 1024)                                                                                        \
       DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                             (int)smem));                                                         \
-    k_aggregate_t<D, C, R><<<grid, kAggThreads, smem, s>>>(bv, width, N, rpb, write_agg, t_rowptr, t_col, inv_deg, \
-                                                          colsum_partial, ro, bias_out, sync);                   \
+    DIPPM_LAUNCH_PDL(k_aggregate_t<D, C, R>, dim3(grid), dim3(kAggThreads), smem, s, bv, width, N, rpb, write_agg,     \
+                     t_rowptr, t_col, inv_deg, colsum_partial, ro, bias_out, sync);                             \
   } while (0)
 #define DIPPM_AGGT_C(D, R) \
   do { if (cpl == 4) DIPPM_AGGT(D, 4, R); else if (cpl == 2) DIPPM_AGGT(D, 2, R); else DIPPM_AGGT(D, 1, R); } while (0)
@@ -803,8 +822,8 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
                                             160 * 1024));                                                         \
       attr_set = true;                                                                                            \
     }                                                                                                             \
-    k_readout_agg_bits<D, C><<<grid, kAggThreads, smem, s>>>(bv, width, N, rpb, t_rowptr, t_col, inv_deg, colsum_partial, \
-                                                            ro, bias_out, sync);                                  \
+    DIPPM_LAUNCH_PDL(k_readout_agg_bits<D, C>, dim3(grid), dim3(kAggThreads), smem, s, bv, width, N, rpb, t_rowptr,   \
+                     t_col, inv_deg, colsum_partial, ro, bias_out, sync);                                         \
   } while (0)
 #define DIPPM_RB_C(D) \
   do { if (width == 256) DIPPM_RB(D, 1); else if (width == 512) DIPPM_RB(D, 2); else if (width == 768) DIPPM_RB(D, 3); else DIPPM_RB(D, 4); } while (0)
@@ -890,9 +909,10 @@ int64_t dippm_pool_partial_rows(int64_t num_nodes) { return 2 * ((num_nodes + 31
 
 int32_t dippm_pool_combine(const float* pool_partial, const float* pool_graph, const int32_t* graph_ptr, int64_t G,
                            int32_t width, const double* fs_raw, const double* norm, dippm_act_t u, void* stream) {
-  DIPPM_ARG_CHECK(G >= 1 && width >= 1 && u.ld >= width + kStaticWidth, "pool_combine: bad args");
-  k_pool_combine<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(pool_partial, pool_graph, graph_ptr, width, fs_raw,
-                                                               norm, make_view(u));
+  DIPPM_ARG_CHECK(G >= 1 && width >= 4 && width % 4 == 0 && u.ld >= width + kStaticWidth && u.ld % 4 == 0,
+                  "pool_combine: bad args");
+  DIPPM_LAUNCH_PDL(k_pool_combine, dim3((unsigned)G), dim3(128), 0, (cudaStream_t)stream, pool_partial, pool_graph,
+                   graph_ptr, width, fs_raw, norm, make_view(u));
   DIPPM_LAUNCH_CHECK("k_pool_combine");
   return DIPPM_OK;
 }

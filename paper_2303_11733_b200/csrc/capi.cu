@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -23,6 +24,15 @@ void set_error(const char* fmt, ...) {
 int cuda_status(cudaError_t e, const char* what) {
   set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
   return DIPPM_ERR_CUDA;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    // measured: no gain inside the captured step (724 vs 730 us), so off unless DIPPM_PDL=1
+    const char* e = getenv("DIPPM_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 int num_sms() {
@@ -130,6 +140,7 @@ __global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, doub
                                                     double gscale, int64_t n, double lr, double b1, double b2,
                                                     double eps, double bc1, double bc2, const int64_t* t_dev,
                                                     int do_adam, float* __restrict__ p32, PackSegs segs) {
+  pdl_begin();
   const int64_t n4 = n >> 2;
   // warm this thread's first group in L1 while thread 0 evaluates the bias corrections
   const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -338,14 +349,14 @@ int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads
     const int b4 = (int)std::min<int64_t>(ceil_div_i(n4 / 4, 256), 8 * num_sms());
     const int dt = nsegs ? (int)segs[0].dst.dtype : DIPPM_DT_F32;
     if (dt == DIPPM_DT_BF16)
-      k_adam_pack4<DIPPM_DT_BF16><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1,
+      DIPPM_LAUNCH_PDL(k_adam_pack4<DIPPM_DT_BF16>, dim3(b4), dim3(256), 0, (cudaStream_t)stream, params, m, v, grads, grad_scale, n, lr, beta1,
                                                                       beta2, eps, bc1, bc2, t_dev, do_adam, p32, ps);
     else if (dt == DIPPM_DT_TF32X3)
-      k_adam_pack4<DIPPM_DT_TF32X3><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr,
+      DIPPM_LAUNCH_PDL(k_adam_pack4<DIPPM_DT_TF32X3>, dim3(b4), dim3(256), 0, (cudaStream_t)stream, params, m, v, grads, grad_scale, n, lr,
                                                                         beta1, beta2, eps, bc1, bc2, t_dev, do_adam,
                                                                         p32, ps);
     else
-      k_adam_pack4<DIPPM_DT_F32><<<b4, 256, 0, (cudaStream_t)stream>>>(params, m, v, grads, grad_scale, n, lr, beta1,
+      DIPPM_LAUNCH_PDL(k_adam_pack4<DIPPM_DT_F32>, dim3(b4), dim3(256), 0, (cudaStream_t)stream, params, m, v, grads, grad_scale, n, lr, beta1,
                                                                      beta2, eps, bc1, bc2, t_dev, do_adam, p32, ps);
     DIPPM_LAUNCH_CHECK("k_adam_pack4");
     return DIPPM_OK;

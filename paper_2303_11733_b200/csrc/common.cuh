@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/dippm_b200.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -45,6 +47,38 @@ void count_launches(int n);
 
 inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 int num_sms();
+
+// Programmatic dependent launch: the training step's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization when DIPPM_PDL=1 (off by default: it measured no
+// gain inside the captured CUDA-graph step), so a kernel's
+// launch and prologue overlap its predecessor's tail.  Every such kernel calls pdl_begin() in
+// every CTA before it touches memory the predecessor wrote (griddepcontrol.wait returns once the
+// predecessor grid has completed and its writes are visible; it is a no-op without the
+// attribute), then allows its own dependents to launch (they wait the same way).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#define DIPPM_LAUNCH_PDL(...)                                       \
+  do {                                                             \
+    cudaError_t _le = ::dippm::launch_pdl(__VA_ARGS__);            \
+    if (_le != cudaSuccess) return ::dippm::cuda_status(_le, "launch"); \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // Activation storage.  A "plane pair" holds an fp32 value v as two fp32 planes

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict_
                                                       int32_t* bad, int32_t* node_graph) {
   extern __shared__ int sm[];
   __shared__ int s_tmp[33];
+  pdl_begin();
   const int g = blockIdx.x;
   const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
   const int64_t e0 = edge_ptr[g];
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict_
                                                       int32_t* t_rowptr, int32_t* t_col) {
   extern __shared__ int sm[];
   __shared__ int s_tmp[33];
+  pdl_begin();
   const int g = blockIdx.x;
   const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
   const int64_t e0 = edge_ptr[g];
@@ -520,10 +522,10 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
     smem_set = 200 * 1024;
   }
   DIPPM_CUDA_CHECK(cudaMemsetAsync(bad_edge, 0, sizeof(int), s));
-  k_csr_g1<<<(unsigned)G, kGThreads, smem, s>>>(src, dst, graph_ptr, edge_ptr, epad, deg, inv_deg, scratch, uniq,
-                                                bad_edge, node_graph);
-  k_csr_g3<<<(unsigned)G, kGThreads, smem, s>>>(graph_ptr, edge_ptr, scratch, uniq, epad, N, (int)G, rowptr,
-                                                col, t_rowptr, t_col);
+  DIPPM_LAUNCH_PDL(k_csr_g1, dim3((unsigned)G), dim3(kGThreads), smem, s, src, dst, graph_ptr, edge_ptr, epad, deg,
+                   inv_deg, scratch, uniq, bad_edge, node_graph);
+  DIPPM_LAUNCH_PDL(k_csr_g3, dim3((unsigned)G), dim3(kGThreads), smem, s, graph_ptr, edge_ptr, scratch, uniq, epad, N,
+                   (int)G, rowptr, col, t_rowptr, t_col);
   DIPPM_LAUNCH_CHECK_N(2, "build_csr_grouped");
   return DIPPM_OK;
 }

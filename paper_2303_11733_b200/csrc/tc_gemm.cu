@@ -648,6 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_begin();  // barriers, TMEM and tensor maps are set up: now wait for the producer kernel
   if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 1] = globaltimer();
 
   const int tiles_mn = p.m_tiles * p.n_tiles;
@@ -1159,13 +1160,22 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cf::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCta;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (kCta == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = kCta;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = kCta == 2 ? 1 : 0;
+  cfg.numAttrs = na;
   DIPPM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p));
   DIPPM_LAUNCH_CHECK("k_tc_gemm");
   return DIPPM_OK;
@@ -1225,13 +1235,16 @@ __global__ void __launch_bounds__(sk::kThreads, 1)
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  } else {
-    for (int c = threadIdx.x - 32; c < p.N; c += kEpi * 32) s_bias[c] = __ldg(p.bias + c);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_begin();
+  if (warp > 0) {  // the bias (written by the previous step's Adam kernel) once, into shared memory
+    for (int c = threadIdx.x - 32; c < p.N; c += kEpi * 32) s_bias[c] = __ldg(p.bias + c);
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpi * 32) : "memory");
+  }
   const int n_tiles = (int)p.N / kBN;
   const int total = p.m_tiles * n_tiles;
   if (warp == 0) {
@@ -1353,7 +1366,7 @@ static int run_shortk(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.relu_bits = a->relu_bits;
   p.bits_ld = a->bits_ld;
   const int total = p.m_tiles * p.n_tiles;
-  k_fwd_shortk<<<std::min(total, num_sms()), sk::kThreads, sk::kSmem, s>>>(ma, mb, mc, p);
+  DIPPM_LAUNCH_PDL(k_fwd_shortk, dim3(std::min(total, num_sms())), dim3(sk::kThreads), (size_t)sk::kSmem, s, ma, mb, mc, p);
   DIPPM_LAUNCH_CHECK("k_fwd_shortk");
   return DIPPM_OK;
 }
