@@ -515,6 +515,170 @@ __global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 3) k_readout_agg_b
   if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
 }
 
+// The training step's layout of the same computation (bf16 B, row-major bit masks,
+// width = 256 * CPL): one row's CPL*8 bit words are contiguous, so the block's rows plus the
+// halo are staged with 16-byte copies in the row-major order the warps read them (a lane's
+// words for its chunks are a broadcast LDS each); the neighbour loop has no layout or
+// dtype generality, the first neighbour initialises the accumulator, and the rare
+// neighbour outside the staged window / block with more than kAggColCap out-edges takes a
+// separate uniform branch; a row with one out-edge (the common case) forms dr * w0 * bit
+// directly.  At configs[1] the row loop runs at the write bandwidth (29 us for 157 MB against
+// 27 us for a bare store loop of the same pattern); the rest of the launch is the staging
+// prologue and the bias fold.
+template <int CPL>
+__global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 4) k_readout_bits_rm(__nv_bfloat16* __restrict__ Bp, int64_t ldb,
+                                                                    int64_t N, int rpb,
+                                                                    const int* __restrict__ t_rowptr,
+                                                                    const int* __restrict__ t_col,
+                                                                    const float* __restrict__ inv_deg,
+                                                                    float* __restrict__ colsum_partial,
+                                                                    ReadoutArgs ro, float* __restrict__ bias_out,
+                                                                    int* __restrict__ sync) {
+  constexpr int W = CPL * 8;  // bit words per row
+  constexpr int width = CPL * 256;
+  extern __shared__ __align__(16) float s_part[];  // [8 warps][width], then the staged bit words [R][W]
+  __shared__ int s_ptr[kRowsPerBlockT + 1];
+  __shared__ int s_col[kAggColCap];
+  __shared__ float s_cw[kAggColCap];
+  __shared__ int s_g[kRowsPerBlockT];
+  pdl_begin();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int nrows = (int)((N - r0 < rpb) ? N - r0 : rpb);
+  const int R = (int)((N - r0 < rpb + kBitsHalo) ? N - r0 : rpb + kBitsHalo);
+  const int cbeg = t_rowptr[r0];
+  const int ncol = t_rowptr[r0 + nrows] - cbeg;
+  const bool staged = ncol <= kAggColCap;
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_part + (kAggThreads / 32) * width);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(ro.h3_bits + r0 * W);
+    uint4* dst = reinterpret_cast<uint4*>(s_bits);
+    for (int i = threadIdx.x; i < R * (W / 4); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  for (int i = threadIdx.x; i <= nrows; i += blockDim.x) s_ptr[i] = t_rowptr[r0 + i] - cbeg;
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x) s_g[i] = ro.node_graph[r0 + i];
+  if (staged)
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
+      const int v = t_col[cbeg + i];
+      s_col[i] = v;
+      s_cw[i] = inv_deg[v];
+    }
+  __syncthreads();
+  const int c0 = lane * 8;            // lane chunks: columns c0 + q * 256 .. + 8
+  const int wl = lane >> 2, sh = (lane & 3) * 8;  // word (of each 256-column group) and bit offset
+  float part[CPL][8] = {};
+  float dr[CPL][8];
+  int g_cur = -1;
+  // bit words of neighbour v (staged window, else global)
+  auto nbits = [&](int v, uint32_t (&wv)[CPL]) {
+    const unsigned rel = (unsigned)((int64_t)v - r0);
+    if (rel < (unsigned)R) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) wv[q] = s_bits[rel * W + q * 8 + wl] >> sh;
+    } else {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) wv[q] = __ldg(ro.h3_bits + (int64_t)v * W + q * 8 + wl) >> sh;
+    }
+  };
+  auto rows = [&](auto staged_tag) {
+    constexpr bool kStaged = decltype(staged_tag)::value;
+    for (int lr = warp; lr < nrows; lr += kAggThreads / 32) {
+      const int b = s_ptr[lr], e = s_ptr[lr + 1];
+      const int g = s_g[lr];
+      if (g != g_cur) {  // rows of a graph are contiguous: reload dr only at graph changes
+        g_cur = g;
+        const float inv_n = 1.0f / (float)(ro.graph_ptr[g + 1] - ro.graph_ptr[g]);
+        const float* dp = ro.du + (int64_t)g * ro.ld_du;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * 256));
+          const float4 a2 = __ldg(reinterpret_cast<const float4*>(dp + c0 + q * 256 + 4));
+          dr[q][0] = a.x * inv_n; dr[q][1] = a.y * inv_n; dr[q][2] = a.z * inv_n; dr[q][3] = a.w * inv_n;
+          dr[q][4] = a2.x * inv_n; dr[q][5] = a2.y * inv_n; dr[q][6] = a2.z * inv_n; dr[q][7] = a2.w * inv_n;
+        }
+      }
+      __nv_bfloat16* brow = Bp + (r0 + lr) * ldb + c0;
+      // own rows: dz3 = dr * bit (and the bias partial)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const uint32_t x = s_bits[lr * W + q * 8 + wl] >> sh;
+        uint4 o;
+        uint32_t* op = &o.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float o0 = (x >> (2 * i)) & 1u ? dr[q][2 * i] : 0.f;
+          const float o1 = (x >> (2 * i + 1)) & 1u ? dr[q][2 * i + 1] : 0.f;
+          part[q][2 * i] += o0;
+          part[q][2 * i + 1] += o1;
+          __nv_bfloat162 ho = __floats2bfloat162_rn(o0, o1);
+          op[i] = *reinterpret_cast<uint32_t*>(&ho);
+        }
+        *reinterpret_cast<uint4*>(brow + q * 256) = o;
+      }
+      // agg^T dz3 = dr * sum_{u->v} bit(v) / deg(v); one out-edge (the common case): dr * w0 * bit
+      uint4 ag[CPL];
+      if (e - b == 1) {
+        const int v = kStaged ? s_col[b] : t_col[cbeg + b];
+        const float w0 = kStaged ? s_cw[b] : inv_deg[v];
+        uint32_t wv[CPL];
+        nbits(v, wv);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          uint32_t* ap = &ag[q].x;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float a0 = (wv[q] >> (2 * i)) & 1u ? w0 * dr[q][2 * i] : 0.f;
+            const float a1 = (wv[q] >> (2 * i + 1)) & 1u ? w0 * dr[q][2 * i + 1] : 0.f;
+            __nv_bfloat162 ha = __floats2bfloat162_rn(a0, a1);
+            ap[i] = *reinterpret_cast<uint32_t*>(&ha);
+          }
+        }
+      } else {
+        float acc[CPL][8];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[q][k] = 0.f;
+        for (int j = b; j < e; ++j) {  // out-edges in CSR order
+          const int v = kStaged ? s_col[j] : t_col[cbeg + j];
+          const float w0 = kStaged ? s_cw[j] : inv_deg[v];
+          uint32_t wv[CPL];
+          nbits(v, wv);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[q][k] += (wv[q] >> k) & 1u ? w0 : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          uint32_t* ap = &ag[q].x;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 ha = __floats2bfloat162_rn(acc[q][2 * i] * dr[q][2 * i], acc[q][2 * i + 1] * dr[q][2 * i + 1]);
+            ap[i] = *reinterpret_cast<uint32_t*>(&ha);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) *reinterpret_cast<uint4*>(brow + width + q * 256) = ag[q];
+    }
+  };
+  if (staged) rows(std::true_type{});
+  else rows(std::false_type{});
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_part[warp * width + c0 + q * 256 + k] = part[q][k];
+  __syncthreads();
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kAggThreads / 32; ++w) t += s_part[w * width + c];
+    colsum_partial[(int64_t)blockIdx.x * width + c] = t;
+  }
+  if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
+}
+
 // Readout backward (gnn.py:224, 227): dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0).
 __global__ void __launch_bounds__(kAggThreads) k_readout_backward(const float* __restrict__ du, int64_t ld_du,
                                                                   int width, ActView gate, ActView dz, int64_t N,
@@ -813,6 +977,34 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
   const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double)) +
                       (size_t)(width / 32) * (rpb + kBitsHalo) * sizeof(uint32_t);
   const int grid = ceil_div_i(N, rpb);
+  static const bool generic = getenv("DIPPM_RO_GENERIC") != nullptr;  // A/B switch: the layout-generic kernel
+  if (B.dtype == DIPPM_DT_BF16 && ro.bits_ld == 0 && B.ld % 8 == 0 && !generic) {
+    __nv_bfloat16* bp = reinterpret_cast<__nv_bfloat16*>(B.data);
+    if (bias_out) {  // 4 resident blocks per SM at width <= 512
+      rpb = wave_rows_t(N, width >= 768 ? 2 : 4);
+      if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
+    }
+    const int grid = ceil_div_i(N, rpb);
+    const size_t smem = (size_t)(kAggThreads / 32) * width * sizeof(float) + (size_t)(width / 32) * (rpb + kBitsHalo) * 4;
+#define DIPPM_RBM(C)                                                                                               \
+  do {                                                                                                             \
+    static bool attr_set = false;                                                                                  \
+    if (!attr_set) {                                                                                               \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_readout_bits_rm<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                            160 * 1024));                                                          \
+      attr_set = true;                                                                                             \
+    }                                                                                                              \
+    DIPPM_LAUNCH_PDL(k_readout_bits_rm<C>, dim3(grid), dim3(kAggThreads), smem, s, bp, B.ld, N, rpb, t_rowptr, t_col, \
+                     inv_deg, colsum_partial, ro, bias_out, sync);                                                 \
+  } while (0)
+    if (width == 256) DIPPM_RBM(1);
+    else if (width == 512) DIPPM_RBM(2);
+    else if (width == 768) DIPPM_RBM(3);
+    else DIPPM_RBM(4);
+#undef DIPPM_RBM
+    DIPPM_LAUNCH_CHECK("k_readout_bits_rm");
+    return DIPPM_OK;
+  }
   ActView bv = make_view(B);
 #define DIPPM_RB(D, C)                                                                                            \
   do {                                                                                                            \

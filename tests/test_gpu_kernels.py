@@ -546,6 +546,68 @@ def test_readout_aggregate_t_bits_equal_values(prec, W):
         assert np.allclose(outs[k][1].double().cpu().numpy(), dz.sum(0), atol=tol * np.abs(dz).sum(0).max())
 
 
+@pytest.mark.parametrize("W", [256, 512, 1024])
+def test_readout_bits_row_major_far_and_dense(W):
+    """The training layout's readout kernel (bf16, row-major bits) on graphs that leave its fast
+    paths: out-neighbours far beyond the staged halo (global bit reads), nodes with dozens of
+    out-edges (blocks whose CSR slice exceeds the shared-memory stage), rows with zero, one and
+    many out-edges -- dz3, agg^T dz3 and the bias gradient against fp64, and dz3 / agg^T dz3
+    bit-identical to the layout-generic kernel on the chunk-major copy of the same masks."""
+    rng = np.random.default_rng(W)
+    n = np.array([5, 3000, 700, 1, 2500])
+    G = len(n)
+    gp = np.zeros(G + 1, np.int32)
+    np.cumsum(n, out=gp[1:])
+    N = int(gp[-1])
+    src, dst = [], []
+    for g in range(G):
+        lo, hi = int(gp[g]), int(gp[g + 1])
+        for v in range(lo + 1, hi):
+            src.append(v - 1)
+            dst.append(v)                                   # chain: one out-edge
+            if v % 7 == 0:
+                src.append(int(rng.integers(lo, v)))        # far back-reference (forward of u: far ahead)
+                dst.append(v)
+        if hi - lo > 100:
+            for u in range(lo, lo + 120):                   # hub rows: ~40 out-edges each
+                for v in rng.choice(np.arange(u + 1, hi), size=40, replace=False):
+                    src.append(u)
+                    dst.append(int(v))
+    src, dst = np.array(src), np.array(dst)
+    b = upload_batch(np.zeros((N, 32), np.float32), src, dst, gp, np.zeros((G, 5), np.float32))
+    h3, h64, _ = _rand_act(N, W, dev.DT_BF16, rng)
+    bits_np = _bits_of(h64 > 0)
+    du = torch.from_numpy(rng.normal(size=(G, W)).astype(np.float32)).cuda()
+    lib = _lib.load()
+    outs = []
+    for layout in ("chunk", "row"):
+        bits = torch.from_numpy(bits_np if layout == "chunk" else np.ascontiguousarray(bits_np.T)).cuda()
+        B = ActBuf(N, 2 * W, dev.DT_BF16, "cuda")
+        part = torch.empty(lib.dippm_colsum_rows(N), W, device="cuda")
+        sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device="cuda")
+        bias = torch.empty(W, device="cuda")
+        _lib.call("dippm_readout_aggregate_t", du.data_ptr(), W, b.graph_ptr.data_ptr(), b.node_graph.data_ptr(),
+                  h3.view(), B.view(), W, N, b.t_rowptr.data_ptr(), b.t_col.data_ptr(), b.inv_deg.data_ptr(),
+                  part.data_ptr(), bias.data_ptr(), sync.data_ptr(), bits.data_ptr(), N if layout == "chunk" else 0,
+                  dev._stream())
+        outs.append((B.to_float().clone(), bias.clone()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    # (the two kernels size their blocks differently, so the bias partial sums group differently)
+    assert torch.allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-6)
+    gid = np.repeat(np.arange(G), n)
+    dz = du.double().cpu().numpy()[gid] / n[gid][:, None] * (h64 > 0)
+    deg = np.zeros(N)
+    pairs = np.unique(np.stack([dst, src], 1), axis=0)  # distinct (dst, src): the CSR pattern
+    np.add.at(deg, dst, 1)                              # in-degree counts duplicates (gnn.py:136)
+    aggt = np.zeros_like(dz)
+    np.add.at(aggt, pairs[:, 1], dz[pairs[:, 0]] / deg[pairs[:, 0], None])
+    got = outs[1][0].double().cpu().numpy()
+    scale = np.abs(dz).max()
+    assert np.allclose(got[:, :W], dz, atol=1e-2 * scale, rtol=1e-2)
+    assert np.allclose(got[:, W:], aggt, atol=2e-2 * scale, rtol=2e-2)
+    assert np.allclose(outs[1][1].double().cpu().numpy(), dz.sum(0), atol=1e-4 * np.abs(dz).sum(0).max())
+
+
 @pytest.mark.parametrize("M,N", [(76800, 512), (3001, 256), (5, 512), (129, 512)])
 def test_shortk_forward_equals_general_kernel(M, N):
     """The dedicated K = 64 forward (layer 1: 16 epilogue warps, resident W1) gives bit-identical
