@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 7
+#define DIPPM_ABI_VERSION 8
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -411,6 +411,80 @@ int32_t dippm_gather_graphs(const int32_t* sel_idx, int64_t count, const int32_t
 /* y_pred[sel_idx[k]] = y_sub[k], mig[sel_idx[k]] = mig_sub[k] for k < count. */
 int32_t dippm_scatter_rescore(const int32_t* sel_idx, int64_t count, const double* y_sub, const int8_t* mig_sub,
                               double* y_pred, int8_t* mig, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Native training-step executor: one batched bf16 training step (the BatchTrainer step of
+ * trainer.py for a single rank: K1 CSR, forward with the fused readout, the fused head with
+ * Huber loss and head backward, readout backward, the SAGE backward with the weight
+ * gradients on a side stream, Adam + operand repack) issued from C++ in ONE call, so the
+ * host cost of a step is its ~18 kernel launches instead of ~18 Python-level library calls
+ * (gnn.py:383-405 objective, numerics.py:93-114 Adam -- the same kernels, arguments and
+ * order as the Python orchestration in device.py, which the GPU tests compare bit for bit).
+ *
+ * The plan holds every device pointer that stays fixed across steps (model, workspace and
+ * CSR buffers sized for the workspace capacity); dippm_train_plan_init creates the side
+ * stream and the fork/join events, dippm_train_plan_destroy releases them. */
+typedef struct dippm_train_plan {
+  /* model: flat fp64 masters / Adam moments, fp32 gradients and compute copy (device.Layout) */
+  int32_t hp, u_width;
+  double *params, *m, *v;
+  float *grads, *p32;
+  int64_t n_params;
+  int64_t* t_dev;             /* device Adam step counter */
+  const double* norm;         /* double[16] */
+  dippm_act_t Wf[3], Wd[3];   /* forward / dgrad operand copies (Wd[0] unused) */
+  dippm_act_t W1h, W2h;
+  const dippm_pack_seg_t* segs;
+  int32_t n_segs;
+  int64_t off_w[3], off_b[3]; /* sage{l}.w_self / sage{l}.bias offsets in the flat layout */
+  int64_t off_fc1w, off_fc1b, off_fc2w, off_fc2b, off_fc3w, off_fc3b;
+  /* workspace (capacity ws_N nodes, ws_G graphs, ws_E edges) */
+  int64_t ws_N, ws_G, ws_E;
+  dippm_act_t A[3], B[3];
+  uint32_t* relu_bits;        /* [3][hp/32][ws_N] */
+  float *pool_part, *pool_graph;
+  dippm_act_t u, x2, x3, d2, d1;
+  float* dhead_f32;           /* [2][ws_G][hp] */
+  uint32_t* head_bits;        /* [hp/32][ws_G] */
+  float *out, *dout, *du;
+  double *loss, *row_loss;
+  int32_t* head_sync;
+  float* colsum;
+  int32_t* colsum_sync;
+  float* splitk;
+  int32_t* tile_sync;
+  /* K1 CSR outputs and scratch (capacity) */
+  int32_t *rowptr, *col, *deg, *t_rowptr, *t_col, *bad, *node_graph;
+  float* inv_deg;
+  void* csr_ws;
+  size_t csr_ws_bytes;
+  /* hyper-parameters */
+  double dropout_p, keep_scale, delta, grad_den, lr, beta1, beta2, eps;
+  uint64_t seed;
+  /* created by dippm_train_plan_init */
+  void* side_stream;
+  void* ev[4];                /* fork events (layers 3, 2, 1) and the join */
+} dippm_train_plan_t;
+
+typedef struct dippm_train_batch {
+  const float* x;             /* [N, 32] */
+  const int64_t *src, *dst;   /* [E] batch-global node ids */
+  const int32_t* graph_ptr;   /* [G+1] */
+  const int64_t* edge_ptr;    /* [G+1] edges grouped by graph, or NULL (global CSR path) */
+  const double *fs, *y;       /* [G, 5], [G, 3] */
+  int64_t N, E, G;
+  int32_t max_nodes, max_edges; /* largest graph (grouped CSR path) */
+  double* loss_out;           /* double[4] for this step's loss, or NULL: plan->loss */
+  int32_t* bad_out;           /* int32[1] for this step's CSR edge flag, or NULL: plan->bad */
+} dippm_train_batch_t;
+
+int32_t dippm_train_plan_init(dippm_train_plan_t* plan);
+int32_t dippm_train_plan_destroy(dippm_train_plan_t* plan);
+/* One step; the loss (double[4], as dippm_huber) goes to batch->loss_out (else plan->loss),
+ * the CSR edge flag to batch->bad_out (else plan->bad): per-step slots let the caller read
+ * them back on another stream while the next step runs.  Returns DIPPM_ERR_ARG (nothing launched) for a batch the plan cannot run
+ * (larger than its capacity, or a head batch outside the fused head's range). */
+int32_t dippm_train_step(const dippm_train_plan_t* plan, const dippm_train_batch_t* batch, void* stream);
 
 #ifdef __cplusplus
 }

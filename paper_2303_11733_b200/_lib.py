@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 7  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 8  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -79,6 +79,36 @@ class PackSeg(C.Structure):
 
 
 MAX_PACK_SEGS = 12
+
+
+class TrainPlan(C.Structure):
+    """dippm_train_plan_t: the fixed device pointers of the native training step."""
+    _fields_ = [
+        ("hp", C.c_int32), ("u_width", C.c_int32),
+        ("params", P), ("m", P), ("v", P), ("grads", P), ("p32", P), ("n_params", C.c_int64), ("t_dev", P),
+        ("norm", P), ("Wf", Act * 3), ("Wd", Act * 3), ("W1h", Act), ("W2h", Act), ("segs", P), ("n_segs", C.c_int32),
+        ("off_w", C.c_int64 * 3), ("off_b", C.c_int64 * 3),
+        ("off_fc1w", C.c_int64), ("off_fc1b", C.c_int64), ("off_fc2w", C.c_int64), ("off_fc2b", C.c_int64),
+        ("off_fc3w", C.c_int64), ("off_fc3b", C.c_int64),
+        ("ws_N", C.c_int64), ("ws_G", C.c_int64), ("ws_E", C.c_int64),
+        ("A", Act * 3), ("B", Act * 3), ("relu_bits", P), ("pool_part", P), ("pool_graph", P),
+        ("u", Act), ("x2", Act), ("x3", Act), ("d2", Act), ("d1", Act), ("dhead_f32", P), ("head_bits", P),
+        ("out", P), ("dout", P), ("du", P), ("loss", P), ("row_loss", P), ("head_sync", P),
+        ("colsum", P), ("colsum_sync", P), ("splitk", P), ("tile_sync", P),
+        ("rowptr", P), ("col", P), ("deg", P), ("t_rowptr", P), ("t_col", P), ("bad", P), ("node_graph", P),
+        ("inv_deg", P), ("csr_ws", P), ("csr_ws_bytes", C.c_size_t),
+        ("dropout_p", C.c_double), ("keep_scale", C.c_double), ("delta", C.c_double), ("grad_den", C.c_double),
+        ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("seed", C.c_uint64),
+        ("side_stream", P), ("ev", P * 4),
+    ]
+
+
+class TrainBatch(C.Structure):
+    """dippm_train_batch_t: one device-resident batch for dippm_train_step."""
+    _fields_ = [("x", P), ("src", P), ("dst", P), ("graph_ptr", P), ("edge_ptr", P), ("fs", P), ("y", P),
+                ("N", C.c_int64), ("E", C.c_int64), ("G", C.c_int64), ("max_nodes", C.c_int32),
+                ("max_edges", C.c_int32), ("loss_out", P), ("bad_out", P)]
+
 
 # name -> (restype, argtypes); must match include/dippm_b200.h
 SIGNATURES = {
@@ -126,6 +156,9 @@ SIGNATURES = {
     "dippm_mig_band_select": (I32, [P, I64, F64, P, P, P, P, P, P, P]),
     "dippm_gather_graphs": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P]),
     "dippm_scatter_rescore": (I32, [P, I64, P, P, P, P, P]),
+    "dippm_train_plan_init": (I32, [C.POINTER(TrainPlan)]),
+    "dippm_train_plan_destroy": (I32, [C.POINTER(TrainPlan)]),
+    "dippm_train_step": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), P]),
 }
 
 _lib = None

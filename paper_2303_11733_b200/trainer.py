@@ -13,14 +13,98 @@ Adam follows numerics.py:93-114 on fp64 masters.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
 
+from . import _lib
 from . import device as dev
 from .device import Batch, Engine, Workspace, build_batch_csr
 from .errors import NonFinite, ShapeMismatch
+
+# DIPPM_NATIVE_STEP=0 keeps the Python-orchestrated step (A/B switch; same kernels and order)
+NATIVE_STEP = os.environ.get("DIPPM_NATIVE_STEP", "1") != "0"
+
+
+class NativeStep:
+    """dippm_train_step's plan for one (engine, workspace): every fixed device pointer of the
+    bf16 single-rank training step, plus capacity-sized K1 CSR buffers.  One library call per
+    step replaces the ~18 Python-level launches of Engine.forward / loss / backward / adam_step
+    (the same kernels, arguments and order; tests/test_gpu_step_native.py compares them)."""
+
+    def __init__(self, trainer: "BatchTrainer", max_edges: int):
+        eng, ws = trainer.engine, trainer.ws
+        L, hp = eng.L, eng.L.hp
+        lib = _lib.load()
+        self.ws, self.E = ws, max(1, int(max_edges))
+        d = eng.device
+        i32 = dict(dtype=torch.int32, device=d)
+        N, G, E = ws.N, ws.G, self.E
+        self.rowptr, self.t_rowptr = torch.empty(N + 1, **i32), torch.empty(N + 1, **i32)
+        self.col, self.t_col = torch.empty(E, **i32), torch.empty(E, **i32)
+        self.deg, self.node_graph = torch.empty(N, **i32), torch.empty(N, **i32)
+        self.inv_deg = torch.empty(N, dtype=torch.float32, device=d)
+        self.bad = torch.zeros(1, **i32)
+        nbytes = max(lib.dippm_csr_grouped_workspace_bytes(G, E), lib.dippm_csr_workspace_bytes(N, E))
+        self.csr_ws = torch.empty(nbytes, dtype=torch.uint8, device=d)
+        p = self.plan = _lib.TrainPlan()
+        ptr = dev._p
+        p.hp, p.u_width = hp, L.u_width
+        p.params, p.m, p.v, p.grads, p.p32 = ptr(eng.params), ptr(eng.m), ptr(eng.v), ptr(eng.grads), ptr(eng.p32)
+        p.n_params, p.t_dev, p.norm = L.total, ptr(eng.t_dev), ptr(eng.norm)
+        for i in range(3):
+            p.Wf[i] = eng.Wf[i].view()
+            p.Wd[i] = eng.Wd[i].view() if eng.Wd[i] is not None else dev.NULL_ACT
+            p.off_w[i], p.off_b[i] = L.offsets[f"sage{i + 1}.w_self"], L.offsets[f"sage{i + 1}.bias"]
+            p.A[i], p.B[i] = ws.A[i].view(0), ws.B[i].view(0)
+        p.W1h, p.W2h = eng.W1h.view(), eng.W2h.view()
+        p.segs, p.n_segs = C.cast(eng._segs, C.c_void_p), len(eng._segs)
+        p.off_fc1w, p.off_fc1b = L.offsets["fc1.w"], L.offsets["fc1.b"]
+        p.off_fc2w, p.off_fc2b = L.offsets["fc2.w"], L.offsets["fc2.b"]
+        p.off_fc3w, p.off_fc3b = L.offsets["fc3.w"], L.offsets["fc3.b"]
+        p.ws_N, p.ws_G, p.ws_E = N, G, E
+        p.relu_bits, p.pool_part, p.pool_graph = ptr(ws.relu_bits), ptr(ws.pool_part), ptr(ws.pool_graph)
+        p.u, p.x2, p.x3, p.d2, p.d1 = ws.u.view(), ws.x2.view(), ws.x3.view(), ws.d2.view(), ws.d1.view()
+        p.dhead_f32, p.head_bits = ptr(ws.dhead_f32), ptr(ws.head_bits)
+        p.out, p.dout, p.du, p.loss, p.row_loss = ptr(ws.out), ptr(ws.dout), ptr(ws.du), ptr(ws.loss), ptr(ws.row_loss)
+        p.head_sync, p.colsum, p.colsum_sync = ptr(ws.head_sync), ptr(ws.colsum), ptr(ws.colsum_sync)
+        p.splitk, p.tile_sync = ptr(ws.splitk), ptr(ws.tile_sync)
+        p.rowptr, p.col, p.deg, p.t_rowptr, p.t_col = (ptr(self.rowptr), ptr(self.col), ptr(self.deg),
+                                                        ptr(self.t_rowptr), ptr(self.t_col))
+        p.bad, p.node_graph, p.inv_deg = ptr(self.bad), ptr(self.node_graph), ptr(self.inv_deg)
+        p.csr_ws, p.csr_ws_bytes = ptr(self.csr_ws), nbytes
+        p.dropout_p = trainer.dropout_p
+        p.keep_scale = 1.0 / (1.0 - trainer.dropout_p) if trainer.dropout_p > 0 else 1.0
+        p.delta, p.grad_den, p.lr = trainer.delta, 0.0, trainer.lr
+        p.beta1, p.beta2, p.eps = 0.9, 0.999, 1e-8
+        p.seed = (trainer.seed * 131 + trainer.rank) & (2**64 - 1)
+        _lib.check(lib.dippm_train_plan_init(C.byref(p)), "dippm_train_plan_init")
+        self.batch = _lib.TrainBatch()
+        self._fn = lib.dippm_train_step
+
+    def fits(self, b: Batch) -> bool:
+        return b.N <= self.ws.N and b.G <= self.ws.G and b.E <= self.E
+
+    def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None) -> None:
+        t = self.batch
+        t.loss_out = loss_out
+        t.bad_out = None if bad_out is None else bad_out.data_ptr()
+        t.x, t.src, t.dst, t.graph_ptr = b.x.data_ptr(), b.src.data_ptr(), b.dst.data_ptr(), b.graph_ptr.data_ptr()
+        t.edge_ptr = b.edge_ptr.data_ptr() if b.edge_ptr is not None else None
+        t.fs, t.y = b.fs.data_ptr(), b.y.data_ptr()
+        t.N, t.E, t.G, t.max_nodes, t.max_edges = b.N, b.E, b.G, b.max_nodes, b.max_edges
+        _lib.check(self._fn(C.byref(self.plan), C.byref(t), torch.cuda.current_stream().cuda_stream),
+                   "dippm_train_step")
+        b.bad = self.bad if bad_out is None else bad_out
+
+    def __del__(self):
+        try:
+            _lib.load().dippm_train_plan_destroy(C.byref(self.plan))
+        except Exception:
+            pass
 
 
 class BatchTrainer:
@@ -46,10 +130,16 @@ class BatchTrainer:
         self._loss_ring = [torch.zeros(1, dtype=torch.float64).pin_memory() for _ in range(64)]
         self._flag_ring = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(64)]
         self._loss_next = 0
+        self._native = None
+        if torch.cuda.is_available():  # native steps: per-step loss / flag slots and their read-back stream
+            self._d2h_stream = torch.cuda.Stream(self.engine.device)
+            self._loss_dev = torch.zeros(len(self._loss_ring), 4, dtype=torch.float64, device=self.engine.device)
+            self._bad_dev = torch.zeros(len(self._loss_ring), dtype=torch.int32, device=self.engine.device)
 
     def reserve(self, max_nodes: int, max_graphs: int, max_edges: int | None = None) -> None:
         """Preallocate the workspace (and host-batch staging) for batches up to this size."""
         self.ws = Workspace(self.engine, max_nodes, max_graphs, train=True)
+        self._native = None   # the native plan points into the old workspace
         self._graphs.clear()  # captured steps point into the old workspace
         self._keep.clear()
         e = max_edges if max_edges is not None else 2 * max_nodes
@@ -109,8 +199,34 @@ class BatchTrainer:
         self._keep.append(b)  # captured pointers must stay alive
         return hit
 
-    def _step(self, b: Batch, global_graphs: int | None) -> None:
+    def _native_ok(self, b: Batch) -> bool:
+        eng = self.engine
+        return (NATIVE_STEP and self.allreduce is None and eng.arch == "sage" and eng.fused_head_ok(b.G)
+                and eng.overlap_wgrad and not dev.HEAD_POOL and eng.cta_pair == 0 and eng.gemm_hook is None
+                and _lib.call is _LIB_CALL and b.y is not None)
+
+    def _step(self, b: Batch, global_graphs: int | None, slot: int | None = None) -> bool:
+        """One step; True if the native executor ran it (with `slot`: its loss and edge flag
+        went to the device ring entry `slot` instead of the workspace)."""
         eng, ws = self.engine, self.ws
+        if self._native_ok(b):
+            nat = self._native
+            if nat is None or nat.ws is not ws or not nat.fits(b):
+                if nat is not None:
+                    if torch.cuda.is_current_stream_capturing() or self._graphs:
+                        self._keep.append(nat)  # captured steps still point at its CSR buffers
+                    else:
+                        torch.cuda.current_stream().synchronize()  # in-flight steps may still use them
+                self._native = nat = NativeStep(self, max(b.E, 2 * ws.N, nat.E if nat is not None else 0))
+            if slot is None:
+                nat.step(b)
+            else:
+                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1])
+            eng._uploaded = None
+            eng._t_advanced = False  # the step's head advanced t and its Adam ran
+            ws.head_pending = None
+            eng.launches += 18
+            return True
         build_batch_csr(b)
         mode = 2 if self.dropout_p > 0 else 0
         eng.forward(b, ws, mask_mode=mode, dropout_p=self.dropout_p, seed=self.seed * 131 + self.rank,
@@ -135,6 +251,7 @@ class BatchTrainer:
             if self.allreduce is not None:
                 self.allreduce(eng.grads)      # the one exchange: sum of per-rank gradient shares
         eng.adam_step(self.lr)
+        return False
 
     def step_host(self, x, src, dst, graph_ptr, fs, y, edge_ptr=None, global_graphs: int | None = None) -> float:
         """End-to-end step from host (ideally pinned) buffers; returns the batch loss.
@@ -191,15 +308,24 @@ class BatchTrainer:
             global_graphs = global_batch_size(G)  # ragged per-rank batches: the true global mean
         self._ensure(b)
         self.steps += 1
-        self._step(b, global_graphs)  # ragged shapes: host batches run eagerly
-        sl["free"].record(compute)
         j = self._loss_next
         self._loss_next = (j + 1) % len(self._loss_ring)
         host, flag = self._loss_ring[j], self._flag_ring[j]
-        host.copy_(self.ws.loss[:1], non_blocking=True)
-        flag.copy_(b.bad[:1], non_blocking=True)
+        native = self._step(b, global_graphs, slot=j)  # ragged shapes: host batches run eagerly
+        sl["free"].record(compute)
         done = torch.cuda.Event()
-        done.record(compute)
+        if native:  # loss / flag went to ring entry j: read back on the D2H stream, off the compute stream
+            done.record(compute)
+            self._d2h_stream.wait_event(done)
+            with torch.cuda.stream(self._d2h_stream):
+                host.copy_(self._loss_dev[j, :1], non_blocking=True)
+                flag.copy_(self._bad_dev[j:j + 1], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self._d2h_stream)
+        else:
+            host.copy_(self.ws.loss[:1], non_blocking=True)
+            flag.copy_(b.bad[:1], non_blocking=True)
+            done.record(compute)
         return StepHandle(done, host, flag)
 
     def sync_model(self):
@@ -208,6 +334,9 @@ class BatchTrainer:
         for name, arr in self.model.param_items():
             arr[...] = final[name]
         return self.model
+
+
+_LIB_CALL = _lib.call  # the unpatched library call (instrumented runs keep the Python step)
 
 
 class StepHandle:
