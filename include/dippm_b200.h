@@ -464,6 +464,8 @@ typedef struct dippm_train_plan {
   /* created by dippm_train_plan_init */
   void* side_stream;
   void* ev[4];                /* fork events (layers 3, 2, 1) and the join */
+  void* graph_exec;           /* dippm_train_step_graphed's executable graph (NULL until first use) */
+  void* capture_stream;       /* the stream dippm_train_step_graphed records on (never the legacy stream) */
 } dippm_train_plan_t;
 
 typedef struct dippm_train_batch {
@@ -485,6 +487,11 @@ int32_t dippm_train_plan_destroy(dippm_train_plan_t* plan);
  * them back on another stream while the next step runs.  Returns DIPPM_ERR_ARG (nothing launched) for a batch the plan cannot run
  * (larger than its capacity, or a head batch outside the fused head's range). */
 int32_t dippm_train_step(const dippm_train_plan_t* plan, const dippm_train_batch_t* batch, void* stream);
+/* The same step as ONE CUDA-graph launch: the step is captured (recorded, not run), the
+ * plan's executable graph is updated in place with the new kernel arguments (ragged N / E
+ * change grids and arguments, not the topology; a topology change re-instantiates) and
+ * launched on `stream` -- no per-kernel launch gaps on the device. */
+int32_t dippm_train_step_graphed(dippm_train_plan_t* plan, const dippm_train_batch_t* batch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -99,7 +99,7 @@ class TrainPlan(C.Structure):
         ("inv_deg", P), ("csr_ws", P), ("csr_ws_bytes", C.c_size_t),
         ("dropout_p", C.c_double), ("keep_scale", C.c_double), ("delta", C.c_double), ("grad_den", C.c_double),
         ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("seed", C.c_uint64),
-        ("side_stream", P), ("ev", P * 4),
+        ("side_stream", P), ("ev", P * 4), ("graph_exec", P), ("capture_stream", P),
     ]
 
 
@@ -159,6 +159,7 @@ SIGNATURES = {
     "dippm_train_plan_init": (I32, [C.POINTER(TrainPlan)]),
     "dippm_train_plan_destroy": (I32, [C.POINTER(TrainPlan)]),
     "dippm_train_step": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), P]),
+    "dippm_train_step_graphed": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), P]),
 }
 
 _lib = None

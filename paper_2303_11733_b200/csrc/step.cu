@@ -50,6 +50,8 @@ int32_t dippm_train_plan_init(dippm_train_plan_t* plan) {
   cudaStream_t s = nullptr;
   DIPPM_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   plan->side_stream = s;
+  DIPPM_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  plan->capture_stream = s;
   for (int i = 0; i < 4; ++i) {
     cudaEvent_t e = nullptr;
     DIPPM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -60,15 +62,20 @@ int32_t dippm_train_plan_init(dippm_train_plan_t* plan) {
 
 int32_t dippm_train_plan_destroy(dippm_train_plan_t* plan) {
   if (!plan) return DIPPM_OK;
+  if (plan->graph_exec) {
+    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(plan->graph_exec));
+    plan->graph_exec = nullptr;
+  }
   for (int i = 0; i < 4; ++i)
     if (plan->ev[i]) {
       cudaEventDestroy(static_cast<cudaEvent_t>(plan->ev[i]));
       plan->ev[i] = nullptr;
     }
-  if (plan->side_stream) {
-    cudaStreamDestroy(static_cast<cudaStream_t>(plan->side_stream));
-    plan->side_stream = nullptr;
-  }
+  for (void** st : {&plan->side_stream, &plan->capture_stream})
+    if (*st) {
+      cudaStreamDestroy(static_cast<cudaStream_t>(*st));
+      *st = nullptr;
+    }
   return DIPPM_OK;
 }
 
@@ -236,6 +243,46 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   // ---- Adam (t already advanced by the head) + refresh of every operand copy
   STEP_CALL(dippm_adam_pack(P->params, P->m, P->v, P->grads, 1.0, P->n_params, 0, P->t_dev, P->lr, P->beta1, P->beta2,
                             P->eps, 1, P->p32, P->segs, P->n_segs, s));
+  return DIPPM_OK;
+}
+
+int32_t dippm_train_step_graphed(dippm_train_plan_t* P, const dippm_train_batch_t* b, void* stream) {
+  DIPPM_ARG_CHECK(P, "train_step_graphed: NULL plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cap = static_cast<cudaStream_t>(P->capture_stream);
+  DIPPM_ARG_CHECK(cap, "train_step_graphed: plan not initialised");
+  // record on the plan's own stream (capture cannot start on the legacy default stream); the
+  // recorded graph is launched on `stream`, so it runs in that stream's order
+  DIPPM_CUDA_CHECK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  const int32_t rc = dippm_train_step(P, b, cap);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+  if (rc != DIPPM_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DIPPM_CUDA_CHECK(ce);
+  cudaGraphExec_t ex = static_cast<cudaGraphExec_t>(P->graph_exec);
+  bool updated = false;
+  if (ex) {
+    cudaGraphExecUpdateResultInfo info{};
+    updated = cudaGraphExecUpdate(ex, g, &info) == cudaSuccess;
+    if (!updated) {
+      cudaGetLastError();  // clear the update failure: re-instantiate below
+      cudaGraphExecDestroy(ex);
+      P->graph_exec = ex = nullptr;
+    }
+  }
+  if (!updated) {
+    const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
+    if (ie != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return cuda_status(ie, "train_step_graphed: instantiate");
+    }
+    P->graph_exec = ex;
+  }
+  cudaGraphDestroy(g);
+  DIPPM_CUDA_CHECK(cudaGraphLaunch(ex, s));
   return DIPPM_OK;
 }
 

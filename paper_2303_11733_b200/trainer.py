@@ -27,6 +27,9 @@ from .errors import NonFinite, ShapeMismatch
 
 # DIPPM_NATIVE_STEP=0 keeps the Python-orchestrated step (A/B switch; same kernels and order)
 NATIVE_STEP = os.environ.get("DIPPM_NATIVE_STEP", "1") != "0"
+# DIPPM_NATIVE_GRAPHED=0: submit() launches the native step's kernels one by one instead of as
+# one updated CUDA graph
+NATIVE_GRAPHED = os.environ.get("DIPPM_NATIVE_GRAPHED", "1") != "0"
 
 
 class NativeStep:
@@ -83,12 +86,16 @@ class NativeStep:
         p.seed = (trainer.seed * 131 + trainer.rank) & (2**64 - 1)
         _lib.check(lib.dippm_train_plan_init(C.byref(p)), "dippm_train_plan_init")
         self.batch = _lib.TrainBatch()
-        self._fn = lib.dippm_train_step
+        self._fn, self._fn_graphed = lib.dippm_train_step, lib.dippm_train_step_graphed
+        self._warm = False  # the plan's first step runs eagerly (kernel attributes, module loads)
 
     def fits(self, b: Batch) -> bool:
         return b.N <= self.ws.N and b.G <= self.ws.G and b.E <= self.E
 
-    def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None) -> None:
+    def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None,
+             graphed: bool = False) -> None:
+        """graphed: run the step as one CUDA-graph launch (dippm_train_step_graphed; the
+        ragged host-batch path, where per-batch torch graphs cannot be reused)."""
         t = self.batch
         t.loss_out = loss_out
         t.bad_out = None if bad_out is None else bad_out.data_ptr()
@@ -96,8 +103,9 @@ class NativeStep:
         t.edge_ptr = b.edge_ptr.data_ptr() if b.edge_ptr is not None else None
         t.fs, t.y = b.fs.data_ptr(), b.y.data_ptr()
         t.N, t.E, t.G, t.max_nodes, t.max_edges = b.N, b.E, b.G, b.max_nodes, b.max_edges
-        _lib.check(self._fn(C.byref(self.plan), C.byref(t), torch.cuda.current_stream().cuda_stream),
-                   "dippm_train_step")
+        fn = self._fn_graphed if graphed and self._warm and not torch.cuda.is_current_stream_capturing() else self._fn
+        _lib.check(fn(C.byref(self.plan), C.byref(t), torch.cuda.current_stream().cuda_stream), "dippm_train_step")
+        self._warm = True
         b.bad = self.bad if bad_out is None else bad_out
 
     def __del__(self):
@@ -221,7 +229,7 @@ class BatchTrainer:
             if slot is None:
                 nat.step(b)
             else:
-                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1])
+                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1], graphed=NATIVE_GRAPHED)
             eng._uploaded = None
             eng._t_advanced = False  # the step's head advanced t and its Adam ran
             ws.head_pending = None

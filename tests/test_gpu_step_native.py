@@ -34,8 +34,9 @@ def data():
     return ds, model, idx
 
 
-def _run(model, ds, idx, native, monkeypatch, use_graphs=False, shuffle_edges=False, host=False):
+def _run(model, ds, idx, native, monkeypatch, use_graphs=False, shuffle_edges=False, host=False, graphed=True):
     monkeypatch.setattr(trainer_mod, "NATIVE_STEP", native)
+    monkeypatch.setattr(trainer_mod, "NATIVE_GRAPHED", graphed)
     tr = BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3, seed=7, use_graphs=use_graphs)
     losses = []
     for rep in range(2 if use_graphs else 1):  # graphs: the second pass replays the captures
@@ -95,6 +96,18 @@ def test_native_step_global_csr_path_and_submit(data, monkeypatch):
     ds, model, idx = data
     _same(_run(model, ds, idx, True, monkeypatch, shuffle_edges=True),
           _run(model, ds, idx, False, monkeypatch, shuffle_edges=True))
+    py = _run(model, ds, idx, False, monkeypatch, host=True)
+    _same(_run(model, ds, idx, True, monkeypatch, host=True), py)  # one updated CUDA graph per step
+    _same(_run(model, ds, idx, True, monkeypatch, host=True, graphed=False), py)  # launch by launch
+
+
+def test_native_graphed_steps_ragged_batches(data, monkeypatch):
+    """submit() over many ragged batches (N, E, G change every step; the edge order switches
+    between grouped and global K1 paths, which changes the captured topology and forces a
+    re-instantiation): identical to the Python orchestration throughout."""
+    ds, model, _ = data
+    rng = np.random.default_rng(11)
+    idx = [rng.choice(ds.num_graphs, size=int(s), replace=False) for s in (200, 256, 7, 256, 131, 256)]
     _same(_run(model, ds, idx, True, monkeypatch, host=True), _run(model, ds, idx, False, monkeypatch, host=True))
 
 
