@@ -88,8 +88,10 @@ size_t dippm_csr_workspace_bytes(int64_t num_nodes, int64_t num_edges);
 /* Grouped fast path (same outputs, bit for bit): the batch is a concatenation of
  * graphs — graph_ptr [G+1] over nodes, edge_ptr [G+1] over edges (int64), every
  * edge inside its own graph (else *bad_edge = 1).  One CTA per graph builds its
- * CSR in shared memory (2 launches per batch).  Limits: G <= 8192, per-graph
- * padded edge count <= 16384; callers fall back to dippm_build_csr beyond.
+ * CSR in shared memory and finds its offset in the packed arrays by a decoupled look-back
+ * (one memset + one launch per batch; the workspace holds the per-graph status words).
+ * Limits: G <= 8192, per-graph edges and nodes <= 8192; callers fall back to
+ * dippm_build_csr beyond.
  * node_graph (nullable): also writes the node -> graph map (dippm_node_graph) in the same pass. */
 size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t num_edges);
 int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,

@@ -290,7 +290,7 @@ extern "C" int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64
 // duplicate semantics), which the GPU tests check bit for bit.
 namespace dippm {
 
-constexpr int kGThreads = 512;
+constexpr int kGThreads = 256;
 
 __device__ __forceinline__ void bitonic_sort_smem(int* a, int n) {  // n power of 2, ascending
   // Featurizer output is usually already in (dst, src) order (featurize.py:154-162): one
@@ -355,136 +355,245 @@ __device__ int block_scan_smem(int* a, int n, int* s_tmp /* >= 33 ints */) {
   return total;
 }
 
-// Phase 1 (CTA per graph): in-degree with duplicates -> deg / inv_deg; sorted
-// distinct (dst, src) keys -> scratch[e0 .. e0 + U); U -> uniq[g].
-__global__ void __launch_bounds__(kGThreads) k_csr_g1(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
-                                                      const int32_t* __restrict__ graph_ptr,
-                                                      const int64_t* __restrict__ edge_ptr, int epad_max,
-                                                      int32_t* deg, float* inv_deg, int32_t* scratch, int32_t* uniq,
-                                                      int32_t* bad, int32_t* node_graph) {
+// One launch per batch, one CTA per graph.  Graphs are claimed in order from an atomic ticket
+// (a CTA only ever waits on graphs claimed before its own, so there is no co-residency
+// requirement for any batch size).  Per graph, in shared memory: in-degree with duplicates ->
+// deg / inv_deg, (dst, src) keys sorted and de-duplicated; the graph's offset in the packed CSR
+// (sum of the distinct-edge counts of earlier graphs) comes from a decoupled look-back over the
+// per-graph status words (flag | value: "aggregate" = own count, "prefix" = inclusive sum), so
+// the whole batch is O(E) work; then CSR rows and the transposed pattern by a stable counting
+// sort.  The caller zeroes the status block (dippm_build_csr_grouped does, with one memset).
+constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exclusive prefix of graph g's value from statuses [0, g), by the whole block: every thread
+// reads up to 4 statuses of a 4 * blockDim window below g at once (spinning until each is
+// published), the block finds the nearest inclusive prefix in the window and sums the
+// aggregates above it; a window without a prefix is summed whole and the next one follows.
+// One L2 round trip for g < 4 * blockDim -- a warp walking back 32 graphs at a time made the
+// last CTAs of a batch wait on g / 32 serial round trips.
+__device__ int64_t lookback_block(const uint64_t* status, int g, long long* s_red /* [33] */) {
+  int64_t acc = 0;
+  int hi = g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  while (hi > 0) {
+    const int lo = max(0, hi - 4 * (int)blockDim.x);
+    uint64_t st[4];
+    int best = -1;  // highest window index holding an inclusive prefix
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = hi - 1 - (int)threadIdx.x - k * (int)blockDim.x;
+      st[k] = 0;
+      if (j >= lo) {
+        do st[k] = ld_volatile_u64(status + j);
+        while ((st[k] >> 62) == 0);
+        if ((st[k] >> 62) == 2) best = max(best, j);
+      }
+    }
+    // block max of best
+#pragma unroll
+    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) s_red[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+      long long b = lane < nw ? s_red[lane] : -1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+      if (lane == 0) s_red[32] = b;
+    }
+    __syncthreads();
+    const int stop = (int)s_red[32];  // -1: no prefix in the window
+    __syncthreads();
+    __threadfence();  // acquire: the published values are read after their flags
+    long long v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = hi - 1 - (int)threadIdx.x - k * (int)blockDim.x;
+      if (j >= lo && j >= stop) v += (long long)(st[k] & kStMask);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    long long tot = 0;
+    for (int w = 0; w < nw; ++w) tot += s_red[w];
+    __syncthreads();
+    acc += tot;
+    if (stop >= 0) break;
+    hi = lo;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kGThreads) k_csr_graph(const int64_t* __restrict__ src,
+                                                         const int64_t* __restrict__ dst,
+                                                         const int32_t* __restrict__ graph_ptr,
+                                                         const int64_t* __restrict__ edge_ptr, int epad_max, int64_t N,
+                                                         int G, int32_t* deg, float* inv_deg, int32_t* rowptr,
+                                                         int32_t* col, int32_t* t_rowptr, int32_t* t_col,
+                                                         int32_t* bad_out, int32_t* node_graph, uint64_t* status,
+                                                         int* ctl /* [0] ticket, [1] done, [2] bad */) {
   extern __shared__ int sm[];
   __shared__ int s_tmp[33];
+  __shared__ long long s_red[33];
+  __shared__ int s_g, s_bad;
   pdl_begin();
-  const int g = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_g = atomicAdd(&ctl[0], 1);
+    s_bad = 0;
+  }
+  __syncthreads();
+  const int g = s_g;
   const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
   const int64_t e0 = edge_ptr[g];
   const int eg = (int)(edge_ptr[g + 1] - e0);
   int epad = 1;
   while (epad < eg) epad <<= 1;
-  int* keys = sm;             // [epad]
-  int* cnt = sm + epad_max;   // [ng]
-  for (int v = threadIdx.x; v < ng; v += blockDim.x) cnt[v] = 0;
+  const int nmax = max(epad_max, ng + 1);   // launcher: epad_max >= max_nodes + 1 as well
+  int* keys = sm;                           // [epad_max]  (dst, src) keys, then the distinct ones
+  int* ra = sm + epad_max;                  // [nmax]  in-degree / flags / row counts
+  int* rb = ra + nmax;                      // [nmax]  transposed counts -> running ends
+  int* tmp = rb + nmax;                     // [epad_max]  transposed entries (dst per src row)
+  for (int v = threadIdx.x; v < ng; v += blockDim.x) ra[v] = 0;
   __syncthreads();
+  int mybad = 0;
   for (int i = threadIdx.x; i < epad; i += blockDim.x) {
     int key = INT_MAX;
     if (i < eg) {
       const int64_t s = src[e0 + i] - n0, d = dst[e0 + i] - n0;
       if (s < 0 || s >= ng || d < 0 || d >= ng) {
-        atomicExch(bad, 1);
+        mybad = 1;
       } else {
         key = ((int)d << 16) | (int)s;  // (dst, src), ng < 2^15 (checked by the launcher)
-        atomicAdd(&cnt[d], 1);
+        atomicAdd(&ra[d], 1);
       }
     }
     keys[i] = key;
   }
+  if (mybad) s_bad = 1;
   __syncthreads();
   for (int v = threadIdx.x; v < ng; v += blockDim.x) {
-    const int d = cnt[v];
+    const int d = ra[v];
     if (node_graph) node_graph[n0 + v] = g;
     deg[n0 + v] = d;
     inv_deg[n0 + v] = d > 0 ? 1.0f / (float)d : 0.0f;  // gnn.py:136 (zero row when isolated)
   }
   bitonic_sort_smem(keys, epad);
-  // distinct keys (sorted -> first of each run), compacted in order
-  int* flag = cnt;  // reuse: need epad ints; cnt region sized max(ng, epad_max)
-  for (int i = threadIdx.x; i < epad; i += blockDim.x)
-    flag[i] = (keys[i] != INT_MAX && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
-  __syncthreads();
-  int* pos = flag;
-  // keep a copy of the flags in registers before the in-place scan
+  // distinct keys (sorted -> first of each run) compacted in order: this thread's keys and
+  // flags are held in registers across the scan (per <= 32 by construction of epad_max)
   const int per = (epad + blockDim.x - 1) / blockDim.x;
-  int myflags = 0;  // bitmask of this thread's flags (per <= 32 by construction of epad_max)
-  for (int k = 0; k < per; ++k) {
-    const int i = threadIdx.x * per + k;
-    if (i < epad && flag[i]) myflags |= 1 << k;
-  }
-  __syncthreads();
-  const int U = block_scan_smem(pos, epad, s_tmp);
-  for (int k = 0; k < per; ++k) {
-    const int i = threadIdx.x * per + k;
-    if (i < epad && ((myflags >> k) & 1)) scratch[e0 + pos[i]] = keys[i];
-  }
-  if (threadIdx.x == 0) uniq[g] = U;
-}
-
-// Phase 3 (CTA per graph): CSR rows from the sorted distinct keys, then the
-// transposed pattern from a (src, dst) re-sort.
-__global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict__ graph_ptr,
-                                                      const int64_t* __restrict__ edge_ptr,
-                                                      const int32_t* __restrict__ scratch,
-                                                      const int32_t* __restrict__ uniq,
-                                                      int epad_max, int64_t N, int G, int32_t* rowptr, int32_t* col,
-                                                      int32_t* t_rowptr, int32_t* t_col) {
-  extern __shared__ int sm[];
-  __shared__ int s_tmp[33];
-  pdl_begin();
-  const int g = blockIdx.x;
-  const int n0 = graph_ptr[g], ng = graph_ptr[g + 1] - n0;
-  const int64_t e0 = edge_ptr[g];
-  const int U = uniq[g];
-  // this graph's offset in the packed CSR = sum of the earlier graphs' unique counts (each
-  // block sums its prefix itself: no separate scan launch; integer sums, order-free)
-  int part = 0;
-  for (int i = threadIdx.x; i < g; i += blockDim.x) part += uniq[i];
+  uint32_t myflags = 0;
+  int mykeys[32];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  if ((threadIdx.x & 31) == 0) s_tmp[threadIdx.x >> 5] = part;
+  for (int k = 0; k < 32; ++k) {
+    if (k < per) {
+      const int i = threadIdx.x * per + k;
+      const int key = i < epad ? keys[i] : INT_MAX;
+      mykeys[k] = key;
+      const bool f = key != INT_MAX && (i == 0 || key != keys[i - 1]);
+      if (f) myflags |= 1u << k;
+      if (i < epad) ra[i] = f ? 1 : 0;
+    }
+  }
   __syncthreads();
-  int off = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) off += s_tmp[w];
+  const int U = block_scan_smem(ra, epad, s_tmp);
+  // this graph's distinct-edge count is published now; its offset is looked up at the end,
+  // after all the offset-free work, by when the earlier graphs have published theirs
+  if (threadIdx.x == 0) st_release_u64(status + g, kStAgg | (uint64_t)U);
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < per && ((myflags >> k) & 1)) keys[ra[threadIdx.x * per + k]] = mykeys[k];
   __syncthreads();
-  const int* keys = scratch + e0;  // sorted distinct (dst, src) keys
-  int* cnt = sm;                   // [ng + 1]
-  for (int v = threadIdx.x; v <= ng; v += blockDim.x) cnt[v] = 0;
+  // row counts (dst) and transposed counts (src) of the distinct pattern, one pass
+  for (int v = threadIdx.x; v <= ng; v += blockDim.x) ra[v] = rb[v] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < U; i += blockDim.x) {
     const int k = keys[i];
-    col[off + i] = n0 + (k & 0xFFFF);  // src, ascending within the dst row
-    atomicAdd(&cnt[k >> 16], 1);
+    atomicAdd(&ra[k >> 16], 1);
+    atomicAdd(&rb[k & 0xFFFF], 1);
   }
   __syncthreads();
-  block_scan_smem(cnt, ng, s_tmp);
-  for (int v = threadIdx.x; v < ng; v += blockDim.x) rowptr[n0 + v] = off + cnt[v];
-  if (g == G - 1 && threadIdx.x == 0) rowptr[N] = off + U;
+  block_scan_smem(ra, ng, s_tmp);  // row starts (local)
+  block_scan_smem(rb, ng, s_tmp);  // transposed row starts (local)
+  // transposed pattern: every entry lands in its src row at an atomic cursor (rb advances to
+  // the row's end), then each row is sorted by dst -- the order a (src, dst) sort gives,
+  // independent of the atomics' order.  Rows are short (out-degrees); a batch whose longest
+  // row exceeds 64 sorts them with the warp walk instead (stable counting placement).
+  int longest = 0;
+  for (int i = threadIdx.x; i < U; i += blockDim.x) {
+    const int k = keys[i];
+    tmp[atomicAdd(&rb[k & 0xFFFF], 1)] = k >> 16;
+  }
   __syncthreads();
-  // transposed pattern by a stable counting sort on src (no re-sort): counts, scan, then one
-  // warp walks the keys in (dst, src) order and places each at its src row's running offset,
-  // lanes with the same src ranked by lane order (__match_any_sync), so every src row lists
-  // its dsts in ascending order -- the order a (src, dst) sort gives
-  for (int v = threadIdx.x; v <= ng; v += blockDim.x) cnt[v] = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < U; i += blockDim.x) atomicAdd(&cnt[keys[i] & 0xFFFF], 1);
-  __syncthreads();
-  block_scan_smem(cnt, ng, s_tmp);
-  for (int v = threadIdx.x; v < ng; v += blockDim.x) t_rowptr[n0 + v] = off + cnt[v];
-  if (g == G - 1 && threadIdx.x == 0) t_rowptr[N] = off + U;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int base = 0; base < U; base += 32) {
-      const int i = base + lane;
-      const int k = i < U ? keys[i] : 0;
-      const int sv = i < U ? (k & 0xFFFF) : -1 - lane;  // inactive lanes match nobody
-      const unsigned grp = __match_any_sync(0xffffffffu, sv);
-      const int rank = __popc(grp & ((1u << lane) - 1u));
-      const int start = i < U ? cnt[sv] : 0;
-      __syncwarp();
-      if (i < U) {
-        t_col[off + start + rank] = n0 + (k >> 16);  // dst, ascending within the src row
-        if (lane == 31 - __clz(grp)) cnt[sv] = start + __popc(grp);  // the group's last lane advances it
+  for (int v = threadIdx.x; v < ng; v += blockDim.x) {
+    const int b = v ? rb[v - 1] : 0, e = rb[v];
+    longest = max(longest, e - b);
+    if (e - b <= 64) {
+      for (int i = b + 1; i < e; ++i) {  // insertion sort by dst
+        const int x = tmp[i];
+        int j = i - 1;
+        while (j >= b && tmp[j] > x) {
+          tmp[j + 1] = tmp[j];
+          --j;
+        }
+        tmp[j + 1] = x;
       }
-      __syncwarp();
+    }
+  }
+  if (__syncthreads_or(longest > 64)) {
+    // hub rows: re-place every entry stably (one warp walks the keys in (dst, src) order,
+    // lanes with the same src ranked by lane order), starting from the row starts
+    for (int v = threadIdx.x; v <= ng; v += blockDim.x) rb[v] = 0;  // row starts again
+    __syncthreads();
+    for (int i = threadIdx.x; i < U; i += blockDim.x) atomicAdd(&rb[keys[i] & 0xFFFF], 1);
+    __syncthreads();
+    block_scan_smem(rb, ng, s_tmp);
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      for (int base = 0; base < U; base += 32) {
+        const int i = base + lane;
+        const int k = i < U ? keys[i] : 0;
+        const int sv = i < U ? (k & 0xFFFF) : -1 - lane;
+        const unsigned grp = __match_any_sync(0xffffffffu, sv);
+        const int rank = __popc(grp & ((1u << lane) - 1u));
+        const int start = i < U ? rb[sv] : 0;
+        __syncwarp();
+        if (i < U) {
+          tmp[start + rank] = k >> 16;
+          if (lane == 31 - __clz(grp)) rb[sv] = start + __popc(grp);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  // offset of this graph in the packed CSR (decoupled look-back), then every output
+  const int off = (int)lookback_block(status, g, s_red);
+  if (threadIdx.x == 0) st_release_u64(status + g, kStPre | (uint64_t)(off + U));
+  for (int v = threadIdx.x; v < ng; v += blockDim.x) {
+    rowptr[n0 + v] = off + ra[v];
+    t_rowptr[n0 + v] = off + (v ? rb[v - 1] : 0);
+  }
+  for (int i = threadIdx.x; i < U; i += blockDim.x) {
+    col[off + i] = n0 + (keys[i] & 0xFFFF);  // src, ascending within the dst row
+    t_col[off + i] = n0 + tmp[i];            // dst, ascending within the src row
+  }
+  if (g == G - 1 && threadIdx.x == 0) rowptr[N] = t_rowptr[N] = off + U;
+  // batch-level edge flag: OR of every graph's, written by the last CTA to finish
+  if (threadIdx.x == 0) {
+    if (s_bad) atomicOr(&ctl[2], 1);
+    __threadfence();
+    if (atomicAdd(&ctl[1], 1) == G - 1) {
+      __threadfence();
+      *bad_out = atomicOr(&ctl[2], 0) ? 1 : 0;
     }
   }
 }
@@ -492,7 +601,8 @@ __global__ void __launch_bounds__(kGThreads) k_csr_g3(const int32_t* __restrict_
 }  // namespace dippm
 
 extern "C" size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t num_edges) {
-  return (size_t)(num_edges > 0 ? num_edges : 1) * 4 + (size_t)(2 * num_graphs + 2) * 4 + 512;
+  (void)num_edges;
+  return (size_t)(num_graphs > 0 ? num_graphs : 1) * 8 + 64;  // status words + ticket / done / flag
 }
 
 extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
@@ -508,24 +618,21 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
   int epad = 1;
   while (epad < max_edges_per_graph) epad <<= 1;
   const int64_t nmax = std::max<int64_t>(max_nodes_per_graph + 1, epad);
-  const size_t smem = (size_t)(epad + nmax) * sizeof(int);
+  const size_t smem = (size_t)(2 * epad + 2 * nmax) * sizeof(int);  // keys, two count rows, transposed
   DIPPM_ARG_CHECK(smem <= 200 * 1024 && epad / kGThreads <= 32 && max_nodes_per_graph < 32768,
                   "build_csr_grouped: graph too large for the per-graph path (%d nodes, %d edges)",
                   max_nodes_per_graph, max_edges_per_graph);
   cudaStream_t s = (cudaStream_t)stream;
-  int32_t* scratch = reinterpret_cast<int32_t*>(workspace);
-  int32_t* uniq = scratch + (E > 0 ? E : 1);
+  uint64_t* status = reinterpret_cast<uint64_t*>(workspace);
+  int* ctl = reinterpret_cast<int*>(status + G);
   static int smem_set = 0;
   if ((int)smem > smem_set) {
-    DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_csr_g1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_csr_g3, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_csr_graph, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     smem_set = 200 * 1024;
   }
-  DIPPM_CUDA_CHECK(cudaMemsetAsync(bad_edge, 0, sizeof(int), s));
-  DIPPM_LAUNCH_PDL(k_csr_g1, dim3((unsigned)G), dim3(kGThreads), smem, s, src, dst, graph_ptr, edge_ptr, epad, deg,
-                   inv_deg, scratch, uniq, bad_edge, node_graph);
-  DIPPM_LAUNCH_PDL(k_csr_g3, dim3((unsigned)G), dim3(kGThreads), smem, s, graph_ptr, edge_ptr, scratch, uniq, epad, N,
-                   (int)G, rowptr, col, t_rowptr, t_col);
-  DIPPM_LAUNCH_CHECK_N(2, "build_csr_grouped");
+  DIPPM_CUDA_CHECK(cudaMemsetAsync(workspace, 0, (size_t)G * 8 + 16, s));
+  DIPPM_LAUNCH_PDL(k_csr_graph, dim3((unsigned)G), dim3(kGThreads), smem, s, src, dst, graph_ptr, edge_ptr, epad, N,
+                   (int)G, deg, inv_deg, rowptr, col, t_rowptr, t_col, bad_edge, node_graph, status, ctl);
+  DIPPM_LAUNCH_CHECK("build_csr_grouped");
   return DIPPM_OK;
 }

@@ -33,7 +33,7 @@ dippm_gemm_args_t gemm_defaults() {
 }
 
 constexpr int64_t kGroupedMaxGraphs = 8192;  // device.GROUPED_MAX_GRAPHS / GROUPED_MAX_EDGES
-constexpr int64_t kGroupedMaxEdges = 16384;
+constexpr int64_t kGroupedMaxEdges = 8192;
 
 #define STEP_CALL(expr)                \
   do {                                 \

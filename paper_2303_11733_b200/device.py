@@ -320,7 +320,7 @@ def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=Tr
     return b
 
 
-GROUPED_MAX_EDGES = 16384  # per-graph limit of the shared-memory CSR kernel (padded to a power of 2)
+GROUPED_MAX_EDGES = 8192  # per-graph limit (edges and nodes) of the shared-memory CSR kernel
 GROUPED_MAX_GRAPHS = 8192
 
 
