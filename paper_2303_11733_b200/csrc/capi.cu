@@ -153,11 +153,12 @@ __global__ void __launch_bounds__(256) k_adam_pack4(double* __restrict__ p, doub
     }
   }
   if (t_dev && do_adam) {
+    // the two fp64 pows (long dependent chains) run in two warps at once; the grid is one wave
+    // (the launcher), so every block pays this latency once, concurrently
     __shared__ double s_bc[2];
-    if (threadIdx.x == 0) {
+    if ((threadIdx.x & 31) == 0 && threadIdx.x < 64) {
       const double t = (double)t_dev[0];
-      s_bc[0] = 1.0 - pow(b1, t);
-      s_bc[1] = 1.0 - pow(b2, t);
+      s_bc[threadIdx.x >> 5] = 1.0 - pow(threadIdx.x ? b2 : b1, t);
     }
     __syncthreads();
     bc1 = s_bc[0];
@@ -346,7 +347,7 @@ int32_t dippm_adam_pack(double* params, double* m, double* v, const float* grads
   vec &= ((uintptr_t)params | (uintptr_t)m | (uintptr_t)v | (uintptr_t)grads | (uintptr_t)p32) % 32 == 0;
   const int64_t n4 = vec ? (n & ~int64_t(3)) : 0;
   if (n4) {
-    const int b4 = (int)std::min<int64_t>(ceil_div_i(n4 / 4, 256), 8 * num_sms());
+    const int b4 = (int)std::min<int64_t>(ceil_div_i(n4 / 4, 256), 3 * num_sms());  // one wave (76 regs: 3 / SM)
     const int dt = nsegs ? (int)segs[0].dst.dtype : DIPPM_DT_F32;
     if (dt == DIPPM_DT_BF16)
       DIPPM_LAUNCH_PDL(k_adam_pack4<DIPPM_DT_BF16>, dim3(b4), dim3(256), 0, (cudaStream_t)stream, params, m, v, grads, grad_scale, n, lr, beta1,
