@@ -69,7 +69,7 @@ struct Params {
   unsigned long long* ts;  // diagnostics only (DIPPM_GEMM_TS=<device address>): per-CTA globaltimer stamps
   int dbg;  // diagnostics only (DIPPM_GEMM_DEBUG): bit 0 skip epilogue stores, bit 1 skip the
             // bit masks, bit 2 skip the whole chunk loop (release the accumulator at once), bit 3
-            // (1-CTA) / bit 4 (pair) use the per-float FWD epilogue instead of the packed one
+            // use the per-float FWD epilogue instead of the packed one (1-CTA tiles)
 };
 
 // ------------------------------------------------------------------ PTX shims
@@ -842,8 +842,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // shuffles, so no load latency sits inside the chunk loop.  Pair tiles (long K, epilogue
       // hidden under the MMAs) load the bias per chunk: fewer instructions.
       // packed FWD epilogue: bf16 output with bias and ReLU and no fused readout (layers 1-2)
-      const bool fast_fwd = kFmt == 1 && kEpi == EPI_FWD && p.out.base && p.out.dtype == DIPPM_DT_BF16 && p.relu &&
-                            p.bias && !p.pool_part && (C::kBiasCols == 0 || p.N <= C::kBiasCols) && !(p.dbg & (kCta == 2 ? 16 : 8));
+      // (1-CTA tiles only: compiled into the pair kernel, the packed path made its register
+      // allocation spill, which cost the layer-3 readout epilogue more than layer 2 gained)
+      const bool fast_fwd = kFmt == 1 && kEpi == EPI_FWD && kCta == 1 && p.out.base && p.out.dtype == DIPPM_DT_BF16 &&
+                            p.relu && p.bias && !p.pool_part && (C::kBiasCols == 0 || p.N <= C::kBiasCols) &&
+                            !(p.dbg & 8);
       float bl[kBN / 64];
       if constexpr ((kEpi == EPI_FWD || kEpi == EPI_FWD_DROP) && kCta == 1) {
         if (!fast_fwd) {
