@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 8
+#define DIPPM_ABI_VERSION 9
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -294,7 +294,8 @@ int32_t dippm_huber(const float* out_norm, const double* y_raw, int64_t num_grap
  *             [u_width,hp]) and, if du != NULL, du = d1 W1[:hp]^T (fp32 [G, hp]).
  * Dropout: mode 0 none, 1 multiply mask1/mask2 ([G, hp] fp32), 2 the counter hash of
  * dippm_gemm (seed1/seed2, seed_dev mixed in identically), so the draws match that path.
- * sync: int32[2] zeroed once by the caller; left ready for the next launch.
+ * sync: int32[dippm_head_fused_sync_ints()] zeroed once by the caller; left ready for the next
+ * launch.
  * Every reduction has a fixed order (deterministic). */
 typedef struct dippm_head_args {
   int64_t G;
@@ -340,6 +341,7 @@ typedef struct dippm_head_args {
   int64_t* step_counter;
 } dippm_head_args_t;
 int32_t dippm_head_fused_max_graphs(void);
+int32_t dippm_head_fused_sync_ints(void);
 int32_t dippm_head_fused(const dippm_head_args_t* args, void* stream);
 /* Diagnostics (synchronous): SM clock cycles, relative to kernel start, of CTA 0 of the last
  * launch: per phase (A, B: slots 1-4 / 5-8; C ends at 9, barrier 10; D 11-14; E 15-18) its

@@ -237,6 +237,23 @@ __device__ __forceinline__ void act_store8_t(const ActView& a, int64_t r, int64_
   }
 }
 
+// Sum of one double per thread over a 256-thread block in a fixed order (xor-shuffle tree in
+// each warp, then the 8 warp sums in warp order by thread 0): deterministic, and ~10 dependent
+// steps instead of a 256-long serial loop.  Result valid in thread 0.  s: >= 8 doubles of
+// shared memory; every thread of the block must call it.
+__device__ __forceinline__ double block_sum256(double v, double* s) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s[w];
+  __syncthreads();
+  return t;
+}
+
 inline ActView make_view(const dippm_act_t& a) {
   ActView v;
   v.base = a.data;

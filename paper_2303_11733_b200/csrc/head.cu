@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(256) k_colsum_act(ActView a, int64_t rows, int
 __global__ void k_huber(const float* __restrict__ out, const double* __restrict__ y_raw, int64_t G,
                         const double* __restrict__ norm, double delta, double grad_den, float* __restrict__ dout,
                         double* __restrict__ loss_out) {
-  __shared__ double s_loss[256], s_ape[3][256];
   double l = 0.0, ape[3] = {0, 0, 0};
   for (int64_t g = threadIdx.x; g < G; g += blockDim.x) {
     double le = 0.0;
@@ -305,15 +304,12 @@ __global__ void k_huber(const float* __restrict__ out, const double* __restrict_
     }
     l += le / 3.0;
   }
-  s_loss[threadIdx.x] = l;
-  for (int k = 0; k < 3; ++k) s_ape[k][threadIdx.x] = ape[k];
-  __syncthreads();
+  // fixed-order block sums (the fused head's loss unit runs the same reduction)
+  __shared__ double s_w[8];
+  const double tl = block_sum256(l, s_w);
+  double ta[3];
+  for (int k = 0; k < 3; ++k) ta[k] = block_sum256(ape[k], s_w);
   if (threadIdx.x == 0) {
-    double tl = 0, ta[3] = {0, 0, 0};
-    for (int i = 0; i < blockDim.x; ++i) {
-      tl += s_loss[i];
-      for (int k = 0; k < 3; ++k) ta[k] += s_ape[k][i];
-    }
     loss_out[0] = tl / (double)G;
     for (int k = 0; k < 3; ++k) loss_out[1 + k] = ta[k];
   }

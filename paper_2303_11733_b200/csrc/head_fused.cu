@@ -360,13 +360,30 @@ __device__ void colsum_unit(const Args& a, uint8_t* smem, int what, int c0) {  /
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, j = c0 + tx;
   const float* src = what == 0 ? a.d2f : a.d1f;
   float cb = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f;
-  for (int g = ty; g < a.G; g += 8) {
-    cb += src[(int64_t)g * a.hp + j];
-    if (what == 0) {
-      const float x = __bfloat162float(a.x3[(int64_t)g * a.hp + j]);
-      w0 = fmaf(x, a.dout[g * 3 + 0], w0);
-      w1 = fmaf(x, a.dout[g * 3 + 1], w1);
-      w2 = fmaf(x, a.dout[g * 3 + 2], w2);
+  // rows g = ty, ty + 8, ... in order, loaded 8 rows at a time (written this launch by other
+  // CTAs: L2 loads; a row-at-a-time loop was a chain of G / 8 dependent L2 round trips)
+  for (int g0 = ty; g0 < a.G; g0 += 64) {
+    float sv[8], xv[8], dv[8][3];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int g = g0 + 8 * i;
+      const bool ok = g < a.G;
+      sv[i] = ok ? __ldcg(src + (int64_t)g * a.hp + j) : 0.f;
+      if (what == 0) {
+        xv[i] = ok ? __bfloat162float(__ldcg(a.x3 + (int64_t)g * a.hp + j)) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dv[i][k] = ok ? __ldcg(a.dout + g * 3 + k) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (g0 + 8 * i >= a.G) break;
+      cb += sv[i];
+      if (what == 0) {
+        w0 = fmaf(xv[i], dv[i][0], w0);
+        w1 = fmaf(xv[i], dv[i][1], w1);
+        w2 = fmaf(xv[i], dv[i][2], w2);
+      }
     }
   }
   s[ty][tx][0] = cb;
@@ -390,27 +407,34 @@ __device__ void colsum_unit(const Args& a, uint8_t* smem, int what, int c0) {  /
   __syncthreads();
 }
 
-// ---- batch loss (k_huber's reduction order) and db3 ----
+// ---- batch loss (k_huber's reduction order: per-thread strided sums, then block_sum256) and db3 ----
 __device__ void loss_unit(const Args& a, uint8_t* smem) {
-  double* sl = reinterpret_cast<double*>(smem);  // [4][256]
-  float* sb = reinterpret_cast<float*>(sl + 4 * kThreads);  // [3][256]
+  double* sw = reinterpret_cast<double*>(smem);  // [8]
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   float b[3] = {0.f, 0.f, 0.f};
   for (int g = threadIdx.x; g < a.G; g += kThreads) {
-    for (int k = 0; k < 4; ++k) acc[k] += a.row_loss[(int64_t)g * 4 + k];
+    for (int k = 0; k < 4; ++k) acc[k] += __ldcg(a.row_loss + (int64_t)g * 4 + k);
     if (a.train)
-      for (int k = 0; k < 3; ++k) b[k] += a.dout[g * 3 + k];
+      for (int k = 0; k < 3; ++k) b[k] += __ldcg(a.dout + g * 3 + k);
   }
-  for (int k = 0; k < 4; ++k) sl[k * kThreads + threadIdx.x] = acc[k];
-  for (int k = 0; k < 3; ++k) sb[k * kThreads + threadIdx.x] = b[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t[4] = {0.0, 0.0, 0.0, 0.0};
-    float tb[3] = {0.f, 0.f, 0.f};
-    for (int i = 0; i < kThreads; ++i) {
-      for (int k = 0; k < 4; ++k) t[k] += sl[k * kThreads + i];
-      for (int k = 0; k < 3; ++k) tb[k] += sb[k * kThreads + i];
+  double t[4];
+  for (int k = 0; k < 4; ++k) t[k] = block_sum256(acc[k], sw);
+  float tb[3] = {0.f, 0.f, 0.f};
+  if (a.train) {
+    // db3 in fp32, fixed order: xor tree per warp, warps in order
+    float* sf = reinterpret_cast<float*>(sw + 8);  // [8][3]
+    for (int k = 0; k < 3; ++k) {
+      float v = b[k];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) sf[(threadIdx.x >> 5) * 3 + k] = v;
     }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < 8; ++w)
+        for (int k = 0; k < 3; ++k) tb[k] += sf[w * 3 + k];
+  }
+  if (threadIdx.x == 0) {
     a.loss_out[0] = t[0] / (double)a.G;
     for (int k = 0; k < 3; ++k) a.loss_out[1 + k] = t[1 + k];
     if (a.train)
@@ -504,7 +528,7 @@ __device__ void head_rows(const Args& a) {
     for (int q = 0; q < 2; ++q) {
       const int c = lane + 32 * q;
       if (c < nch) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xr + c * 8);
+        const uint4 xv = __ldcg(reinterpret_cast<const uint4*>(xr + c * 8));  // written this launch
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xv);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -544,38 +568,42 @@ __device__ void head_rows(const Args& a) {
     }
     const float o3[3] = {s0 + a.b3[0], s1 + a.b3[1], s2 + a.b3[2]};
     float e[3] = {0.f, 0.f, 0.f};
-    if (lane == 0) {
-      for (int k = 0; k < 3; ++k) a.out[g * 3 + k] = o3[k];
-      if (a.y_pred) {
-        for (int k = 0; k < 3; ++k) a.y_pred[g * 3 + k] = (double)o3[k] * a.norm[3 + k] + a.norm[k];
-        const double mem = a.y_pred[g * 3 + 1];
-        if (!isfinite(mem)) {
-          atomicExch(a.nonfinite, 1);
-          a.mig[g] = -1;
-        } else {
-          a.mig[g] = (int8_t)mig_rule(mem);
-        }
-      }
+    // lanes 0..2 each take one output column (the fp64 divisions of the three run in parallel)
+    const float ok = lane == 0 ? o3[0] : (lane == 1 ? o3[1] : o3[2]);
+    double le_k = 0.0;
+    if (lane < 3) {
+      const int k = lane;
+      a.out[g * 3 + k] = ok;
+      if (a.y_pred) a.y_pred[g * 3 + k] = (double)ok * a.norm[3 + k] + a.norm[k];
       if (a.y_raw) {  // k_huber's per-graph terms (head.cu)
-        double le = 0.0;
-        for (int k = 0; k < 3; ++k) {
-          const double pred = (double)o3[k], y = a.y_raw[g * 3 + k];
-          const double t = (y - a.norm[k]) / a.norm[3 + k];
-          const double r = pred - t, ab = fabs(r);
-          const bool quad = ab <= a.delta;
-          le += quad ? 0.5 * r * r : a.delta * (ab - 0.5 * a.delta);
-          const double gr = quad ? r : a.delta * (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0));
-          e[k] = (float)(gr / 3.0 / a.grad_den);
-          if (a.dout) a.dout[g * 3 + k] = e[k];
-          const double den = pred * a.norm[3 + k] + a.norm[k];
-          a.row_loss[(int64_t)g * 4 + 1 + k] = fabs(den - y) / fabs(y);
-        }
-        a.row_loss[(int64_t)g * 4] = le / 3.0;
+        const double pred = (double)ok, y = a.y_raw[g * 3 + k];
+        const double t = (y - a.norm[k]) / a.norm[3 + k];
+        const double r = pred - t, ab = fabs(r);
+        const bool quad = ab <= a.delta;
+        le_k = quad ? 0.5 * r * r : a.delta * (ab - 0.5 * a.delta);
+        const double gr = quad ? r : a.delta * (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0));
+        e[k] = (float)(gr / 3.0 / a.grad_den);
+        if (a.dout) a.dout[g * 3 + k] = e[k];
+        const double den = pred * a.norm[3 + k] + a.norm[k];
+        a.row_loss[(int64_t)g * 4 + 1 + k] = fabs(den - y) / fabs(y);
       }
+    }
+    if (a.y_pred && lane == 1) {  // the memory column picks the MIG profile
+      const double mem = (double)ok * a.norm[4] + a.norm[1];
+      if (!isfinite(mem)) {
+        atomicExch(a.nonfinite, 1);
+        a.mig[g] = -1;
+      } else {
+        a.mig[g] = (int8_t)mig_rule(mem);
+      }
+    }
+    if (a.y_raw) {  // le = ((l0 + l1) + l2) / 3, k_huber's order
+      const double l1 = __shfl_sync(0xffffffffu, le_k, 1), l2 = __shfl_sync(0xffffffffu, le_k, 2);
+      if (lane == 0) a.row_loss[(int64_t)g * 4] = ((0.0 + le_k) + l1 + l2) / 3.0;
     }
     if (!a.train) continue;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) e[k] = __shfl_sync(0xffffffffu, e[k], 0);
+    for (int k = 0; k < 3; ++k) e[k] = __shfl_sync(0xffffffffu, e[k], k);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {  // d2 = (dout W3^T) * [x3 > 0] * keep (k_fc3_backward, head.cu)
       const int c = lane + 32 * q;
@@ -692,6 +720,7 @@ using namespace dippm;
 extern "C" {
 
 int32_t dippm_head_fused_max_graphs(void) { return hf::kMaxK; }
+int32_t dippm_head_fused_sync_ints(void) { return 2; }  // the grid barrier's {count, generation}
 
 int32_t dippm_head_fused_trace(int64_t* out24) {
   long long t[hf::kTrace];

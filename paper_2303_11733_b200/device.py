@@ -395,7 +395,7 @@ class Workspace:
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.loss = torch.zeros(4, dtype=torch.float64, device=dev)
         self.row_loss = torch.empty(G, 4, dtype=torch.float64, device=dev)   # fused head: per-graph loss terms
-        self.head_sync = torch.zeros(2, dtype=torch.int32, device=dev)        # fused head: grid barrier
+        self.head_sync = torch.zeros(lib.dippm_head_fused_sync_ints(), dtype=torch.int32, device=dev)  # fused head
         self.head_pending = None  # forward(defer_head=True) -> loss() -> backward() runs the fused head once
         self.u_pending = None     # batch whose u the fused head still has to form (its phase 0)
         self.train = train
