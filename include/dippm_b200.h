@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 9
+#define DIPPM_ABI_VERSION 10
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -123,10 +123,14 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
  * NULL the kernel finishes the reduction itself (two fixed-order levels, last
  * block of each group / last group, fp64 sums) and writes bias_grad [width];
  * sync is device int32[dippm_colsum_sync_ints(N)], zeroed once by the caller
- * and left zero by every launch.  With bias_grad == NULL only the first
- * dippm_colsum_blocks(N) partial rows are written (reduce with
- * dippm_reduce_rows).  write_agg = 0 computes the column sums only. */
+ * and left zero by every launch.  With bias_grad == NULL and sync == NULL only the first
+ * dippm_colsum_blocks(N) partial rows are written (reduce with dippm_reduce_rows).  With
+ * bias_grad == NULL and sync != NULL (deferred fold) the kernel keeps its wave-sized blocks,
+ * writes their partial rows and their count (int32 at dippm_colsum_count_slot) for the
+ * layer's weight-gradient GEMM to fold (dippm_gemm_args_t.bias_partial).
+ * write_agg = 0 computes the column sums only. */
 int32_t dippm_colsum_blocks(int64_t num_nodes);
+int32_t* dippm_colsum_count_slot(float* colsum_partial, int64_t num_nodes, int32_t width);
 int32_t dippm_colsum_rows(int64_t num_nodes);
 int32_t dippm_colsum_sync_ints(int64_t num_nodes);
 int32_t dippm_sage_aggregate_t(dippm_act_t B, int32_t width, int64_t num_nodes, int32_t write_agg,
@@ -214,6 +218,13 @@ typedef struct dippm_gemm_args {
   float* pool_graph;
   const int32_t* node_graph;   /* [M] node -> graph */
   const int32_t* graph_ptr;    /* [G+1] */
+  /* WGRAD (optional): also fold the layer's bias gradient, bias_grad[N] = column sums of the
+   * partial rows an agg^T / readout kernel left in deferred mode (bias_grad NULL, sync given)
+   * in bias_partial ([dippm_colsum_rows(K), N]; K = the rows reduced = the layer's nodes).  The
+   * fold rides in the weight-gradient launch (off the dgrad chain) instead of the tail of the
+   * aggregation kernel. */
+  const float* bias_partial;
+  float* bias_grad;
 } dippm_gemm_args_t;
 
 /* Split count the tensor-core WGRAD would like for this problem. */
@@ -453,7 +464,8 @@ typedef struct dippm_train_plan {
   float *out, *dout, *du;
   double *loss, *row_loss;
   int32_t* head_sync;
-  float* colsum;
+  float* colsum;              /* layer 2's deferred bias partials ... */
+  float* colsum3;             /* ... and layer 3's (folded by their weight-gradient GEMMs) */
   int32_t* colsum_sync;
   float* splitk;
   int32_t* tile_sync;

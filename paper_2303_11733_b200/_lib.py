@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 9  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 10  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -48,7 +48,7 @@ class GemmArgs(C.Structure):
         ("relu_bits", C.c_void_p), ("gate_bits", C.c_void_p), ("bits_ld", C.c_int64), ("cta_pair", C.c_int64),
         ("tile_sync", C.c_void_p), ("out_scale", C.c_double),
         ("pool_partial", C.c_void_p), ("pool_graph", C.c_void_p), ("node_graph", C.c_void_p),
-        ("graph_ptr", C.c_void_p),
+        ("graph_ptr", C.c_void_p), ("bias_partial", C.c_void_p), ("bias_grad", C.c_void_p),
     ]
 
 
@@ -94,7 +94,7 @@ class TrainPlan(C.Structure):
         ("A", Act * 3), ("B", Act * 3), ("relu_bits", P), ("pool_part", P), ("pool_graph", P),
         ("u", Act), ("x2", Act), ("x3", Act), ("d2", Act), ("d1", Act), ("dhead_f32", P), ("head_bits", P),
         ("out", P), ("dout", P), ("du", P), ("loss", P), ("row_loss", P), ("head_sync", P),
-        ("colsum", P), ("colsum_sync", P), ("splitk", P), ("tile_sync", P),
+        ("colsum", P), ("colsum3", P), ("colsum_sync", P), ("splitk", P), ("tile_sync", P),
         ("rowptr", P), ("col", P), ("deg", P), ("t_rowptr", P), ("t_col", P), ("bad", P), ("node_graph", P),
         ("inv_deg", P), ("csr_ws", P), ("csr_ws_bytes", C.c_size_t),
         ("dropout_p", C.c_double), ("keep_scale", C.c_double), ("delta", C.c_double), ("grad_den", C.c_double),
@@ -124,6 +124,7 @@ SIGNATURES = {
     "dippm_build_csr_grouped": (I32, [P, P, P, P, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, P, SZ, P]),
     "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
     "dippm_colsum_blocks": (I32, [I64]),
+    "dippm_colsum_count_slot": (P, [P, I64, I32]),
     "dippm_colsum_rows": (I32, [I64]),
     "dippm_colsum_sync_ints": (I32, [I64]),
     "dippm_sage_aggregate_t": (I32, [Act, I32, I64, I32, P, P, P, P, P, P, P]),

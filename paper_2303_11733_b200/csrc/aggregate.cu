@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kAggThreads, kReadout ? 2 : 3) k_aggregate_t(A
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
   if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
+  else if (sync && blockIdx.x == 0 && threadIdx.x == 0) *sync = (int)gridDim.x;  // deferred fold: the row count
 }
 
 // Layer-3 readout backward gated by the forward's bit masks (the fast path of
@@ -513,6 +514,7 @@ __global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 3) k_readout_agg_b
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
   if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
+  else if (sync && blockIdx.x == 0 && threadIdx.x == 0) *sync = (int)gridDim.x;  // deferred fold: the row count
 }
 
 // The training step's layout of the same computation (bf16 B, row-major bit masks,
@@ -677,6 +679,7 @@ __global__ void __launch_bounds__(kAggThreads, CPL >= 3 ? 2 : 4) k_readout_bits_
     colsum_partial[(int64_t)blockIdx.x * width + c] = t;
   }
   if (bias_out) finish_bias(colsum_partial, width, bias_out, sync, s_part);
+  else if (sync && blockIdx.x == 0 && threadIdx.x == 0) *sync = (int)gridDim.x;  // deferred fold: the row count
 }
 
 // Readout backward (gnn.py:224, 227): dz3[v] = du[g(v), :width] / N_g * (h3[v] > 0).
@@ -883,6 +886,17 @@ static int64_t colsum_bound(int64_t num_nodes) {
   return std::max<int64_t>(ceil_div_i(num_nodes, kRowsPerBlock), waves * P);
 }
 
+// Deferred bias fold (the consumer -- the layer's weight-gradient GEMM -- folds the partial rows):
+// the kernel stores its partial-row count as int32 in the last row of colsum_partial, a level-2
+// row the deferred mode never uses.  dippm_gemm finds it the same way (dippm_colsum_count_slot).
+static int32_t* deferred_count_slot(float* colsum_partial, int64_t N, int width) {
+  const int64_t nb = colsum_bound(N);
+  return reinterpret_cast<int32_t*>(colsum_partial + (nb + colsum_groups((int)nb) - 1) * (int64_t)width);
+}
+int32_t* dippm_colsum_count_slot(float* colsum_partial, int64_t num_nodes, int32_t width) {
+  return deferred_count_slot(colsum_partial, num_nodes, width);
+}
+
 int32_t dippm_colsum_blocks(int64_t num_nodes) { return ceil_div_i(num_nodes, kRowsPerBlock); }
 int32_t dippm_colsum_rows(int64_t num_nodes) {
   const int nblk = (int)colsum_bound(num_nodes);
@@ -940,8 +954,11 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
   DIPPM_ARG_CHECK(!bias_out || width / 4 <= kAggThreads, "sage_aggregate_t: fused bias reduce needs width <= %d",
                   4 * kAggThreads);
   if (bias_out) smem = std::max(smem, (size_t)kAggThreads * 4 * sizeof(double));  // fold scratch
-  int rpb = bias_out ? wave_rows_t(N, readout ? 2 : 3) : kRowsPerBlock;  // caller-reduced partials: fixed blocks
+  // bias_out: fold in the kernel; sync only: deferred fold (wave-sized blocks, row count to the
+  // slot); neither: caller-reduced partials over fixed 64-row blocks
+  int rpb = (bias_out || sync) ? wave_rows_t(N, readout ? 2 : 3) : kRowsPerBlock;
   if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;           // partial rows are sized for this bound
+  if (!bias_out && sync) sync = deferred_count_slot(colsum_partial, N, width);
   const int grid = ceil_div_i(N, rpb);
   ActView bv = make_view(B);
 #define DIPPM_AGGT(D, C, R)                                                                                      \
@@ -971,8 +988,9 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
   DIPPM_ARG_CHECK(N >= 1 && width % 256 == 0 && width <= 1024, "readout_aggregate_t: width %d must be 256/512/768/1024",
                   width);
   DIPPM_ARG_CHECK(!bias_out || sync, "readout_aggregate_t: bias_grad needs the sync counters");
-  int rpb = bias_out ? wave_rows_t(N, width >= 768 ? 2 : 3) : kRowsPerBlock;  // the kernel's residency
+  int rpb = (bias_out || sync) ? wave_rows_t(N, width >= 768 ? 2 : 3) : kRowsPerBlock;  // the kernel's residency
   if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
+  if (!bias_out && sync) sync = deferred_count_slot(colsum_partial, N, width);  // deferred fold
   // [warp partials | fold scratch] then the staged bit words of rpb + halo rows
   const size_t smem = std::max((size_t)(kAggThreads / 32) * width * sizeof(float), (size_t)kAggThreads * 4 * sizeof(double)) +
                       (size_t)(width / 32) * (rpb + kBitsHalo) * sizeof(uint32_t);
@@ -980,7 +998,7 @@ static int launch_readout_bits(dippm_act_t B, int32_t width, int64_t N, const in
   static const bool generic = getenv("DIPPM_RO_GENERIC") != nullptr;  // A/B switch: the layout-generic kernel
   if (B.dtype == DIPPM_DT_BF16 && ro.bits_ld == 0 && B.ld % 8 == 0 && !generic) {
     __nv_bfloat16* bp = reinterpret_cast<__nv_bfloat16*>(B.data);
-    if (bias_out) {  // 4 resident blocks per SM at width <= 512
+    if (bias_out || sync) {  // 4 resident blocks per SM at width <= 512
       rpb = wave_rows_t(N, width >= 768 ? 2 : 4);
       if (ceil_div_i(N, rpb) > colsum_bound(N)) rpb = kRowsPerBlock;
     }

@@ -194,13 +194,15 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   // ---- SAGE backward: dgrad chain on the main stream, weight gradients on the side stream
   for (int i = 2; i >= 0; --i) {
     const dippm_act_t Bi = P->B[i];
+    // layers 2-3: the bias partial rows are folded by the layer's weight-gradient GEMM (deferred mode)
+    float* part = i == 2 ? P->colsum3 : P->colsum;
     if (i == 2) {
       STEP_CALL(dippm_readout_aggregate_t(P->du, hp, b->graph_ptr, P->node_graph, kNullAct, Bi, (int32_t)hp, N,
-                                          P->t_rowptr, P->t_col, P->inv_deg, P->colsum, g32(P->off_b[i]),
-                                          P->colsum_sync, bits(2), 0, s));
+                                          P->t_rowptr, P->t_col, P->inv_deg, part, nullptr, P->colsum_sync, bits(2),
+                                          0, s));
     } else if (i == 1) {
-      STEP_CALL(dippm_sage_aggregate_t(Bi, (int32_t)hp, N, 1, P->t_rowptr, P->t_col, P->inv_deg, P->colsum,
-                                       g32(P->off_b[i]), P->colsum_sync, s));
+      STEP_CALL(dippm_sage_aggregate_t(Bi, (int32_t)hp, N, 1, P->t_rowptr, P->t_col, P->inv_deg, part, nullptr,
+                                       P->colsum_sync, s));
     }
     // weight gradient [2d (+1: layer 1's ones column = the bias row), hp] on the side stream
     cudaEvent_t ev = static_cast<cudaEvent_t>(P->ev[2 - i]);
@@ -221,6 +223,10 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     w.ldc = hp;
     w.splits = dippm_wgrad_splits(width, hp, N);
     w.tile_sync = P->tile_sync;
+    if (i > 0) {
+      w.bias_partial = part;
+      w.bias_grad = g32(P->off_b[i]);
+    }
     STEP_CALL(dippm_gemm(&w, 0, side));
     if (i == 0) break;
     dippm_gemm_args_t g = gemm_defaults();

@@ -66,6 +66,9 @@ struct Params {
   float* pool_graph;
   const int* node_graph;
   const int* graph_ptr;
+  const float* bias_part;  // WGRAD (optional): fold these partial rows of the layer's bias gradient
+  const int* bias_count;   //   (their count, written by the producing aggregation kernel)
+  float* bias_fold;        //   into this [N] fp32 vector (column sums in row order, fp64)
   unsigned long long* ts;  // diagnostics only (DIPPM_GEMM_TS=<device address>): per-CTA globaltimer stamps
   int dbg;  // diagnostics only (DIPPM_GEMM_DEBUG): bit 0 skip epilogue stores, bit 1 skip the
             // bit masks, bit 2 skip the whole chunk loop (release the accumulator at once), bit 3
@@ -1027,6 +1030,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores drained
+    if constexpr (kEpi == EPI_PARTIAL) {
+      // deferred bias fold (gnn.py:230): the layer's agg^T kernel left per-block column sums of dz;
+      // CTA b folds float4 column group b (b, b + grid, ...): every thread sums its rows in row
+      // order, the 256 thread sums meet in shared memory in thread order -- deterministic
+      if (p.bias_part) {
+        const int tid = threadIdx.x - 64;
+        const int rows = __ldcg(p.bias_count);
+        double4* s_red = reinterpret_cast<double4*>(epi_stage);  // staging is idle now (stores drained)
+        for (int g4 = blockIdx.x; g4 < (int)(p.N / 4); g4 += gridDim.x) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          for (int r = tid; r < rows; r += kEpiWarps * 32) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(p.bias_part + (int64_t)r * p.N) + g4);
+            a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {  // fixed xor tree within the warp, then the warps in order
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+          }
+          epi_sync();
+          if (lane == 0) s_red[tid >> 5] = make_double4(a0, a1, a2, a3);
+          epi_sync();
+          if (tid < 4) {
+            double t = 0.0;
+            for (int w = 0; w < kEpiWarps; ++w) {
+              const double4 q = s_red[w];
+              t += tid == 0 ? q.x : (tid == 1 ? q.y : (tid == 2 ? q.z : q.w));
+            }
+            p.bias_fold[g4 * 4 + tid] = (float)t;
+          }
+        }
+      }
+    }
   }
   if (p.ts && threadIdx.x == 64) p.ts[blockIdx.x * 8 + 2] = globaltimer();  // first epilogue thread done
   tc_fence_before();
@@ -1135,6 +1173,15 @@ static int run(const dippm_gemm_args_t* a, cudaStream_t s) {
   p.graph_ptr = a->graph_ptr;
   p.gate_bits = a->gate_bits;
   p.bits_ld = a->bits_ld;
+  if (kEpi == EPI_PARTIAL && a->bias_partial) {
+    if (!a->bias_grad) {
+      set_error("gemm WGRAD: bias_partial needs bias_grad");
+      return DIPPM_ERR_ARG;
+    }
+    p.bias_part = a->bias_partial;
+    p.bias_count = dippm_colsum_count_slot(const_cast<float*>(a->bias_partial), a->K, (int32_t)a->N);
+    p.bias_fold = a->bias_grad;
+  }
   static const int dbg = getenv("DIPPM_GEMM_DEBUG") ? atoi(getenv("DIPPM_GEMM_DEBUG")) : 0;
   p.dbg = dbg;
   static unsigned long long* ts = getenv("DIPPM_GEMM_TS") ? (unsigned long long*)strtoull(getenv("DIPPM_GEMM_TS"), nullptr, 0) : nullptr;

@@ -415,6 +415,9 @@ class Workspace:
                 # chunk-major [3, Hp/32, N]: word (c/32, r); a warp's 32 rows store/load 128 contiguous bytes
                 self.relu_bits = torch.empty(3, hp // 32, N, dtype=torch.int32, device=dev)  # h1, h2, h3
                 self.colsum = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
+                # layer 3's partials apart from layer 2's: each is folded by its layer's weight-gradient
+                # GEMM on the side stream, which may still read layer 3's while layer 2's are written
+                self.colsum3 = torch.empty(lib.dippm_colsum_rows(N), hp, **f32)
                 self.colsum_sync = torch.zeros(lib.dippm_colsum_sync_ints(N), dtype=torch.int32, device=dev)
             # WGRAD outputs are [width, Hp] (M = width, N = Hp, reduction over rows), split-K
             # partials reduced inside the GEMM kernel (tile_sync counters stay zero between launches)
@@ -568,10 +571,11 @@ class Engine:
     def _gemm(self, kind, M, N, K, a, a_mn, b, b_mn, bias=None, relu=0, out=NULL_ACT, c=None, ldc=0, splits=1,
               gate=NULL_ACT, gate_scale=1.0, drop_mode=0, mask=None, ldm=0, drop_p=0.0, seed=0, seed_dev=None,
               relu_bits=None, gate_bits=None, bits_ld=0, tile_sync=None, out_scale=1.0, pool_partial=None,
-              pool_graph=None, node_graph=None, graph_ptr=None):
+              pool_graph=None, node_graph=None, graph_ptr=None, bias_partial=None, bias_grad=None):
         args = GemmArgs(kind, M, N, K, a, a_mn, b, b_mn, bias, relu, out, c, ldc, splits, gate, gate_scale,
                         drop_mode, mask, ldm, drop_p, int(seed) & (2**64 - 1), seed_dev, relu_bits, gate_bits,
-                        bits_ld, self.cta_pair, tile_sync, out_scale, pool_partial, pool_graph, node_graph, graph_ptr)
+                        bits_ld, self.cta_pair, tile_sync, out_scale, pool_partial, pool_graph, node_graph, graph_ptr,
+                        bias_partial, bias_grad)
         if self.gemm_hook is not None:
             self.gemm_hook("pre", 2.0 * M * N * K)
         _lib.check(_lib.load().dippm_gemm(args, self.backend, _stream()), "dippm_gemm")
@@ -579,13 +583,16 @@ class Engine:
             self.gemm_hook("post", 2.0 * M * N * K)
         self.launches += 1
 
-    def _wgrad(self, dz: Act, x: Act, rows: int, width: int, ws: Workspace, out_name: str) -> None:
+    def _wgrad(self, dz: Act, x: Act, rows: int, width: int, ws: Workspace, out_name: str,
+               bias_partial: int | None = None, bias_grad: int | None = None) -> None:
         """grads[out_name] (as [width, Hp]) = x^T @ dz over `rows` rows (gnn.py:228-229, 296):
-        one split-K tcgen05 launch that also reduces its partials in fixed split order."""
+        one split-K tcgen05 launch that also reduces its partials in fixed split order (and, with
+        bias_partial, folds the layer's deferred bias-gradient partial rows into bias_grad)."""
         hp = self.L.hp
         splits = _lib.load().dippm_wgrad_splits(width, hp, rows)
         self._gemm(GEMM_WGRAD, width, hp, rows, x, 1, dz, 1, out=Act(self._g32(out_name), hp, 0, DT_F32),
-                   c=_p(ws.splitk), ldc=hp, splits=splits, tile_sync=_p(ws.tile_sync), out_scale=1.0)
+                   c=_p(ws.splitk), ldc=hp, splits=splits, tile_sync=_p(ws.tile_sync), out_scale=1.0,
+                   bias_partial=bias_partial, bias_grad=bias_grad)
 
     def fused_head_ok(self, G: int) -> bool:
         """The fused head kernel covers this batch (bf16 tensor-core path, small batch)."""
@@ -757,32 +764,38 @@ class Engine:
             side = self._side
         main = torch.cuda.current_stream()
 
-        def wgrad(B, i):
+        # layers 2-3: the bias gradient (gnn.py:230) is folded by the layer's weight-gradient GEMM
+        # from the agg^T kernel's partial rows (tensor-core backend), not in the agg^T kernel's tail
+        defer = self.backend == 0
+
+        def wgrad(B, i, part=None):
             width = 2 * L.d_in[i] + (1 if i == 0 else 0)  # layer 1: + the ones row (bias gradient)
+            fold = dict(bias_partial=_p(part), bias_grad=self._g32(f"sage{i + 1}.bias")) if part is not None else {}
             if side is None:
-                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self")
+                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self", **fold)
                 return
             ev = torch.cuda.Event()
             ev.record(main)
             side.wait_event(ev)
             with torch.cuda.stream(side):
-                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self")
+                self._wgrad(B.view(0), ws.A[i].view(0), N, width, ws, f"sage{i + 1}.w_self", **fold)
 
         for i in (2, 1, 0):
             B = ws.B[i]
-            bias = self._g32(f"sage{i + 1}.bias")  # gnn.py:230, reduced inside the kernel
+            bias = None if defer else self._g32(f"sage{i + 1}.bias")  # gnn.py:230
+            part = ws.colsum3 if i == 2 else ws.colsum
             if i == 0:  # layer 1: the bias gradient comes out of the WGRAD GEMM (ones column of A1)
                 wgrad(B, 0)
                 continue
             if i == 2:  # readout backward fused: dz3 formed on the fly (gnn.py:224, 227)
                 _lib.call("dippm_readout_aggregate_t", _p(ws.du), hp, _p(b.graph_ptr), _p(b.node_graph),
                           NULL_ACT if ws.H3 is None else ws.H3.view(0), B.view(0), hp, N, _p(b.t_rowptr),
-                          _p(b.t_col), _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync),
+                          _p(b.t_col), _p(b.inv_deg), _p(part), bias, _p(ws.colsum_sync),
                           _p(ws.relu_bits[2]) if self.backend == 0 else None, 0, s)  # row-major; SIMT: no bits
             else:
                 _lib.call("dippm_sage_aggregate_t", B.view(0), hp, N, int(i > 0), _p(b.t_rowptr), _p(b.t_col),
-                          _p(b.inv_deg), _p(ws.colsum), bias, _p(ws.colsum_sync), s)
-            wgrad(B, i)
+                          _p(b.inv_deg), _p(part), bias, _p(ws.colsum_sync), s)
+            wgrad(B, i, part if defer else None)
             self._gemm(GEMM_GATE, N, L.d_in[i], 2 * hp, B.view(0), 0, self.Wd[i].view(), 0,
                        out=ws.B[i - 1].view(0), gate=ws.A[i].view(0), gate_scale=1.0,
                        gate_bits=_p(ws.relu_bits[i - 1]), bits_ld=ws.N)

@@ -73,7 +73,8 @@ class NativeStep:
         p.u, p.x2, p.x3, p.d2, p.d1 = ws.u.view(), ws.x2.view(), ws.x3.view(), ws.d2.view(), ws.d1.view()
         p.dhead_f32, p.head_bits = ptr(ws.dhead_f32), ptr(ws.head_bits)
         p.out, p.dout, p.du, p.loss, p.row_loss = ptr(ws.out), ptr(ws.dout), ptr(ws.du), ptr(ws.loss), ptr(ws.row_loss)
-        p.head_sync, p.colsum, p.colsum_sync = ptr(ws.head_sync), ptr(ws.colsum), ptr(ws.colsum_sync)
+        p.head_sync, p.colsum, p.colsum3, p.colsum_sync = (ptr(ws.head_sync), ptr(ws.colsum), ptr(ws.colsum3),
+                                                            ptr(ws.colsum_sync))
         p.splitk, p.tile_sync = ptr(ws.splitk), ptr(ws.tile_sync)
         p.rowptr, p.col, p.deg, p.t_rowptr, p.t_col = (ptr(self.rowptr), ptr(self.col), ptr(self.deg),
                                                         ptr(self.t_rowptr), ptr(self.t_col))
