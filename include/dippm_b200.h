@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 10
+#define DIPPM_ABI_VERSION 11
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -353,6 +353,15 @@ typedef struct dippm_head_args {
 } dippm_head_args_t;
 int32_t dippm_head_fused_max_graphs(void);
 int32_t dippm_head_fused_sync_ints(void);
+/* Opt-in tensor-core head: training-step heads with G <= 256, hp == 512, u_width == 576 (and no
+ * phase 0 / predict / mask-mode dropout) on one cluster of 8 CTAs, tcgen05 + TMA + TMEM
+ * (head_tc.cu; ~4x slower than the default 148-CTA kernel at configs[1], kept as the tested
+ * tcgen05 formulation).  on = 0 / 1 switches it off / on (on < 0: query); returns the previous
+ * state.  Also DIPPM_HEAD_TC=1 at load. */
+int32_t dippm_head_tc_enable(int32_t on);
+/* Diagnostics (synchronous): globaltimer stamps of CTA 0 of the last tensor-core head launch:
+ * kernel start (after setup) and the end of each of its 8 phases (P1 P2 C D P3 P4 P5 P6). */
+int32_t dippm_head_tc_trace(uint64_t* out16);
 int32_t dippm_head_fused(const dippm_head_args_t* args, void* stream);
 /* Diagnostics (synchronous): SM clock cycles, relative to kernel start, of CTA 0 of the last
  * launch: per phase (A, B: slots 1-4 / 5-8; C ends at 9, barrier 10; D 11-14; E 15-18) its

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 10  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 11  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -144,6 +144,8 @@ SIGNATURES = {
     "dippm_fc3_backward": (I32, [Act, I64, I32, P, P, F32, P, P, Act, P, P]),
     "dippm_head_fused_max_graphs": (I32, []),
     "dippm_head_fused_sync_ints": (I32, []),
+    "dippm_head_tc_enable": (I32, [I32]),
+    "dippm_head_tc_trace": (I32, [P]),
     "dippm_head_fused": (I32, [C.POINTER(HeadArgs), P]),
     "dippm_head_fused_trace": (I32, [P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdippm_b200.so"
-SOURCES = ["capi.cu", "csr.cu", "aggregate.cu", "head.cu", "head_fused.cu", "tc_gemm.cu", "numerics.cu", "rescore.cu", "step.cu"]
+SOURCES = ["capi.cu", "csr.cu", "aggregate.cu", "head.cu", "head_fused.cu", "tc_gemm.cu", "numerics.cu", "rescore.cu", "step.cu", "head_tc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

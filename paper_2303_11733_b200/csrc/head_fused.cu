@@ -717,10 +717,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
 
 using namespace dippm;
 
+namespace dippm {
+bool head_tc_launch(const dippm_head_args_t* h, cudaStream_t s, int32_t* status);  // head_tc.cu
+int head_tc_trace(unsigned long long* out16);
+// the tensor-core head (head_tc.cu) for the shapes it covers: opt-in, DIPPM_HEAD_TC=1 or
+// dippm_head_tc_enable(1) -- it measured ~4x slower than this kernel at configs[1]
+static int g_head_tc = -1;
+static bool head_tc_enabled() {
+  if (g_head_tc < 0) g_head_tc = getenv("DIPPM_HEAD_TC") && getenv("DIPPM_HEAD_TC")[0] == '1';
+  return g_head_tc != 0;
+}
+}
+
 extern "C" {
 
 int32_t dippm_head_fused_max_graphs(void) { return hf::kMaxK; }
 int32_t dippm_head_fused_sync_ints(void) { return 2; }  // the grid barrier's {count, generation}
+int32_t dippm_head_tc_trace(uint64_t* out16) { return head_tc_trace(reinterpret_cast<unsigned long long*>(out16)); }
+int32_t dippm_head_tc_enable(int32_t on) {
+  const int32_t was = head_tc_enabled() ? 1 : 0;
+  if (on >= 0) g_head_tc = on ? 1 : 0;
+  return was;
+}
 
 int32_t dippm_head_fused_trace(int64_t* out24) {
   long long t[hf::kTrace];
@@ -748,6 +766,9 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   DIPPM_ARG_CHECK(!h->train || (h->y_raw && h->bits && h->dout && h->d1 && h->d2 && h->d1f && h->d2f && h->gw1 &&
                                 h->gb1 && h->gw2 && h->gb2 && h->gw3 && h->gb3),
                   "head_fused: training needs targets, bit masks, gradient buffers");
+  // opt-in: the configs[1] head (G <= 256, hidden 512, training step) on the tensor cores (head_tc.cu)
+  int32_t st = DIPPM_OK;
+  if (head_tc_enabled() && head_tc_launch(h, (cudaStream_t)stream, &st)) return st;
   hf::Args a{};
   a.G = (int)h->G;
   a.hp = h->hp;

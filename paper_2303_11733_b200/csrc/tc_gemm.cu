@@ -1458,6 +1458,12 @@ static int dispatch(const dippm_gemm_args_t* a, cudaStream_t s) {
   }
 }
 
+// 128B-swizzled 3-D tensor map of a row-major operand (cols, rows, plane); box = box_cols x
+// box_rows.  For kernels in other translation units (the tensor-core FC head).
+int make_map_sw128(CUtensorMap* map, const dippm_act_t& v, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+  return make_map(map, v, rows, cols, box_cols, box_rows);
+}
+
 }  // namespace tc
 }  // namespace dippm
 
