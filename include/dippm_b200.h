@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 11
+#define DIPPM_ABI_VERSION 12
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -94,6 +94,16 @@ size_t dippm_csr_workspace_bytes(int64_t num_nodes, int64_t num_edges);
  * dippm_build_csr beyond.
  * node_graph (nullable): also writes the node -> graph map (dippm_node_graph) in the same pass. */
 size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t num_edges);
+/* The same, fused with the layer-1 operand of the training step (gnn.py:157-158 for the fp32
+ * 32-wide input x [N, 32]): a1[v, 0:32] = bf16(x[v]), a1[v, 32:64] = bf16(inv_deg[v] * sum over
+ * v's in-neighbours of x, CSR order) -- dippm_sage_aggregate's result bit for bit, without its
+ * launch.  a1: bf16 view, ld >= 64 (columns >= 64 untouched). */
+int32_t dippm_build_csr_grouped_l1(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
+                                   const int64_t* edge_ptr, int64_t num_graphs, int64_t num_nodes, int64_t num_edges,
+                                   int32_t max_nodes_per_graph, int32_t max_edges_per_graph, int32_t* rowptr,
+                                   int32_t* col, int32_t* deg, float* inv_deg, int32_t* t_rowptr, int32_t* t_col,
+                                   int32_t* bad_edge, int32_t* node_graph, void* workspace, size_t workspace_bytes,
+                                   const float* x, dippm_act_t a1, void* stream);
 int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
                                 const int64_t* edge_ptr, int64_t num_graphs, int64_t num_nodes, int64_t num_edges,
                                 int32_t max_nodes_per_graph, int32_t max_edges_per_graph,

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 11  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 12  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -122,6 +122,7 @@ SIGNATURES = {
     "dippm_build_csr": (I32, [P, P, I64, I64, P, P, P, P, P, P, P, P, SZ, P]),
     "dippm_csr_grouped_workspace_bytes": (SZ, [I64, I64]),
     "dippm_build_csr_grouped": (I32, [P, P, P, P, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "dippm_build_csr_grouped_l1": (I32, [P, P, P, P, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, P, SZ, P, Act, P]),
     "dippm_sage_aggregate": (I32, [Act, Act, Act, I64, I32, P, P, P, P]),
     "dippm_colsum_blocks": (I32, [I64]),
     "dippm_colsum_count_slot": (P, [P, I64, I32]),

@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(kGThreads) k_csr_graph(const int64_t* __restri
                                                          int G, int32_t* deg, float* inv_deg, int32_t* rowptr,
                                                          int32_t* col, int32_t* t_rowptr, int32_t* t_col,
                                                          int32_t* bad_out, int32_t* node_graph, uint64_t* status,
-                                                         int* ctl /* [0] ticket, [1] done, [2] bad */) {
+                                                         int* ctl /* [0] ticket, [1] done, [2] bad */,
+                                                         const float* __restrict__ x, __nv_bfloat16* a1, int64_t a1_ld) {
   extern __shared__ int sm[];
   __shared__ int s_tmp[33];
   __shared__ long long s_red[33];
@@ -587,6 +588,32 @@ __global__ void __launch_bounds__(kGThreads) k_csr_graph(const int64_t* __restri
     t_col[off + i] = n0 + tmp[i];            // dst, ascending within the src row
   }
   if (g == G - 1 && threadIdx.x == 0) rowptr[N] = t_rowptr[N] = off + U;
+  if (x) {
+    // layer-1 operand (the training step's first aggregation, fused here while the graph's CSR
+    // is in shared memory): a1[v] = [bf16 x[v] | bf16(inv_deg[v] * sum_{u->v} x[u])], the sum in
+    // CSR order -- dippm_sage_aggregate's arithmetic for the fp32 32-wide input, bit for bit.
+    // 8 threads per node, 4 features each.
+    __syncthreads();  // inv_deg (written above by this CTA) is visible
+    const int sub = threadIdx.x & 7;
+    for (int lv = threadIdx.x >> 3; lv < ng; lv += blockDim.x >> 3) {
+      const int64_t v = n0 + lv;
+      const float4 xs = __ldg(reinterpret_cast<const float4*>(x + v * 32) + sub);
+      float ac[4] = {0.f, 0.f, 0.f, 0.f};
+      const int e = lv + 1 < ng ? ra[lv + 1] : U;
+      for (int i = ra[lv]; i < e; ++i) {
+        const float4 xn = __ldg(reinterpret_cast<const float4*>(x + (int64_t)(n0 + (keys[i] & 0xFFFF)) * 32) + sub);
+        ac[0] += xn.x;
+        ac[1] += xn.y;
+        ac[2] += xn.z;
+        ac[3] += xn.w;
+      }
+      const float w = inv_deg[v];
+      __nv_bfloat162 hx[2] = {__floats2bfloat162_rn(xs.x, xs.y), __floats2bfloat162_rn(xs.z, xs.w)};
+      __nv_bfloat162 hm[2] = {__floats2bfloat162_rn(ac[0] * w, ac[1] * w), __floats2bfloat162_rn(ac[2] * w, ac[3] * w)};
+      *reinterpret_cast<uint2*>(a1 + v * a1_ld + sub * 4) = *reinterpret_cast<uint2*>(hx);
+      *reinterpret_cast<uint2*>(a1 + v * a1_ld + 32 + sub * 4) = *reinterpret_cast<uint2*>(hm);
+    }
+  }
   // batch-level edge flag: OR of every graph's, written by the last CTA to finish
   if (threadIdx.x == 0) {
     if (s_bad) atomicOr(&ctl[2], 1);
@@ -605,12 +632,12 @@ extern "C" size_t dippm_csr_grouped_workspace_bytes(int64_t num_graphs, int64_t 
   return (size_t)(num_graphs > 0 ? num_graphs : 1) * 8 + 64;  // status words + ticket / done / flag
 }
 
-extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
-                                           const int64_t* edge_ptr, int64_t G, int64_t N, int64_t E,
-                                           int32_t max_nodes_per_graph, int32_t max_edges_per_graph,
-                                           int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,
-                                           int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge, int32_t* node_graph,
-                                           void* workspace, size_t workspace_bytes, void* stream) {
+static int32_t build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
+                                 const int64_t* edge_ptr, int64_t G, int64_t N, int64_t E, int32_t max_nodes_per_graph,
+                                 int32_t max_edges_per_graph, int32_t* rowptr, int32_t* col, int32_t* deg,
+                                 float* inv_deg, int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge,
+                                 int32_t* node_graph, void* workspace, size_t workspace_bytes, const float* x,
+                                 dippm_act_t a1, void* stream) {
   using namespace dippm;
   DIPPM_ARG_CHECK(G >= 1 && N >= 1 && E >= 0, "build_csr_grouped: bad sizes");
   DIPPM_ARG_CHECK(G <= 8192, "build_csr_grouped: %lld graphs per batch (max 8192)", (long long)G);
@@ -631,8 +658,35 @@ extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* ds
     smem_set = 200 * 1024;
   }
   DIPPM_CUDA_CHECK(cudaMemsetAsync(workspace, 0, (size_t)G * 8 + 16, s));
+  DIPPM_ARG_CHECK(!x || (a1.data && a1.dtype == DIPPM_DT_BF16 && a1.ld >= 64),
+                  "build_csr_grouped_l1: the layer-1 operand must be a bf16 view with >= 64 columns");
   DIPPM_LAUNCH_PDL(k_csr_graph, dim3((unsigned)G), dim3(kGThreads), smem, s, src, dst, graph_ptr, edge_ptr, epad, N,
-                   (int)G, deg, inv_deg, rowptr, col, t_rowptr, t_col, bad_edge, node_graph, status, ctl);
+                   (int)G, deg, inv_deg, rowptr, col, t_rowptr, t_col, bad_edge, node_graph, status, ctl, x,
+                   reinterpret_cast<__nv_bfloat16*>(a1.data), a1.ld);
   DIPPM_LAUNCH_CHECK("build_csr_grouped");
   return DIPPM_OK;
+}
+
+extern "C" int32_t dippm_build_csr_grouped(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
+                                           const int64_t* edge_ptr, int64_t G, int64_t N, int64_t E,
+                                           int32_t max_nodes_per_graph, int32_t max_edges_per_graph,
+                                           int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,
+                                           int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge, int32_t* node_graph,
+                                           void* workspace, size_t workspace_bytes, void* stream) {
+  return build_csr_grouped(src, dst, graph_ptr, edge_ptr, G, N, E, max_nodes_per_graph, max_edges_per_graph, rowptr, col,
+                           deg, inv_deg, t_rowptr, t_col, bad_edge, node_graph, workspace, workspace_bytes, nullptr,
+                           dippm_act_t{nullptr, 0, 0, 0}, stream);
+}
+
+extern "C" int32_t dippm_build_csr_grouped_l1(const int64_t* src, const int64_t* dst, const int32_t* graph_ptr,
+                                              const int64_t* edge_ptr, int64_t G, int64_t N, int64_t E,
+                                              int32_t max_nodes_per_graph, int32_t max_edges_per_graph,
+                                              int32_t* rowptr, int32_t* col, int32_t* deg, float* inv_deg,
+                                              int32_t* t_rowptr, int32_t* t_col, int32_t* bad_edge,
+                                              int32_t* node_graph, void* workspace, size_t workspace_bytes,
+                                              const float* x, dippm_act_t a1, void* stream) {
+  DIPPM_ARG_CHECK(x != nullptr, "build_csr_grouped_l1: x is NULL");
+  return build_csr_grouped(src, dst, graph_ptr, edge_ptr, G, N, E, max_nodes_per_graph, max_edges_per_graph, rowptr, col,
+                           deg, inv_deg, t_rowptr, t_col, bad_edge, node_graph, workspace, workspace_bytes, x, a1,
+                           stream);
 }

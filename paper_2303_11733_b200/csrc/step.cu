@@ -104,9 +104,10 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
                        b->max_nodes <= kGroupedMaxEdges;
   if (grouped) {
     DIPPM_ARG_CHECK(P->csr_ws_bytes >= dippm_csr_grouped_workspace_bytes(G, b->E), "train_step: CSR workspace");
-    STEP_CALL(dippm_build_csr_grouped(b->src, b->dst, b->graph_ptr, b->edge_ptr, G, N, b->E, b->max_nodes,
-                                      b->max_edges, P->rowptr, P->col, P->deg, P->inv_deg, P->t_rowptr, P->t_col,
-                                      bad, P->node_graph, P->csr_ws, P->csr_ws_bytes, s));
+    // + the layer-1 operand [x | agg x] while each graph's CSR is in shared memory
+    STEP_CALL(dippm_build_csr_grouped_l1(b->src, b->dst, b->graph_ptr, b->edge_ptr, G, N, b->E, b->max_nodes,
+                                         b->max_edges, P->rowptr, P->col, P->deg, P->inv_deg, P->t_rowptr,
+                                         P->t_col, bad, P->node_graph, P->csr_ws, P->csr_ws_bytes, b->x, P->A[0], s));
   } else {
     DIPPM_ARG_CHECK(P->csr_ws_bytes >= dippm_csr_workspace_bytes(N, b->E), "train_step: CSR workspace");
     STEP_CALL(dippm_node_graph(b->graph_ptr, G, P->node_graph, s));
@@ -115,8 +116,9 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   }
 
   // ---- forward (Engine.forward, train mode, head deferred to the backward)
-  STEP_CALL(dippm_sage_aggregate(f32_act(b->x, 32), at_col(P->A[0], 32), P->A[0], N, 32, P->rowptr, P->col,
-                                 P->inv_deg, s));
+  if (!grouped)  // (the grouped K1 above already formed it)
+    STEP_CALL(dippm_sage_aggregate(f32_act(b->x, 32), at_col(P->A[0], 32), P->A[0], N, 32, P->rowptr, P->col,
+                                   P->inv_deg, s));
   for (int i = 0; i < 3; ++i) {
     if (i > 0)
       STEP_CALL(dippm_sage_aggregate(P->A[i], at_col(P->A[i], hp), kNullAct, N, (int32_t)hp, P->rowptr, P->col,
