@@ -80,15 +80,20 @@ class NativeStep:
                                                         ptr(self.t_rowptr), ptr(self.t_col))
         p.bad, p.node_graph, p.inv_deg = ptr(self.bad), ptr(self.node_graph), ptr(self.inv_deg)
         p.csr_ws, p.csr_ws_bytes = ptr(self.csr_ws), nbytes
-        p.dropout_p = trainer.dropout_p
-        p.keep_scale = 1.0 / (1.0 - trainer.dropout_p) if trainer.dropout_p > 0 else 1.0
-        p.delta, p.grad_den, p.lr = trainer.delta, 0.0, trainer.lr
-        p.beta1, p.beta2, p.eps = 0.9, 0.999, 1e-8
-        p.seed = (trainer.seed * 131 + trainer.rank) & (2**64 - 1)
+        p.beta1, p.beta2, p.eps, p.grad_den = 0.9, 0.999, 1e-8, 0.0
+        self.sync_hparams(trainer)
         _lib.check(lib.dippm_train_plan_init(C.byref(p)), "dippm_train_plan_init")
         self.batch = _lib.TrainBatch()
         self._fn, self._fn_graphed = lib.dippm_train_step, lib.dippm_train_step_graphed
         self._warm = False  # the plan's first step runs eagerly (kernel attributes, module loads)
+
+    def sync_hparams(self, trainer: "BatchTrainer") -> None:
+        """The trainer's current learning rate, Huber delta, dropout and seed (read every step,
+        as the Python step reads them, so a schedule that changes trainer.lr takes effect)."""
+        p = self.plan
+        p.lr, p.delta, p.dropout_p = float(trainer.lr), float(trainer.delta), float(trainer.dropout_p)
+        p.keep_scale = 1.0 / (1.0 - trainer.dropout_p) if trainer.dropout_p > 0 else 1.0
+        p.seed = (trainer.seed * 131 + trainer.rank) & (2**64 - 1)
 
     def fits(self, b: Batch) -> bool:
         return b.N <= self.ws.N and b.G <= self.ws.G and b.E <= self.E
@@ -227,6 +232,7 @@ class BatchTrainer:
                     else:
                         torch.cuda.current_stream().synchronize()  # in-flight steps may still use them
                 self._native = nat = NativeStep(self, max(b.E, 2 * ws.N, nat.E if nat is not None else 0))
+            nat.sync_hparams(self)
             if slot is None:
                 nat.step(b)
             else:

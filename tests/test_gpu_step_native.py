@@ -128,3 +128,18 @@ def test_native_step_flags_bad_edges(data, monkeypatch):
     assert int(b.bad[0]) == 1
     with pytest.raises(ShapeMismatch):
         tr.submit(x, src, dst, gp, fs, y, edge_ptr=ep).loss()
+
+
+def test_native_step_follows_learning_rate_changes(data, monkeypatch):
+    """A learning-rate schedule (trainer.lr changed between steps) reaches the native step."""
+    ds, model, idx = data
+    res = []
+    for native in (True, False):
+        monkeypatch.setattr(trainer_mod, "NATIVE_STEP", native)
+        tr = BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3, seed=7)
+        for k, ix in enumerate(idx):
+            tr.lr = 1e-3 * (0.5 ** k)
+            tr.step_resident(upload_batch(*ds.collate(ix), device="cuda", build_csr=False))
+        torch.cuda.synchronize()
+        res.append(tr.engine.params.clone())
+    assert torch.equal(res[0], res[1])
