@@ -901,7 +901,10 @@ def main():
                                             "frac": step_flops / (step_ms / 1000.0) / 1e12 / peak_tf,
                                             "what": "algorithmic GEMM FLOPs of a step / the timed step time"},
                              "hbm_kernels": dict(hbm, peak_gbs=pk["hbm_gbs"],
-                                                 note="event-timed per launch in the roofline pass; algorithmic "
+                                                 note="event-timed per launch in the roofline pass (the step's "
+                                                      "Python orchestration, which the hooks require: the same "
+                                                      "kernels as the timed native step, except that the native "
+                                                      "step forms K2's layer-1 pass inside K1); algorithmic "
                                                       "bytes per DESIGN.md §3")},
                 "cpu_baseline": cpu, "clocks": clocks, "wall_s_timed_region": wall, "train_fp32": train_fp32,
                 "configs0_inference": cfg0, "inference": infer}
