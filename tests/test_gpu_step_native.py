@@ -143,3 +143,23 @@ def test_native_step_follows_learning_rate_changes(data, monkeypatch):
         torch.cuda.synchronize()
         res.append(tr.engine.params.clone())
     assert torch.equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("hidden", [40, 128])
+def test_native_step_other_widths(monkeypatch, hidden):
+    """Narrow hidden widths (padded to 64 / 128: the layout-generic readout and aggregation
+    kernels, the fused head's small tiles) and tiny ragged batches: native == Python."""
+    ds = make_dataset(96, seed=hidden)
+    norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+    model = gnn.create_model(hidden=hidden, seed=1, normalizer=norm)
+    idx = [np.arange(0, 64), np.arange(64, 65), np.arange(65, 96)]
+    res = []
+    for native in (True, False):
+        monkeypatch.setattr(trainer_mod, "NATIVE_STEP", native)
+        tr = BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3, seed=3)
+        for ix in idx:
+            tr.step_resident(upload_batch(*ds.collate(ix), device="cuda", build_csr=False))
+        torch.cuda.synchronize()
+        assert (tr._native is not None) == native
+        res.append((tr.engine.params.clone(), float(tr.ws.loss[0])))
+    assert torch.equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
