@@ -306,8 +306,11 @@ def upload_batch(x, src, dst, graph_ptr, fs, y=None, device="cuda", build_csr=Tr
                 raise
             edge_ptr = None
     arrays = [x, src, dst, graph_ptr, fs] + ([y] if y is not None else [])
-    b = Batch(G=int(len(graph_ptr) - 1), N=int(graph_ptr[-1]), E=int(len(src)), x=h2d(x), src=h2d(src),
-              dst=h2d(dst), graph_ptr=h2d(graph_ptr), fs=h2d(fs, torch.float64),
+    # the kernels' layouts: f32 features, int64 edge endpoints, int32 graph_ptr (an int32 edge list
+    # reinterpreted as int64 would read garbage endpoints)
+    b = Batch(G=int(len(graph_ptr) - 1), N=int(graph_ptr[-1]), E=int(len(src)), x=h2d(x, torch.float32),
+              src=h2d(src, torch.int64), dst=h2d(dst, torch.int64), graph_ptr=h2d(graph_ptr, torch.int32),
+              fs=h2d(fs, torch.float64),
               y=None if y is None else h2d(y, torch.float64),
               h2d_bytes=int(sum(np.asarray(a).nbytes for a in arrays)))
     if edge_ptr is not None:

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_kernels.py tests/test_gpu_step_native.py tests/test_gpu_scale.py 2>&1 | tail -3
-timeout 300 python tools/call_bench.py csr 2>&1 | tail -2
+python tools/csr_repro_tmp.py 2>&1 | tail -3
+timeout 900 python -m pytest -q -p no:cacheprovider tests/test_gpu_scale.py tests/test_gpu_kernels.py 2>&1 | tail -2
