@@ -119,7 +119,8 @@ int32_t dippm_build_csr(const int64_t* src, const int64_t* dst, int64_t num_edge
  * K2 — neighbour mean m = agg @ h (gnn.py:157-158 via _embed gnn.py:206).
  * h: [N, width] activation view; m_out: [N, width] view (usually the right
  * half of the layer's [h | m] GEMM operand).  If self_out.data is non-NULL
- * the kernel also copies h into it (layer-1 operand assembly).  width % 8 == 0. */
+ * the kernel also copies h into it (layer-1 operand assembly).  width: 8 * 2^k (8..1024) or 24 * 2^k (24..768) columns -- the
+ * 8-column chunks of a row must tile a warp (three per lane for the 3 * 2^k widths). */
 int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_out, int64_t num_nodes,
                              int32_t width, const int32_t* rowptr, const int32_t* col,
                              const float* inv_deg, void* stream);

@@ -904,8 +904,17 @@ int32_t dippm_colsum_rows(int64_t num_nodes) {
 }
 int32_t dippm_colsum_sync_ints(int64_t num_nodes) { return colsum_groups((int)colsum_bound(num_nodes)) + 1; }
 
+// 8-column chunks per lane: the lanes of a row (chunks / CPL) must tile a warp, so widths of
+// 8 * 2^k chunks use CPL 1 / 2 / 4 and widths of 3 * 2^k chunks (24, 48, 96, 192, 384, 768
+// columns) CPL 3
+// dynamic shared memory launchable without the opt-in attribute: 48 KB less the kernels' static
+// arrays (up to ~18 KB in k_aggregate_t)
+constexpr size_t kDynSmemNoAttr = 24 * 1024;
+
 static int cpl_for(int width) {
   const int chunks = width / 8;
+  const int third = chunks / 3;
+  if (chunks % 3 == 0 && third <= 32 && (third & (third - 1)) == 0) return 3;
   return chunks >= 128 ? 4 : (chunks >= 64 ? 2 : 1);
 }
 
@@ -924,7 +933,8 @@ int32_t dippm_sage_aggregate(dippm_act_t h, dippm_act_t m_out, dippm_act_t self_
   DIPPM_LAUNCH_PDL(k_aggregate<DI, DO, C>, dim3(grid), dim3(kAggThreads), 0, s, hv, mv, sv, N, rpb, width, rowptr, col, \
                    inv_deg)
 #define DIPPM_AGG_C(DI, DO) \
-  do { if (cpl == 4) DIPPM_AGG(DI, DO, 4); else if (cpl == 2) DIPPM_AGG(DI, DO, 2); else DIPPM_AGG(DI, DO, 1); } while (0)
+  do { if (cpl == 4) DIPPM_AGG(DI, DO, 4); else if (cpl == 3) DIPPM_AGG(DI, DO, 3); else if (cpl == 2) DIPPM_AGG(DI, DO, 2); \
+       else DIPPM_AGG(DI, DO, 1); } while (0)
 #define DIPPM_AGG_O(DI)                                                   \
   do {                                                                    \
     if (m_out.dtype == DIPPM_DT_BF16) DIPPM_AGG_C(DI, DIPPM_DT_BF16);     \
@@ -963,14 +973,17 @@ static int launch_aggregate_t(dippm_act_t B, int32_t width, int64_t N, int32_t w
   ActView bv = make_view(B);
 #define DIPPM_AGGT(D, C, R)                                                                                      \
   do {                                                                                                           \
-    if (smem > 48 * 1024)                                                                                        \
-      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                            (int)smem));                                                         \
+    static bool attr_set = false; /* once per instantiation: dynamic + static can pass 48 KB */              \
+    if (!attr_set && smem > kDynSmemNoAttr) {                                                                     \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_aggregate_t<D, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));  \
+      attr_set = true;                                                                                             \
+    }                                                                                                             \
     DIPPM_LAUNCH_PDL(k_aggregate_t<D, C, R>, dim3(grid), dim3(kAggThreads), smem, s, bv, width, N, rpb, write_agg,     \
                      t_rowptr, t_col, inv_deg, colsum_partial, ro, bias_out, sync);                             \
   } while (0)
 #define DIPPM_AGGT_C(D, R) \
-  do { if (cpl == 4) DIPPM_AGGT(D, 4, R); else if (cpl == 2) DIPPM_AGGT(D, 2, R); else DIPPM_AGGT(D, 1, R); } while (0)
+  do { if (cpl == 4) DIPPM_AGGT(D, 4, R); else if (cpl == 3) DIPPM_AGGT(D, 3, R); else if (cpl == 2) DIPPM_AGGT(D, 2, R); \
+       else DIPPM_AGGT(D, 1, R); } while (0)
 #define DIPPM_AGGT_R(D) do { if (readout) DIPPM_AGGT_C(D, true); else DIPPM_AGGT_C(D, false); } while (0)
   if (B.dtype == DIPPM_DT_BF16) DIPPM_AGGT_R(DIPPM_DT_BF16);
   else if (B.dtype == DIPPM_DT_TF32X3) DIPPM_AGGT_R(DIPPM_DT_TF32X3);
@@ -1099,13 +1112,16 @@ int32_t dippm_pool_concat(dippm_act_t h, const int32_t* graph_ptr, int64_t G, in
   ActView hv = make_view(h), uv = make_view(u);
 #define DIPPM_POOL(D, C)                                                                                         \
   do {                                                                                                           \
-    if (smem > 48 * 1024)                                                                                        \
-      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_pool_concat<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                            (int)smem));                                                         \
+    static bool attr_set = false; /* once per instantiation: dynamic + static can pass 48 KB */              \
+    if (!attr_set && smem > kDynSmemNoAttr) {                                                                     \
+      DIPPM_CUDA_CHECK(cudaFuncSetAttribute(k_pool_concat<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));  \
+      attr_set = true;                                                                                             \
+    }                                                                                                             \
     k_pool_concat<D, C><<<(unsigned)G, kPoolThreads, smem, s>>>(hv, graph_ptr, width, fs_raw, norm, uv);         \
   } while (0)
 #define DIPPM_POOL_C(D) \
-  do { if (cpl == 4) DIPPM_POOL(D, 4); else if (cpl == 2) DIPPM_POOL(D, 2); else DIPPM_POOL(D, 1); } while (0)
+  do { if (cpl == 4) DIPPM_POOL(D, 4); else if (cpl == 3) DIPPM_POOL(D, 3); else if (cpl == 2) DIPPM_POOL(D, 2); \
+       else DIPPM_POOL(D, 1); } while (0)
   if (h.dtype == DIPPM_DT_BF16) DIPPM_POOL_C(DIPPM_DT_BF16);
   else if (h.dtype == DIPPM_DT_TF32X3) DIPPM_POOL_C(DIPPM_DT_TF32X3);
   else DIPPM_POOL_C(DIPPM_DT_F32);

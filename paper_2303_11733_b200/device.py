@@ -4,9 +4,10 @@ batched GraphSAGE forward / backward / Adam step over the C ABI.
 PyTorch is used for device memory (caching allocator), streams and pinned
 host buffers only; every FLOP runs in libdippm_b200.so.
 
-HBM layout (hidden H padded to Hp = ceil64(H), rounded up to a power of two for the SAGE
-layers (the aggregation kernels tile 8-column chunks over a warp); padded weights are zero and
-stay exactly zero under Adam, so results equal the unpadded network):
+HBM layout (hidden H padded to Hp = ceil64(H), rounded up for the SAGE layers to the next
+width whose 8-column chunks tile a warp in the aggregation kernels -- 64, 128, 192, 256, 384,
+512, 768, 1024 (agg_width); padded weights are zero and stay exactly zero under Adam, so
+results equal the unpadded network):
   params  fp64 [P]   master weights, reference order gnn.py:488-491, with
                      sage{l}.w_self/w_neigh adjacent -> W_cat_l [2 d_l, Hp];
                      fc1.w padded to [Hp+64, Hp] (fs rows at Hp..Hp+4)
@@ -112,6 +113,20 @@ NULL_ACT = Act(None, 0, 0, 0)
 ARCHS = ("sage", "mlp")
 
 
+# widths the aggregation / pooling kernels take (csrc/aggregate.cu cpl_for): 8 * 2^k columns
+# (1-128 chunks of 8) and 24 * 2^k columns (3-96 chunks, three per lane)
+AGG_WIDTHS = tuple(sorted({8 << k for k in range(8)} | {24 << k for k in range(6)}))
+
+
+def agg_width(d: int, align: int = 8) -> int:
+    """Smallest width >= d (and >= align) that the aggregation kernels take and that is a
+    multiple of align; beyond 1024 columns a multiple of 1024 (callers split the columns)."""
+    d = max(int(d), align, 1)
+    if d > 1024:
+        return -(-d // 1024) * 1024
+    return next(w for w in AGG_WIDTHS if w >= d and w % align == 0)
+
+
 class Layout:
     """Flat parameter layout with hidden padded to a multiple of 64.
 
@@ -124,12 +139,13 @@ class Layout:
         if arch not in ARCHS:
             raise ValueError(f"arch must be one of {ARCHS}, got {arch!r}")
         self.hidden, self.arch = hidden, arch
-        # padded width: a multiple of 64 (tensor-core K blocks); for the SAGE layers a power of two,
-        # the widths whose 8-column chunks tile a warp exactly in the aggregation kernels (64, 128,
-        # 256, 512, 1024).  Padded weights are zero and stay zero, so results equal the unpadded net.
+        # padded width: a multiple of 64 (tensor-core K blocks); for the SAGE layers also one whose
+        # 8-column chunks tile a warp in the aggregation kernels (64, 128, 192, 256, 384, 512, 768,
+        # 1024; a power of two beyond).  Padded weights are zero and stay zero, so results equal
+        # the unpadded net.
         hp = -(-hidden // 64) * 64
         if arch == "sage":
-            hp = 1 << (hp - 1).bit_length()
+            hp = agg_width(hp, 64) if hp <= 1024 else 1 << (hp - 1).bit_length()
         self.hp = hp
         self.d_in = [FEATURE_WIDTH, hp, hp] if arch == "sage" else []
         shapes = []

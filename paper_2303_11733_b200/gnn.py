@@ -441,7 +441,7 @@ def sage_forward(encoding, layer: SageLayerParams, h_in: np.ndarray, precision: 
     Wt = ActBuf(dop, 2 * dip, dt, device)
     out = ActBuf(n, dop, dev.DT_F32, device)
     s = dev._stream()
-    for c0 in range(0, dip, 1024):  # the aggregation kernel takes power-of-two widths up to 1024
+    for c0 in range(0, dip, 1024):  # the aggregation kernel takes widths up to 1024
         w = min(dip - c0, 1024)
         _lib.call("dippm_sage_aggregate", Act(xt.data_ptr() + 4 * c0, dip, 0, dev.DT_F32), A.view(dip + c0),
                   A.view(c0), n, w, b.rowptr.data_ptr(), b.col.data_ptr(), b.inv_deg.data_ptr(), s)
@@ -453,11 +453,9 @@ def sage_forward(encoding, layer: SageLayerParams, h_in: np.ndarray, precision: 
 
 
 def _agg_width(d: int, lo: int) -> int:
-    """Padded width for the aggregation / pooling kernels: a power of two >= lo up to 1024
-    (their 8-column chunks tile a warp), beyond that a multiple of 1024 (column chunks)."""
-    if d <= 1024:
-        return max(lo, 1 << (max(d, 1) - 1).bit_length())
-    return -(-d // 1024) * 1024
+    """Padded width for the aggregation / pooling kernels (device.agg_width): the next width
+    whose 8-column chunks tile a warp, a multiple of lo; beyond 1024 a multiple of 1024."""
+    return dev.agg_width(d, lo)
 
 
 def readout_mean(z: np.ndarray) -> np.ndarray:

@@ -85,7 +85,7 @@ def test_csr_deterministic_and_bad_edges():
         upload_batch(x, np.array([0, N + 3]), np.array([1, 2]), gp, fs)
 
 
-@pytest.mark.parametrize("width", [32, 64, 512])
+@pytest.mark.parametrize("width", [24, 32, 48, 64, 96, 192, 384, 512, 768, 1024])
 def test_aggregate_matches_dense(width):
     rng = np.random.default_rng(width)
     N = 777
@@ -108,7 +108,7 @@ def test_aggregate_matches_dense(width):
     assert torch.equal(m, m2)
 
 
-@pytest.mark.parametrize("width", [64, 512])
+@pytest.mark.parametrize("width", [64, 192, 384, 512, 768, 1024])
 def test_aggregate_t_with_fused_bias_reduce(width):
     """agg^T + the in-kernel bias-gradient reduction agree with fp64 numpy; counters end at zero."""
     rng = np.random.default_rng(width + 1)
@@ -220,6 +220,28 @@ def test_pool_concat_and_mig_codes(golden):
     _lib.call("dippm_mig_codes", alphas.data_ptr(), 1, len(alphas), codes.data_ptr(), flag.data_ptr(), dev._stream())
     assert codes.cpu().numpy().tolist() == golden["mig_code"].tolist()
     assert int(flag.item()) == 0
+
+
+@pytest.mark.parametrize("width", [24, 96, 192, 384, 768, 1024])
+def test_pool_concat_widths(width):
+    """Mean readout + static-feature columns at the three-chunk widths and 1024 (more dynamic
+    shared memory than launches without the opt-in attribute)."""
+    rng = np.random.default_rng(width)
+    G = 9
+    gp = np.zeros(G + 1, np.int32)
+    np.cumsum(rng.integers(1, 300, G), out=gp[1:])
+    h = rng.normal(size=(gp[-1], width)).astype(np.float32)
+    fs = rng.normal(size=(G, 5))
+    norm = np.concatenate([np.zeros(6), rng.normal(size=5), rng.uniform(0.5, 2, 5)])
+    u = torch.full((G, width + 64), float("nan"), device="cuda")
+    keep = [torch.from_numpy(a).cuda() for a in (h, gp, fs, norm)]
+    _lib.call("dippm_pool_concat", dev.f32_act(keep[0]), keep[1].data_ptr(), G, width, keep[2].data_ptr(),
+              keep[3].data_ptr(), dev.f32_act(u), dev._stream())
+    got = u.cpu().numpy()
+    for g in range(G):
+        assert np.allclose(got[g, :width], h[gp[g]:gp[g + 1]].astype(np.float64).mean(0), atol=1e-5)
+        assert np.allclose(got[g, width:width + 5], (fs[g] - norm[6:11]) / norm[11:16], atol=1e-6)
+        assert np.all(got[g, width + 5:] == 0)
 
 
 def _gemm(kind, M, N, K, a, a_mn, b, b_mn, backend=0, **kw):

@@ -145,10 +145,12 @@ def test_native_step_follows_learning_rate_changes(data, monkeypatch):
     assert torch.equal(res[0], res[1])
 
 
-@pytest.mark.parametrize("hidden", [40, 128])
+@pytest.mark.parametrize("hidden", [40, 128, 300])
 def test_native_step_other_widths(monkeypatch, hidden):
-    """Narrow hidden widths (padded to 64 / 128: the layout-generic readout and aggregation
-    kernels, the fused head's small tiles) and tiny ragged batches: native == Python."""
+    """Other hidden widths (padded to 64 / 128 / 384: the layout-generic readout and
+    aggregation kernels, three-chunk lanes, the fused head's small tiles) and tiny ragged
+    batches: native == Python.  (Beyond 512 the fused head, and with it the native executor,
+    is not used.)"""
     ds = make_dataset(96, seed=hidden)
     norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
     model = gnn.create_model(hidden=hidden, seed=1, normalizer=norm)
