@@ -1,5 +1,6 @@
 """Data-parallel training on the device path, two ranks sharing one GPU (gloo carries the
-all-reduce; the pool grants one GPU, so NCCL itself is not exercised here).
+all-reduce; the pool grants one GPU, so NCCL itself runs only as a one-rank group, in
+test_nccl_one_rank_collectives_on_device).
 
 Each rank runs the engine's forward / loss (global-batch gradient denominator) / backward
 with the two-bucket OverlappedAllReduce of BatchTrainer._step on its half of a batch; the
@@ -81,3 +82,55 @@ def test_data_parallel_step_equals_single_process(tmp_path, prec, rel):
     for name, g in ref.items():
         err = np.linalg.norm(dp[name] - g) / max(np.linalg.norm(g), 1e-30)
         assert err < rel, (name, err)
+
+
+class _ForcedAllReduce:
+    """OverlappedAllReduce with the world-size gate removed, so a one-rank NCCL group still
+    issues the asynchronous all-reduces (sum over one rank: the identity)."""
+
+    def __new__(cls):
+        from paper_2303_11733_b200.dist import OverlappedAllReduce
+
+        class Forced(OverlappedAllReduce):
+            def _active(self):
+                return True
+        return Forced()
+
+
+def _nccl_worker(rank, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_11733_b200.dist import gather_predictions, global_batch_size
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        assert dist.get_backend() == "nccl"
+        g = _grads("bf16", np.arange(256), 256, _ForcedAllReduce())
+        assert global_batch_size(256) == 256
+        y = torch.arange(12, dtype=torch.float32, device="cuda").view(4, 3)
+        mig = torch.tensor([0, 1, -1, 3], dtype=torch.int8, device="cuda")
+        ys, ms = gather_predictions(y, mig)
+        assert torch.equal(ys, y) and torch.equal(ms, mig)
+        np.savez(out, **g)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_one_rank_collectives_on_device():
+    """The NCCL leg of the DP path on the one GPU the pool grants: a one-rank NCCL group runs
+    the two-bucket asynchronous gradient all-reduce inside the backward (issued on NCCL's
+    stream after the layer-3 weight gradient, waited on before Adam), the global-batch
+    all-reduce and the prediction all-gather; the gradients are bit-identical to the
+    no-collective step (a one-rank sum is the identity, and the ordering must not race)."""
+    import tempfile
+
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "nccl.npz")
+        mp.spawn(_nccl_worker, args=(_free_port(), out), nprocs=1, join=True)
+        got = dict(np.load(out))
+    ref = _grads("bf16", np.arange(256), 256)
+    for name, g in ref.items():
+        assert np.array_equal(got[name], g), name
