@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 12
+#define DIPPM_ABI_VERSION 13
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -502,7 +502,24 @@ typedef struct dippm_train_plan {
   void* ev[4];                /* fork events (layers 3, 2, 1) and the join */
   void* graph_exec;           /* dippm_train_step_graphed's executable graph (NULL until first use) */
   void* capture_stream;       /* the stream dippm_train_step_graphed records on (never the legacy stream) */
+  void* head_done;            /* recorded by each step after its fused head launch (also inside a
+                                 captured step); dippm_train_prep waits on the latest record, so the
+                                 next batch's K1 runs beside this step's backward */
 } dippm_train_plan_t;
+
+/* One batch's K1 outputs: the CSR / transposed CSR, the node->graph map and the layer-1
+ * operand A1 = [x | agg x | 0] (bf16, [N, 128] view).  dippm_train_prep builds a set ahead of
+ * the step, on another stream, so K1 runs beside the previous step instead of at the head of
+ * this one (its CTAs fill the SMs the previous step's kernel tails and the fused head leave
+ * idle); the plan's own CSR buffers + A[0] form the default set. */
+typedef struct dippm_csr_set {
+  int32_t *rowptr, *col, *deg, *t_rowptr, *t_col, *node_graph;
+  float* inv_deg;
+  void* csr_ws;
+  size_t csr_ws_bytes;
+  dippm_act_t a1;
+  int64_t cap_N, cap_E;       /* capacity (nodes, edges) */
+} dippm_csr_set_t;
 
 typedef struct dippm_train_batch {
   const float* x;             /* [N, 32] */
@@ -514,6 +531,9 @@ typedef struct dippm_train_batch {
   int32_t max_nodes, max_edges; /* largest graph (grouped CSR path) */
   double* loss_out;           /* double[4] for this step's loss, or NULL: plan->loss */
   int32_t* bad_out;           /* int32[1] for this step's CSR edge flag, or NULL: plan->bad */
+  const dippm_csr_set_t* csr; /* K1 outputs already built by dippm_train_prep (the step's stream
+                                 must be ordered after that prep), or NULL: the step runs K1
+                                 itself into the plan's buffers */
 } dippm_train_batch_t;
 
 int32_t dippm_train_plan_init(dippm_train_plan_t* plan);
@@ -528,6 +548,15 @@ int32_t dippm_train_step(const dippm_train_plan_t* plan, const dippm_train_batch
  * change grids and arguments, not the topology; a topology change re-instantiates) and
  * launched on `stream` -- no per-kernel launch gaps on the device. */
 int32_t dippm_train_step_graphed(dippm_train_plan_t* plan, const dippm_train_batch_t* batch, void* stream);
+/* K1 of `batch` into `set` on `stream` (grouped per-graph CSR + A1 in one launch, or the
+ * global CSR path + the layer-1 aggregation), ordered after the fused head of the step last
+ * launched with this plan (plan->head_done: K1's CTAs then share the SMs with that step's
+ * backward instead of its GEMM mainloops); the edge flag goes to batch->bad_out (else
+ * plan->bad).  batch->csr is ignored.  A later dippm_train_step with batch->csr = set, on a
+ * stream ordered after this one, skips K1.  The caller keeps `set` untouched until that step
+ * has finished (the next prep into it must be ordered after the step). */
+int32_t dippm_train_prep(const dippm_train_plan_t* plan, const dippm_train_batch_t* batch, const dippm_csr_set_t* set,
+                         void* stream);
 
 #ifdef __cplusplus
 }

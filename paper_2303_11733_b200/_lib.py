@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 12  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 13  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -99,15 +99,22 @@ class TrainPlan(C.Structure):
         ("inv_deg", P), ("csr_ws", P), ("csr_ws_bytes", C.c_size_t),
         ("dropout_p", C.c_double), ("keep_scale", C.c_double), ("delta", C.c_double), ("grad_den", C.c_double),
         ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("seed", C.c_uint64),
-        ("side_stream", P), ("ev", P * 4), ("graph_exec", P), ("capture_stream", P),
+        ("side_stream", P), ("ev", P * 4), ("graph_exec", P), ("capture_stream", P), ("head_done", P),
     ]
+
+
+class CsrSet(C.Structure):
+    """dippm_csr_set_t: one batch's K1 outputs (CSR, transposed CSR, node->graph, A1)."""
+    _fields_ = [("rowptr", P), ("col", P), ("deg", P), ("t_rowptr", P), ("t_col", P), ("node_graph", P),
+                ("inv_deg", P), ("csr_ws", P), ("csr_ws_bytes", SZ), ("a1", Act), ("cap_N", C.c_int64),
+                ("cap_E", C.c_int64)]
 
 
 class TrainBatch(C.Structure):
     """dippm_train_batch_t: one device-resident batch for dippm_train_step."""
     _fields_ = [("x", P), ("src", P), ("dst", P), ("graph_ptr", P), ("edge_ptr", P), ("fs", P), ("y", P),
                 ("N", C.c_int64), ("E", C.c_int64), ("G", C.c_int64), ("max_nodes", C.c_int32),
-                ("max_edges", C.c_int32), ("loss_out", P), ("bad_out", P)]
+                ("max_edges", C.c_int32), ("loss_out", P), ("bad_out", P), ("csr", C.POINTER(CsrSet))]
 
 
 # name -> (restype, argtypes); must match include/dippm_b200.h
@@ -165,6 +172,7 @@ SIGNATURES = {
     "dippm_train_plan_destroy": (I32, [C.POINTER(TrainPlan)]),
     "dippm_train_step": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), P]),
     "dippm_train_step_graphed": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), P]),
+    "dippm_train_prep": (I32, [C.POINTER(TrainPlan), C.POINTER(TrainBatch), C.POINTER(CsrSet), P]),
 }
 
 _lib = None

@@ -41,6 +41,47 @@ constexpr int64_t kGroupedMaxEdges = 8192;
     if (_rc != DIPPM_OK) return _rc;   \
   } while (0)
 
+// the plan's own K1 buffers (+ A[0]) as a set: the default when the batch brings none
+dippm_csr_set_t plan_set(const dippm_train_plan_t* P) {
+  dippm_csr_set_t c{};
+  c.rowptr = P->rowptr;
+  c.col = P->col;
+  c.deg = P->deg;
+  c.t_rowptr = P->t_rowptr;
+  c.t_col = P->t_col;
+  c.node_graph = P->node_graph;
+  c.inv_deg = P->inv_deg;
+  c.csr_ws = P->csr_ws;
+  c.csr_ws_bytes = P->csr_ws_bytes;
+  c.a1 = P->A[0];
+  c.cap_N = P->ws_N;
+  c.cap_E = P->ws_E;
+  return c;
+}
+
+// ---- K1: CSR + transposed CSR (device.build_batch_csr) and the layer-1 operand
+// A1 = [x | agg x] (Engine.forward's first aggregation)
+int32_t build_k1(const dippm_train_batch_t* b, const dippm_csr_set_t& c, int32_t* bad, cudaStream_t s) {
+  const int64_t N = b->N, G = b->G;
+  DIPPM_ARG_CHECK(N <= c.cap_N && b->E <= c.cap_E && c.a1.data && c.a1.dtype == DIPPM_DT_BF16,
+                  "train_step: CSR set (capacity %lld nodes, %lld edges) for %lld nodes, %lld edges",
+                  (long long)c.cap_N, (long long)c.cap_E, (long long)N, (long long)b->E);
+  const bool grouped = b->edge_ptr && G <= kGroupedMaxGraphs && b->max_edges <= kGroupedMaxEdges &&
+                       b->max_nodes <= kGroupedMaxEdges;
+  if (grouped) {
+    DIPPM_ARG_CHECK(c.csr_ws_bytes >= dippm_csr_grouped_workspace_bytes(G, b->E), "train_step: CSR workspace");
+    // + the layer-1 operand [x | agg x] while each graph's CSR is in shared memory
+    return dippm_build_csr_grouped_l1(b->src, b->dst, b->graph_ptr, b->edge_ptr, G, N, b->E, b->max_nodes,
+                                      b->max_edges, c.rowptr, c.col, c.deg, c.inv_deg, c.t_rowptr, c.t_col, bad,
+                                      c.node_graph, c.csr_ws, c.csr_ws_bytes, b->x, c.a1, s);
+  }
+  DIPPM_ARG_CHECK(c.csr_ws_bytes >= dippm_csr_workspace_bytes(N, b->E), "train_step: CSR workspace");
+  STEP_CALL(dippm_node_graph(b->graph_ptr, G, c.node_graph, s));
+  STEP_CALL(dippm_build_csr(b->src, b->dst, b->E, N, c.rowptr, c.col, c.deg, c.inv_deg, c.t_rowptr, c.t_col, bad,
+                            c.csr_ws, c.csr_ws_bytes, s));
+  return dippm_sage_aggregate(f32_act(b->x, 32), at_col(c.a1, 32), c.a1, N, 32, c.rowptr, c.col, c.inv_deg, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -52,6 +93,9 @@ int32_t dippm_train_plan_init(dippm_train_plan_t* plan) {
   plan->side_stream = s;
   DIPPM_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   plan->capture_stream = s;
+  cudaEvent_t hd = nullptr;
+  DIPPM_CUDA_CHECK(cudaEventCreateWithFlags(&hd, cudaEventDisableTiming));
+  plan->head_done = hd;
   for (int i = 0; i < 4; ++i) {
     cudaEvent_t e = nullptr;
     DIPPM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -71,6 +115,10 @@ int32_t dippm_train_plan_destroy(dippm_train_plan_t* plan) {
       cudaEventDestroy(static_cast<cudaEvent_t>(plan->ev[i]));
       plan->ev[i] = nullptr;
     }
+  if (plan->head_done) {
+    cudaEventDestroy(static_cast<cudaEvent_t>(plan->head_done));
+    plan->head_done = nullptr;
+  }
   for (void** st : {&plan->side_stream, &plan->capture_stream})
     if (*st) {
       cudaStreamDestroy(static_cast<cudaStream_t>(*st));
@@ -82,12 +130,14 @@ int32_t dippm_train_plan_destroy(dippm_train_plan_t* plan) {
 int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t* b, void* stream) {
   DIPPM_ARG_CHECK(P && b && P->side_stream, "train_step: plan not initialised");
   DIPPM_ARG_CHECK(b->N >= 1 && b->G >= 1 && b->E >= 0, "train_step: empty batch");
-  DIPPM_ARG_CHECK(b->N <= P->ws_N && b->G <= P->ws_G && b->E <= P->ws_E,
+  DIPPM_ARG_CHECK(b->N <= P->ws_N && b->G <= P->ws_G && (b->csr || b->E <= P->ws_E),
                   "train_step: batch (%lld nodes, %lld graphs, %lld edges) exceeds the plan's capacity",
                   (long long)b->N, (long long)b->G, (long long)b->E);
   DIPPM_ARG_CHECK(b->G <= dippm_head_fused_max_graphs() && P->hp <= 512 && P->u_width <= 576 &&
                       P->A[0].dtype == DIPPM_DT_BF16,
                   "train_step: batch outside the fused bf16 head's range");
+  DIPPM_ARG_CHECK(!b->csr || (b->N <= b->csr->cap_N && b->E <= b->csr->cap_E),
+                  "train_step: batch larger than its prepared CSR set");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaStream_t side = static_cast<cudaStream_t>(P->side_stream);
   const int64_t N = b->N, G = b->G, hp = P->hp;
@@ -99,36 +149,21 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   auto p32 = [&](int64_t off) { return P->p32 + off; };
   auto g32 = [&](int64_t off) { return P->grads + off; };
 
-  // ---- K1: CSR + transposed CSR (device.build_batch_csr)
-  const bool grouped = b->edge_ptr && G <= kGroupedMaxGraphs && b->max_edges <= kGroupedMaxEdges &&
-                       b->max_nodes <= kGroupedMaxEdges;
-  if (grouped) {
-    DIPPM_ARG_CHECK(P->csr_ws_bytes >= dippm_csr_grouped_workspace_bytes(G, b->E), "train_step: CSR workspace");
-    // + the layer-1 operand [x | agg x] while each graph's CSR is in shared memory
-    STEP_CALL(dippm_build_csr_grouped_l1(b->src, b->dst, b->graph_ptr, b->edge_ptr, G, N, b->E, b->max_nodes,
-                                         b->max_edges, P->rowptr, P->col, P->deg, P->inv_deg, P->t_rowptr,
-                                         P->t_col, bad, P->node_graph, P->csr_ws, P->csr_ws_bytes, b->x, P->A[0], s));
-  } else {
-    DIPPM_ARG_CHECK(P->csr_ws_bytes >= dippm_csr_workspace_bytes(N, b->E), "train_step: CSR workspace");
-    STEP_CALL(dippm_node_graph(b->graph_ptr, G, P->node_graph, s));
-    STEP_CALL(dippm_build_csr(b->src, b->dst, b->E, N, P->rowptr, P->col, P->deg, P->inv_deg, P->t_rowptr,
-                              P->t_col, bad, P->csr_ws, P->csr_ws_bytes, s));
-  }
+  // ---- K1 (here, or already run by dippm_train_prep into the batch's set)
+  const dippm_csr_set_t C = b->csr ? *b->csr : plan_set(P);
+  if (!b->csr) STEP_CALL(build_k1(b, C, bad, s));
 
   // ---- forward (Engine.forward, train mode, head deferred to the backward)
-  if (!grouped)  // (the grouped K1 above already formed it)
-    STEP_CALL(dippm_sage_aggregate(f32_act(b->x, 32), at_col(P->A[0], 32), P->A[0], N, 32, P->rowptr, P->col,
-                                   P->inv_deg, s));
   for (int i = 0; i < 3; ++i) {
     if (i > 0)
-      STEP_CALL(dippm_sage_aggregate(P->A[i], at_col(P->A[i], hp), kNullAct, N, (int32_t)hp, P->rowptr, P->col,
-                                     P->inv_deg, s));
+      STEP_CALL(dippm_sage_aggregate(P->A[i], at_col(P->A[i], hp), kNullAct, N, (int32_t)hp, C.rowptr, C.col,
+                                     C.inv_deg, s));
     dippm_gemm_args_t a = gemm_defaults();
     a.kind = DIPPM_GEMM_FWD;
     a.M = N;
     a.N = hp;
     a.K = 2 * d_in[i];
-    a.a = P->A[i];
+    a.a = i == 0 ? C.a1 : P->A[i];
     a.b = P->Wf[i];
     a.b_mn_major = 1;
     a.bias = p32(P->off_b[i]);
@@ -139,7 +174,7 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     if (i == 2) {
       a.pool_partial = P->pool_part;
       a.pool_graph = P->pool_graph;
-      a.node_graph = P->node_graph;
+      a.node_graph = C.node_graph;
       a.graph_ptr = b->graph_ptr;
     }
     STEP_CALL(dippm_gemm(&a, 0, s));
@@ -192,6 +227,13 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   h.step_counter = P->t_dev;  // this step's t += 1 (no separate dippm_step_counter launch)
   h.sync = P->head_sync;
   STEP_CALL(dippm_head_fused(&h, s));
+  if (P->head_done) {  // the next batch's K1 (dippm_train_prep) may start from here
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    DIPPM_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+    DIPPM_CUDA_CHECK(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(P->head_done), s,
+                                              cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                                  : cudaEventRecordDefault));
+  }
 
   // ---- SAGE backward: dgrad chain on the main stream, weight gradients on the side stream
   for (int i = 2; i >= 0; --i) {
@@ -199,11 +241,11 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     // layers 2-3: the bias partial rows are folded by the layer's weight-gradient GEMM (deferred mode)
     float* part = i == 2 ? P->colsum3 : P->colsum;
     if (i == 2) {
-      STEP_CALL(dippm_readout_aggregate_t(P->du, hp, b->graph_ptr, P->node_graph, kNullAct, Bi, (int32_t)hp, N,
-                                          P->t_rowptr, P->t_col, P->inv_deg, part, nullptr, P->colsum_sync, bits(2),
+      STEP_CALL(dippm_readout_aggregate_t(P->du, hp, b->graph_ptr, C.node_graph, kNullAct, Bi, (int32_t)hp, N,
+                                          C.t_rowptr, C.t_col, C.inv_deg, part, nullptr, P->colsum_sync, bits(2),
                                           0, s));
     } else if (i == 1) {
-      STEP_CALL(dippm_sage_aggregate_t(Bi, (int32_t)hp, N, 1, P->t_rowptr, P->t_col, P->inv_deg, part, nullptr,
+      STEP_CALL(dippm_sage_aggregate_t(Bi, (int32_t)hp, N, 1, C.t_rowptr, C.t_col, C.inv_deg, part, nullptr,
                                        P->colsum_sync, s));
     }
     // weight gradient [2d (+1: layer 1's ones column = the bias row), hp] on the side stream
@@ -216,7 +258,7 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     w.M = width;
     w.N = hp;
     w.K = N;
-    w.a = P->A[i];
+    w.a = i == 0 ? C.a1 : P->A[i];
     w.a_mn_major = 1;
     w.b = Bi;
     w.b_mn_major = 1;
@@ -252,6 +294,15 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   STEP_CALL(dippm_adam_pack(P->params, P->m, P->v, P->grads, 1.0, P->n_params, 0, P->t_dev, P->lr, P->beta1, P->beta2,
                             P->eps, 1, P->p32, P->segs, P->n_segs, s));
   return DIPPM_OK;
+}
+
+int32_t dippm_train_prep(const dippm_train_plan_t* P, const dippm_train_batch_t* b, const dippm_csr_set_t* set,
+                         void* stream) {
+  DIPPM_ARG_CHECK(P && b && set, "train_prep: NULL argument");
+  DIPPM_ARG_CHECK(b->N >= 1 && b->G >= 1 && b->E >= 0, "train_prep: empty batch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (P->head_done) DIPPM_CUDA_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(P->head_done), 0));
+  return build_k1(b, *set, b->bad_out ? b->bad_out : P->bad, s);
 }
 
 int32_t dippm_train_step_graphed(dippm_train_plan_t* P, const dippm_train_batch_t* b, void* stream) {

@@ -30,6 +30,38 @@ NATIVE_STEP = os.environ.get("DIPPM_NATIVE_STEP", "1") != "0"
 # DIPPM_NATIVE_GRAPHED=0: submit() launches the native step's kernels one by one instead of as
 # one updated CUDA graph
 NATIVE_GRAPHED = os.environ.get("DIPPM_NATIVE_GRAPHED", "1") != "0"
+# DIPPM_NATIVE_PREP=0: the native step runs K1 (CSR build + layer-1 operand) at its head instead
+# of ahead of it on a separate stream (dippm_train_prep), where it overlaps the previous step
+NATIVE_PREP = os.environ.get("DIPPM_NATIVE_PREP", "1") != "0"
+
+
+class CsrBuffers:
+    """One batch's K1 outputs for the native step (dippm_csr_set_t): CSR and transposed CSR,
+    node -> graph map, and the layer-1 operand A1 = [x | agg x | 1 | 0] (bf16 [N, 128], the
+    constant ones column as in Workspace).  Built by dippm_train_prep on a side stream ahead of
+    the step that reads it; `free` marks the last step that read it, `ready` the prep."""
+
+    def __init__(self, N: int, E: int, G: int, device):
+        lib = _lib.load()
+        i32 = dict(dtype=torch.int32, device=device)
+        N, E, G = max(1, int(N)), max(1, int(E)), max(1, int(G))
+        self.N, self.E, self.G = N, E, G
+        self.rowptr, self.t_rowptr = torch.empty(N + 1, **i32), torch.empty(N + 1, **i32)
+        self.col, self.t_col = torch.empty(E, **i32), torch.empty(E, **i32)
+        self.deg, self.node_graph = torch.empty(N, **i32), torch.empty(N, **i32)
+        self.inv_deg = torch.empty(N, dtype=torch.float32, device=device)
+        nbytes = max(lib.dippm_csr_grouped_workspace_bytes(G, E), lib.dippm_csr_workspace_bytes(N, E))
+        self.csr_ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.a1 = dev.ActBuf(N, 4 * dev.FEATURE_WIDTH, dev.DT_BF16, device)
+        self.a1.t[:, 2 * dev.FEATURE_WIDTH:].zero_()
+        self.a1.t[:, 2 * dev.FEATURE_WIDTH] = 1.0
+        p = dev._p
+        self.s = _lib.CsrSet(p(self.rowptr), p(self.col), p(self.deg), p(self.t_rowptr), p(self.t_col),
+                             p(self.node_graph), p(self.inv_deg), p(self.csr_ws), nbytes, self.a1.view(), N, E)
+        self.free, self.ready = None, torch.cuda.Event()
+
+    def fits(self, b: Batch) -> bool:
+        return b.N <= self.N and b.E <= self.E and b.G <= self.G
 
 
 class NativeStep:
@@ -85,6 +117,7 @@ class NativeStep:
         _lib.check(lib.dippm_train_plan_init(C.byref(p)), "dippm_train_plan_init")
         self.batch = _lib.TrainBatch()
         self._fn, self._fn_graphed = lib.dippm_train_step, lib.dippm_train_step_graphed
+        self._prep = lib.dippm_train_prep
         self._warm = False  # the plan's first step runs eagerly (kernel attributes, module loads)
 
     def sync_hparams(self, trainer: "BatchTrainer") -> None:
@@ -98,10 +131,7 @@ class NativeStep:
     def fits(self, b: Batch) -> bool:
         return b.N <= self.ws.N and b.G <= self.ws.G and b.E <= self.E
 
-    def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None,
-             graphed: bool = False) -> None:
-        """graphed: run the step as one CUDA-graph launch (dippm_train_step_graphed; the
-        ragged host-batch path, where per-batch torch graphs cannot be reused)."""
+    def _fill(self, b: Batch, loss_out, bad_out, cset: CsrBuffers | None) -> _lib.TrainBatch:
         t = self.batch
         t.loss_out = loss_out
         t.bad_out = None if bad_out is None else bad_out.data_ptr()
@@ -109,6 +139,23 @@ class NativeStep:
         t.edge_ptr = b.edge_ptr.data_ptr() if b.edge_ptr is not None else None
         t.fs, t.y = b.fs.data_ptr(), b.y.data_ptr()
         t.N, t.E, t.G, t.max_nodes, t.max_edges = b.N, b.E, b.G, b.max_nodes, b.max_edges
+        t.csr = C.pointer(cset.s) if cset is not None else None
+        return t
+
+    def prep(self, b: Batch, cset: CsrBuffers, stream: torch.cuda.Stream,
+             bad_out: torch.Tensor | None = None) -> None:
+        """K1 of batch b into cset on `stream` (dippm_train_prep); the caller orders the step
+        that reads cset after it."""
+        t = self._fill(b, None, bad_out, None)
+        _lib.check(self._prep(C.byref(self.plan), C.byref(t), C.byref(cset.s), stream.cuda_stream),
+                   "dippm_train_prep")
+
+    def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None,
+             graphed: bool = False, cset: CsrBuffers | None = None) -> None:
+        """graphed: run the step as one CUDA-graph launch (dippm_train_step_graphed; the
+        ragged host-batch path, where per-batch torch graphs cannot be reused).  cset: K1
+        outputs already built by prep() (else the step runs K1 itself)."""
+        t = self._fill(b, loss_out, bad_out, cset)
         fn = self._fn_graphed if graphed and self._warm and not torch.cuda.is_current_stream_capturing() else self._fn
         _lib.check(fn(C.byref(self.plan), C.byref(t), torch.cuda.current_stream().cuda_stream), "dippm_train_step")
         self._warm = True
@@ -145,7 +192,9 @@ class BatchTrainer:
         self._flag_ring = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(64)]
         self._loss_next = 0
         self._native = None
+        self._csr_ring, self._csr_next = [None, None], 0
         if torch.cuda.is_available():  # native steps: per-step loss / flag slots and their read-back stream
+            self._prep_stream = torch.cuda.Stream(self.engine.device)
             self._d2h_stream = torch.cuda.Stream(self.engine.device)
             self._loss_dev = torch.zeros(len(self._loss_ring), 4, dtype=torch.float64, device=self.engine.device)
             self._bad_dev = torch.zeros(len(self._loss_ring), dtype=torch.int32, device=self.engine.device)
@@ -182,8 +231,10 @@ class BatchTrainer:
         self._ensure(b)
         self.steps += 1
         self.engine._uploaded = None  # the step moves the device parameters
+        cset = self._resident_prep(b)
         if not self.use_graphs:
-            self._step(b, global_graphs)
+            self._step(b, global_graphs, cset=cset)
+            self._release(cset)
             return
         # CUDA graphs: the trainer's first step runs eagerly (module load, kernel
         # attributes); afterwards each resident batch's step is captured once
@@ -192,23 +243,28 @@ class BatchTrainer:
         hit = self._graphs.get(id(b))
         if hit is None:
             if not self._warm:
-                self._step(b, global_graphs)
+                self._step(b, global_graphs, cset=cset)
+                self._release(cset)
                 self._warm = True
                 return
-            hit = self.capture(b, global_graphs)
+            hit = self.capture(b, global_graphs, cset)
         hit[0].replay()
-        self.replayed_launches += hit[1]
+        self._release(cset)
+        self.replayed_launches += hit[1]  # (the prep's K1 launch is counted by the library)
 
-    def capture(self, b: Batch, global_graphs: int | None = None):
-        """Record (without executing) the training step on resident batch `b` as a CUDA graph."""
+    def capture(self, b: Batch, global_graphs: int | None = None, cset: CsrBuffers | None = None):
+        """Record (without executing) the training step on resident batch `b` as a CUDA graph
+        (with cset: the step reads K1's outputs from it, prepared before each replay)."""
         if id(b) in self._graphs:
             return self._graphs[id(b)]
         self._ensure(b)
+        if cset is None:
+            cset = self._batch_set(b)  # the set step_resident prepares before each replay
         g = torch.cuda.CUDAGraph()
         lib = dev._lib.load()
         l0 = lib.dippm_launch_count()
         with torch.cuda.graph(g, pool=self._pool):
-            self._step(b, global_graphs)
+            self._step(b, global_graphs, cset=cset)
         hit = self._graphs[id(b)] = (g, lib.dippm_launch_count() - l0)
         self._keep.append(b)  # captured pointers must stay alive
         return hit
@@ -219,24 +275,90 @@ class BatchTrainer:
                 and eng.overlap_wgrad and not dev.HEAD_POOL and eng.cta_pair == 0 and eng.gemm_hook is None
                 and _lib.call is _LIB_CALL and b.y is not None)
 
-    def _step(self, b: Batch, global_graphs: int | None, slot: int | None = None) -> bool:
+    def _native_for(self, b: Batch) -> NativeStep | None:
+        """The native executor's plan for batch b (built or rebuilt to fit), or None when the
+        step has to run the Python orchestration."""
+        if not self._native_ok(b):
+            return None
+        ws, nat = self.ws, self._native
+        if nat is None or nat.ws is not ws or not nat.fits(b):
+            if nat is not None:
+                if torch.cuda.is_current_stream_capturing() or self._graphs:
+                    self._keep.append(nat)  # captured steps still point at its CSR buffers
+                else:
+                    torch.cuda.current_stream().synchronize()  # in-flight steps may still use them
+            self._native = nat = NativeStep(self, max(b.E, 2 * ws.N, nat.E if nat is not None else 0))
+        return nat
+
+    def _prep(self, nat: NativeStep, b: Batch, cset: CsrBuffers, stream: torch.cuda.Stream,
+              bad_out: torch.Tensor | None = None) -> None:
+        """K1 of b into cset on `stream`, after the last step that read cset; the compute
+        stream waits for it.  Issued before the step, it runs while the previous step still
+        computes (the host is ahead of the device)."""
+        if cset.free is not None:
+            stream.wait_event(cset.free)
+        nat.prep(b, cset, stream, bad_out)
+        cset.ready.record(stream)
+        torch.cuda.current_stream().wait_event(cset.ready)
+
+    def _release(self, cset: CsrBuffers | None) -> None:
+        if cset is not None:
+            if cset.free is None:
+                cset.free = torch.cuda.Event()
+            cset.free.record(torch.cuda.current_stream())
+
+    def _resident_prep(self, b: Batch) -> CsrBuffers | None:
+        """K1 ahead of a resident batch's native step: a CSR set per batch when steps are
+        captured (the graph holds its pointers), else a ring of two."""
+        if not NATIVE_PREP or torch.cuda.is_current_stream_capturing():
+            return None
+        nat = self._native_for(b)
+        if nat is None:
+            return None
+        if self.use_graphs:
+            cset = self._batch_set(b)
+        else:
+            ring = self._csr_ring
+            k = self._csr_next
+            self._csr_next = 1 - k
+            if ring[k] is None or not ring[k].fits(b):
+                if ring[k] is not None and ring[k].free is not None:
+                    ring[k].free.synchronize()
+                ring[k] = CsrBuffers(max(b.N, self.ws.N), max(b.E, 2 * self.ws.N), max(b.G, self.ws.G),
+                                     self.engine.device)
+            cset = ring[k]
+        ready = getattr(b, "_inputs_ready", None)  # the batch's own uploads (issued on the compute stream)
+        if ready is None:
+            ready = b._inputs_ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream())
+        self._prep_stream.wait_event(ready)
+        self._prep(nat, b, cset, self._prep_stream)
+        return cset
+
+    def _batch_set(self, b: Batch) -> CsrBuffers | None:
+        """The resident batch's own CSR set when its captured step reads K1's outputs from one
+        (None: the step runs K1 itself)."""
+        if not (NATIVE_PREP and self.use_graphs) or self._native_for(b) is None:
+            return None
+        cset = getattr(b, "_csr_set", None)
+        if cset is None or not cset.fits(b):
+            cset = b._csr_set = CsrBuffers(b.N, b.E, b.G, self.engine.device)
+        return cset
+
+    def _step(self, b: Batch, global_graphs: int | None, slot: int | None = None,
+              cset: CsrBuffers | None = None) -> bool:
         """One step; True if the native executor ran it (with `slot`: its loss and edge flag
-        went to the device ring entry `slot` instead of the workspace)."""
+        went to the device ring entry `slot` instead of the workspace; with `cset`: K1 already
+        ran into it)."""
         eng, ws = self.engine, self.ws
-        if self._native_ok(b):
-            nat = self._native
-            if nat is None or nat.ws is not ws or not nat.fits(b):
-                if nat is not None:
-                    if torch.cuda.is_current_stream_capturing() or self._graphs:
-                        self._keep.append(nat)  # captured steps still point at its CSR buffers
-                    else:
-                        torch.cuda.current_stream().synchronize()  # in-flight steps may still use them
-                self._native = nat = NativeStep(self, max(b.E, 2 * ws.N, nat.E if nat is not None else 0))
+        nat = self._native_for(b)
+        if nat is not None:
             nat.sync_hparams(self)
             if slot is None:
-                nat.step(b)
+                nat.step(b, cset=cset)
             else:
-                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1], graphed=NATIVE_GRAPHED)
+                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1], graphed=NATIVE_GRAPHED,
+                         cset=cset)
             eng._uploaded = None
             eng._t_advanced = False  # the step's head advanced t and its Adam ran
             ws.head_pending = None
@@ -304,14 +426,8 @@ class BatchTrainer:
         self._slot_next = 1 - k
         sl = slots[k]
         compute = torch.cuda.current_stream()
-        with torch.cuda.stream(self._copy_stream):
-            self._copy_stream.wait_event(sl["free"])  # the step that last read this slot is done
-            views = [sl["x"][:N], sl["src"][:E], sl["dst"][:E], sl["gp"][:G + 1], sl["fs"][:G], sl["y"][:G],
-                     sl["ep"][:G + 1]]
-            for d_, h in zip(views, t):
-                d_.copy_(h, non_blocking=True)
-            sl["ready"].record(self._copy_stream)
-        compute.wait_event(sl["ready"])
+        views = [sl["x"][:N], sl["src"][:E], sl["dst"][:E], sl["gp"][:G + 1], sl["fs"][:G], sl["y"][:G],
+                 sl["ep"][:G + 1]]
         b = Batch(G=G, N=N, E=E, x=views[0], src=views[1], dst=views[2], graph_ptr=views[3], fs=views[4], y=views[5],
                   h2d_bytes=sum(a.numel() * a.element_size() for a in t))
         if edge_ptr is not None:
@@ -326,7 +442,24 @@ class BatchTrainer:
         j = self._loss_next
         self._loss_next = (j + 1) % len(self._loss_ring)
         host, flag = self._loss_ring[j], self._flag_ring[j]
-        native = self._step(b, global_graphs, slot=j)  # ragged shapes: host batches run eagerly
+        # native steps: K1 runs on the copy stream right behind this batch's copies, into the
+        # slot's CSR set, so it overlaps the previous step
+        nat = self._native_for(b) if NATIVE_PREP and not torch.cuda.is_current_stream_capturing() else None
+        cset = None
+        if nat is not None:
+            cset = sl.get("csr")
+            if cset is None or not cset.fits(b):
+                cset = sl["csr"] = CsrBuffers(sl["x"].shape[0], max(sl["src"].numel(), E), sl["gp"].numel() - 1,
+                                              self.engine.device)
+        with torch.cuda.stream(self._copy_stream):
+            self._copy_stream.wait_event(sl["free"])  # the step that last read this slot is done
+            for d_, h in zip(views, t):
+                d_.copy_(h, non_blocking=True)
+            if cset is not None:
+                nat.prep(b, cset, self._copy_stream, self._bad_dev[j:j + 1])
+            sl["ready"].record(self._copy_stream)
+        compute.wait_event(sl["ready"])
+        native = self._step(b, global_graphs, slot=j, cset=cset)  # ragged shapes: host batches run eagerly
         sl["free"].record(compute)
         done = torch.cuda.Event()
         if native:  # loss / flag went to ring entry j: read back on the D2H stream, off the compute stream

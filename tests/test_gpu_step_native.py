@@ -34,9 +34,11 @@ def data():
     return ds, model, idx
 
 
-def _run(model, ds, idx, native, monkeypatch, use_graphs=False, shuffle_edges=False, host=False, graphed=True):
+def _run(model, ds, idx, native, monkeypatch, use_graphs=False, shuffle_edges=False, host=False, graphed=True,
+         prep=True):
     monkeypatch.setattr(trainer_mod, "NATIVE_STEP", native)
     monkeypatch.setattr(trainer_mod, "NATIVE_GRAPHED", graphed)
+    monkeypatch.setattr(trainer_mod, "NATIVE_PREP", prep)
     tr = BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3, seed=7, use_graphs=use_graphs)
     losses = []
     for rep in range(2 if use_graphs else 1):  # graphs: the second pass replays the captures
@@ -109,6 +111,18 @@ def test_native_graphed_steps_ragged_batches(data, monkeypatch):
     rng = np.random.default_rng(11)
     idx = [rng.choice(ds.num_graphs, size=int(s), replace=False) for s in (200, 256, 7, 256, 131, 256)]
     _same(_run(model, ds, idx, True, monkeypatch, host=True), _run(model, ds, idx, False, monkeypatch, host=True))
+
+
+@pytest.mark.parametrize("mode", ["eager", "graphs", "host"])
+def test_native_step_k1_inline_equals_prepared(data, monkeypatch, mode):
+    """K1 at the head of the step (the plan's CSR buffers) and K1 ahead of it on another
+    stream into per-batch / per-slot CSR sets (dippm_train_prep): identical results."""
+    ds, model, idx = data
+    kw = dict(use_graphs=mode == "graphs", host=mode == "host")
+    _same(_run(model, ds, idx, True, monkeypatch, prep=False, **kw), _run(model, ds, idx, True, monkeypatch, **kw))
+    if mode == "host":  # the global-CSR K1 path (edges not grouped by graph) prepared ahead too
+        _same(_run(model, ds, idx, True, monkeypatch, prep=False, shuffle_edges=True),
+              _run(model, ds, idx, True, monkeypatch, shuffle_edges=True))
 
 
 def test_native_step_flags_bad_edges(data, monkeypatch):
