@@ -347,7 +347,10 @@ typedef struct dippm_head_args {
   float* dout;                   /* [G, 3] (train) */
   void *d2, *d1;                 /* bf16 [G, hp] */
   float *d2f, *d1f;              /* fp32 [G, hp] */
-  float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3;
+  float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3; /* gw1 / gw2 may be NULL in training: the caller then
+                                    computes dW1 = u^T d1 and dW2 = x2^T d2 itself from the bf16 d1 /
+                                    d2 this launch writes (off the critical path: dippm_train_step runs
+                                    them as weight-gradient GEMMs on its side stream) */
   float* du;                     /* fp32 [G, hp] or NULL (MLP: no readout below) */
   int32_t* sync;
   int32_t train;

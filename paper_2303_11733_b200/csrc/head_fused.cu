@@ -16,6 +16,9 @@
 //   D  d1 = (d2 @ W2^T) * [x2 > 0] * keep, dW2 = x2^T d2, dW3 = x3^T dout,  gnn.py:293-298
 //      db2 = sum d2, db3 = sum dout, loss / APE sums
 //   E  dW1 = u^T d1, db1 = sum d1, du = d1 @ W1^T (sage: the readout gradient)
+// With gw1 / gw2 NULL the dW2 / dW1 units are left to the caller (the training step runs them
+// as tcgen05 weight-gradient GEMMs beside the backward): D and E then hold one wave of units
+// each, on the critical path only what the readout backward needs.
 //
 // Every reduction runs in a fixed order (no atomics on values): results are deterministic.
 // Dropout in generated mode uses the same counter hash and index as the GEMM epilogue
@@ -353,20 +356,22 @@ __device__ void fwd_epilogue(const Args& a, const Unit& u, const float (&acc)[4]
   }
 }
 
-// ---- column sums of 32 columns over the G rows (8 row groups, fixed order) ----
-// what: 0 = db2 (d2f) + dW3 (x3^T dout), 1 = db1 (d1f)
+// ---- column sums of kCsCols columns over the G rows (32 row groups, fixed order) ----
+// what: 0 = db2 (d2f) + dW3 (x3^T dout), 1 = db1 (d1f).  Narrow units, many row groups: each
+// thread's rows (G / 32 of them, written this launch by other CTAs) load in one batch of L2
+// reads for G <= 256; 32 columns x 8 row groups was a chain of G / 64 dependent round trips
+// and the longest unit of phases D / E.
+constexpr int kCsCols = 8;
 __device__ void colsum_unit(const Args& a, uint8_t* smem, int what, int c0) {  // smem: scratch
-  float(*s)[kT][4] = reinterpret_cast<float(*)[kT][4]>(smem);  // [8][32][4]
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, j = c0 + tx;
+  float(*s)[kCsCols][4] = reinterpret_cast<float(*)[kCsCols][4]>(smem);  // [32][kCsCols][4]
+  const int tx = threadIdx.x % kCsCols, ty = threadIdx.x / kCsCols, j = c0 + tx;
   const float* src = what == 0 ? a.d2f : a.d1f;
   float cb = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f;
-  // rows g = ty, ty + 8, ... in order, loaded 8 rows at a time (written this launch by other
-  // CTAs: L2 loads; a row-at-a-time loop was a chain of G / 8 dependent L2 round trips)
-  for (int g0 = ty; g0 < a.G; g0 += 64) {
+  for (int g0 = ty; g0 < a.G; g0 += 32 * 8) {  // rows g0, g0 + 32, ... (8 per batch)
     float sv[8], xv[8], dv[8][3];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int g = g0 + 8 * i;
+      const int g = g0 + 32 * i;
       const bool ok = g < a.G;
       sv[i] = ok ? __ldcg(src + (int64_t)g * a.hp + j) : 0.f;
       if (what == 0) {
@@ -377,7 +382,7 @@ __device__ void colsum_unit(const Args& a, uint8_t* smem, int what, int c0) {  /
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (g0 + 8 * i >= a.G) break;
+      if (g0 + 32 * i >= a.G) break;
       cb += sv[i];
       if (what == 0) {
         w0 = fmaf(xv[i], dv[i][0], w0);
@@ -391,9 +396,9 @@ __device__ void colsum_unit(const Args& a, uint8_t* smem, int what, int c0) {  /
   s[ty][tx][2] = w1;
   s[ty][tx][3] = w2;
   __syncthreads();
-  if (ty == 0) {
+  if (threadIdx.x < kCsCols) {
     float r[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < 32; ++q)
       for (int k = 0; k < 4; ++k) r[k] += s[q][tx][k];
     if (what == 0) {
       a.gb2[j] = r[0];
@@ -683,13 +688,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   stamp(10);
   // D: dW2, GATE d1, db2 + dW3, loss + db3 (longest units first)
   {
-    const int n_w = a.train ? nh * nh : 0, n_g = a.train ? mt * nh : 0, n_c = a.train ? nh : 0;
+    const int n_w = a.train && a.gw2 ? nh * nh : 0, n_g = a.train ? mt * nh : 0;
+    const int n_c = a.train ? a.hp / kCsCols : 0;
     run_phase(a, smem, n_w + n_g + n_c + 1, [&](int t) {
       if (t < n_w) return Unit{U_WG2, (t / nh) * kT, (t % nh) * kT};
       t -= n_w;
       if (t < n_g) return Unit{U_GATE, (t / nh) * kT, (t % nh) * kT};
       t -= n_g;
-      if (t < n_c) return Unit{U_CS2, 0, t * kT};
+      if (t < n_c) return Unit{U_CS2, 0, t * kCsCols};
       return Unit{U_LOSS, 0, 0};
     }, 11);
   }
@@ -699,16 +705,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   if (a.step_counter && blockIdx.x == 0 && threadIdx.x == 0) a.step_counter[0] += 1;  // phases A/B are done
   // E: dW1, du, db1
   {
-    const int n_w = nu * nh, n_s = a.du ? mt * nh : 0, n_c = nh;
+    const int n_w = a.gw1 ? nu * nh : 0, n_s = a.du ? mt * nh : 0, n_c = a.hp / kCsCols;  // (gw1 NULL: dW1 by the caller)
     run_phase(a, smem, n_w + n_s + n_c, [&](int t) {
       if (t < n_w) return Unit{U_WG1, (t / nh) * kT, (t % nh) * kT};
       t -= n_w;
       if (t < n_s) return Unit{U_STORE, (t / nh) * kT, (t % nh) * kT};
       t -= n_s;
-      return Unit{U_CS1, 0, t * kT};
+      return Unit{U_CS1, 0, t * kCsCols};
     }, 15);
   }
-  bar.sync();
+  // no closing grid barrier: the kernel's completion orders phase E's writes for the next
+  // launch, and the barrier pair is already reset (the last arriver of D returned count to 0)
   stamp(18);
 }
 
@@ -763,8 +770,8 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   DIPPM_ARG_CHECK(!h->y_pred || (h->norm && h->mig && h->nonfinite), "head_fused: y_pred needs norm, mig, nonfinite");
   DIPPM_ARG_CHECK(!h->y_raw || (h->norm && h->loss_out && h->row_loss && h->delta > 0),
                   "head_fused: loss needs norm, loss_out, row_loss, delta > 0");
-  DIPPM_ARG_CHECK(!h->train || (h->y_raw && h->bits && h->dout && h->d1 && h->d2 && h->d1f && h->d2f && h->gw1 &&
-                                h->gb1 && h->gw2 && h->gb2 && h->gw3 && h->gb3),
+  DIPPM_ARG_CHECK(!h->train || (h->y_raw && h->bits && h->dout && h->d1 && h->d2 && h->d1f && h->d2f &&
+                                h->gb1 && h->gb2 && h->gw3 && h->gb3 && (h->gw1 != nullptr) == (h->gw2 != nullptr)),
                   "head_fused: training needs targets, bit masks, gradient buffers");
   // opt-in: the configs[1] head (G <= 256, hidden 512, training step) on the tensor cores (head_tc.cu)
   int32_t st = DIPPM_OK;

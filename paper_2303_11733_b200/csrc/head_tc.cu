@@ -585,6 +585,7 @@ int head_tc_trace(unsigned long long* out16) {
 bool head_tc_launch(const dippm_head_args_t* h, cudaStream_t s, int32_t* status) {
   using namespace htc;
   if (!(h->G >= 1 && h->G <= kMaxG && h->hp == kHp && h->u_width == kUw && h->train && h->y_raw && h->du &&
+        h->gw1 && h->gw2 &&
         h->drop_mode != 1 && !h->pool_partial && !h->y_pred && h->bits && h->bits_ld >= h->G))
     return false;
   *status = DIPPM_OK;

@@ -10,6 +10,8 @@
 // so the end-to-end path was host-bound) to the kernel launches themselves.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -226,6 +228,10 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   h.train = 1;
   h.step_counter = P->t_dev;  // this step's t += 1 (no separate dippm_step_counter launch)
   h.sync = P->head_sync;
+  // dW1 / dW2: weight-gradient GEMMs on the side stream (below); DIPPM_HEAD_WGRAD_INLINE=1
+  // keeps them in the head kernel (A/B switch, as device.HEAD_WGRAD_DEFER)
+  static const bool head_wgrad_inline = getenv("DIPPM_HEAD_WGRAD_INLINE") && getenv("DIPPM_HEAD_WGRAD_INLINE")[0] == '1';
+  if (!head_wgrad_inline) h.gw1 = h.gw2 = nullptr;
   STEP_CALL(dippm_head_fused(&h, s));
   if (P->head_done) {  // the next batch's K1 (dippm_train_prep) may start from here
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -233,6 +239,36 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     DIPPM_CUDA_CHECK(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(P->head_done), s,
                                               cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
                                                                                   : cudaEventRecordDefault));
+  }
+
+  // ---- weight gradients (side stream): one [width, hp] = A^T dz GEMM, split over K in fixed order
+  auto wgrad = [&](const dippm_act_t& A, const dippm_act_t& dz, int64_t width, int64_t rows, int64_t off_out,
+                   float* bias_partial, float* bias_grad) -> int32_t {
+    dippm_gemm_args_t w = gemm_defaults();
+    w.kind = DIPPM_GEMM_WGRAD;
+    w.M = width;
+    w.N = hp;
+    w.K = rows;
+    w.a = A;
+    w.a_mn_major = 1;
+    w.b = dz;
+    w.b_mn_major = 1;
+    w.out = f32_act(g32(off_out), hp);
+    w.c = P->splitk;
+    w.ldc = hp;
+    w.splits = dippm_wgrad_splits(width, hp, rows);
+    w.tile_sync = P->tile_sync;
+    w.bias_partial = bias_partial;
+    w.bias_grad = bias_grad;
+    return dippm_gemm(&w, 0, side);
+  };
+  // the head's dW2 = x2^T d2 and dW1 = u^T d1 (device.Engine.backward, head_wgrads)
+  if (!head_wgrad_inline) {
+    cudaEvent_t ev = static_cast<cudaEvent_t>(P->ev[3]);
+    DIPPM_CUDA_CHECK(cudaEventRecord(ev, s));
+    DIPPM_CUDA_CHECK(cudaStreamWaitEvent(side, ev, 0));
+    STEP_CALL(wgrad(P->x2, P->d2, hp, G, P->off_fc2w, nullptr, nullptr));
+    STEP_CALL(wgrad(P->u, P->d1, P->u_width, G, P->off_fc1w, nullptr, nullptr));
   }
 
   // ---- SAGE backward: dgrad chain on the main stream, weight gradients on the side stream
@@ -253,25 +289,8 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     DIPPM_CUDA_CHECK(cudaEventRecord(ev, s));
     DIPPM_CUDA_CHECK(cudaStreamWaitEvent(side, ev, 0));
     const int64_t width = 2 * d_in[i] + (i == 0 ? 1 : 0);
-    dippm_gemm_args_t w = gemm_defaults();
-    w.kind = DIPPM_GEMM_WGRAD;
-    w.M = width;
-    w.N = hp;
-    w.K = N;
-    w.a = i == 0 ? C.a1 : P->A[i];
-    w.a_mn_major = 1;
-    w.b = Bi;
-    w.b_mn_major = 1;
-    w.out = f32_act(g32(P->off_w[i]), hp);
-    w.c = P->splitk;
-    w.ldc = hp;
-    w.splits = dippm_wgrad_splits(width, hp, N);
-    w.tile_sync = P->tile_sync;
-    if (i > 0) {
-      w.bias_partial = part;
-      w.bias_grad = g32(P->off_b[i]);
-    }
-    STEP_CALL(dippm_gemm(&w, 0, side));
+    STEP_CALL(wgrad(i == 0 ? C.a1 : P->A[i], Bi, width, N, P->off_w[i], i > 0 ? part : nullptr,
+                    i > 0 ? g32(P->off_b[i]) : nullptr));
     if (i == 0) break;
     dippm_gemm_args_t g = gemm_defaults();
     g.kind = DIPPM_GEMM_GATE;

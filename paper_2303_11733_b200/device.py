@@ -48,6 +48,10 @@ FUSED_HEAD = os.environ.get("DIPPM_FUSED_HEAD", "1") != "0"
 # the readout's second stage as the fused head's phase 0 instead of its own launch: measured ~8 us
 # slower per step (one graph per CTA, latency-bound, plus a grid barrier), so off unless asked for
 HEAD_POOL = os.environ.get("DIPPM_HEAD_POOL", "0") == "1"
+# the fused head's dW1 / dW2 as side-stream weight-gradient GEMMs (off the dgrad chain);
+# DIPPM_HEAD_WGRAD_INLINE=1 keeps them inside the head kernel (A/B switch; the native step
+# reads the same variable)
+HEAD_WGRAD_DEFER = os.environ.get("DIPPM_HEAD_WGRAD_INLINE", "0") != "1"
 BACKENDS = {"tc": 0, "simt": 1}
 
 
@@ -672,9 +676,11 @@ class Engine:
         self._head_forward(b, ws, mask_mode, dropout_p, seed, predict)
 
     def _head_fused(self, b: Batch, ws: Workspace, mask_mode: int, dropout_p: float, seed: int, predict: bool,
-                    loss=None, keep_scale: float = 1.0, advance_step: bool = False) -> None:
+                    loss=None, keep_scale: float = 1.0, advance_step: bool = False,
+                    defer_wgrad: bool = False) -> None:
         """K5/K6 in one cooperative launch (head_fused.cu): forward, and with loss = (delta,
-        grad_den) the Huber loss and, on a training workspace, the whole head backward."""
+        grad_den) the Huber loss and, on a training workspace, the whole head backward
+        (defer_wgrad: except dW1 / dW2, which the caller runs as weight-gradient GEMMs)."""
         L, hp = self.L, self.L.hp
         drop = mask_mode if dropout_p > 0.0 or mask_mode == 1 else 0
         train = loss is not None and ws.train
@@ -702,6 +708,8 @@ class Engine:
             a.dout, a.d2, a.d1 = _p(ws.dout), _p(ws.d2.t), _p(ws.d1.t)
             a.d2f, a.d1f = _p(ws.dhead_f32[0]), _p(ws.dhead_f32[1])
             a.gw1, a.gb1, a.gw2, a.gb2 = self._g32("fc1.w"), self._g32("fc1.b"), self._g32("fc2.w"), self._g32("fc2.b")
+            if defer_wgrad:
+                a.gw1 = a.gw2 = None
             a.gw3, a.gb3 = self._g32("fc3.w"), self._g32("fc3.b")
             a.du = _p(ws.du) if self.arch == "sage" else None
             a.train = 1
@@ -759,12 +767,15 @@ class Engine:
                 raise RuntimeError("forward(defer_head=True) needs loss() before backward()")
             # advance_step: an adam_step follows this backward, so the fused head may advance the
             # device step counter itself (one launch fewer)
+            # sage: dW1 / dW2 leave the head's critical path (weight-gradient GEMMs below)
+            head_wgrad = self.arch == "sage" and HEAD_WGRAD_DEFER
             self._head_fused(b, ws, pend["mask_mode"], pend["dropout_p"], pend["seed"], False,
                              loss=(pend["delta"], pend["grad_den"]), keep_scale=keep_scale,
-                             advance_step=advance_step)
+                             advance_step=advance_step, defer_wgrad=head_wgrad)
             if self.arch == "mlp":
                 return
         else:
+            head_wgrad = False
             _lib.call("dippm_fc3_backward", ws.x3.view(), b.G, hp, self._f32("fc3.w"), _p(ws.dout),
                       float(keep_scale), self._g32("fc3.w"), self._g32("fc3.b"), ws.d2.view(), self._g32("fc2.b"), s)
             self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
@@ -782,6 +793,19 @@ class Engine:
                 self._side = torch.cuda.Stream(self.device)
             side = self._side
         main = torch.cuda.current_stream()
+        if head_wgrad:  # the fused head's dW2 = x2^T d2, dW1 = u^T d1 (off the dgrad chain)
+            def head_wgrads():
+                self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
+                self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
+            if side is None:
+                head_wgrads()
+            else:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    head_wgrads()
+            self.launches += 2
 
         # layers 2-3: the bias gradient (gnn.py:230) is folded by the layer's weight-gradient GEMM
         # from the agg^T kernel's partial rows (tensor-core backend), not in the agg^T kernel's tail

@@ -10,7 +10,7 @@ from paper_2303_11733_b200 import _lib, gnn  # noqa: E402
 from paper_2303_11733_b200.device import Engine, Workspace, upload_batch  # noqa: E402
 from paper_2303_11733_b200.synth import make_dataset  # noqa: E402
 
-G = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+G = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 256
 ds = make_dataset(G, seed=2)
 model = gnn.create_model(hidden=512, seed=0, normalizer=gnn.Normalizer.fit(ds.y.astype(float), ds.fs.astype(float)))
 b = upload_batch(*ds.collate(range(G)), device="cuda")
@@ -26,7 +26,7 @@ out = np.zeros(24, np.int64)
 rows = []
 for it in range(20):
     eng._head_fused(b, ws, pend["mask_mode"], pend["dropout_p"], pend["seed"], False,
-                    loss=(pend["delta"], pend["grad_den"]))
+                    loss=(pend["delta"], pend["grad_den"]), defer_wgrad="--defer" in sys.argv)
     torch.cuda.synchronize()
     lib.dippm_head_fused_trace(out.ctypes.data)
     rows.append(out.copy())
