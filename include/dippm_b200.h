@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 13
+#define DIPPM_ABI_VERSION 14
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -364,7 +364,14 @@ typedef struct dippm_head_args {
   /* optional (training): step_counter[0] += 1 once every CTA is past the forward's dropout
    * draws (which read it through seed_dev) -- dippm_step_counter folded into this launch. */
   int64_t* step_counter;
+  /* training: 1 leaves the column sums (db1, db2, dW3) and the batch loss + db3 to
+   * dippm_head_reduce, launched after this kernel (the training step runs it on its side stream:
+   * phases D / E then hold only what the readout backward waits for) */
+  int32_t defer_reduce;
 } dippm_head_args_t;
+/* The reductions a defer_reduce head left: db2 + dW3, db1, loss_out + db3 (same units, same
+ * results as inside the head kernel); stream-ordered after that head launch. */
+int32_t dippm_head_reduce(const dippm_head_args_t* h, void* stream);
 int32_t dippm_head_fused_max_graphs(void);
 int32_t dippm_head_fused_sync_ints(void);
 /* Opt-in tensor-core head: training-step heads with G <= 256, hp == 512, u_width == 576 (and no

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 13  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 14  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -69,6 +69,7 @@ class HeadArgs(C.Structure):
         ("gw1", P), ("gb1", P), ("gw2", P), ("gb2", P), ("gw3", P), ("gb3", P), ("du", P),
         ("sync", P), ("train", C.c_int32),
         ("pool_partial", P), ("pool_graph", P), ("graph_ptr", P), ("fs_raw", P), ("step_counter", P),
+        ("defer_reduce", C.c_int32),
     ]
 
 
@@ -155,6 +156,7 @@ SIGNATURES = {
     "dippm_head_tc_enable": (I32, [I32]),
     "dippm_head_tc_trace": (I32, [P]),
     "dippm_head_fused": (I32, [C.POINTER(HeadArgs), P]),
+    "dippm_head_reduce": (I32, [C.POINTER(HeadArgs), P]),
     "dippm_head_fused_trace": (I32, [P]),
     "dippm_colsum_act": (I32, [Act, I64, I32, P, P]),
     "dippm_huber": (I32, [P, P, I64, P, F64, F64, P, P, P]),

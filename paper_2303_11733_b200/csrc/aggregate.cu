@@ -797,8 +797,9 @@ __global__ void __launch_bounds__(128) k_pool_combine(const float* __restrict__ 
                                                       const double* __restrict__ fs_raw, const double* __restrict__ norm,
                                                       ActView u) {
   pdl_begin();
-  // one thread per 4 columns: the block sums of the graph's 32-row blocks are loaded up to 8
-  // float4 at a time (one L2 round trip per 8 blocks) and added in block order (fp64)
+  // one thread per 4 columns: the first block's partial and the following block sums of the
+  // graph's 32-row blocks are loaded up to 16 float4 at a time (one L2 round trip per 16
+  // blocks: a 300-node graph spans <= 11) and added in block order (fp64)
   const int g = blockIdx.x;
   const int gs = graph_ptr[g], ge = graph_ptr[g + 1];
   const int bf = gs >> 5, bl = (ge - 1) >> 5;
@@ -810,15 +811,25 @@ __global__ void __launch_bounds__(128) k_pool_combine(const float* __restrict__ 
       const float4 v = __ldg(reinterpret_cast<const float4*>(whole + (int64_t)g * width + c));
       t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
     } else {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c));
-      t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
-      for (int b = bf + 1; b <= bl; b += 8) {  // middle blocks (slot 0), then the last block
-        float4 w[8];
+      constexpr int kB = 16;
+      float4 w[kB];
+      // batch 0: the first block's partial row, then the middle blocks (slot 0) and the last block
+      w[0] = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)bf * 2 + ((gs & 31) == 0 ? 0 : 1)) * width + c));
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+      for (int j = 1; j < kB; ++j)
+        if (bf + j <= bl) w[j] = __ldg(reinterpret_cast<const float4*>(part + (int64_t)(bf + j) * rs + c));
+      t[0] = w[0].x; t[1] = w[0].y; t[2] = w[0].z; t[3] = w[0].w;
+#pragma unroll
+      for (int j = 1; j < kB; ++j)
+        if (bf + j <= bl) {
+          t[0] += w[j].x; t[1] += w[j].y; t[2] += w[j].z; t[3] += w[j].w;
+        }
+      for (int b = bf + kB; b <= bl; b += kB) {  // larger graphs: further batches, in order
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
           if (b + j <= bl) w[j] = __ldg(reinterpret_cast<const float4*>(part + (int64_t)(b + j) * rs + c));
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < kB; ++j)
           if (b + j <= bl) {
             t[0] += w[j].x; t[1] += w[j].y; t[2] += w[j].z; t[3] += w[j].w;
           }

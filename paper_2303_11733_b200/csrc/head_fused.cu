@@ -60,6 +60,7 @@ struct Args {
   float *gw1, *gb1, *gw2, *gb2, *gw3, *gb3, *du;
   int* sync;
   int train;
+  int defer_reduce;  // the column-sum / loss units run in k_head_reduce (dippm_head_reduce) instead
   const float *pool_part, *pool_graph;
   const double* fs_raw;  // phase 0 (optional): u from the readout's block sums
   const int* graph_ptr;
@@ -689,8 +690,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   // D: dW2, GATE d1, db2 + dW3, loss + db3 (longest units first)
   {
     const int n_w = a.train && a.gw2 ? nh * nh : 0, n_g = a.train ? mt * nh : 0;
-    const int n_c = a.train ? a.hp / kCsCols : 0;
-    run_phase(a, smem, n_w + n_g + n_c + 1, [&](int t) {
+    const int n_c = a.train && !a.defer_reduce ? a.hp / kCsCols : 0, n_l = a.defer_reduce ? 0 : 1;
+    run_phase(a, smem, n_w + n_g + n_c + n_l, [&](int t) {
       if (t < n_w) return Unit{U_WG2, (t / nh) * kT, (t % nh) * kT};
       t -= n_w;
       if (t < n_g) return Unit{U_GATE, (t / nh) * kT, (t % nh) * kT};
@@ -705,7 +706,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   if (a.step_counter && blockIdx.x == 0 && threadIdx.x == 0) a.step_counter[0] += 1;  // phases A/B are done
   // E: dW1, du, db1
   {
-    const int n_w = a.gw1 ? nu * nh : 0, n_s = a.du ? mt * nh : 0, n_c = a.hp / kCsCols;  // (gw1 NULL: dW1 by the caller)
+    const int n_w = a.gw1 ? nu * nh : 0, n_s = a.du ? mt * nh : 0;  // (gw1 NULL: dW1 by the caller)
+    const int n_c = a.defer_reduce ? 0 : a.hp / kCsCols;
     run_phase(a, smem, n_w + n_s + n_c, [&](int t) {
       if (t < n_w) return Unit{U_WG1, (t / nh) * kT, (t % nh) * kT};
       t -= n_w;
@@ -717,6 +719,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_head_fused(Args a) {
   // no closing grid barrier: the kernel's completion orders phase E's writes for the next
   // launch, and the barrier pair is already reset (the last arriver of D returned count to 0)
   stamp(18);
+}
+
+// The head's reductions as their own launch (training step, side stream): db2 + dW3 and db1
+// column sums (colsum_unit) and the batch loss + db3 (loss_unit) -- the same units, so the
+// same results as inside k_head_fused; one unit per CTA.
+__global__ void __launch_bounds__(kThreads) k_head_reduce(const Args a) {
+  __shared__ __align__(16) uint8_t scratch[32 * kCsCols * 4 * 4];
+  const int nc = a.hp / kCsCols;
+  const int t = blockIdx.x;
+  if (t < nc) colsum_unit(a, scratch, 0, t * kCsCols);
+  else if (t < 2 * nc) colsum_unit(a, scratch, 1, (t - nc) * kCsCols);
+  else loss_unit(a, scratch);
 }
 
 }  // namespace hf
@@ -736,46 +750,8 @@ static bool head_tc_enabled() {
 }
 }
 
-extern "C" {
-
-int32_t dippm_head_fused_max_graphs(void) { return hf::kMaxK; }
-int32_t dippm_head_fused_sync_ints(void) { return 2; }  // the grid barrier's {count, generation}
-int32_t dippm_head_tc_trace(uint64_t* out16) { return head_tc_trace(reinterpret_cast<unsigned long long*>(out16)); }
-int32_t dippm_head_tc_enable(int32_t on) {
-  const int32_t was = head_tc_enabled() ? 1 : 0;
-  if (on >= 0) g_head_tc = on ? 1 : 0;
-  return was;
-}
-
-int32_t dippm_head_fused_trace(int64_t* out24) {
-  long long t[hf::kTrace];
-  DIPPM_CUDA_CHECK(cudaMemcpyFromSymbol(t, hf::g_trace, sizeof(t)));
-  for (int i = 0; i < hf::kTrace; ++i) out24[i] = (int64_t)(t[i] - t[0]);
-  return DIPPM_OK;
-}
-
-int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
-  DIPPM_ARG_CHECK(h && h->G >= 1 && h->G <= hf::kMaxK, "head_fused: G must be in [1, %d]", hf::kMaxK);
-  DIPPM_ARG_CHECK(h->hp >= 32 && h->hp % 64 == 0 && h->hp <= 512, "head_fused: hidden width must be a multiple of 64 <= 512");
-  DIPPM_ARG_CHECK(h->u_width % 64 == 0 && h->u_width >= 64 && h->u_width <= hf::kMaxK, "head_fused: bad u_width");
-  DIPPM_ARG_CHECK(h->u && h->w1 && h->w2 && h->b1 && h->b2 && h->w3 && h->b3 && h->x2 && h->x3 && h->out && h->sync,
-                  "head_fused: missing operand");
-  DIPPM_ARG_CHECK(!h->bits || h->bits_ld >= h->G, "head_fused: bits_ld < G");
-  DIPPM_ARG_CHECK(!h->pool_partial || (h->pool_graph && h->graph_ptr && h->fs_raw && h->norm &&
-                                       h->u_width >= h->hp + kStaticWidth),
-                  "head_fused: in-kernel readout needs pool_graph, graph_ptr, fs_raw, norm, u_width >= hp + 5");
-  DIPPM_ARG_CHECK(h->drop_mode >= 0 && h->drop_mode <= 2 && h->drop_p >= 0 && h->drop_p < 1,
-                  "head_fused: bad dropout arguments");
-  DIPPM_ARG_CHECK(h->drop_mode != 1 || (h->mask1 && h->mask2), "head_fused: dropout mode 1 needs both masks");
-  DIPPM_ARG_CHECK(!h->y_pred || (h->norm && h->mig && h->nonfinite), "head_fused: y_pred needs norm, mig, nonfinite");
-  DIPPM_ARG_CHECK(!h->y_raw || (h->norm && h->loss_out && h->row_loss && h->delta > 0),
-                  "head_fused: loss needs norm, loss_out, row_loss, delta > 0");
-  DIPPM_ARG_CHECK(!h->train || (h->y_raw && h->bits && h->dout && h->d1 && h->d2 && h->d1f && h->d2f &&
-                                h->gb1 && h->gb2 && h->gw3 && h->gb3 && (h->gw1 != nullptr) == (h->gw2 != nullptr)),
-                  "head_fused: training needs targets, bit masks, gradient buffers");
-  // opt-in: the configs[1] head (G <= 256, hidden 512, training step) on the tensor cores (head_tc.cu)
-  int32_t st = DIPPM_OK;
-  if (head_tc_enabled() && head_tc_launch(h, (cudaStream_t)stream, &st)) return st;
+namespace dippm {
+static hf::Args head_args(const dippm_head_args_t* h) {
   hf::Args a{};
   a.G = (int)h->G;
   a.hp = h->hp;
@@ -828,6 +804,53 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   a.graph_ptr = h->graph_ptr;
   a.fs_raw = h->fs_raw;
   a.step_counter = reinterpret_cast<long long*>(h->step_counter);
+  a.defer_reduce = h->defer_reduce ? 1 : 0;
+  return a;
+}
+
+}  // namespace dippm
+
+extern "C" {
+
+int32_t dippm_head_fused_max_graphs(void) { return hf::kMaxK; }
+int32_t dippm_head_fused_sync_ints(void) { return 2; }  // the grid barrier's {count, generation}
+int32_t dippm_head_tc_trace(uint64_t* out16) { return head_tc_trace(reinterpret_cast<unsigned long long*>(out16)); }
+int32_t dippm_head_tc_enable(int32_t on) {
+  const int32_t was = head_tc_enabled() ? 1 : 0;
+  if (on >= 0) g_head_tc = on ? 1 : 0;
+  return was;
+}
+
+int32_t dippm_head_fused_trace(int64_t* out24) {
+  long long t[hf::kTrace];
+  DIPPM_CUDA_CHECK(cudaMemcpyFromSymbol(t, hf::g_trace, sizeof(t)));
+  for (int i = 0; i < hf::kTrace; ++i) out24[i] = (int64_t)(t[i] - t[0]);
+  return DIPPM_OK;
+}
+
+int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
+  DIPPM_ARG_CHECK(h && h->G >= 1 && h->G <= hf::kMaxK, "head_fused: G must be in [1, %d]", hf::kMaxK);
+  DIPPM_ARG_CHECK(h->hp >= 32 && h->hp % 64 == 0 && h->hp <= 512, "head_fused: hidden width must be a multiple of 64 <= 512");
+  DIPPM_ARG_CHECK(h->u_width % 64 == 0 && h->u_width >= 64 && h->u_width <= hf::kMaxK, "head_fused: bad u_width");
+  DIPPM_ARG_CHECK(h->u && h->w1 && h->w2 && h->b1 && h->b2 && h->w3 && h->b3 && h->x2 && h->x3 && h->out && h->sync,
+                  "head_fused: missing operand");
+  DIPPM_ARG_CHECK(!h->bits || h->bits_ld >= h->G, "head_fused: bits_ld < G");
+  DIPPM_ARG_CHECK(!h->pool_partial || (h->pool_graph && h->graph_ptr && h->fs_raw && h->norm &&
+                                       h->u_width >= h->hp + kStaticWidth),
+                  "head_fused: in-kernel readout needs pool_graph, graph_ptr, fs_raw, norm, u_width >= hp + 5");
+  DIPPM_ARG_CHECK(h->drop_mode >= 0 && h->drop_mode <= 2 && h->drop_p >= 0 && h->drop_p < 1,
+                  "head_fused: bad dropout arguments");
+  DIPPM_ARG_CHECK(h->drop_mode != 1 || (h->mask1 && h->mask2), "head_fused: dropout mode 1 needs both masks");
+  DIPPM_ARG_CHECK(!h->y_pred || (h->norm && h->mig && h->nonfinite), "head_fused: y_pred needs norm, mig, nonfinite");
+  DIPPM_ARG_CHECK(!h->y_raw || (h->norm && h->loss_out && h->row_loss && h->delta > 0),
+                  "head_fused: loss needs norm, loss_out, row_loss, delta > 0");
+  DIPPM_ARG_CHECK(!h->train || (h->y_raw && h->bits && h->dout && h->d1 && h->d2 && h->d1f && h->d2f &&
+                                h->gb1 && h->gb2 && h->gw3 && h->gb3 && (h->gw1 != nullptr) == (h->gw2 != nullptr)),
+                  "head_fused: training needs targets, bit masks, gradient buffers");
+  // opt-in: the configs[1] head (G <= 256, hidden 512, training step) on the tensor cores (head_tc.cu)
+  int32_t st = DIPPM_OK;
+  if (head_tc_enabled() && head_tc_launch(h, (cudaStream_t)stream, &st)) return st;
+  const hf::Args a = head_args(h);
   static bool attr = false;
   if (!attr) {
     DIPPM_CUDA_CHECK(cudaFuncSetAttribute(hf::k_head_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -847,6 +870,17 @@ int32_t dippm_head_fused(const dippm_head_args_t* h, void* stream) {
   cfg.numAttrs = 1;
   DIPPM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, hf::k_head_fused, a));
   DIPPM_LAUNCH_CHECK("k_head_fused");
+  return DIPPM_OK;
+}
+
+int32_t dippm_head_reduce(const dippm_head_args_t* h, void* stream) {
+  DIPPM_ARG_CHECK(h && h->train && h->defer_reduce && h->G >= 1 && h->hp % hf::kCsCols == 0 && h->d1f &&
+                      h->d2f && h->x3 && h->dout && h->row_loss && h->loss_out && h->gb1 && h->gb2 && h->gw3 &&
+                      h->gb3,
+                  "head_reduce: needs the training head's arguments with defer_reduce set");
+  const hf::Args a = head_args(h);
+  hf::k_head_reduce<<<2 * (h->hp / hf::kCsCols) + 1, hf::kThreads, 0, (cudaStream_t)stream>>>(a);
+  DIPPM_LAUNCH_CHECK("k_head_reduce");
   return DIPPM_OK;
 }
 

@@ -231,7 +231,10 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   // dW1 / dW2: weight-gradient GEMMs on the side stream (below); DIPPM_HEAD_WGRAD_INLINE=1
   // keeps them in the head kernel (A/B switch, as device.HEAD_WGRAD_DEFER)
   static const bool head_wgrad_inline = getenv("DIPPM_HEAD_WGRAD_INLINE") && getenv("DIPPM_HEAD_WGRAD_INLINE")[0] == '1';
-  if (!head_wgrad_inline) h.gw1 = h.gw2 = nullptr;
+  if (!head_wgrad_inline) {
+    h.gw1 = h.gw2 = nullptr;
+    h.defer_reduce = 1;  // column sums + loss: dippm_head_reduce on the side stream
+  }
   STEP_CALL(dippm_head_fused(&h, s));
   if (P->head_done) {  // the next batch's K1 (dippm_train_prep) may start from here
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -267,6 +270,7 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     cudaEvent_t ev = static_cast<cudaEvent_t>(P->ev[3]);
     DIPPM_CUDA_CHECK(cudaEventRecord(ev, s));
     DIPPM_CUDA_CHECK(cudaStreamWaitEvent(side, ev, 0));
+    STEP_CALL(dippm_head_reduce(&h, side));
     STEP_CALL(wgrad(P->x2, P->d2, hp, G, P->off_fc2w, nullptr, nullptr));
     STEP_CALL(wgrad(P->u, P->d1, P->u_width, G, P->off_fc1w, nullptr, nullptr));
   }

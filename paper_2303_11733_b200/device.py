@@ -708,8 +708,10 @@ class Engine:
             a.dout, a.d2, a.d1 = _p(ws.dout), _p(ws.d2.t), _p(ws.d1.t)
             a.d2f, a.d1f = _p(ws.dhead_f32[0]), _p(ws.dhead_f32[1])
             a.gw1, a.gb1, a.gw2, a.gb2 = self._g32("fc1.w"), self._g32("fc1.b"), self._g32("fc2.w"), self._g32("fc2.b")
-            if defer_wgrad:
+            if defer_wgrad:  # dW1 / dW2 and the column sums + loss: launched by backward()
                 a.gw1 = a.gw2 = None
+                a.defer_reduce = 1
+                ws.head_args = a
             a.gw3, a.gb3 = self._g32("fc3.w"), self._g32("fc3.b")
             a.du = _p(ws.du) if self.arch == "sage" else None
             a.train = 1
@@ -793,8 +795,9 @@ class Engine:
                 self._side = torch.cuda.Stream(self.device)
             side = self._side
         main = torch.cuda.current_stream()
-        if head_wgrad:  # the fused head's dW2 = x2^T d2, dW1 = u^T d1 (off the dgrad chain)
+        if head_wgrad:  # the fused head's reductions, dW2 = x2^T d2, dW1 = u^T d1 (off the dgrad chain)
             def head_wgrads():
+                _lib.call("dippm_head_reduce", C.byref(ws.head_args), _stream())
                 self._wgrad(ws.d2.view(), ws.x2.view(), b.G, hp, ws, "fc2.w")
                 self._wgrad(ws.d1.view(), ws.u.view(), b.G, L.u_width, ws, "fc1.w")
             if side is None:
@@ -805,7 +808,7 @@ class Engine:
                 side.wait_event(ev)
                 with torch.cuda.stream(side):
                     head_wgrads()
-            self.launches += 2
+            self.launches += 3
 
         # layers 2-3: the bias gradient (gnn.py:230) is folded by the layer's weight-gradient GEMM
         # from the agg^T kernel's partial rows (tensor-core backend), not in the agg^T kernel's tail
