@@ -212,3 +212,28 @@ def test_fused_head_small_shapes_match_per_op_path(hidden, G):
     g1, g0 = e1.get_grads(), e0.get_grads()
     for name in g0:
         assert _rel(g1[name], g0[name]) < REL, (name, _rel(g1[name], g0[name]))
+
+
+@pytest.mark.parametrize("G,drop_p", [(256, 0.05), (37, 0.0)])
+def test_deferred_head_equals_in_kernel_head(monkeypatch, G, drop_p):
+    """The training step's head (device.HEAD_WGRAD_DEFER): the column sums + loss in
+    dippm_head_reduce, dW1 / dW2 as weight-gradient GEMMs on the side stream -- against the
+    head doing all of it in-kernel.  The same device functions form the loss terms and the
+    reductions, so the loss and every gradient except fc1.w / fc2.w are bit-identical; those
+    two differ only in fp32 accumulation order."""
+    from paper_2303_11733_b200 import device as dev_mod
+    ds = make_dataset(G, seed=23)
+    model = _model(ds, 512, seed=4)
+    b = upload_batch(*ds.collate(range(G)), device="cuda")
+    res = []
+    for defer in (False, True):
+        monkeypatch.setattr(dev_mod, "HEAD_WGRAD_DEFER", defer)
+        eng, ws = _step(model, b, True, drop_p)
+        res.append((ws.loss.clone(), eng.get_grads(), ws.du[:G].clone()))
+    assert torch.equal(res[0][0], res[1][0])
+    assert torch.equal(res[0][2], res[1][2])
+    for name, g in res[0][1].items():
+        if name in ("fc1.w", "fc2.w"):
+            assert _rel(res[1][1][name], g) < 1e-5, name
+        else:
+            assert np.array_equal(res[1][1][name], g), name
