@@ -179,3 +179,22 @@ def test_native_step_other_widths(monkeypatch, hidden):
         assert (tr._native is not None) == native
         res.append((tr.engine.params.clone(), float(tr.ws.loss[0])))
     assert torch.equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
+
+
+def test_native_prep_rejects_small_sets_and_plans(data, monkeypatch):
+    """dippm_train_prep / dippm_train_step return DIPPM_ERR_ARG (nothing launched; raised as
+    ShapeMismatch) for a CSR set smaller than the batch."""
+    from paper_2303_11733_b200.errors import ShapeMismatch
+    from paper_2303_11733_b200.trainer import CsrBuffers
+    ds, model, idx = data
+    monkeypatch.setattr(trainer_mod, "NATIVE_STEP", True)
+    tr = BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3)
+    b = upload_batch(*ds.collate(idx[0]), device="cuda", build_csr=False)
+    tr.step_resident(b)  # builds the plan
+    nat = tr._native
+    small = CsrBuffers(b.N // 2, b.E // 2, b.G, b.x.device)
+    with pytest.raises(ShapeMismatch, match="CSR set"):
+        nat.prep(b, small, torch.cuda.current_stream())
+    with pytest.raises(ShapeMismatch, match="prepared CSR set"):
+        nat.step(b, cset=small)
+    torch.cuda.synchronize()
