@@ -28,6 +28,7 @@ Node rows of a graph are contiguous (graph_ptr), edges carry global ids.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 from dataclasses import dataclass
@@ -267,36 +268,60 @@ def group_edges(src, dst, graph_ptr):
     return ep
 
 
+def _edge_pairs(edges) -> np.ndarray:
+    """[m, 2] int64 view of one graph's edge list: an ndarray as is, a list of (src, dst)
+    pairs flattened with np.fromiter (~3x faster than np.asarray on a list of tuples)."""
+    if isinstance(edges, np.ndarray):
+        return edges.astype(np.int64, copy=False).reshape(-1, 2)
+    m = len(edges)
+    try:
+        flat = np.fromiter(itertools.chain.from_iterable(edges), dtype=np.int64)
+    except (TypeError, ValueError):
+        flat = None
+    if flat is None or flat.size != 2 * m:  # not a list of pairs: the general (slow) conversion
+        return np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    return flat.reshape(m, 2)
+
+
 def collate_host(encodings, fs_vectors, targets=None):
     """Host-side collation of reference-style encodings into flat arrays.
 
     Validation mirrors gnn.py:141-144 (EmptyGraph for N < 1, ShapeMismatch for
-    a feature matrix that is not (N, 32)).  Returns numpy arrays.
-    """
+    a feature matrix that is not (N, 32), or an edge endpoint outside [0, N)).
+    Returns numpy arrays.  One pass per graph: features converted straight into the f32
+    node matrix, edges flattened with np.fromiter; the endpoint check is one vectorised
+    test over the batch."""
     G = len(encodings)
     n = np.empty(G, dtype=np.int64)
-    xs, srcs, dsts = [], [], []
-    off = 0
+    feats, edges = [], []
     for g, enc in enumerate(encodings):
         ng = int(enc.num_nodes)
         if ng < 1:
             raise EmptyGraph("encoding has no nodes")
-        feats = np.asarray(enc.features)
-        if feats.shape != (ng, FEATURE_WIDTH):
-            raise ShapeMismatch(f"feature matrix {feats.shape} does not match {ng} nodes")
-        e = np.asarray(enc.edges, dtype=np.int64).reshape(-1, 2)
-        if e.size and (e.min() < 0 or e.max() >= ng):
-            raise ShapeMismatch(f"edge endpoint outside [0, {ng})")
-        xs.append(feats)
-        srcs.append(e[:, 0] + off)
-        dsts.append(e[:, 1] + off)
+        f = enc.features
+        if not isinstance(f, np.ndarray):
+            f = np.asarray(f)
+        if f.shape != (ng, FEATURE_WIDTH):
+            raise ShapeMismatch(f"feature matrix {f.shape} does not match {ng} nodes")
+        feats.append(f)
+        edges.append(_edge_pairs(enc.edges))
         n[g] = ng
-        off += ng
     graph_ptr = np.zeros(G + 1, dtype=np.int32)
     np.cumsum(n, out=graph_ptr[1:])
-    x = np.concatenate(xs).astype(np.float32) if G else np.zeros((0, FEATURE_WIDTH), np.float32)
-    src = np.concatenate(srcs) if G else np.zeros(0, np.int64)
-    dst = np.concatenate(dsts) if G else np.zeros(0, np.int64)
+    N = int(graph_ptr[-1]) if G else 0
+    x = np.empty((N, FEATURE_WIDTH), np.float32)
+    for g, f in enumerate(feats):
+        x[graph_ptr[g]:graph_ptr[g + 1]] = f
+    ne = np.array([e.shape[0] for e in edges], dtype=np.int64)
+    e_all = np.concatenate(edges) if G else np.zeros((0, 2), np.int64)
+    if e_all.size:
+        lo = np.repeat(graph_ptr[:-1].astype(np.int64), ne)  # each edge's graph offset
+        hi = np.repeat(n, ne)
+        if (e_all.min() < 0) or bool(((e_all[:, 0] >= hi) | (e_all[:, 1] >= hi)).any()):
+            raise ShapeMismatch("edge endpoint outside [0, num_nodes)")
+        src, dst = e_all[:, 0] + lo, e_all[:, 1] + lo
+    else:
+        src = dst = np.zeros(0, np.int64)
     # static features and targets stay float64 (StaticFeatures.as_vector, TargetVector.as_array):
     # the device z-scores them in fp64, so a small fs / y std cannot amplify an fp32 rounding
     fs = np.asarray(fs_vectors, dtype=np.float64).reshape(G, STATIC_WIDTH)
