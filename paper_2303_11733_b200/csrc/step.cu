@@ -275,6 +275,26 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     STEP_CALL(wgrad(P->u, P->d1, P->u_width, G, P->off_fc1w, nullptr, nullptr));
   }
 
+  // Adam split at sage3's first parameter (flat layout sage1 | sage2 | sage3 | fc1..fc3,
+  // gnn.py:488-491): the upper range's operand-copy segments, rebased; DIPPM_SPLIT_ADAM=0 keeps
+  // one launch at the end (A/B switch).  Element-wise update: the same results either way.
+  static const bool split_env = !(getenv("DIPPM_SPLIT_ADAM") && getenv("DIPPM_SPLIT_ADAM")[0] == '0');
+  const int64_t off3 = P->off_w[2];
+  dippm_pack_seg_t seg_lo[DIPPM_MAX_PACK_SEGS], seg_hi[DIPPM_MAX_PACK_SEGS];
+  int n_lo = 0, n_hi = 0;
+  bool split_adam = split_env && off3 % 8 == 0 && P->n_segs <= DIPPM_MAX_PACK_SEGS;
+  for (int k = 0; split_adam && k < P->n_segs; ++k) {
+    dippm_pack_seg_t sg = P->segs[k];
+    if (sg.src_off >= off3) {
+      sg.src_off -= off3;
+      seg_hi[n_hi++] = sg;
+    } else if (sg.src_off + sg.rows * sg.cols <= off3) {
+      seg_lo[n_lo++] = sg;
+    } else {
+      split_adam = false;  // a segment straddles the split: one launch
+    }
+  }
+
   // ---- SAGE backward: dgrad chain on the main stream, weight gradients on the side stream
   for (int i = 2; i >= 0; --i) {
     const dippm_act_t Bi = P->B[i];
@@ -308,14 +328,30 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
     g.gate_bits = bits(i - 1);
     g.bits_ld = P->ws_N;
     STEP_CALL(dippm_gemm(&g, 0, s));
+    if (i == 2 && split_adam) {
+      // sage3 + head gradients are final (head reductions / WGRADs and WGRAD_3 ran on the side
+      // stream); once GATE_3, the last reader of sage3's dgrad copy, is done, their Adam update
+      // runs on the side stream beside agg^T_2 -- off the step's tail
+      cudaEvent_t ev = static_cast<cudaEvent_t>(P->ev[3]);
+      DIPPM_CUDA_CHECK(cudaEventRecord(ev, s));
+      DIPPM_CUDA_CHECK(cudaStreamWaitEvent(side, ev, 0));
+      STEP_CALL(dippm_adam_pack(P->params + off3, P->m + off3, P->v + off3, P->grads + off3, 1.0,
+                                P->n_params - off3, 0, P->t_dev, P->lr, P->beta1, P->beta2, P->eps, 1, P->p32 + off3,
+                                seg_hi, n_hi, side));
+    }
   }
   cudaEvent_t join = static_cast<cudaEvent_t>(P->ev[3]);
   DIPPM_CUDA_CHECK(cudaEventRecord(join, side));
   DIPPM_CUDA_CHECK(cudaStreamWaitEvent(s, join, 0));
 
-  // ---- Adam (t already advanced by the head) + refresh of every operand copy
-  STEP_CALL(dippm_adam_pack(P->params, P->m, P->v, P->grads, 1.0, P->n_params, 0, P->t_dev, P->lr, P->beta1, P->beta2,
-                            P->eps, 1, P->p32, P->segs, P->n_segs, s));
+  // ---- Adam (t already advanced by the head) + refresh of every operand copy: sage1 + sage2
+  // here (sage3 + head already updated on the side stream), or everything
+  if (split_adam)
+    STEP_CALL(dippm_adam_pack(P->params, P->m, P->v, P->grads, 1.0, off3, 0, P->t_dev, P->lr, P->beta1, P->beta2,
+                              P->eps, 1, P->p32, seg_lo, n_lo, s));
+  else
+    STEP_CALL(dippm_adam_pack(P->params, P->m, P->v, P->grads, 1.0, P->n_params, 0, P->t_dev, P->lr, P->beta1,
+                              P->beta2, P->eps, 1, P->p32, P->segs, P->n_segs, s));
   return DIPPM_OK;
 }
 
