@@ -961,22 +961,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.out.base)
             epi_store_chunk(epi_stage + (warp - 2) * kStageWarpBytes, &tmC, p.out.dtype, lane, v, n, m0 + q * 32,
                             local * (kBN / 64) + (ch >> 1));
-        } else if (row < p.M) {
-          if (kEpi == EPI_PARTIAL && p.reduce_mode == 3) {  // single split: final output, scaled
-            float* dst = p.wout + row * p.ldo + n;
+        } else {
+          // fp32 rows (weight-gradient split partials or final output, STORE): staged through this
+          // warp's 4 KB slot (128B-swizzled 16-byte units) and written 4 rows per instruction,
+          // 8 lanes x 16 B per row -- coalesced 128-byte row pieces instead of a 16-byte piece of
+          // each of 32 rows per instruction (the partial rows were LSU-transaction bound)
+          const bool fin = kEpi == EPI_PARTIAL && p.reduce_mode == 3;  // single split: final output, scaled
+          float4* st = reinterpret_cast<float4*>(epi_stage + (warp - 2) * kStageWarpBytes);
+          __syncwarp();  // the previous chunk's reads of the slot are done
 #pragma unroll
-            for (int g = 0; g < 8; ++g)
-              reinterpret_cast<float4*>(dst)[g] =
-                  make_float4(__uint_as_float(raw[4 * g]) * p.out_scale, __uint_as_float(raw[4 * g + 1]) * p.out_scale,
-                              __uint_as_float(raw[4 * g + 2]) * p.out_scale,
-                              __uint_as_float(raw[4 * g + 3]) * p.out_scale);
-          } else {
-            float* dst = p.c + (kEpi == EPI_PARTIAL ? (int64_t)split * p.M * p.ldc : 0) + row * p.ldc + n;
+          for (int g = 0; g < 8; ++g) {
+            float4 f = make_float4(__uint_as_float(raw[4 * g]), __uint_as_float(raw[4 * g + 1]),
+                                   __uint_as_float(raw[4 * g + 2]), __uint_as_float(raw[4 * g + 3]));
+            if (fin)
+              f = make_float4((float)(f.x * p.out_scale), (float)(f.y * p.out_scale), (float)(f.z * p.out_scale),
+                              (float)(f.w * p.out_scale));
+            st[lane * 8 + (g ^ (lane & 7))] = f;
+          }
+          __syncwarp();
+          float* base = fin ? p.wout : p.c + (kEpi == EPI_PARTIAL ? (int64_t)split * p.M * p.ldc : 0);
+          const int64_t ld = fin ? p.ldo : p.ldc;
+          const int u = lane & 7;
 #pragma unroll
-            for (int g = 0; g < 8; ++g)
-              reinterpret_cast<float4*>(dst)[g] =
-                  make_float4(__uint_as_float(raw[4 * g]), __uint_as_float(raw[4 * g + 1]),
-                              __uint_as_float(raw[4 * g + 2]), __uint_as_float(raw[4 * g + 3]));
+          for (int k = 0; k < 8; ++k) {
+            const int rr = (lane >> 3) + 4 * k;
+            const int64_t grow = m0 + q * 32 + rr;
+            const float4 val = st[rr * 8 + (u ^ (rr & 7))];
+            if (grow < p.M) *reinterpret_cast<float4*>(base + grow * ld + n + 4 * u) = val;
           }
         }
         tmem_wait_ld();  // chunk i+1 has landed
