@@ -468,6 +468,15 @@ __device__ __forceinline__ void sum_splits(const Params& p, const float* src, in
       a[0] += v[j].x; a[1] += v[j].y; a[2] += v[j].z; a[3] += v[j].w;
     }
   }
+  for (; s + 8 <= s1; s += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src + (s + j) * plane));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[0] += v[j].x; a[1] += v[j].y; a[2] += v[j].z; a[3] += v[j].w;
+    }
+  }
   for (; s + 4 <= s1; s += 4) {
     float4 v[4];
 #pragma unroll
