@@ -492,6 +492,32 @@ __device__ __forceinline__ void sum_splits(const Params& p, const float* src, in
   }
 }
 
+// two items at once (twice the loads in flight per round trip), each summed in split order
+__device__ __forceinline__ void sum_splits2(const Params& p, const float* src0, const float* src1, int s0, int s1,
+                                            double (&a)[4], double (&b)[4]) {
+  const int64_t plane = p.M * p.ldc;
+  int s = s0;
+  for (; s + 8 <= s1; s += 8) {
+    float4 v[8], w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = __ldcg(reinterpret_cast<const float4*>(src0 + (s + j) * plane));
+      w[j] = __ldcg(reinterpret_cast<const float4*>(src1 + (s + j) * plane));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[0] += v[j].x; a[1] += v[j].y; a[2] += v[j].z; a[3] += v[j].w;
+      b[0] += w[j].x; b[1] += w[j].y; b[2] += w[j].z; b[3] += w[j].w;
+    }
+  }
+  for (; s < s1; ++s) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(src0 + s * plane));
+    const float4 w = __ldcg(reinterpret_cast<const float4*>(src1 + s * plane));
+    a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
+    b[0] += w.x; b[1] += w.y; b[2] += w.z; b[3] += w.w;
+  }
+}
+
 template <int kBN>
 __device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, int n0, int r0, int r1, int tid,
                                                   double4* s_red /* kEpiWarps * 32 entries */) {
@@ -502,7 +528,18 @@ __device__ __forceinline__ void reduce_rows_slice(const Params& p, int64_t m0, i
   while (G < 8 && 2 * G * items <= kT && 4 * G <= p.splits) G <<= 1;
   const double sc = p.out_scale;
   if (G == 1) {
-    for (int idx = tid; idx < items; idx += kT) {
+    int idx = tid;
+    for (; idx + kT < items; idx += 2 * kT) {  // items idx and idx + kT together
+      const int64_t ra = m0 + r0 + idx / kC4, rb = m0 + r0 + (idx + kT) / kC4;
+      const int ca = n0 + (idx % kC4) * 4, cb = n0 + ((idx + kT) % kC4) * 4;
+      double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+      sum_splits2(p, p.c + ra * p.ldc + ca, p.c + rb * p.ldc + cb, 0, p.splits, a, b);
+      *reinterpret_cast<float4*>(p.wout + ra * p.ldo + ca) =
+          make_float4((float)(a[0] * sc), (float)(a[1] * sc), (float)(a[2] * sc), (float)(a[3] * sc));
+      *reinterpret_cast<float4*>(p.wout + rb * p.ldo + cb) =
+          make_float4((float)(b[0] * sc), (float)(b[1] * sc), (float)(b[2] * sc), (float)(b[3] * sc));
+    }
+    if (idx < items) {
       const int64_t r = m0 + r0 + idx / kC4;
       const int c = n0 + (idx % kC4) * 4;
       double a[4] = {0.0, 0.0, 0.0, 0.0};
