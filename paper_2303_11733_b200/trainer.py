@@ -362,7 +362,7 @@ class BatchTrainer:
             eng._uploaded = None
             eng._t_advanced = False  # the step's head advanced t and its Adam ran
             ws.head_pending = None
-            eng.launches += 21
+            eng.launches += 20
             return True
         build_batch_csr(b)
         mode = 2 if self.dropout_p > 0 else 0
