@@ -227,7 +227,11 @@ class BatchTrainer:
 
         Data parallel: the gradient denominator is the global batch
         (`global_graphs`, default G x world), so the all-reduced SUM of the
-        per-rank gradients is the global batch mean (gnn.py:402-404)."""
+        per-rank gradients is the global batch mean (gnn.py:402-404).
+
+        Native steps build the batch's CSR (K1) on a separate stream ahead of the step, ordered
+        after the batch's uploads as they stood at its first step: a resident batch's tensors
+        are not rewritten afterwards (upload a new Batch instead)."""
         self._ensure(b)
         self.steps += 1
         self.engine._uploaded = None  # the step moves the device parameters
