@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DIPPM_ABI_VERSION 14
+#define DIPPM_ABI_VERSION 15
 
 enum dippm_status {
   DIPPM_OK = 0,
@@ -544,6 +544,9 @@ typedef struct dippm_train_batch {
   const dippm_csr_set_t* csr; /* K1 outputs already built by dippm_train_prep (the step's stream
                                  must be ordered after that prep), or NULL: the step runs K1
                                  itself into the plan's buffers */
+  int32_t no_adam;            /* 1: stop once every gradient is final (data parallel: the caller
+                                 all-reduces plan->grads, then runs dippm_adam_pack; the head has
+                                 already advanced plan->t_dev) */
 } dippm_train_batch_t;
 
 int32_t dippm_train_plan_init(dippm_train_plan_t* plan);

@@ -33,7 +33,7 @@ class Act(C.Structure):
     _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("plane_stride", C.c_int64), ("dtype", C.c_int64)]
 
 
-ABI_VERSION = 14  # DIPPM_ABI_VERSION in include/dippm_b200.h
+ABI_VERSION = 15  # DIPPM_ABI_VERSION in include/dippm_b200.h
 
 
 class GemmArgs(C.Structure):
@@ -115,7 +115,8 @@ class TrainBatch(C.Structure):
     """dippm_train_batch_t: one device-resident batch for dippm_train_step."""
     _fields_ = [("x", P), ("src", P), ("dst", P), ("graph_ptr", P), ("edge_ptr", P), ("fs", P), ("y", P),
                 ("N", C.c_int64), ("E", C.c_int64), ("G", C.c_int64), ("max_nodes", C.c_int32),
-                ("max_edges", C.c_int32), ("loss_out", P), ("bad_out", P), ("csr", C.POINTER(CsrSet))]
+                ("max_edges", C.c_int32), ("loss_out", P), ("bad_out", P), ("csr", C.POINTER(CsrSet)),
+                ("no_adam", C.c_int32)]
 
 
 # name -> (restype, argtypes); must match include/dippm_b200.h

@@ -282,7 +282,7 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   const int64_t off3 = P->off_w[2];
   dippm_pack_seg_t seg_lo[DIPPM_MAX_PACK_SEGS], seg_hi[DIPPM_MAX_PACK_SEGS];
   int n_lo = 0, n_hi = 0;
-  bool split_adam = split_env && off3 % 8 == 0 && P->n_segs <= DIPPM_MAX_PACK_SEGS;
+  bool split_adam = split_env && !b->no_adam && off3 % 8 == 0 && P->n_segs <= DIPPM_MAX_PACK_SEGS;
   for (int k = 0; split_adam && k < P->n_segs; ++k) {
     dippm_pack_seg_t sg = P->segs[k];
     if (sg.src_off >= off3) {
@@ -344,6 +344,7 @@ int32_t dippm_train_step(const dippm_train_plan_t* P, const dippm_train_batch_t*
   DIPPM_CUDA_CHECK(cudaEventRecord(join, side));
   DIPPM_CUDA_CHECK(cudaStreamWaitEvent(s, join, 0));
 
+  if (b->no_adam) return DIPPM_OK;  // data parallel: the caller all-reduces, then runs Adam
   // ---- Adam (t already advanced by the head) + refresh of every operand copy: sage1 + sage2
   // here (sage3 + head already updated on the side stream), or everything
   if (split_adam)

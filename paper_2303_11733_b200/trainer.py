@@ -131,8 +131,9 @@ class NativeStep:
     def fits(self, b: Batch) -> bool:
         return b.N <= self.ws.N and b.G <= self.ws.G and b.E <= self.E
 
-    def _fill(self, b: Batch, loss_out, bad_out, cset: CsrBuffers | None) -> _lib.TrainBatch:
+    def _fill(self, b: Batch, loss_out, bad_out, cset: CsrBuffers | None, no_adam: bool = False) -> _lib.TrainBatch:
         t = self.batch
+        t.no_adam = 1 if no_adam else 0
         t.loss_out = loss_out
         t.bad_out = None if bad_out is None else bad_out.data_ptr()
         t.x, t.src, t.dst, t.graph_ptr = b.x.data_ptr(), b.src.data_ptr(), b.dst.data_ptr(), b.graph_ptr.data_ptr()
@@ -151,11 +152,12 @@ class NativeStep:
                    "dippm_train_prep")
 
     def step(self, b: Batch, loss_out: int | None = None, bad_out: torch.Tensor | None = None,
-             graphed: bool = False, cset: CsrBuffers | None = None) -> None:
+             graphed: bool = False, cset: CsrBuffers | None = None, no_adam: bool = False) -> None:
         """graphed: run the step as one CUDA-graph launch (dippm_train_step_graphed; the
         ragged host-batch path, where per-batch torch graphs cannot be reused).  cset: K1
-        outputs already built by prep() (else the step runs K1 itself)."""
-        t = self._fill(b, loss_out, bad_out, cset)
+        outputs already built by prep() (else the step runs K1 itself).  no_adam: stop at the
+        final gradients (data parallel: the caller all-reduces them and runs Adam)."""
+        t = self._fill(b, loss_out, bad_out, cset, no_adam)
         fn = self._fn_graphed if graphed and self._warm and not torch.cuda.is_current_stream_capturing() else self._fn
         _lib.check(fn(C.byref(self.plan), C.byref(t), torch.cuda.current_stream().cuda_stream), "dippm_train_step")
         self._warm = True
@@ -275,7 +277,7 @@ class BatchTrainer:
 
     def _native_ok(self, b: Batch) -> bool:
         eng = self.engine
-        return (NATIVE_STEP and self.allreduce is None and eng.arch == "sage" and eng.fused_head_ok(b.G)
+        return (NATIVE_STEP and eng.arch == "sage" and eng.fused_head_ok(b.G)
                 and eng.overlap_wgrad and not dev.HEAD_POOL and eng.cta_pair == 0 and eng.gemm_hook is None
                 and _lib.call is _LIB_CALL and b.y is not None)
 
@@ -358,15 +360,24 @@ class BatchTrainer:
         nat = self._native_for(b)
         if nat is not None:
             nat.sync_hparams(self)
+            dp = self.allreduce is not None
+            # data parallel: the global-batch denominator (gnn.py:402-404), then the native step up
+            # to the final gradients, one all-reduce of the flat gradient, and Adam
+            nat.plan.grad_den = float(global_graphs if global_graphs else b.G * self.world_size) if dp else 0.0
             if slot is None:
-                nat.step(b, cset=cset)
+                nat.step(b, cset=cset, no_adam=dp)
             else:
-                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1], graphed=NATIVE_GRAPHED,
-                         cset=cset)
+                nat.step(b, self._loss_dev[slot].data_ptr(), self._bad_dev[slot:slot + 1],
+                         graphed=NATIVE_GRAPHED and not dp, cset=cset, no_adam=dp)
             eng._uploaded = None
-            eng._t_advanced = False  # the step's head advanced t and its Adam ran
             ws.head_pending = None
             eng.launches += 20
+            if dp:
+                self.allreduce(eng.grads)  # sum of the per-rank gradient shares (NCCL on this stream)
+                eng._t_advanced = True     # the step's head advanced t
+                eng.adam_step(self.lr)
+                eng.launches += 1
+            eng._t_advanced = False  # the step's head advanced t and its Adam ran
             return True
         build_batch_csr(b)
         mode = 2 if self.dropout_p > 0 else 0

@@ -134,3 +134,46 @@ def test_nccl_one_rank_collectives_on_device():
     ref = _grads("bf16", np.arange(256), 256)
     for name, g in ref.items():
         assert np.array_equal(got[name], g), name
+
+
+def _trainer_worker(rank, port, native, out):
+    import copy
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_11733_b200 import gnn, trainer as trainer_mod
+    from paper_2303_11733_b200.device import upload_batch
+    from paper_2303_11733_b200.dist import OverlappedAllReduce
+    from paper_2303_11733_b200.synth import make_dataset
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        trainer_mod.NATIVE_STEP = native
+        ds = make_dataset(256, seed=29)
+        norm = gnn.Normalizer.fit(ds.y.astype(np.float64), ds.fs.astype(np.float64))
+        model = gnn.create_model(hidden=256, seed=8, normalizer=norm)
+        tr = trainer_mod.BatchTrainer(copy.deepcopy(model), precision="bf16", lr=1e-3, seed=5,
+                                      allreduce=OverlappedAllReduce(), world_size=2, rank=rank)
+        for k in range(2):  # rank r takes graphs [r * 64, (r + 1) * 64) of each 128-graph batch
+            ids = np.arange(k * 128 + rank * 64, k * 128 + (rank + 1) * 64)
+            tr.step_resident(upload_batch(*ds.collate(ids), device="cuda", build_csr=False))
+        torch.cuda.synchronize()
+        assert (tr._native is not None) == native
+        if rank == 0:
+            np.save(out, tr.engine.params.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_data_parallel_native_step_equals_python_step(tmp_path):
+    """Two ranks (gloo, sharing the GPU) training through BatchTrainer with the all-reduce:
+    the native executor (gradients, one all-reduce, Adam) and the Python orchestration (its
+    two overlapped buckets) end with bit-identical parameters."""
+    import torch.multiprocessing as mp
+    res = []
+    for native in (True, False):
+        out = str(tmp_path / f"dp_{int(native)}.npy")
+        mp.spawn(_trainer_worker, args=(_free_port(), native, out), nprocs=2, join=True)
+        res.append(np.load(out))
+    assert np.array_equal(res[0], res[1])
